@@ -1,0 +1,218 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container only (the reference does not exist on the GPU
+box):
+
+    PYTHONDONTWRITEBYTECODE=1 PYTHONPATH=/root/reference/pkg/src \
+        python tests/golden/make_golden.py
+
+Writes small .npz fixtures next to this file.  They pin the oracle
+(`oracle/`) and, through it, the CUDA path.  Nothing here is copied from
+the reference sources: the reference package is imported and executed.
+The two BASELINE initial conditions missing from the reference registry
+(3-D density wave, circular explosion) are passed as callables through
+`Simulation.project_initial_condition`, exactly as SURVEY.md §0 prescribes.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import aderdg  # noqa: E402  (reference, from PYTHONPATH)
+from aderdg import corrector, limiter, predictor  # noqa: E402
+from aderdg.basis import basis_tables  # noqa: E402
+from aderdg.systems import CompressibleEuler  # noqa: E402
+
+from oracle import problems  # noqa: E402  (pure IC formulas)
+
+GAMMA = 1.4
+
+
+def euler_states(dim, count, seed):
+    """Seeded states with the distribution of the reference's
+    random_euler_states (pkg/tests/test_systems.py:15-25)."""
+    rng = np.random.default_rng(seed)
+    q = np.empty((count, dim + 2))
+    rho = rng.uniform(0.1, 3.0, count)
+    vel = rng.uniform(-2.0, 2.0, (count, dim))
+    p = rng.uniform(0.05, 5.0, count)
+    q[:, 0] = rho
+    for j in range(dim):
+        q[:, 1 + j] = rho * vel[:, j]
+    q[:, -1] = p / (GAMMA - 1.0) + 0.5 * rho * np.sum(vel * vel, axis=1)
+    return q
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+def gen_tables():
+    out = {}
+    for n in range(10):
+        t = basis_tables(n)
+        ops = predictor.time_operators(n)
+        for key, val in (("nodes", t.nodes), ("weights", t.weights), ("diff", t.diff),
+                         ("left", t.left_vals), ("right", t.right_vals),
+                         ("sub_project", t.sub_project), ("sub_recover", t.sub_recover),
+                         ("k1", ops.k1), ("k1_inv", ops.k1_inv), ("g0", ops.g0),
+                         ("gw", ops.gw), ("k1_opnorm", np.array(ops.k1_opnorm))):
+            out[f"N{n}_{key}"] = np.asarray(val)
+    save("tables", **out)
+
+
+def gen_pointwise():
+    out = {}
+    for d in (1, 2, 3):
+        sysd = CompressibleEuler(d, gamma=GAMMA)
+        q = euler_states(d, 256, seed=10 + d)
+        # a few inadmissible probes: negative density, negative pressure, nan
+        bad = q[:4].copy()
+        bad[0, 0] = -0.5
+        bad[1, -1] = 0.0
+        bad[2, 1] = np.nan
+        bad[3, -1] = 1e-3
+        qa = np.concatenate([q, bad])
+        out[f"d{d}_q"] = qa
+        out[f"d{d}_flux"] = sysd.flux(q)
+        out[f"d{d}_pressure"] = sysd.pressure(q)
+        out[f"d{d}_admissible"] = sysd.admissible(qa)
+        for j in range(d):
+            out[f"d{d}_lam{j}"] = sysd.max_abs_eigenvalue(q, np.eye(d)[j])
+        # Rusanov terms across axis 0 between shifted states
+        qm, qp = q[:128], q[128:]
+        for j in range(d):
+            lo, hi = corrector.face_fluxes(qm, qp, j, sysd)
+            out[f"d{d}_dlow{j}"] = lo
+            out[f"d{d}_dhigh{j}"] = hi
+    save("pointwise", **out)
+
+
+def wave_mesh(cells, extent_x=1.0):
+    d = len(cells)
+    ext = [(0.0, extent_x)] + [(0.0, 1.0)] * (d - 1)
+    return aderdg.CartesianMesh(ext, cells)
+
+
+def gen_predictor():
+    """Element-local predictor + corrector pieces on small 3-D / 2-D grids."""
+    out = {}
+    for d, cells, degrees in ((3, (2, 2, 2), (1, 2, 3, 4, 5)), (2, (3, 3), (3, 5))):
+        sysd = CompressibleEuler(d, gamma=GAMMA)
+        for n in degrees:
+            mesh = wave_mesh(cells)
+            cfl = 0.9 / (d * (2 * n + 1))
+            sim = aderdg.Simulation(mesh, sysd, n, cfl)
+            ic, _ = problems.density_wave(vel=(1.0, 0.5, -0.7)[:d])
+            u = sim.project_initial_condition(ic)
+            rng = np.random.default_rng(n)
+            u = u * (1.0 + 0.01 * rng.uniform(-1, 1, u.shape))
+            t = basis_tables(n)
+            dt = corrector.compute_timestep(u, sysd, mesh.spacings, cfl, n)
+            res = predictor.picard_solve(u, sysd, mesh.spacings, dt, t)
+            tr = predictor.extract_traces(res.q, t, d)
+            vol = corrector.volume_integral(res.q, sysd, mesh.spacings, dt, t)
+            key = f"d{d}_N{n}"
+            out[key + "_u"] = u
+            out[key + "_dt"] = np.array(dt)
+            out[key + "_q"] = res.q
+            out[key + "_iters"] = np.array(res.iterations)
+            out[key + "_converged"] = res.converged
+            out[key + "_admissible"] = res.admissible
+            out[key + "_vol"] = vol
+            out[key + "_defect"] = predictor.weak_form_defect(res.q, u, sysd, mesh.spacings,
+                                                               dt, t)
+            for (j, s), arr in tr.items():
+                out[key + f"_tr{j}{s}"] = arr
+    save("predictor", **out)
+
+
+def run_case(name, mesh, sysd, degree, cfl, ic, steps, boundary="periodic",
+             use_limiter=False, store_first=False):
+    sim = aderdg.Simulation(mesh, sysd, degree, cfl, boundary=boundary,
+                            use_limiter=use_limiter)
+    u0 = sim.project_initial_condition(ic).copy()
+    dts, iters, flags, fracs, lam = [], [], [], [], []
+    orig = predictor.picard_solve
+
+    def spy(*a, **k):
+        r = orig(*a, **k)
+        iters.append(r.iterations)
+        return r
+
+    predictor.picard_solve = spy
+    first = None
+    try:
+        for _ in range(steps):
+            lam.append([float(np.max(sysd.max_abs_eigenvalue(
+                sim.u.reshape(-1, sysd.n_vars)[sysd.admissible(sim.u.reshape(-1, sysd.n_vars))],
+                np.eye(mesh.dim)[j]))) for j in range(mesh.dim)])
+            sim.run(np.inf, max_steps=sim.step_count + 1)
+            dts.append(sim.history[-1]["dt"])
+            fracs.append(sim.last_limited_fraction)
+            if use_limiter:
+                flags.append(np.asarray(sim.last_troubled, dtype=bool))
+            if store_first and first is None:
+                first = sim.u.copy()
+    finally:
+        predictor.picard_solve = orig
+    arrays = dict(u0=u0, u=sim.u, dts=np.array(dts), iters=np.array(iters),
+                  fracs=np.array(fracs), lam=np.array(lam),
+                  totals=np.array([h["totals"] for h in sim.history]),
+                  degree=np.array(degree), cfl=np.array(cfl),
+                  cells=np.array(mesh.cells),
+                  extents=np.array(mesh.extents))
+    if use_limiter:
+        arrays["troubled"] = np.stack(flags)
+    if first is not None:
+        arrays["u1"] = first
+    save(name, **arrays)
+
+
+def gen_cases():
+    e2 = CompressibleEuler(2, gamma=GAMMA)
+    e3 = CompressibleEuler(3, gamma=GAMMA)
+    e1 = CompressibleEuler(1, gamma=GAMMA)
+    # C1: full config (2-D vortex, 32^2, N=3, cfl 0.9/(2*7), 10 steps)
+    ic, _ = problems.vortex()
+    run_case("c1_vortex", aderdg.CartesianMesh([(0, 10), (0, 10)], (32, 32)), e2, 3,
+             0.9 / 14.0, ic, 10, store_first=True)
+    # C2 shape at oracle size: density wave N=4, 4^3, cfl 1/30, 3 steps
+    ic, _ = problems.density_wave()
+    run_case("c2_wave_4", wave_mesh((4, 4, 4)), e3, 4, 0.9 / 27.0, ic, 3,
+             store_first=True)
+    # C3 degree sweep at oracle size
+    for n in range(2, 10):
+        cells = (3, 3, 3) if n <= 5 else (2, 2, 2)
+        run_case(f"c3_wave_N{n}", wave_mesh(cells), e3, n, 0.9 / (3 * (2 * n + 1)), ic, 2)
+    # C4 shape at oracle size: circular explosion, N=5, limiter, outflow
+    ic4, _ = problems.explosion()
+    run_case("c4_explosion_16", aderdg.CartesianMesh([(-1, 1), (-1, 1)], (16, 16)), e2, 5,
+             0.9 / 22.0, ic4, 6, boundary="outflow", use_limiter=True)
+    # C5 weak-scaling domain: x extended to [0, 2], 4x2x2 cells (2 slabs of 2x2x2)
+    run_case("c5_wave_ext", wave_mesh((4, 2, 2), extent_x=2.0), e3, 4, 0.9 / 27.0, ic, 2)
+    # limiter in 1-D (Sod, outflow) and 2-D walls (blast) for rescue coverage
+    ics, _ = problems.sod()
+    run_case("sod_1d", aderdg.CartesianMesh([(0, 1)], (40,)), e1, 3, 0.09, ics, 12,
+             boundary="outflow", use_limiter=True)
+    icb, _ = problems.blast(p_ambient=1e-2)
+    run_case("blast_wall", aderdg.CartesianMesh([(-1, 1), (-1, 1)], (12, 12)), e2, 2,
+             0.15, icb, 4, boundary="wall", use_limiter=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["tables", "pointwise", "predictor", "cases"]
+    if "tables" in which:
+        gen_tables()
+    if "pointwise" in which:
+        gen_pointwise()
+    if "predictor" in which:
+        gen_predictor()
+    if "cases" in which:
+        gen_cases()
