@@ -1,0 +1,185 @@
+/*
+ * aderdg_b200.h -- C-ABI of libaderdg_b200.so, the B200 (sm_100a) ADER-DG
+ * time step for the compressible Euler equations.
+ *
+ * The reference (/root/reference/pkg/src/aderdg, arXiv:1808.03788 desk
+ * implementation) is pure Python/numpy and has no FFI of its own; its
+ * boundary for this path is the Python solver API.  Each entry point below
+ * replaces one reference function (file:line cited) and is bound by the
+ * drop-in host layer `paper_1808_03788_b200/_lib.py` through ctypes.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers to caller-owned fp64 buffers in
+ *    the reference layout: u[cells_0..cells_{d-1}, P (x) .. P (last), m],
+ *    quantity fastest (driver.py:131-133, mesh.py:48-63).
+ *  - All calls are stream ordered on `stream` (a cudaStream_t) and never
+ *    synchronise the host; scalars that change per step (dt, t) live in
+ *    device memory so a step sequence is CUDA-graph capturable.
+ *  - Return value: ADG_OK or an error code; adg_last_error() describes it.
+ *    The host layer maps ADG_ERR_INVALID -> ValueError, ADG_ERR_RUNTIME ->
+ *    RuntimeError, ADG_ERR_UNSUPPORTED -> NotImplementedError.
+ *  - A handle is bound to one device and is not thread safe.
+ */
+#ifndef ADERDG_B200_H
+#define ADERDG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADG_OK 0
+#define ADG_ERR_INVALID 1
+#define ADG_ERR_RUNTIME 2
+#define ADG_ERR_CUDA 3
+#define ADG_ERR_UNSUPPORTED 4
+
+/* face kinds, driver.py:23 BOUNDARY_KINDS; ADG_BC_GHOST = exterior trace
+ * supplied by the caller (reference "exact" faces, or a neighbour rank's
+ * halo under slab decomposition) */
+#define ADG_BC_PERIODIC 0
+#define ADG_BC_OUTFLOW 1
+#define ADG_BC_WALL 2
+#define ADG_BC_GHOST 3
+
+/* status word bits written by adg_timestep / adg_update (device int32) */
+#define ADG_STATUS_NO_ADMISSIBLE 1   /* corrector.py:44-45 RuntimeError */
+#define ADG_STATUS_NONFINITE 2       /* driver.py:197-199 RuntimeError  */
+
+typedef struct adg_handle adg_handle;
+
+/* Grid descriptor (POD).  cells are the LOCAL element counts of this rank;
+ * dx are the element widths (mesh.py:32).  dim in 1..3, degree in 0..9,
+ * nvars = dim + 2 (Euler). */
+typedef struct adg_grid {
+  int32_t dim;
+  int32_t degree;
+  int32_t nvars;
+  int32_t reserved;
+  int64_t cells[3];
+  double dx[3];
+  double gamma;
+  int32_t bc[3][2];
+} adg_grid;
+
+/* Reduction record filled on device by adg_wavespeed / adg_update and read
+ * by adg_timestep: per-axis max |lambda| over admissible nodes as uint64
+ * bit patterns of non-negative doubles (max is order independent, so the
+ * result is bitwise deterministic), admissible and non-finite counts. */
+typedef struct adg_reduce {
+  uint64_t lam_bits[3];
+  uint64_t n_admissible;
+  uint64_t n_nonfinite;
+  uint64_t reserved[3];
+} adg_reduce;
+
+/* -- lifetime ------------------------------------------------------------ */
+int adg_create(int device, adg_handle** out);
+int adg_destroy(adg_handle* h);
+const char* adg_last_error(const adg_handle* h);
+int adg_version(void);
+
+/* Upload the per-degree constants (replaces basis.py:166-202 BasisTables and
+ * predictor.py:21-47 TimeOperators).  blob layout (P = degree + 1, S = 2N+1):
+ * nodes[P] weights[P] diff[P*P] left[P] right[P] gw[P*P] g0[P] k1_opnorm[1]
+ * sub_project[S*P] sub_recover[P*S]; n = total doubles.  Process-wide. */
+int adg_set_tables(adg_handle* h, int degree, const double* host_blob, int64_t n);
+
+/* -- corrector.compute_timestep (corrector.py:30-55) --------------------- */
+/* zero *red, then fold max |lambda_j| / admissible / non-finite counts of
+ * the nodal states u into it */
+int adg_wavespeed(adg_handle* h, const adg_grid* g, const double* u, adg_reduce* red,
+                  void* stream);
+/* dt = min(cfl / sum_j lam_j/dx_j, t_end - t) written to *dt_dev (inf when
+ * every speed is zero); sets ADG_STATUS_* bits in *status_dev.  t_dev may be
+ * NULL (t = 0). */
+int adg_timestep(adg_handle* h, const adg_grid* g, const adg_reduce* red, double cfl,
+                 const double* t_dev, double t_end, double* dt_dev, int32_t* status_dev,
+                 void* stream);
+
+/* t += dt on device; t_out (may be NULL) receives the new time (the
+ * `self.t += trial` of driver.py:175) */
+int adg_advance_time(adg_handle* h, double* t_dev, const double* dt_dev, double* t_out,
+                     void* stream);
+
+/* -- predictor: startup_guess + picard_solve + extract_traces + the
+ *    corrector's volume_integral, fused per element
+ *    (predictor.py:99-191, :218-230; corrector.py:141-177) -------------- */
+/* u       : nodal states at t_n
+ * dt_dev  : device scalar time step
+ * tol, max_iter (<=0 -> 2N+2), min_iter: Picard control; an element stops
+ *           at its first converged sweep >= min_iter
+ * q_out   : optional [E, P^d, P_t, m] space-time predictor (NULL to skip)
+ * vol_out : [E, P^d, m] volume accumulator (true integral)
+ * traces  : [d][2][E, P^(d-1), P_t, m] face traces (side 0 = low face)
+ * pred_bad: [E] uint8, !(converged && admissible)   (driver.py:212)
+ * sweeps  : [E] int32 Picard sweeps taken                                 */
+int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double* dt_dev,
+                double tol, int max_iter, int min_iter, double* q_out, double* vol_out,
+                double* traces, uint8_t* pred_bad, int32_t* sweeps, void* stream);
+
+/* -- face coupling along one axis: driver._face_states (driver.py:234-261)
+ *    + corrector.face_fluxes (corrector.py:100-129) + the time weighting of
+ *    face_integral (corrector.py:186) ------------------------------------ */
+/* dbar_out: [faces (cells with cells[axis]+1 along axis), P^(d-1), m], the
+ * time-integrated low-side term sum_t w_t d_low; the high-side term is its
+ * exact negation.  ghost_lo / ghost_hi: exterior traces for ADG_BC_GHOST
+ * faces, [cells with 1 along axis, P^(d-1), P_t, m], else NULL. */
+int adg_face_flux(adg_handle* h, const adg_grid* g, int axis, const double* traces,
+                  const double* ghost_lo, const double* ghost_hi, double* dbar_out,
+                  void* stream);
+
+/* -- corrector.face_integral + element_update (corrector.py:180-205) with a
+ *    fused epilogue: wave speeds of u_out folded into red_next (the next
+ *    step's compute_timestep) and per-block conserved-total partials
+ *    (driver.py:344-350).  dbar[a] from adg_face_flux for axis a.
+ *    totals_partial: [adg_update_blocks(g), m] (may be NULL).            */
+int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
+               const double* dbar0, const double* dbar1, const double* dbar2,
+               const double* dt_dev, double* u_out, adg_reduce* red_next,
+               double* totals_partial, void* stream);
+int64_t adg_update_blocks(const adg_grid* g);
+/* totals[m] = cell_volume * fixed-order sum of the partials */
+int adg_totals_finalize(adg_handle* h, const adg_grid* g, const double* totals_partial,
+                        int64_t nblocks, double* totals_out, void* stream);
+
+/* conserved totals of u directly (driver.py:344-350); partial has
+ * adg_update_blocks(g) * m doubles */
+int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partial,
+               double* totals_out, void* stream);
+
+/* -- a posteriori subcell limiter (limiter.py; driver.py:265-299) ------- */
+/* Subcell averages of u (limiter.project_to_subcells, limiter.py:27-33):
+ * sub_out [E, S^d, m] */
+int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, double* sub_out,
+                         void* stream);
+/* Troubled-cell detection (limiter.py:51-86 + driver.py:272-285):
+ * prev_sub / cand_sub [E, S^d, m] subcell averages of u^n and the
+ * candidate, cand the candidate nodal states, pred_bad from adg_predict,
+ * halo_prev [per axis/side: cells with 1 along axis, S^d, m] subcell data of
+ * neighbour ranks for ADG_BC_GHOST faces (NULL otherwise).  Writes
+ * troubled[E] (uint8), the compacted list idx[E] (int32, ascending) and
+ * *count (int32).  force_all != 0 marks every cell. */
+int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub,
+               const double* cand_sub, const double* cand, const uint8_t* pred_bad,
+               double delta0, double eps, int force_all, uint8_t* troubled, int32_t* idx,
+               int32_t* count, void* stream);
+/* MUSCL-Hancock rescue of the listed cells from t^n subcell averages
+ * (limiter.py:89-223 + driver.py:286-298), writing recovered nodal states
+ * into u_out for listed cells (other cells untouched) and setting
+ * *failed_dev != 0 if any cell failed after the first-order retry
+ * (driver.py:292-293 restart). */
+int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const int32_t* idx,
+               const int32_t* count_dev, int32_t count_host_max, const double* dt_dev,
+               double* u_out, int32_t* failed_dev, void* stream);
+/* IC flattening (driver.py:137-152): cells whose nodal or subcell states are
+ * inadmissible are replaced by their weighted mean; *nflat = count */
+int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADERDG_B200_H */

@@ -1,0 +1,148 @@
+"""ctypes binding of libaderdg_b200.so (the C-ABI in include/aderdg_b200.h).
+
+The shared library is built in-tree by `python setup_ext.py` /
+`__graft_entry__.build()` (nvcc, -gencode arch=compute_100a,code=sm_100a).
+There is no fallback: if the library or a CUDA device is missing, every
+entry point raises.
+"""
+
+import ctypes
+import os
+
+LIB_NAME = "libaderdg_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+ADG_OK = 0
+ADG_ERR_INVALID = 1
+ADG_ERR_RUNTIME = 2
+ADG_ERR_CUDA = 3
+ADG_ERR_UNSUPPORTED = 4
+
+BC_CODES = {"periodic": 0, "outflow": 1, "wall": 2, "exact": 3, "ghost": 3}
+
+STATUS_NO_ADMISSIBLE = 1
+STATUS_NONFINITE = 2
+
+# every symbol declared in include/aderdg_b200.h (checked by the CPU tests)
+EXPORTS = (
+    "adg_create", "adg_destroy", "adg_last_error", "adg_version", "adg_set_tables",
+    "adg_wavespeed", "adg_timestep", "adg_advance_time", "adg_predict", "adg_face_flux", "adg_update",
+    "adg_update_blocks", "adg_totals_finalize", "adg_totals", "adg_project_subcells",
+    "adg_detect", "adg_rescue", "adg_flatten_ic",
+)
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("degree", ctypes.c_int32),
+                ("nvars", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("cells", ctypes.c_int64 * 3), ("dx", ctypes.c_double * 3),
+                ("gamma", ctypes.c_double), ("bc", (ctypes.c_int32 * 2) * 3)]
+
+
+class Reduce(ctypes.Structure):
+    _fields_ = [("lam_bits", ctypes.c_uint64 * 3), ("n_admissible", ctypes.c_uint64),
+                ("n_nonfinite", ctypes.c_uint64), ("reserved", ctypes.c_uint64 * 3)]
+
+
+REDUCE_WORDS = ctypes.sizeof(Reduce) // 8
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+
+_SIGS = {
+    "adg_create": (_I, [_I, ctypes.POINTER(_P)]),
+    "adg_destroy": (_I, [_P]),
+    "adg_last_error": (ctypes.c_char_p, [_P]),
+    "adg_version": (_I, []),
+    "adg_set_tables": (_I, [_P, _I, _P, _I64]),
+    "adg_wavespeed": (_I, [_P, _P, _P, _P, _P]),
+    "adg_timestep": (_I, [_P, _P, _P, _D, _P, _D, _P, _P, _P]),
+    "adg_advance_time": (_I, [_P, _P, _P, _P, _P]),
+    "adg_predict": (_I, [_P, _P, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "adg_face_flux": (_I, [_P, _P, _I, _P, _P, _P, _P, _P]),
+    "adg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "adg_update_blocks": (_I64, [_P]),
+    "adg_totals_finalize": (_I, [_P, _P, _P, _I64, _P, _P]),
+    "adg_totals": (_I, [_P, _P, _P, _P, _P, _P]),
+    "adg_project_subcells": (_I, [_P, _P, _P, _P, _P]),
+    "adg_detect": (_I, [_P, _P, _P, _P, _P, _P, _D, _D, _I, _P, _P, _P, _P]),
+    "adg_rescue": (_I, [_P, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P]),
+    "adg_flatten_ic": (_I, [_P, _P, _P, _P, _P]),
+}
+
+_lib = None
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+def load(path=LIB_PATH):
+    """Load (once) and type the shared library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise LibraryMissing(
+            f"{path} not found: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (nvcc, sm_100a).  There is no CPU fallback.")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(handle, rc, what):
+    if rc == ADG_OK:
+        return
+    lib = load()
+    msg = lib.adg_last_error(handle)
+    msg = msg.decode() if msg else ""
+    text = f"{what}: {msg}"
+    if rc == ADG_ERR_INVALID:
+        raise ValueError(text)
+    if rc == ADG_ERR_UNSUPPORTED:
+        raise NotImplementedError(text)
+    raise RuntimeError(text)
+
+
+class Handle:
+    """One adg_handle per CUDA device; tables are uploaded on demand."""
+
+    _per_device = {}
+
+    def __init__(self, device_index):
+        lib = load()
+        h = _P()
+        rc = lib.adg_create(int(device_index), ctypes.byref(h))
+        if rc != ADG_OK:
+            raise RuntimeError(f"adg_create failed on device {device_index} (rc={rc})")
+        self.ptr = h
+        self.device_index = device_index
+        self.lib = lib
+        self._degrees = set()
+
+    @classmethod
+    def get(cls, device_index):
+        if device_index not in cls._per_device:
+            cls._per_device[device_index] = Handle(device_index)
+        return cls._per_device[device_index]
+
+    def ensure_tables(self, tables):
+        if tables.degree in self._degrees:
+            return
+        import numpy as np
+
+        blob = np.ascontiguousarray(tables.device_blob(), dtype=np.float64)
+        rc = self.lib.adg_set_tables(self.ptr, tables.degree, blob.ctypes.data, blob.size)
+        check(self.ptr, rc, "adg_set_tables")
+        self._degrees.add(tables.degree)
+
+    def call(self, name, *args):
+        rc = getattr(self.lib, name)(self.ptr, *args)
+        check(self.ptr, rc, name)

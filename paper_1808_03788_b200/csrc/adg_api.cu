@@ -1,0 +1,245 @@
+// adg_api.cu -- extern "C" entry points of libaderdg_b200.so.
+// Each maps onto one reference function; see include/aderdg_b200.h.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "adg_common.cuh"
+#include "adg_internal.h"
+
+namespace adg {
+__constant__ DegreeTables c_tab[kMaxP];
+
+void upload_tables(int degree, const double* blob, int64_t n, std::string* err, int* rc) {
+  const int P = degree + 1, S = 2 * degree + 1;
+  const int64_t need = 5 * P + 2 * P * P + 1 + 2 * S * P;
+  if (degree < 0 || degree > 9 || n != need) {
+    *err = "bad table blob (degree " + std::to_string(degree) + ", n=" + std::to_string(n) +
+           ", need " + std::to_string(need) + ")";
+    *rc = ADG_ERR_INVALID;
+    return;
+  }
+  DegreeTables t;
+  std::memset(&t, 0, sizeof(t));
+  const double* p = blob;
+  std::memcpy(t.nodes, p, P * 8); p += P;
+  std::memcpy(t.weights, p, P * 8); p += P;
+  std::memcpy(t.diff, p, P * P * 8); p += P * P;
+  std::memcpy(t.left, p, P * 8); p += P;
+  std::memcpy(t.right, p, P * 8); p += P;
+  std::memcpy(t.gw, p, P * P * 8); p += P * P;
+  std::memcpy(t.g0, p, P * 8); p += P;
+  t.k1_opnorm = *p; p += 1;
+  std::memcpy(t.sub_project, p, S * P * 8); p += S * P;
+  std::memcpy(t.sub_recover, p, P * S * 8); p += P * S;
+  // stiff[k, l] = diff[l, k] * w[l]  ((diff * w[:, None]).T, corrector.py:168)
+  for (int k = 0; k < P; ++k)
+    for (int l = 0; l < P; ++l) t.stiff[k * P + l] = t.diff[l * P + k] * t.weights[l];
+  t.loaded = 1;
+  cudaError_t ce = cudaMemcpyToSymbol(c_tab, &t, sizeof(t), sizeof(t) * degree);
+  if (ce != cudaSuccess) {
+    *err = cudaGetErrorString(ce);
+    *rc = ADG_ERR_CUDA;
+    return;
+  }
+  *rc = ADG_OK;
+}
+}  // namespace adg
+
+struct adg_handle {
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+  bool tables_loaded[10] = {false};
+  double* ws = nullptr;   // predictor global-tile workspace (large 3-D tiles)
+  size_t ws_bytes = 0;
+};
+
+static int fail(adg_handle* h, int rc, const std::string& msg) {
+  if (h) h->err = msg;
+  return rc;
+}
+
+static int check_grid(adg_handle* h, const adg_grid* g) {
+  if (!g) return fail(h, ADG_ERR_INVALID, "null grid");
+  if (g->dim < 1 || g->dim > 3) return fail(h, ADG_ERR_INVALID, "dim must be 1..3");
+  if (g->degree < 0 || g->degree > 9) return fail(h, ADG_ERR_INVALID, "degree must be 0..9");
+  if (g->nvars != g->dim + 2) return fail(h, ADG_ERR_UNSUPPORTED, "only Euler (m = d+2)");
+  for (int j = 0; j < g->dim; ++j) {
+    if (g->cells[j] < 1) return fail(h, ADG_ERR_INVALID, "cell counts must be positive");
+    if (!(g->dx[j] > 0.0)) return fail(h, ADG_ERR_INVALID, "spacings must be positive");
+    for (int s = 0; s < 2; ++s)
+      if (g->bc[j][s] < 0 || g->bc[j][s] > 3) return fail(h, ADG_ERR_INVALID, "bad bc kind");
+  }
+  if (!h->tables_loaded[g->degree])
+    return fail(h, ADG_ERR_INVALID, "tables for this degree not uploaded (adg_set_tables)");
+  return ADG_OK;
+}
+
+static int wrap(adg_handle* h, int rc, const std::string& e) {
+  if (rc != ADG_OK) h->err = e;
+  return rc;
+}
+
+extern "C" {
+
+int adg_version(void) { return 1; }
+
+int adg_create(int device, adg_handle** out) {
+  if (!out) return ADG_ERR_INVALID;
+  *out = nullptr;
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) return ADG_ERR_CUDA;
+  adg_handle* h = new adg_handle();
+  h->device = device;
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  *out = h;
+  return ADG_OK;
+}
+
+int adg_destroy(adg_handle* h) {
+  if (!h) return ADG_OK;
+  if (h->ws) cudaFree(h->ws);
+  delete h;
+  return ADG_OK;
+}
+
+const char* adg_last_error(const adg_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int adg_set_tables(adg_handle* h, int degree, const double* host_blob, int64_t n) {
+  if (!h || !host_blob) return ADG_ERR_INVALID;
+  std::string e;
+  int rc = ADG_OK;
+  adg::upload_tables(degree, host_blob, n, &e, &rc);
+  if (rc == ADG_OK) h->tables_loaded[degree] = true;
+  return wrap(h, rc, e);
+}
+
+int adg_wavespeed(adg_handle* h, const adg_grid* g, const double* u, adg_reduce* red,
+                  void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::state_reduce(g, u, red, nullptr, (cudaStream_t)stream, &e), e);
+}
+
+int adg_timestep(adg_handle* h, const adg_grid* g, const adg_reduce* red, double cfl,
+                 const double* t_dev, double t_end, double* dt_dev, int32_t* status_dev,
+                 void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (!(cfl < 1.0 / (2 * g->degree + 1)))
+    return fail(h, ADG_ERR_INVALID, "cfl violates the stability bound 1/(2N+1)");
+  std::string e;
+  return wrap(h, adg::timestep(g, red, cfl, t_dev, t_end, dt_dev, status_dev,
+                               (cudaStream_t)stream, &e), e);
+}
+
+int adg_advance_time(adg_handle* h, double* t_dev, const double* dt_dev, double* t_out,
+                     void* stream) {
+  if (!h || !t_dev || !dt_dev) return ADG_ERR_INVALID;
+  std::string e;
+  return wrap(h, adg::advance_time(t_dev, dt_dev, t_out, (cudaStream_t)stream, &e), e);
+}
+
+int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double* dt_dev,
+                double tol, int max_iter, int min_iter, double* q_out, double* vol_out,
+                double* traces, uint8_t* pred_bad, int32_t* sweeps, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  const size_t need = adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms);
+  if (need > h->ws_bytes) {
+    if (h->ws) cudaFree(h->ws);
+    h->ws = nullptr;
+    h->ws_bytes = 0;
+    if (cudaMalloc(&h->ws, need) != cudaSuccess)
+      return fail(h, ADG_ERR_CUDA, "cannot allocate predictor workspace");
+    h->ws_bytes = need;
+  }
+  std::string e;
+  return wrap(h, adg::predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out, traces,
+                              pred_bad, sweeps, (cudaStream_t)stream, h->num_sms, h->ws,
+                              h->ws_bytes, &e), e);
+}
+
+int adg_face_flux(adg_handle* h, const adg_grid* g, int axis, const double* traces,
+                  const double* ghost_lo, const double* ghost_hi, double* dbar_out,
+                  void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::face_flux(g, axis, traces, ghost_lo, ghost_hi, dbar_out,
+                                (cudaStream_t)stream, &e), e);
+}
+
+int64_t adg_update_blocks(const adg_grid* g) { return adg::reduce_blocks(g); }
+
+int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
+               const double* dbar0, const double* dbar1, const double* dbar2,
+               const double* dt_dev, double* u_out, adg_reduce* red_next,
+               double* totals_partial, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  const double* db[3] = {dbar0, dbar1, dbar2};
+  std::string e;
+  return wrap(h, adg::update(g, u, vol, db, dt_dev, u_out, red_next, totals_partial,
+                             (cudaStream_t)stream, &e), e);
+}
+
+int adg_totals_finalize(adg_handle* h, const adg_grid* g, const double* totals_partial,
+                        int64_t nblocks, double* totals_out, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::totals_finalize(g, totals_partial, nblocks, totals_out,
+                                      (cudaStream_t)stream, &e), e);
+}
+
+int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partial,
+               double* totals_out, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  rc = adg::state_reduce(g, u, nullptr, partial, (cudaStream_t)stream, &e);
+  if (rc) return wrap(h, rc, e);
+  return wrap(h, adg::totals_finalize(g, partial, adg::reduce_blocks(g), totals_out,
+                                      (cudaStream_t)stream, &e), e);
+}
+
+int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, double* sub_out,
+                         void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::project_subcells(g, u, sub_out, (cudaStream_t)stream, &e), e);
+}
+
+int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub,
+               const double* cand_sub, const double* cand, const uint8_t* pred_bad,
+               double delta0, double eps, int force_all, uint8_t* troubled, int32_t* idx,
+               int32_t* count, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::detect(g, prev_sub, cand_sub, cand, pred_bad, delta0, eps, force_all,
+                             troubled, idx, count, (cudaStream_t)stream, &e), e);
+}
+
+int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const int32_t* idx,
+               const int32_t* count_dev, int32_t count_host_max, const double* dt_dev,
+               double* u_out, int32_t* failed_dev, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::rescue(g, prev_sub, idx, count_dev, count_host_max, dt_dev, u_out,
+                             failed_dev, (cudaStream_t)stream, &e), e);
+}
+
+int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::flatten_ic(g, u, nflat, (cudaStream_t)stream, &e), e);
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// adg_common.cuh -- shared device code of libaderdg_b200.so (sm_100a).
+//
+// Per-degree constant tables (basis.py:166-202, predictor.py:21-47) live in
+// __constant__ memory for every degree 0..9 at once, so kernels templated on
+// P = N+1 index them at compile time (uniform access -> constant cache).
+// Euler pointwise physics follows systems.py:112-234 operation by operation.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/aderdg_b200.h"
+
+namespace adg {
+
+constexpr int kMaxP = 10;
+constexpr int kMaxS = 2 * kMaxP - 1;
+
+struct DegreeTables {
+  double nodes[kMaxP];
+  double weights[kMaxP];
+  double diff[kMaxP * kMaxP];     // diff[k*P + l] = ell_l'(xi_k)
+  double left[kMaxP];
+  double right[kMaxP];
+  double gw[kMaxP * kMaxP];       // K1^-1 diag(w)
+  double g0[kMaxP];               // K1^-1 phi(0)
+  double k1_opnorm;
+  double sub_project[kMaxS * kMaxP];  // [S][P]
+  double sub_recover[kMaxP * kMaxS];  // [P][S]
+  double stiff[kMaxP * kMaxP];    // stiff[k*P+l] = diff[l*P+k] * w[l]  (corrector.py:168)
+  int loaded;
+};
+
+extern __constant__ DegreeTables c_tab[kMaxP];
+
+template <int P> __device__ __forceinline__ const DegreeTables& tab() { return c_tab[P - 1]; }
+
+__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+// ---------------------------------------------------------------- Euler
+// systems.py:128-133 pressure; identical operation order.
+template <int D>
+__device__ __forceinline__ double pressure(const double* q, double gm1) {
+  double kin = q[1] * q[1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
+  return gm1 * (q[D + 1] - 0.5 * kin / q[0]);
+}
+
+// systems.py:140-156: F[j][v].  One IEEE division (1/rho) as in the reference.
+template <int D>
+__device__ __forceinline__ void flux_all(const double* q, double gm1, double f[D][D + 2]) {
+  const double r = 1.0 / q[0];
+  double kin = q[1] * q[1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
+  const double p = gm1 * (q[D + 1] - 0.5 * kin * r);
+  const double ep = q[D + 1] + p;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double vj = q[1 + j] * r;
+    f[j][0] = q[1 + j];
+#pragma unroll
+    for (int i = 0; i < D; ++i) f[j][1 + i] = q[1 + i] * vj;
+    f[j][1 + j] += p;
+    f[j][D + 1] = ep * vj;
+  }
+}
+
+// Flux along a single axis a (same arithmetic as flux_all's row a).
+template <int D>
+__device__ __forceinline__ void flux_axis(const double* q, double gm1, int a, double f[D + 2]) {
+  const double r = 1.0 / q[0];
+  double kin = q[1] * q[1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
+  const double p = gm1 * (q[D + 1] - 0.5 * kin * r);
+  const double ep = q[D + 1] + p;
+  const double va = q[1 + a] * r;
+  f[0] = q[1 + a];
+#pragma unroll
+  for (int i = 0; i < D; ++i) f[1 + i] = q[1 + i] * va;
+  f[1 + a] += p;
+  f[D + 1] = ep * va;
+}
+
+// systems.py:173-178 with normal e_a: |u_n / rho| + sqrt(gamma p / rho),
+// u_n accumulated as 0 + sum_j q_j n_j exactly like the reference.
+template <int D>
+__device__ __forceinline__ double max_abs_eig(const double* q, double gamma, double gm1, int a) {
+  double un = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) un = un + q[1 + j] * (j == a ? 1.0 : 0.0);
+  const double p = pressure<D>(q, gm1);
+  return fabs(un / q[0]) + sqrt(gamma * p / q[0]);
+}
+
+// systems.py:225-229: all finite, rho > 0, p > 0.
+template <int D>
+__device__ __forceinline__ bool admissible(const double* q, double gm1) {
+  bool fin = true;
+#pragma unroll
+  for (int v = 0; v < D + 2; ++v) fin = fin && isfinite(q[v]);
+  const double p = pressure<D>(q, gm1);
+  return fin && (q[0] > 0.0) && (p > 0.0);
+}
+
+__device__ __forceinline__ void atomic_max_pos(uint64_t* addr, double v) {
+  // v >= 0 and finite: IEEE bit patterns order like unsigned integers
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// Host-side launch helpers ------------------------------------------------
+struct LaunchCtx {
+  cudaStream_t stream;
+  int num_sms;
+};
+
+}  // namespace adg

@@ -1,0 +1,534 @@
+// adg_corrector.cu -- CFL reduction, Rusanov face coupling and the element
+// update with a fused next-step wave-speed / conserved-total epilogue.
+//
+// References: corrector.compute_timestep (corrector.py:30-55),
+// driver._face_states/_ghost_trace (driver.py:234-261),
+// corrector.face_fluxes (corrector.py:100-129), face_integral
+// (corrector.py:180-196), element_update (corrector.py:199-205),
+// Simulation.conserved_totals (driver.py:344-350).
+#include <algorithm>
+
+#include "adg_common.cuh"
+#include "adg_internal.h"
+
+namespace adg {
+
+int64_t n_elements(const adg_grid* g) {
+  int64_t n = 1;
+  for (int j = 0; j < g->dim; ++j) n *= g->cells[j];
+  return n;
+}
+
+int64_t reduce_blocks(const adg_grid* g) {
+  const int64_t P = g->degree + 1;
+  int64_t pd = 1;
+  for (int j = 0; j < g->dim; ++j) pd *= P;
+  const int64_t work = n_elements(g) * pd;
+  return std::max<int64_t>(1, std::min<int64_t>((work + kReduceThreads - 1) / kReduceThreads,
+                                                kReduceBlocksCap));
+}
+
+// -------------------------------------------------------------------------
+// Block-level fold of per-thread wave speeds / counts / totals.  Max is
+// order independent; totals use a fixed shuffle tree + fixed warp order, so
+// results are bitwise reproducible for a given grid.
+template <int D>
+__device__ void block_fold(double lam[3], unsigned nadm, unsigned nnf, const double* tot,
+                           adg_reduce* red, double* partial) {
+  constexpr int M = D + 2;
+  constexpr int NW = kReduceThreads / 32;
+  __shared__ double s_lam[NW][3];
+  __shared__ unsigned s_cnt[NW][2];
+  __shared__ double s_tot[NW][M];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) lam[j] = fmax(lam[j], __shfl_xor_sync(0xffffffffu, lam[j], o));
+  }
+  nadm = __reduce_add_sync(0xffffffffu, nadm);
+  nnf = __reduce_add_sync(0xffffffffu, nnf);
+  double t[M];
+  if (partial) {
+#pragma unroll
+    for (int v = 0; v < M; ++v) {
+      t[v] = tot[v];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t[v] += __shfl_xor_sync(0xffffffffu, t[v], o);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) s_lam[warp][j] = lam[j];
+    s_cnt[warp][0] = nadm;
+    s_cnt[warp][1] = nnf;
+    if (partial) {
+#pragma unroll
+      for (int v = 0; v < M; ++v) s_tot[warp][v] = t[v];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double L[3] = {0.0, 0.0, 0.0};
+    unsigned long long na = 0, nn = 0;
+    double T[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) T[v] = 0.0;
+    for (int w = 0; w < NW; ++w) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) L[j] = fmax(L[j], s_lam[w][j]);
+      na += s_cnt[w][0];
+      nn += s_cnt[w][1];
+      if (partial) {
+#pragma unroll
+        for (int v = 0; v < M; ++v) T[v] += s_tot[w][v];
+      }
+    }
+    if (red) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) atomic_max_pos(&red->lam_bits[j], L[j]);
+      if (na) atomicAdd(reinterpret_cast<unsigned long long*>(&red->n_admissible), na);
+      if (nn) atomicAdd(reinterpret_cast<unsigned long long*>(&red->n_nonfinite), nn);
+    }
+    if (partial) {
+#pragma unroll
+      for (int v = 0; v < M; ++v) partial[(size_t)blockIdx.x * M + v] = T[v];
+    }
+  }
+}
+
+// Per-node contribution to the fold: wave speeds over admissible nodes
+// (corrector.py:42-52), non-finite detection (driver.py:197), weighted
+// totals (driver.py:347-350 without the cell volume).
+template <int D>
+__device__ __forceinline__ void node_fold(const double* q, double gamma, double gm1, double wnode,
+                                          double lam[3], unsigned& nadm, unsigned& nnf,
+                                          double* tot) {
+  constexpr int M = D + 2;
+  bool fin = true;
+#pragma unroll
+  for (int v = 0; v < M; ++v) fin = fin && isfinite(q[v]);
+  nnf += fin ? 0u : 1u;
+  if (admissible<D>(q, gm1)) {
+    ++nadm;
+#pragma unroll
+    for (int j = 0; j < D; ++j) lam[j] = fmax(lam[j], max_abs_eig<D>(q, gamma, gm1, j));
+  }
+  if (tot) {
+#pragma unroll
+    for (int v = 0; v < M; ++v) tot[v] = fma(q[v], wnode, tot[v]);
+  }
+}
+
+template <int D, int P>
+__device__ __forceinline__ double node_weight(int node) {
+  const DegreeTables& T = tab<P>();
+  if (D == 1) return T.weights[node];
+  if (D == 2) return T.weights[node / P] * T.weights[node % P];
+  return T.weights[node / (P * P)] * T.weights[(node / P) % P] * T.weights[node % P];
+}
+
+template <int D, int P>
+__global__ void __launch_bounds__(kReduceThreads)
+state_reduce_kernel(const double* __restrict__ u, int64_t nodes, double gamma,
+                    adg_reduce* red, double* partial) {
+  constexpr int M = D + 2;
+  constexpr int PD = ipow(P, D);
+  const double gm1 = gamma - 1.0;
+  double lam[3] = {0.0, 0.0, 0.0};
+  unsigned nadm = 0, nnf = 0;
+  double tot[M];
+#pragma unroll
+  for (int v = 0; v < M; ++v) tot[v] = 0.0;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nodes;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    double q[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) q[v] = u[n * M + v];
+    node_fold<D>(q, gamma, gm1, node_weight<D, P>((int)(n % PD)), lam, nadm, nnf,
+                 partial ? tot : nullptr);
+  }
+  block_fold<D>(lam, nadm, nnf, tot, red, partial);
+}
+
+__global__ void zero_reduce_kernel(adg_reduce* red) {
+  if (threadIdx.x < sizeof(adg_reduce) / 8)
+    reinterpret_cast<unsigned long long*>(red)[threadIdx.x] = 0ull;
+}
+
+// corrector.py:47-55 plus the t_end clamp of driver.py:195
+__global__ void timestep_kernel(const adg_reduce* red, int dim, double dx0, double dx1,
+                                double dx2, double cfl, const double* t_dev, double t_end,
+                                double* dt_out, int32_t* status) {
+  const double dxs[3] = {dx0, dx1, dx2};
+  int st = 0;
+  if (red->n_admissible == 0) st |= ADG_STATUS_NO_ADMISSIBLE;
+  if (red->n_nonfinite != 0) st |= ADG_STATUS_NONFINITE;
+  double denom = 0.0;
+  for (int j = 0; j < dim; ++j) denom += __longlong_as_double((long long)red->lam_bits[j]) / dxs[j];
+  double dt = denom == 0.0 ? __longlong_as_double(0x7ff0000000000000LL) : cfl / denom;
+  const double t = t_dev ? *t_dev : 0.0;
+  const double rem = t_end - t;
+  if (rem < dt) dt = rem;
+  *dt_out = dt;
+  if (status) *status |= st;
+}
+
+__global__ void advance_time_kernel(double* t, const double* dt, double* t_out) {
+  const double tn = *t + *dt;
+  *t = tn;
+  if (t_out) *t_out = tn;
+}
+
+// -------------------------------------------------------------------------
+// Face coupling.  Thread per (face, tangential node); loops over the P time
+// nodes and integrates sum_t w_t d_low(t) (corrector.py:186).
+template <int D, int P>
+__global__ void __launch_bounds__(256)
+face_kernel(const double* __restrict__ traces, const double* __restrict__ ghost_lo,
+            const double* __restrict__ ghost_hi, double* __restrict__ dbar, int axis,
+            int64_t c0, int64_t c1, int64_t c2, int bc_lo, int bc_hi, double gamma) {
+  constexpr int M = D + 2;
+  constexpr int PD = ipow(P, D);
+  constexpr int PF = PD / P;  // tangential nodes per face
+  const DegreeTables& T = tab<P>();
+  const double gm1 = gamma - 1.0;
+  int64_t n[3] = {c0, c1, c2};
+  int64_t nf[3] = {c0, c1, c2};
+  nf[axis] += 1;
+  const int64_t faces = nf[0] * (D >= 2 ? nf[1] : 1) * (D == 3 ? nf[2] : 1);
+  const int64_t E = n[0] * (D >= 2 ? n[1] : 1) * (D == 3 ? n[2] : 1);
+  const size_t fstride = (size_t)E * PD * M;
+  const double* tr_lo = traces + (size_t)(2 * axis) * fstride;
+  const double* tr_hi = tr_lo + fstride;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < faces * PF;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = x / PF;
+    const int tg = (int)(x - f * PF);
+    int64_t c[3] = {0, 0, 0};
+    {
+      int64_t r = f;
+      for (int j = D - 1; j >= 0; --j) {
+        c[j] = r % nf[j];
+        r /= nf[j];
+      }
+    }
+    const int64_t ca = c[axis];
+    auto elem = [&](int64_t caxis) {
+      int64_t cc[3] = {c[0], c[1], c[2]};
+      cc[axis] = caxis;
+      int64_t e = 0;
+      for (int j = 0; j < D; ++j) e = e * n[j] + cc[j];
+      return e;
+    };
+    auto plane = [&]() {  // index within the boundary plane (axis removed)
+      int64_t e = 0;
+      for (int j = 0; j < D; ++j)
+        if (j != axis) e = e * n[j] + c[j];
+      return e;
+    };
+    // minus state source (low side), plus state source (high side)
+    const double* pm;
+    const double* pp;
+    bool reflect_m = false, reflect_p = false;
+    if (ca == 0) {
+      if (bc_lo == ADG_BC_PERIODIC) pm = tr_hi + (size_t)elem(n[axis] - 1) * PD * M;
+      else if (bc_lo == ADG_BC_GHOST) pm = ghost_lo + (size_t)plane() * PD * M;
+      else {
+        pm = tr_lo + (size_t)elem(0) * PD * M;
+        reflect_m = bc_lo == ADG_BC_WALL;
+      }
+    } else {
+      pm = tr_hi + (size_t)elem(ca - 1) * PD * M;
+    }
+    if (ca == n[axis]) {
+      if (bc_hi == ADG_BC_PERIODIC) pp = tr_lo + (size_t)elem(0) * PD * M;
+      else if (bc_hi == ADG_BC_GHOST) pp = ghost_hi + (size_t)plane() * PD * M;
+      else {
+        pp = tr_hi + (size_t)elem(n[axis] - 1) * PD * M;
+        reflect_p = bc_hi == ADG_BC_WALL;
+      }
+    } else {
+      pp = tr_lo + (size_t)elem(ca) * PD * M;
+    }
+    pm += (size_t)tg * P * M;
+    pp += (size_t)tg * P * M;
+    double acc[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) acc[v] = 0.0;
+#pragma unroll
+    for (int t = 0; t < P; ++t) {
+      double qm[M], qp[M];
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        qm[v] = pm[t * M + v];
+        qp[v] = pp[t * M + v];
+      }
+      if (reflect_m) qm[1 + axis] = -qm[1 + axis];   // systems.py:231-234
+      if (reflect_p) qp[1 + axis] = -qp[1 + axis];
+      const double s = fmax(max_abs_eig<D>(qm, gamma, gm1, axis),
+                            max_abs_eig<D>(qp, gamma, gm1, axis));
+      double fm[M], fp[M];
+      flux_axis<D>(qm, gm1, axis, fm);
+      flux_axis<D>(qp, gm1, axis, fp);
+      const double hs = 0.5 * s;
+      const double wt = T.weights[t];
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        const double central = 0.5 * (fm[v] + fp[v]);
+        const double dlow = (central + 0.0) - hs * (qp[v] - qm[v]);
+        acc[v] = fma(wt, dlow, acc[v]);
+      }
+    }
+    double* o = dbar + (size_t)x * M;
+#pragma unroll
+    for (int v = 0; v < M; ++v) o[v] = acc[v];
+  }
+}
+
+// -------------------------------------------------------------------------
+// Element update, thread per (element, node), grid-stride with a fixed grid.
+template <int D, int P>
+__global__ void __launch_bounds__(kReduceThreads)
+update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
+              const double* __restrict__ db0, const double* __restrict__ db1,
+              const double* __restrict__ db2, const double* __restrict__ dt_dev,
+              double* __restrict__ u_out, int64_t c0, int64_t c1, int64_t c2, double dx0,
+              double dx1, double dx2, double gamma, adg_reduce* red, double* partial) {
+  constexpr int M = D + 2;
+  constexpr int PD = ipow(P, D);
+  constexpr int PF = PD / P;
+  const DegreeTables& T = tab<P>();
+  const double gm1 = gamma - 1.0;
+  const double dt = *dt_dev;
+  const int64_t n[3] = {c0, c1, c2};
+  const double dx[3] = {dx0, dx1, dx2};
+  const double* dbs[3] = {db0, db1, db2};
+  const int64_t E = n[0] * (D >= 2 ? n[1] : 1) * (D == 3 ? n[2] : 1);
+  const double cv = dx0 * (D >= 2 ? dx1 : 1.0) * (D == 3 ? dx2 : 1.0);
+  double lam[3] = {0.0, 0.0, 0.0};
+  unsigned nadm = 0, nnf = 0;
+  double tot[M];
+#pragma unroll
+  for (int v = 0; v < M; ++v) tot[v] = 0.0;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < E * PD;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = x / PD;
+    const int node = (int)(x - e * PD);
+    int k[3] = {0, 0, 0};
+    if (D == 1) k[0] = node;
+    if (D == 2) { k[0] = node / P; k[1] = node % P; }
+    if (D == 3) { k[0] = node / (P * P); k[1] = (node / P) % P; k[2] = node % P; }
+    int64_t c[3] = {0, 0, 0};
+    {
+      int64_t r = e;
+      for (int j = D - 1; j >= 0; --j) {
+        c[j] = r % n[j];
+        r /= n[j];
+      }
+    }
+    double total[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) total[v] = vol[x * M + v];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      // face index of the element's low face along a in the (n_a+1) face grid
+      int64_t flo = 0;
+      for (int j = 0; j < D; ++j) flo = flo * (n[j] + (j == a ? 1 : 0)) + c[j];
+      int64_t stride_a = 1;
+      for (int j = D - 1; j > a; --j) stride_a *= n[j];
+      const int64_t fhi = flo + stride_a;
+      int tg = 0;
+      double wtan = 1.0;
+      bool first = true;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        if (j == a) continue;
+        tg = tg * P + k[j];
+        wtan = first ? T.weights[k[j]] : wtan * T.weights[k[j]];
+        first = false;
+      }
+      const double area = cv / dx[a];
+      const double sc = dt * area;
+      const double* dlo = dbs[a] + ((size_t)flo * PF + tg) * M;
+      const double* dhi = dbs[a] + ((size_t)fhi * PF + tg) * M;
+      const double vl = T.left[k[a]], vr = T.right[k[a]];
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        const double blo = (D > 1) ? (-dlo[v]) * wtan : -dlo[v];
+        total[v] -= sc * (vl * blo);
+      }
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        const double bhi = (D > 1) ? dhi[v] * wtan : dhi[v];
+        total[v] -= sc * (vr * bhi);
+      }
+    }
+    const double wnode = node_weight<D, P>(node);
+    const double mass = cv * wnode;
+    double q[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) {
+      q[v] = u[x * M + v] + total[v] / mass;
+      u_out[x * M + v] = q[v];
+    }
+    node_fold<D>(q, gamma, gm1, wnode, lam, nadm, nnf, partial ? tot : nullptr);
+  }
+  block_fold<D>(lam, nadm, nnf, tot, red, partial);
+}
+
+template <int M>
+__global__ void totals_finalize_kernel(const double* __restrict__ partial, int64_t nb, double cv,
+                                       double* out) {
+  // one warp per quantity, fixed strided order + fixed shuffle tree
+  const int v = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (v >= M) return;
+  double s = 0.0;
+  for (int64_t b = lane; b < nb; b += 32) s += partial[b * M + v];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[v] = cv * s;
+}
+
+// ------------------------------------------------------------------ launchers
+#define ADG_SWITCH_DP(FN, ...)                                                   \
+  do {                                                                           \
+    const int P_ = g->degree + 1;                                                \
+    switch (g->dim * 16 + P_) {                                                  \
+      case 16 + 1: FN<1, 1>(__VA_ARGS__); break;                                 \
+      case 16 + 2: FN<1, 2>(__VA_ARGS__); break;                                 \
+      case 16 + 3: FN<1, 3>(__VA_ARGS__); break;                                 \
+      case 16 + 4: FN<1, 4>(__VA_ARGS__); break;                                 \
+      case 16 + 5: FN<1, 5>(__VA_ARGS__); break;                                 \
+      case 16 + 6: FN<1, 6>(__VA_ARGS__); break;                                 \
+      case 16 + 7: FN<1, 7>(__VA_ARGS__); break;                                 \
+      case 16 + 8: FN<1, 8>(__VA_ARGS__); break;                                 \
+      case 16 + 9: FN<1, 9>(__VA_ARGS__); break;                                 \
+      case 16 + 10: FN<1, 10>(__VA_ARGS__); break;                               \
+      case 32 + 1: FN<2, 1>(__VA_ARGS__); break;                                 \
+      case 32 + 2: FN<2, 2>(__VA_ARGS__); break;                                 \
+      case 32 + 3: FN<2, 3>(__VA_ARGS__); break;                                 \
+      case 32 + 4: FN<2, 4>(__VA_ARGS__); break;                                 \
+      case 32 + 5: FN<2, 5>(__VA_ARGS__); break;                                 \
+      case 32 + 6: FN<2, 6>(__VA_ARGS__); break;                                 \
+      case 32 + 7: FN<2, 7>(__VA_ARGS__); break;                                 \
+      case 32 + 8: FN<2, 8>(__VA_ARGS__); break;                                 \
+      case 32 + 9: FN<2, 9>(__VA_ARGS__); break;                                 \
+      case 32 + 10: FN<2, 10>(__VA_ARGS__); break;                               \
+      case 48 + 1: FN<3, 1>(__VA_ARGS__); break;                                 \
+      case 48 + 2: FN<3, 2>(__VA_ARGS__); break;                                 \
+      case 48 + 3: FN<3, 3>(__VA_ARGS__); break;                                 \
+      case 48 + 4: FN<3, 4>(__VA_ARGS__); break;                                 \
+      case 48 + 5: FN<3, 5>(__VA_ARGS__); break;                                 \
+      case 48 + 6: FN<3, 6>(__VA_ARGS__); break;                                 \
+      case 48 + 7: FN<3, 7>(__VA_ARGS__); break;                                 \
+      case 48 + 8: FN<3, 8>(__VA_ARGS__); break;                                 \
+      case 48 + 9: FN<3, 9>(__VA_ARGS__); break;                                 \
+      case 48 + 10: FN<3, 10>(__VA_ARGS__); break;                               \
+      default: *err = "unsupported dim/degree"; return ADG_ERR_UNSUPPORTED;      \
+    }                                                                            \
+  } while (0)
+
+static int check_launch(std::string* err) {
+  cudaError_t ce = cudaGetLastError();
+  if (ce != cudaSuccess) {
+    *err = cudaGetErrorString(ce);
+    return ADG_ERR_CUDA;
+  }
+  return ADG_OK;
+}
+
+template <int D, int P>
+static void launch_state_reduce(const adg_grid* g, const double* u, adg_reduce* red,
+                                double* partial, cudaStream_t st) {
+  const int64_t nodes = n_elements(g) * ipow(P, D);
+  state_reduce_kernel<D, P><<<(unsigned)reduce_blocks(g), kReduceThreads, 0, st>>>(
+      u, nodes, g->gamma, red, partial);
+}
+
+int state_reduce(const adg_grid* g, const double* u, adg_reduce* red, double* partial,
+                 cudaStream_t st, std::string* err) {
+  if (red) zero_reduce_kernel<<<1, 32, 0, st>>>(red);
+  ADG_SWITCH_DP(launch_state_reduce, g, u, red, partial, st);
+  return check_launch(err);
+}
+
+int timestep(const adg_grid* g, const adg_reduce* red, double cfl, const double* t_dev,
+             double t_end, double* dt_dev, int32_t* status, cudaStream_t st, std::string* err) {
+  timestep_kernel<<<1, 1, 0, st>>>(red, g->dim, g->dx[0], g->dx[1], g->dx[2], cfl, t_dev, t_end,
+                                   dt_dev, status);
+  return check_launch(err);
+}
+
+int advance_time(double* t_dev, const double* dt_dev, double* t_out, cudaStream_t st,
+                 std::string* err) {
+  advance_time_kernel<<<1, 1, 0, st>>>(t_dev, dt_dev, t_out);
+  return check_launch(err);
+}
+
+template <int D, int P>
+static void launch_face(const adg_grid* g, int axis, const double* traces, const double* glo,
+                        const double* ghi, double* dbar, cudaStream_t st) {
+  int64_t nf[3] = {g->cells[0], g->cells[1], g->cells[2]};
+  nf[axis] += 1;
+  int64_t faces = 1;
+  for (int j = 0; j < D; ++j) faces *= nf[j];
+  const int64_t work = faces * (ipow(P, D) / P);
+  const int64_t blocks = std::min<int64_t>((work + 255) / 256, 1 << 20);
+  face_kernel<D, P><<<(unsigned)blocks, 256, 0, st>>>(
+      traces, glo, ghi, dbar, axis, g->cells[0], D >= 2 ? g->cells[1] : 1,
+      D == 3 ? g->cells[2] : 1, g->bc[axis][0], g->bc[axis][1], g->gamma);
+}
+
+int face_flux(const adg_grid* g, int axis, const double* traces, const double* ghost_lo,
+              const double* ghost_hi, double* dbar, cudaStream_t st, std::string* err) {
+  if (axis < 0 || axis >= g->dim) {
+    *err = "axis out of range";
+    return ADG_ERR_INVALID;
+  }
+  if ((g->bc[axis][0] == ADG_BC_GHOST && !ghost_lo) ||
+      (g->bc[axis][1] == ADG_BC_GHOST && !ghost_hi)) {
+    *err = "ghost boundary without ghost traces";
+    return ADG_ERR_INVALID;
+  }
+  ADG_SWITCH_DP(launch_face, g, axis, traces, ghost_lo, ghost_hi, dbar, st);
+  return check_launch(err);
+}
+
+template <int D, int P>
+static void launch_update(const adg_grid* g, const double* u, const double* vol,
+                          const double* const dbar[3], const double* dt_dev, double* u_out,
+                          adg_reduce* red, double* partial, cudaStream_t st) {
+  update_kernel<D, P><<<(unsigned)reduce_blocks(g), kReduceThreads, 0, st>>>(
+      u, vol, dbar[0], dbar[1], dbar[2], dt_dev, u_out, g->cells[0], D >= 2 ? g->cells[1] : 1,
+      D == 3 ? g->cells[2] : 1, g->dx[0], D >= 2 ? g->dx[1] : 1.0, D == 3 ? g->dx[2] : 1.0,
+      g->gamma, red, partial);
+}
+
+int update(const adg_grid* g, const double* u, const double* vol, const double* const dbar[3],
+           const double* dt_dev, double* u_out, adg_reduce* red_next, double* partial,
+           cudaStream_t st, std::string* err) {
+  for (int a = 0; a < g->dim; ++a)
+    if (!dbar[a]) {
+      *err = "missing face data";
+      return ADG_ERR_INVALID;
+    }
+  if (red_next) zero_reduce_kernel<<<1, 32, 0, st>>>(red_next);
+  ADG_SWITCH_DP(launch_update, g, u, vol, dbar, dt_dev, u_out, red_next, partial, st);
+  return check_launch(err);
+}
+
+int totals_finalize(const adg_grid* g, const double* partial, int64_t nb, double* out,
+                    cudaStream_t st, std::string* err) {
+  double cv = 1.0;
+  for (int j = 0; j < g->dim; ++j) cv *= g->dx[j];
+  switch (g->dim) {
+    case 1: totals_finalize_kernel<3><<<1, 96, 0, st>>>(partial, nb, cv, out); break;
+    case 2: totals_finalize_kernel<4><<<1, 128, 0, st>>>(partial, nb, cv, out); break;
+    case 3: totals_finalize_kernel<5><<<1, 160, 0, st>>>(partial, nb, cv, out); break;
+    default: *err = "bad dim"; return ADG_ERR_INVALID;
+  }
+  return check_launch(err);
+}
+
+}  // namespace adg

@@ -1,0 +1,54 @@
+// adg_internal.h -- host-side launchers shared between the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/aderdg_b200.h"
+
+namespace adg {
+
+constexpr int kReduceThreads = 256;
+constexpr int64_t kReduceBlocksCap = 4096;  // fixed -> bitwise-reproducible totals
+
+int64_t n_elements(const adg_grid* g);
+int64_t reduce_blocks(const adg_grid* g);
+
+size_t predict_workspace_bytes(int dim, int P, int num_sms);
+int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol, int max_iter,
+            int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
+            int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
+            std::string* err);
+
+int state_reduce(const adg_grid* g, const double* u, adg_reduce* red, double* partial,
+                 cudaStream_t st, std::string* err);
+int timestep(const adg_grid* g, const adg_reduce* red, double cfl, const double* t_dev,
+             double t_end, double* dt_dev, int32_t* status, cudaStream_t st, std::string* err);
+int advance_time(double* t_dev, const double* dt_dev, double* t_out, cudaStream_t st,
+                 std::string* err);
+int face_flux(const adg_grid* g, int axis, const double* traces, const double* ghost_lo,
+              const double* ghost_hi, double* dbar, cudaStream_t st, std::string* err);
+int update(const adg_grid* g, const double* u, const double* vol, const double* const dbar[3],
+           const double* dt_dev, double* u_out, adg_reduce* red_next, double* partial,
+           cudaStream_t st, std::string* err);
+int totals_finalize(const adg_grid* g, const double* partial, int64_t nblocks, double* out,
+                    cudaStream_t st, std::string* err);
+
+// limiter
+int project_subcells(const adg_grid* g, const double* u, double* sub, cudaStream_t st,
+                     std::string* err);
+int detect(const adg_grid* g, const double* prev_sub, const double* cand_sub,
+           const double* cand, const uint8_t* pred_bad, double delta0, double eps,
+           int force_all, uint8_t* troubled, int32_t* idx, int32_t* count, cudaStream_t st,
+           std::string* err);
+int rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
+           const int32_t* count_dev, int32_t count_max, const double* dt_dev, double* u_out,
+           int32_t* failed, cudaStream_t st, std::string* err);
+int flatten_ic(const adg_grid* g, double* u, int32_t* nflat, cudaStream_t st,
+               std::string* err);
+
+void upload_tables(int degree, const double* blob, int64_t n, std::string* err, int* rc);
+
+}  // namespace adg

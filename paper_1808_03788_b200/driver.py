@@ -1,0 +1,436 @@
+"""Single-grid time marching on a B200 (drop-in for reference driver.py).
+
+`Simulation` keeps the reference constructor, attributes and methods
+(driver.py:72-377); the state `u` is a CUDA fp64 torch tensor in the
+reference layout (cells..., P..., m).  One accepted step is the kernel
+sequence
+
+    adg_timestep   dt = cfl / sum_j lambda_j / dx_j   (lambda from the previous
+                   update's epilogue, or adg_wavespeed for a fresh state)
+    adg_predict    startup + Picard + traces + volume integral, per element
+    adg_face_flux  Rusanov face terms, one launch per axis
+    adg_update     face integrals + element update + next-step wave speeds
+                   + conserved-total partials
+    [limiter]      adg_project_subcells / adg_detect / adg_rescue (C4)
+
+all stream ordered with dt and t resident on the device, so
+`run(max_steps=K)` without a limiter or callback issues K steps with no
+host synchronisation; status words (no admissible state, non-finite
+state) are checked once at the end and raised as the reference's
+RuntimeErrors.
+"""
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .basis import basis_tables, weight_tensor
+
+BOUNDARY_KINDS = ("periodic", "outflow", "wall", "exact")
+
+DMP_DELTA0 = 1e-3   # limiter.py:22
+DMP_EPS = 1e-3      # limiter.py:23
+MAX_HALVINGS = 3    # limiter.py:24
+
+DEFAULT_CFL = {0: 0.9, 1: 0.30, 2: 0.15, 3: 0.09, 4: 0.062, 5: 0.044,
+               6: 0.033, 7: 0.026, 8: 0.021, 9: 0.018}   # driver.py:27-28
+
+
+def default_cfl(degree):
+    return DEFAULT_CFL.get(degree, 0.4 / (2 * degree + 1))
+
+
+def max_cfl_number(degree):
+    return 1.0 / (2 * degree + 1)
+
+
+def normalize_boundary(spec, dim):
+    """{(axis, side): kind} from a kind, a per-axis mapping or a per-face dict
+    (driver.py:36-69, same accepted forms and errors)."""
+    table = {}
+    if isinstance(spec, str):
+        table = {(j, s): spec for j in range(dim) for s in (0, 1)}
+    elif isinstance(spec, dict) and spec and all(isinstance(k, tuple) for k in spec):
+        table = dict(spec)
+    elif isinstance(spec, dict):
+        for j in range(dim):
+            kind = spec.get(j, "periodic")
+            pair = (kind, kind) if isinstance(kind, str) else tuple(kind)
+            table[(j, 0)], table[(j, 1)] = pair
+    else:
+        raise ValueError(f"unsupported boundary spec: {spec!r}")
+    for j in range(dim):
+        for s in (0, 1):
+            kind = table.get((j, s))
+            if kind not in BOUNDARY_KINDS:
+                raise ValueError(f"unknown boundary kind {kind!r} on axis {j} side {s}")
+        lo, hi = table[(j, 0)], table[(j, 1)]
+        if "periodic" in (lo, hi) and lo != hi:
+            raise ValueError(f"axis {j}: periodic must be set on both sides")
+    return table
+
+
+def _stream_ptr():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+class StepBuffers:
+    """Device workspaces of one grid (all torch CUDA tensors)."""
+
+    def __init__(self, grid, n_elem, pd, m, dim, device, cells, limiter=False):
+        f64 = dict(dtype=torch.float64, device=device)
+        self.vol = torch.empty(n_elem * pd * m, **f64)
+        self.traces = torch.empty(2 * dim * n_elem * pd * m, **f64)
+        self.dbar = []
+        p = round(pd ** (1.0 / dim))
+        for a in range(dim):
+            nf = 1
+            for j in range(dim):
+                nf *= cells[j] + (1 if j == a else 0)
+            self.dbar.append(torch.empty(nf * (pd // p) * m, **f64))
+        self.pred_bad = torch.empty(n_elem, dtype=torch.uint8, device=device)
+        self.sweeps = torch.empty(n_elem, dtype=torch.int32, device=device)
+        self.red = torch.zeros(2, _lib.REDUCE_WORDS, dtype=torch.int64, device=device)
+        self.nblocks = int(_lib.load().adg_update_blocks(_lib.ctypes.byref(grid)))
+        self.partial = torch.empty(self.nblocks * m, **f64)
+        self.t = torch.zeros(1, **f64)
+
+
+class Simulation:
+    """Owns the device state and marches it in time (driver.py:72-123).
+
+    Extra keyword (not in the reference): `device` (CUDA device index or
+    torch.device; default the current device), `min_picard_iter` (an element
+    keeps sweeping until at least this many sweeps, default 1).
+    """
+
+    def __init__(self, mesh, system, degree, cfl, boundary="periodic",
+                 use_limiter=False, predictor_mode="conservative",
+                 exact_solution=None, dmp_delta0=DMP_DELTA0,
+                 dmp_eps=DMP_EPS, batch_width=None, picard_tol=1e-12,
+                 device=None, min_picard_iter=1, _ghost=None):
+        if mesh.dim != system.dim:
+            raise ValueError("mesh and system dimensions differ")
+        if not 0.0 < cfl < max_cfl_number(degree):
+            raise ValueError(
+                f"cfl must lie in (0, {max_cfl_number(degree)}) "
+                f"for degree {degree}, got {cfl}")
+        if getattr(system, "name", None) != "euler":
+            raise NotImplementedError(
+                f"system '{getattr(system, 'name', system)}' has no B200 kernels (Euler only)")
+        if predictor_mode not in ("conservative", "primitive"):
+            raise ValueError(f"unknown predictor mode {predictor_mode!r}")
+        if predictor_mode == "primitive":
+            raise NotImplementedError("primitive-variable predictor is not on the B200 path yet")
+        self.mesh = mesh
+        self.system = system
+        self.tables = basis_tables(degree)
+        self.cfl = float(cfl)
+        self.boundary = normalize_boundary(boundary, mesh.dim)
+        self.use_limiter = bool(use_limiter)
+        self.predictor_mode = predictor_mode
+        self.exact_solution = exact_solution
+        self.dmp_delta0 = float(dmp_delta0)
+        self.dmp_eps = float(dmp_eps)
+        self.batch_width = batch_width
+        self.picard_tol = float(picard_tol)
+        self.min_picard_iter = int(min_picard_iter)
+        if exact_solution is None and any(k == "exact" for k in self.boundary.values()):
+            raise ValueError("exact boundaries need an exact_solution")
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1808_03788_b200 needs a CUDA device (B200); "
+                               "there is no CPU fallback")
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", torch.device(device).index
+                                   if isinstance(device, torch.device) else int(device))
+        self._h = _lib.Handle.get(self.device.index)
+        self._h.ensure_tables(self.tables)
+        self._ghost = _ghost or {}
+        d = mesh.dim
+        self._P = degree + 1
+        self._m = system.n_vars
+        self._pd = self._P ** d
+        self._shape = tuple(mesh.cells) + (self._P,) * d + (self._m,)
+        self._grid = self._make_grid(mesh.cells, mesh.spacings)
+        self._buf = None
+        self._u = None
+        self._u_next = None
+        self._red_cur = None      # index into buf.red holding lambda of u (or None)
+        self.t = 0.0
+        self.step_count = 0
+        self.force_limit_all = False
+        self.last_limited_fraction = 0.0
+        self.last_troubled = None
+        self.last_sweeps = None
+        self.history = []
+        self.sweep_log = []
+
+    # -- plumbing ------------------------------------------------------
+    def _make_grid(self, cells, spacings):
+        g = _lib.Grid()
+        d = self.mesh.dim
+        g.dim = d
+        g.degree = self.tables.degree
+        g.nvars = self.system.n_vars
+        for j in range(3):
+            g.cells[j] = int(cells[j]) if j < d else 1
+            g.dx[j] = float(spacings[j]) if j < d else 1.0
+        g.gamma = float(self.system.gamma)
+        for j in range(d):
+            for s in (0, 1):
+                kind = self.boundary[(j, s)]
+                if (j, s) in self._ghost:
+                    kind = "ghost"
+                g.bc[j][s] = _lib.BC_CODES[kind]
+        return g
+
+    def _gp(self):
+        return _lib.ctypes.byref(self._grid)
+
+    def _ensure_buffers(self):
+        if self._buf is None:
+            self._buf = StepBuffers(self._grid, self.mesh.n_elements, self._pd, self._m,
+                                    self.mesh.dim, self.device, self.mesh.cells,
+                                    self.use_limiter)
+            self._u_next = torch.empty(self._shape, dtype=torch.float64, device=self.device)
+        return self._buf
+
+    # -- setup ---------------------------------------------------------
+    def project_initial_condition(self, fn):
+        """Collocate fn at the quadrature nodes (driver.py:127-154) and upload.
+        With the limiter on, cells with an inadmissible nodal or subcell state
+        are flattened to their weighted mean on the device (adg_flatten_ic)."""
+        coords = self.mesh.node_coords(self.tables)
+        u = np.asarray(fn(coords), dtype=float)
+        if u.shape != self._shape:
+            raise ValueError(f"initial condition returned shape {u.shape}, "
+                             f"expected {self._shape}")
+        self.set_state(u)
+        if self.use_limiter:
+            nflat = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self._h.call("adg_flatten_ic", self._gp(), _ptr(self._u), _ptr(nflat),
+                         _stream_ptr())
+            self.ic_flattened = int(nflat.item())
+            self._red_cur = None
+        return self._u
+
+    def set_state(self, u):
+        """driver.py:156-157; accepts numpy arrays or tensors of the state shape."""
+        t = torch.as_tensor(np.asarray(u, dtype=float) if not isinstance(u, torch.Tensor) else u)
+        t = t.to(device=self.device, dtype=torch.float64).contiguous()
+        if tuple(t.shape) != self._shape:
+            raise ValueError(f"state shape {tuple(t.shape)} != {self._shape}")
+        self._ensure_buffers()
+        self._u = t.clone()
+        self._red_cur = None
+
+    @property
+    def u(self):
+        return self._u
+
+    @u.setter
+    def u(self, value):
+        self.set_state(value)
+
+    # -- device step pieces -------------------------------------------
+    def _wavespeed(self):
+        buf = self._ensure_buffers()
+        red = buf.red[0]
+        self._h.call("adg_wavespeed", self._gp(), _ptr(self._u), _ptr(red), _stream_ptr())
+        self._red_cur = 0
+
+    def _timestep_into(self, dt_dst, status_dst, t_end):
+        buf = self._buf
+        if self._red_cur is None:
+            self._wavespeed()
+        red = buf.red[self._red_cur]
+        self._h.call("adg_timestep", self._gp(), _ptr(red), self.cfl, _ptr(buf.t),
+                     float(t_end), _ptr(dt_dst), _ptr(status_dst), _stream_ptr())
+
+    def _predict(self, dt_dev, q_out=None):
+        buf = self._buf
+        self._h.call("adg_predict", self._gp(), _ptr(self._u), _ptr(dt_dev), self.picard_tol,
+                     0, self.min_picard_iter, _ptr(q_out), _ptr(buf.vol), _ptr(buf.traces),
+                     _ptr(buf.pred_bad), _ptr(buf.sweeps), _stream_ptr())
+
+    def _faces(self):
+        buf = self._buf
+        for a in range(self.mesh.dim):
+            glo = self._ghost.get((a, 0))
+            ghi = self._ghost.get((a, 1))
+            self._h.call("adg_face_flux", self._gp(), a, _ptr(buf.traces), _ptr(glo),
+                         _ptr(ghi), _ptr(buf.dbar[a]), _stream_ptr())
+
+    def _update(self, dt_dev, totals_dst):
+        buf = self._buf
+        nxt = 1 - (self._red_cur or 0)
+        db = [_ptr(buf.dbar[a]) if a < self.mesh.dim else None for a in range(3)]
+        self._h.call("adg_update", self._gp(), _ptr(self._u), _ptr(buf.vol), db[0], db[1],
+                     db[2], _ptr(dt_dev), _ptr(self._u_next), _ptr(buf.red[nxt]),
+                     _ptr(buf.partial), _stream_ptr())
+        if totals_dst is not None:
+            self._h.call("adg_totals_finalize", self._gp(), _ptr(buf.partial), buf.nblocks,
+                         _ptr(totals_dst), _stream_ptr())
+        return nxt
+
+    def _enqueue_unlimited(self, dt_dev, totals_dst, t_dst):
+        """One unlimited step on the stream; commits u <- u_next."""
+        buf = self._buf
+        self._predict(dt_dev)
+        if self._exchange is not None:
+            self._exchange(self)   # neighbour-rank face traces -> ghost buffers
+        self._faces()
+        nxt = self._update(dt_dev, totals_dst)
+        self._h.call("adg_advance_time", _ptr(buf.t), _ptr(dt_dev), _ptr(t_dst), _stream_ptr())
+        self._u, self._u_next = self._u_next, self._u
+        self._red_cur = nxt
+
+    _exchange = None   # hook for slab decomposition (decomp.SlabSimulation)
+
+    # -- stepping ------------------------------------------------------
+    def max_timestep(self):
+        """corrector.compute_timestep on the device (corrector.py:30-55)."""
+        if self._u is None:
+            raise RuntimeError("no initial state set")
+        self._ensure_buffers()
+        out = torch.empty(1, dtype=torch.float64, device=self.device)
+        status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._timestep_into(out, status, math.inf)
+        st = int(status.item())
+        if st & _lib.STATUS_NO_ADMISSIBLE:
+            raise RuntimeError("no admissible state found while sizing the time step")
+        return float(out.item())
+
+    def advance(self, dt):
+        """One step of (at most) dt with stability restarts (driver.py:166-184)."""
+        if self._u is None:
+            raise RuntimeError("no initial state set")
+        self._ensure_buffers()
+        trial = float(dt)
+        m = self._m
+        row = torch.empty(2 + m, dtype=torch.float64, device=self.device)
+        for _ in range(MAX_HALVINGS + 1):
+            row[0] = trial
+            ok, fraction, troubled = self._attempt(row, trial)
+            if ok:
+                self.t += trial
+                self.step_count += 1
+                self.last_limited_fraction = fraction
+                self.last_troubled = troubled
+                host = row.cpu().numpy()
+                self._record(trial, host[2:2 + m])
+                return trial
+            trial *= 0.5
+        raise RuntimeError(f"step at t={self.t:.6g} failed after "
+                           f"{MAX_HALVINGS} step halvings")
+
+    def _attempt(self, row, trial):
+        buf = self._buf
+        dt_dev = row[0:1]
+        if not self.use_limiter:
+            self._enqueue_unlimited(dt_dev, row[2:], row[1:2])
+            self.sweep_log.append(int(buf.sweeps.max().item()))
+            return True, 0.0, None
+        return self._attempt_limited(row, trial)
+
+    def _attempt_limited(self, row, trial):
+        from . import limiter as _limiter  # noqa: F401  (kernels live in the .so)
+
+        raise NotImplementedError("subcell limiter kernels are not built yet")
+
+    def run(self, t_end, max_steps=None, on_step=None):
+        """March until t_end or max_steps (driver.py:186-202)."""
+        if self._u is None:
+            raise RuntimeError("no initial state set")
+        self._ensure_buffers()
+        scale = abs(t_end) if np.isfinite(t_end) else 1.0
+        tiny = 1e-12 * max(1.0, scale)
+        fast = (on_step is None and not self.use_limiter and not np.isfinite(t_end)
+                and max_steps is not None)
+        if fast:
+            self._run_batch(max(0, max_steps - self.step_count))
+            return self.step_count
+        while self.t < t_end - tiny:
+            if max_steps is not None and self.step_count >= max_steps:
+                break
+            dt = min(self.max_timestep(), t_end - self.t)
+            self.advance(dt)
+            if not self._state_finite():
+                raise RuntimeError(f"non-finite state after step {self.step_count}")
+            if on_step is not None:
+                on_step(self)
+        return self.step_count
+
+    def _state_finite(self):
+        red = self._buf.red[self._red_cur]
+        return int(red[4].item()) == 0
+
+    def _run_batch(self, k):
+        """k device-resident steps with one host synchronisation at the end."""
+        if k <= 0:
+            return
+        buf = self._buf
+        m = self._m
+        rows = torch.zeros(k, 2 + m, dtype=torch.float64, device=self.device)
+        status = torch.zeros(k, dtype=torch.int32, device=self.device)
+        sweeps = torch.zeros(k, dtype=torch.int32, device=self.device)
+        buf.t.fill_(self.t)
+        for s in range(k):
+            self._timestep_into(rows[s, 0:1], status[s:s + 1], math.inf)
+            self._enqueue_unlimited(rows[s, 0:1], rows[s, 2:], rows[s, 1:2])
+            torch.amax(buf.sweeps, dim=0, keepdim=True, out=sweeps[s:s + 1])
+        host = rows.cpu().numpy()
+        st = status.cpu().numpy()
+        sw = sweeps.cpu().numpy()
+        final_nonfinite = not self._state_finite()
+        for s in range(k):
+            if st[s] & _lib.STATUS_NO_ADMISSIBLE:
+                raise RuntimeError("no admissible state found while sizing the time step")
+            if s > 0 and st[s] & _lib.STATUS_NONFINITE:
+                raise RuntimeError(f"non-finite state after step {self.step_count}")
+            self.t = float(host[s, 1])
+            self.step_count += 1
+            self.last_limited_fraction = 0.0
+            self.last_troubled = None
+            self.sweep_log.append(int(sw[s]))
+            self._record(float(host[s, 0]), host[s, 2:2 + m])
+        if final_nonfinite:
+            raise RuntimeError(f"non-finite state after step {self.step_count}")
+
+    # -- reductions ----------------------------------------------------
+    def conserved_totals(self):
+        """Domain integrals per quantity (driver.py:344-350), device reduction."""
+        buf = self._ensure_buffers()
+        out = torch.empty(self._m, dtype=torch.float64, device=self.device)
+        self._h.call("adg_totals", self._gp(), _ptr(self._u), _ptr(buf.partial), _ptr(out),
+                     _stream_ptr())
+        return out.cpu().numpy()
+
+    def error_norms(self, reference=None, t=None):
+        """Quadrature L1/L2/Linf errors (driver.py:352-367), evaluated on device."""
+        fn = reference if reference is not None else self.exact_solution
+        if fn is None:
+            raise ValueError("no reference solution available")
+        when = self.t if t is None else t
+        ref = torch.as_tensor(np.asarray(fn(self.mesh.node_coords(self.tables), when), float),
+                              device=self.device)
+        diff = self._u - ref
+        w = torch.as_tensor(weight_tensor(self.tables.weights, self.mesh.dim),
+                            device=self.device)[..., None]
+        vol = self.mesh.cell_volume
+        red = tuple(range(diff.ndim - 1))
+        return {"l1": (vol * (diff.abs() * w).sum(dim=red)).cpu().numpy(),
+                "l2": torch.sqrt(vol * (diff * diff * w).sum(dim=red)).cpu().numpy(),
+                "linf": diff.abs().amax(dim=red).cpu().numpy()}
+
+    def _record(self, dt, totals):
+        self.history.append({"step": self.step_count, "time": self.t, "dt": dt,
+                             "totals": np.array(totals, dtype=float),
+                             "limited_fraction": self.last_limited_fraction})

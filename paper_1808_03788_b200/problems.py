@@ -1,0 +1,157 @@
+"""Initial conditions of the benchmark configurations (setup, host side).
+
+`build_problem(name, system, **params)` mirrors the reference registry
+(problems.py:208-242) for the Euler cases and adds the two BASELINE
+initial states the reference lacks: the 3-D smooth
+density wave (C2/C3/C5) and the 2-D circular explosion (C4).  Each builder
+returns (ic, exact): ic(points) -> states, exact(points, t) or None.
+"""
+
+import numpy as np
+
+
+def isentropic_vortex(system, beta=5.0, center=(5.0, 5.0), domain_size=(10.0, 10.0)):
+    """problems.py:14-51 (C1)."""
+    if system.name != "euler" or system.dim != 2:
+        raise ValueError("the vortex case needs 2-D Euler")
+    g = system.gamma
+    cx, cy = (float(c) for c in center)
+    lx, ly = (float(s) for s in domain_size)
+    amp = float(beta) / (2.0 * np.pi)
+    b = float(beta)
+    tcoef = (g - 1.0) * b * b / (8.0 * g * np.pi * np.pi)
+
+    def exact(points, t):
+        rx = points[..., 0] - cx - t
+        ry = points[..., 1] - cy - t
+        rx -= lx * np.round(rx / lx)
+        ry -= ly * np.round(ry / ly)
+        r2 = rx * rx + ry * ry
+        bump = np.exp(0.5 * (1.0 - r2))
+        vx = 1.0 + (-amp * bump * ry)
+        vy = 1.0 + amp * bump * rx
+        temp = 1.0 - tcoef * np.exp(1.0 - r2)
+        rho = temp ** (1.0 / (g - 1.0))
+        p = temp ** (g / (g - 1.0))
+        energy = p / (g - 1.0) + 0.5 * rho * (vx * vx + vy * vy)
+        return np.stack([rho, rho * vx, rho * vy, energy], axis=-1)
+
+    return (lambda points: exact(points, 0.0)), exact
+
+
+def density_wave(system, amplitude=0.2, velocity=None, pressure=1.0):
+    """rho = 1 + a sin(2 pi sum_j x_j), v = velocity (default all ones),
+    p = pressure; exact solution is translation (BASELINE C2/C3/C5)."""
+    if system.name != "euler":
+        raise ValueError("the density wave needs Euler")
+    d = system.dim
+    g = system.gamma
+    vel = np.ones(d) if velocity is None else np.asarray(velocity, float)
+
+    def exact(points, t):
+        arg = np.zeros(points.shape[:-1])
+        for j in range(d):
+            arg = arg + (points[..., j] - vel[j] * t)
+        rho = 1.0 + amplitude * np.sin(2.0 * np.pi * arg)
+        out = np.empty(points.shape[:-1] + (d + 2,))
+        out[..., 0] = rho
+        v2 = 0.0
+        for j in range(d):
+            out[..., 1 + j] = rho * vel[j]
+            v2 = v2 + vel[j] * vel[j]
+        out[..., -1] = pressure / (g - 1.0) + 0.5 * rho * v2
+        return out
+
+    return (lambda points: exact(points, 0.0)), exact
+
+
+def circular_explosion(system, radius=0.5, inner=(1.0, 1.0), outer=(0.125, 0.1)):
+    """(rho, p) = inner for r < radius else outer, at rest (BASELINE C4)."""
+    if system.name != "euler" or system.dim != 2:
+        raise ValueError("the explosion case needs 2-D Euler")
+    g = system.gamma
+
+    def ic(points):
+        inside = points[..., 0] ** 2 + points[..., 1] ** 2 < radius * radius
+        rho = np.where(inside, inner[0], outer[0])
+        p = np.where(inside, inner[1], outer[1])
+        zero = np.zeros_like(rho)
+        return np.stack([rho, zero, zero, p / (g - 1.0)], axis=-1)
+
+    return ic, None
+
+
+def sod_shock_tube(system, split=0.5):
+    """problems.py:96-110."""
+    if system.name != "euler" or system.dim != 1:
+        raise ValueError("the shock tube needs 1-D Euler")
+    g = system.gamma
+
+    def ic(points):
+        left = points[..., 0] < split
+        rho = np.where(left, 1.0, 0.125)
+        p = np.where(left, 1.0, 0.1)
+        return np.stack([rho, np.zeros_like(rho), p / (g - 1.0)], axis=-1)
+
+    return ic, None
+
+
+def blast_2d(system, r0=0.1, e0=1.0, p_ambient=1e-14):
+    """problems.py:113-132."""
+    if system.name != "euler" or system.dim != 2:
+        raise ValueError("the blast case needs 2-D Euler")
+    g = system.gamma
+    p_in = (g - 1.0) * e0 / (np.pi * r0 * r0)
+
+    def ic(points):
+        inside = points[..., 0] ** 2 + points[..., 1] ** 2 <= r0 * r0
+        p = np.where(inside, p_in, p_ambient)
+        zero = np.zeros_like(p)
+        return np.stack([np.ones_like(p), zero, zero, p / (g - 1.0)], axis=-1)
+
+    return ic, None
+
+
+def constant_state(system, values=None):
+    """problems.py:176-192 (Euler)."""
+    q0 = np.asarray([1.0] + [0.1] * system.dim + [2.5] if values is None else values, float)
+    if q0.shape != (system.n_vars,):
+        raise ValueError(f"constant state needs {system.n_vars} entries")
+
+    def exact(points, t):
+        return np.broadcast_to(q0, points.shape[:-1] + q0.shape).copy()
+
+    return (lambda points: exact(points, 0.0)), exact
+
+
+class ProblemSpec:
+    def __init__(self, builder, dim, extents, boundary, suggested_tend):
+        self.builder = builder
+        self.system = "euler"
+        self.dim = dim
+        self.extents = extents
+        self.boundary = boundary
+        self.suggested_tend = suggested_tend
+
+
+PROBLEMS = {
+    "vortex": ProblemSpec(isentropic_vortex, 2, ((0.0, 10.0), (0.0, 10.0)), "periodic", 10.0),
+    "sod": ProblemSpec(sod_shock_tube, 1, ((0.0, 1.0),), "outflow", 0.2),
+    "blast": ProblemSpec(blast_2d, 2, ((-1.0, 1.0), (-1.0, 1.0)), "wall", 0.05),
+    "constant": ProblemSpec(constant_state, None, None, "periodic", 1.0),
+    "density_wave": ProblemSpec(density_wave, None, None, "periodic", 1.0),
+    "explosion": ProblemSpec(circular_explosion, 2, ((-1.0, 1.0), (-1.0, 1.0)), "outflow",
+                             0.25),
+}
+
+
+def build_problem(name, system, **params):
+    try:
+        spec = PROBLEMS[name]
+    except KeyError:
+        raise ValueError(f"unknown problem '{name}' (choose from {sorted(PROBLEMS)})")
+    if system.name != spec.system:
+        raise ValueError(f"problem '{name}' needs the {spec.system} system, got {system.name}")
+    if spec.dim is not None and system.dim != spec.dim:
+        raise ValueError(f"problem '{name}' is {spec.dim}-D")
+    return spec.builder(system, **params)

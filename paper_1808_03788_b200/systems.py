@@ -1,0 +1,111 @@
+"""PDE plugin descriptors (reference contract: systems.py:16-74).
+
+On the B200 path the physics is a compile-time policy inside the CUDA
+kernels (csrc/adg_common.cuh: flux_all, max_abs_eig, admissible); these
+classes carry the plugin's identity and parameters (`name`, `dim`,
+`n_vars`, `gamma`, ...) across the C-ABI, exactly the attributes the
+reference's driver reads.  The elementwise methods are kept for API
+compatibility (user-side IC / diagnostics code calls them); they accept
+numpy arrays or torch tensors and are never on the time-step path.
+"""
+
+import numpy as np
+
+
+def _xp(a):
+    try:
+        import torch
+
+        if isinstance(a, torch.Tensor):
+            return torch
+    except ImportError:  # pragma: no cover
+        pass
+    return np
+
+
+class HyperbolicSystem:
+    name = "base"
+    has_flux = False
+    has_ncp = False
+    has_source = False
+    identity_primitives = True
+    diss_mask = None
+
+    def __init__(self, dim, n_vars, quantity_names):
+        self.dim = dim
+        self.n_vars = n_vars
+        self.quantity_names = tuple(quantity_names)
+
+
+class CompressibleEuler(HyperbolicSystem):
+    """Ideal-gas Euler, conserved (rho, rho v_1..d, rho E) (systems.py:112-234)."""
+
+    name = "euler"
+    has_flux = True
+
+    def __init__(self, dim, gamma=1.4):
+        if not 1 <= dim <= 3:
+            raise ValueError("dim must be 1, 2 or 3")
+        names = ("rho",) + tuple(f"mom_{'xyz'[j]}" for j in range(dim)) + ("energy",)
+        super().__init__(dim, dim + 2, names)
+        self.gamma = float(gamma)
+        self.identity_primitives = False
+
+    def pressure(self, q):
+        kin = q[..., 1] * q[..., 1]
+        for j in range(1, self.dim):
+            kin = kin + q[..., 1 + j] * q[..., 1 + j]
+        return (self.gamma - 1.0) * (q[..., -1] - 0.5 * kin / q[..., 0])
+
+    def sound_speed(self, q):
+        xp = _xp(q)
+        return xp.sqrt(self.gamma * self.pressure(q) / q[..., 0])
+
+    def flux(self, q):
+        xp = _xp(q)
+        d = self.dim
+        r = 1.0 / q[..., 0]
+        p = self.pressure(q)
+        ep = q[..., d + 1] + p
+        rows = []
+        for j in range(d):
+            vj = q[..., 1 + j] * r
+            comp = [q[..., 1 + j]] + [q[..., 1 + i] * vj + (p if i == j else 0.0)
+                                     for i in range(d)] + [ep * vj]
+            rows.append(xp.stack(comp, axis=-1) if xp is np else xp.stack(comp, dim=-1))
+        return np.stack(rows, axis=-2) if xp is np else xp.stack(rows, dim=-2)
+
+    def max_abs_eigenvalue(self, q, normal):
+        un = 0.0
+        for j in range(self.dim):
+            un = un + q[..., 1 + j] * float(normal[j])
+        return abs(un / q[..., 0]) + self.sound_speed(q)
+
+    def admissible(self, q):
+        xp = _xp(q)
+        if xp is np:
+            fin = np.all(np.isfinite(q), axis=-1)
+            with np.errstate(invalid="ignore", divide="ignore"):
+                return fin & (q[..., 0] > 0.0) & (self.pressure(q) > 0.0)
+        return xp.isfinite(q).all(dim=-1) & (q[..., 0] > 0.0) & (self.pressure(q) > 0.0)
+
+    def reflect(self, q, axis):
+        out = q.copy() if _xp(q) is np else q.clone()
+        out[..., 1 + axis] = -q[..., 1 + axis]
+        return out
+
+
+_SYSTEMS = {"euler": CompressibleEuler}
+
+
+def make_system(name, dim, **params):
+    """Registered systems (systems.py:355-361).  Only Euler has a B200 path;
+    'advection' / 'elasticity-di' raise NotImplementedError."""
+    if name in ("advection", "elasticity-di"):
+        raise NotImplementedError(f"system '{name}' has no B200 kernels (Euler only)")
+    try:
+        cls = _SYSTEMS[name]
+    except KeyError:
+        raise ValueError(f"unknown system '{name}' (choose from ['advection', "
+                         "'elasticity-di', 'euler'])")
+    return cls(dim, **params)

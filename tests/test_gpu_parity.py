@@ -1,0 +1,178 @@
+"""GPU parity of the B200 path against the reference's golden vectors and the
+CPU oracle (`oracle/`, the checker).  Bar (BASELINE.json north_star):
+fp64 relative L-inf <= 1e-10 and identical limiter flags.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def rel_linf(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1808_03788_b200 as p
+    from paper_1808_03788_b200 import _lib
+
+    _lib.load()  # must exist: no fallback
+    return p
+
+
+def _sim_from_golden(pkg, g, problem, bc="periodic", use_limiter=False, **kw):
+    mesh = pkg.CartesianMesh([tuple(e) for e in g["extents"]], [int(c) for c in g["cells"]])
+    system = pkg.make_system("euler", mesh.dim)
+    sim = pkg.Simulation(mesh, system, int(g["degree"]), float(g["cfl"]), boundary=bc,
+                         use_limiter=use_limiter, **kw)
+    ic, _ = pkg.build_problem(problem, system)
+    sim.project_initial_condition(ic)
+    return sim
+
+
+@pytest.mark.parametrize("fast", [True, False])
+def test_c1_vortex_full_config(pkg, golden, fast):
+    g = golden("c1_vortex")
+    sim = _sim_from_golden(pkg, g, "vortex")
+    assert rel_linf(sim.u, g["u0"]) <= 1e-14
+    if fast:
+        sim.run(np.inf, max_steps=10)
+    else:
+        sim.run(np.inf, max_steps=10, on_step=lambda s: None)
+    assert sim.step_count == 10
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-12)
+    assert sim.sweep_log == [int(x) for x in g["iters"]]
+    assert rel_linf(sim.u, g["u"]) <= TOL
+    np.testing.assert_allclose(np.array([h["totals"] for h in sim.history]), g["totals"],
+                               rtol=1e-11, atol=1e-13)
+
+
+@pytest.mark.parametrize("name", ["c2_wave_4", "c5_wave_ext"] +
+                         [f"c3_wave_N{n}" for n in range(2, 10)])
+def test_density_wave_cases(pkg, golden, name):
+    g = golden(name)
+    sim = _sim_from_golden(pkg, g, "density_wave")
+    assert rel_linf(sim.u, g["u0"]) <= 1e-14
+    n = len(g["dts"])
+    sim.run(np.inf, max_steps=n)
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-12)
+    assert rel_linf(sim.u, g["u"]) <= TOL
+    assert max(sim.sweep_log) <= max(int(x) for x in g["iters"])
+
+
+@pytest.mark.parametrize("key", ["d3_N1", "d3_N2", "d3_N3", "d3_N4", "d3_N5", "d2_N3",
+                                 "d2_N5"])
+def test_predictor_pieces(pkg, golden, key):
+    from paper_1808_03788_b200.predictor import run_predictor
+
+    g = golden("predictor")
+    d = int(key[1])
+    n = int(key.split("N")[1])
+    u = g[key + "_u"]
+    cells = u.shape[:d]
+    sp = tuple(1.0 / c for c in cells)
+    system = pkg.make_system("euler", d)
+    res, good = run_predictor(torch.as_tensor(u).cuda(), system, sp, float(g[key + "_dt"]),
+                              pkg.basis_tables(n), min_iter=int(g[key + "_iters"]))
+    ref_ok = g[key + "_converged"] & g[key + "_admissible"]
+    np.testing.assert_array_equal(good.cpu().numpy(), ref_ok)
+    assert rel_linf(res.q, g[key + "_q"]) <= 1e-12
+    assert rel_linf(res.volume, g[key + "_vol"]) <= 1e-11
+    for j in range(d):
+        for s in (0, 1):
+            assert rel_linf(res.traces[(j, s)], g[key + f"_tr{j}{s}"]) <= 1e-12
+
+
+def test_predictor_matches_oracle_per_element(pkg):
+    """Per-element Picard freezing (the kernel rule) against the oracle's
+    per-element mode on seeded states, 3-D N=4."""
+    from oracle import dg
+    from oracle.basis import oracle_tables
+    from oracle.euler import EulerOracle
+    from paper_1808_03788_b200.predictor import run_predictor
+
+    rng = np.random.default_rng(0)
+    n, cells = 4, (3, 2, 2)
+    P = n + 1
+    x = rng.uniform(0, 1, cells + (P,) * 3)
+    u = np.empty(cells + (P,) * 3 + (5,))
+    rho = 1.0 + 0.3 * np.sin(2 * np.pi * x)
+    u[..., 0] = rho
+    u[..., 1] = rho * 0.7
+    u[..., 2] = rho * -0.4
+    u[..., 3] = rho * 0.2
+    u[..., 4] = 2.5 + 0.5 * rho * (0.49 + 0.16 + 0.04)
+    sp = (0.1, 0.2, 0.15)
+    dt = 2e-3
+    ref = dg.picard_solve(u, EulerOracle(3), sp, dt, oracle_tables(n), per_element=True)
+    res, good = run_predictor(torch.as_tensor(u).cuda(), pkg.make_system("euler", 3), sp, dt,
+                              pkg.basis_tables(n))
+    assert rel_linf(res.q, ref.q) <= 1e-12
+    np.testing.assert_array_equal(res.sweeps.cpu().numpy(), ref.sweeps)
+    np.testing.assert_array_equal(good.cpu().numpy(), ref.converged & ref.admissible)
+
+
+def test_density_wave_8cubed_vs_oracle(pkg):
+    """C2 shape at 8^3 (oracle-feasible), 2 steps, against the CPU oracle."""
+    from oracle import problems as oprob
+    from oracle.euler import EulerOracle
+    from oracle.sim import OracleMesh, OracleSimulation
+
+    cells = (8, 8, 8)
+    ext = [(0.0, 1.0)] * 3
+    cfl = 0.9 / 27.0
+    osim = OracleSimulation(OracleMesh(ext, cells), EulerOracle(3), 4, cfl,
+                            per_element_picard=True)
+    osim.project_initial_condition(oprob.density_wave()[0])
+    osim.run(np.inf, max_steps=2)
+    mesh = pkg.CartesianMesh(ext, cells)
+    system = pkg.make_system("euler", 3)
+    sim = pkg.Simulation(mesh, system, 4, cfl)
+    sim.project_initial_condition(pkg.build_problem("density_wave", system)[0])
+    sim.run(np.inf, max_steps=2)
+    assert rel_linf(sim.u, osim.u) <= TOL
+    np.testing.assert_allclose([h["dt"] for h in sim.history],
+                               [h["dt"] for h in osim.history], rtol=1e-13)
+
+
+def test_free_stream_and_determinism(pkg):
+    """Constant state is preserved (test_mesh_driver.py:320-330) and two runs
+    are bitwise identical (test_mesh_driver.py:239-251)."""
+    mesh = pkg.CartesianMesh([(0, 1)] * 3, (6, 5, 4))
+    system = pkg.make_system("euler", 3)
+    outs = []
+    for _ in range(2):
+        sim = pkg.Simulation(mesh, system, 3, 0.9 / 21.0)
+        ic, _ = pkg.build_problem("constant", system)
+        u0 = sim.project_initial_condition(ic).clone()
+        sim.run(np.inf, max_steps=5)
+        assert rel_linf(sim.u, u0.cpu().numpy()) <= 1e-12
+        outs.append(sim.u.clone())
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_conservation_full_size_c2(pkg):
+    """C2 at its full 64^3 N=4 size, 3 steps: periodic totals are conserved to
+    1e-11 relative (test_acceptance.py:116-135) and the solution stays within
+    the exact translation's neighbourhood."""
+    mesh = pkg.CartesianMesh([(0, 1)] * 3, (64, 64, 64))
+    system = pkg.make_system("euler", 3)
+    sim = pkg.Simulation(mesh, system, 4, 0.9 / 27.0)
+    ic, exact = pkg.build_problem("density_wave", system)
+    sim.project_initial_condition(ic)
+    t0 = sim.conserved_totals()
+    sim.run(np.inf, max_steps=3)
+    t1 = sim.history[-1]["totals"]
+    assert np.max(np.abs(t1 - t0) / np.maximum(np.abs(t0), 1e-300)) <= 1e-11
+    err = sim.error_norms(exact)
+    assert err["linf"].max() < 1e-6
+    assert max(sim.sweep_log) <= 3
