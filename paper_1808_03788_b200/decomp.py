@@ -1,0 +1,139 @@
+"""Slab domain decomposition across GPUs.
+
+One process per GPU (torch.distributed, NCCL).  The global Cartesian grid is
+split along x into equal slabs; rank r owns cells [r*n0/W, (r+1)*n0/W) of
+axis 0.  Per step the only exchanges are
+
+  * face-trace halos: after the predictor, each rank sends the low-x trace
+    plane of its first element layer to rank r-1 and the high-x plane of
+    its last layer to rank r+1 (the reference's ghost/periodic face states,
+    driver.py:234-248, across the slab cut); received planes become the
+    ADG_BC_GHOST exterior traces of adg_face_flux;
+  * the CFL reduction: a MAX all-reduce of the per-axis wave-speed bits and
+    a SUM of the admissible / non-finite counts (corrector.py:47-55 taken
+    over the global grid -- exactly the reference's dt, not a min of
+    per-rank dts);
+  * conserved totals: a SUM all-reduce of the per-step totals rows, once per
+    batch of steps.
+
+No collective touches the element data itself.  The exchange helpers work
+on any torch.distributed backend, so the CPU test suite covers them with
+gloo at world_size 2.
+"""
+
+import torch
+import torch.distributed as dist
+
+from .driver import Simulation
+from .mesh import CartesianMesh
+
+
+def slab_bounds(n0, world, rank):
+    if n0 % world:
+        raise ValueError(f"{n0} cells along x do not split evenly over {world} ranks")
+    k = n0 // world
+    return rank * k, (rank + 1) * k
+
+
+def local_mesh(global_mesh, world, rank):
+    lo, hi = slab_bounds(global_mesh.cells[0], world, rank)
+    x0, x1 = global_mesh.extents[0]
+    dx = (x1 - x0) / global_mesh.cells[0]
+    ext = [(x0 + lo * dx, x0 + hi * dx)] + list(global_mesh.extents[1:])
+    return CartesianMesh(ext, (hi - lo,) + tuple(global_mesh.cells[1:]))
+
+
+def exchange_planes(send_lo, send_hi, recv_lo, recv_hi, group=None):
+    """Periodic ring halo swap along x.
+
+    send_lo -> rank-1 (it becomes that rank's high ghost), send_hi -> rank+1
+    (its low ghost); recv_lo <- rank-1's send_hi, recv_hi <- rank+1's send_lo.
+    All four are contiguous tensors on this rank's device.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    left = (rank - 1) % world
+    right = (rank + 1) % world
+    if world == 1:
+        recv_lo.copy_(send_hi)
+        recv_hi.copy_(send_lo)
+        return
+    g = lambda r: dist.get_global_rank(group, r) if group is not None else r  # noqa: E731
+    ops = [dist.P2POp(dist.isend, send_lo, g(left), group),
+           dist.P2POp(dist.irecv, recv_hi, g(right), group),
+           dist.P2POp(dist.isend, send_hi, g(right), group),
+           dist.P2POp(dist.irecv, recv_lo, g(left), group)]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
+def combine_reduce(red, group=None):
+    """adg_reduce record: MAX of lam bit patterns (non-negative doubles order
+    like integers), SUM of the admissible / non-finite counts."""
+    dist.all_reduce(red[0:3], op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(red[3:5], op=dist.ReduceOp.SUM, group=group)
+
+
+class SlabSimulation(Simulation):
+    """Simulation of one x-slab of `global_mesh` on this rank's GPU.
+
+    Only periodic x boundaries are supported across the cut (the C5 setup);
+    y / z keep the requested boundary kinds.
+    """
+
+    def __init__(self, global_mesh, system, degree, cfl, boundary="periodic", group=None,
+                 **kw):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.global_mesh = global_mesh
+        mesh = local_mesh(global_mesh, self.world, self.rank)
+        ghost = {}
+        if self.world > 1:
+            if boundary != "periodic":
+                raise NotImplementedError("slab decomposition needs periodic x faces")
+            P = degree + 1
+            plane = 1
+            for c in mesh.cells[1:]:
+                plane *= c
+            n = plane * P ** mesh.dim * system.n_vars
+            dev = kw.get("device")
+            dev = torch.device("cuda", torch.cuda.current_device() if dev is None else int(dev))
+            ghost = {(0, 0): torch.empty(n, dtype=torch.float64, device=dev),
+                     (0, 1): torch.empty(n, dtype=torch.float64, device=dev)}
+        super().__init__(mesh, system, degree, cfl, boundary=boundary, _ghost=ghost, **kw)
+        if self.world > 1:
+            self._exchange = SlabSimulation._swap_halos
+
+    def _swap_halos(self):
+        buf = self._buf
+        n = self._ghost[(0, 0)].numel()
+        face = self.mesh.n_elements * self._pd * self._m
+        lo_plane = buf.traces[0:n]                       # axis 0, side 0, first layer
+        hi_plane = buf.traces[2 * face - n:2 * face]     # axis 0, side 1, last layer
+        exchange_planes(lo_plane, hi_plane, self._ghost[(0, 0)], self._ghost[(0, 1)],
+                        self.group)
+
+    def _timestep_into(self, dt_dst, status_dst, t_end):
+        if self._red_cur is None:
+            self._wavespeed()
+        if self.world > 1:
+            combine_reduce(self._buf.red[self._red_cur], self.group)
+        super()._timestep_into(dt_dst, status_dst, t_end)
+
+    def _combine_rows(self, rows):
+        if self.world > 1:
+            dist.all_reduce(rows[:, 2:], op=dist.ReduceOp.SUM, group=self.group)
+
+    def _state_finite(self):
+        if self.world > 1:
+            red = self._buf.red[self._red_cur].clone()
+            dist.all_reduce(red[4:5], op=dist.ReduceOp.SUM, group=self.group)
+            return int(red[4].item()) == 0
+        return super()._state_finite()
+
+    def conserved_totals(self):
+        tot = torch.as_tensor(super().conserved_totals(), device=self.device)
+        if self.world > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=self.group)
+        return tot.cpu().numpy()

@@ -223,12 +223,15 @@ class Simulation:
 
     def set_state(self, u):
         """driver.py:156-157; accepts numpy arrays or tensors of the state shape."""
-        t = torch.as_tensor(np.asarray(u, dtype=float) if not isinstance(u, torch.Tensor) else u)
-        t = t.to(device=self.device, dtype=torch.float64).contiguous()
-        if tuple(t.shape) != self._shape:
-            raise ValueError(f"state shape {tuple(t.shape)} != {self._shape}")
+        if not isinstance(u, torch.Tensor):
+            u = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64))
+        if tuple(u.shape) != self._shape:
+            raise ValueError(f"state shape {tuple(u.shape)} != {self._shape}")
         self._ensure_buffers()
-        self._u = t.clone()
+        if self._u is None:
+            self._u = torch.empty(self._shape, dtype=torch.float64, device=self.device)
+        # pinned host tensors are copied asynchronously on the current stream
+        self._u.copy_(u, non_blocking=u.device.type == "cpu" and u.is_pinned())
         self._red_cur = None
 
     @property
@@ -324,6 +327,7 @@ class Simulation:
                 self.step_count += 1
                 self.last_limited_fraction = fraction
                 self.last_troubled = troubled
+                self._combine_rows(row[None])
                 host = row.cpu().numpy()
                 self._record(trial, host[2:2 + m])
                 return trial
@@ -368,6 +372,9 @@ class Simulation:
                 on_step(self)
         return self.step_count
 
+    def _combine_rows(self, rows):
+        """Hook: cross-rank SUM of per-step totals (decomp.SlabSimulation)."""
+
     def _state_finite(self):
         red = self._buf.red[self._red_cur]
         return int(red[4].item()) == 0
@@ -386,6 +393,7 @@ class Simulation:
             self._timestep_into(rows[s, 0:1], status[s:s + 1], math.inf)
             self._enqueue_unlimited(rows[s, 0:1], rows[s, 2:], rows[s, 1:2])
             torch.amax(buf.sweeps, dim=0, keepdim=True, out=sweeps[s:s + 1])
+        self._combine_rows(rows)
         host = rows.cpu().numpy()
         st = status.cpu().numpy()
         sw = sweeps.cpu().numpy()
