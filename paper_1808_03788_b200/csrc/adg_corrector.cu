@@ -183,11 +183,12 @@ __global__ void advance_time_kernel(double* t, const double* dt, double* t_out) 
 // -------------------------------------------------------------------------
 // Face coupling.  Thread per (face, tangential node); loops over the P time
 // nodes and integrates sum_t w_t d_low(t) (corrector.py:186).
-template <int D, int P>
+template <int D, int P, int AX>
 __global__ void __launch_bounds__(256)
 face_kernel(const double* __restrict__ traces, const double* __restrict__ ghost_lo,
-            const double* __restrict__ ghost_hi, double* __restrict__ dbar, int axis,
+            const double* __restrict__ ghost_hi, double* __restrict__ dbar,
             int64_t c0, int64_t c1, int64_t c2, int bc_lo, int bc_hi, double gamma) {
+  constexpr int axis = AX;  // compile-time: keeps the state arrays in registers
   constexpr int M = D + 2;
   constexpr int PD = ipow(P, D);
   constexpr int PF = PD / P;  // tangential nodes per face
@@ -475,8 +476,11 @@ static void launch_face(const adg_grid* g, int axis, const double* traces, const
   for (int j = 0; j < D; ++j) faces *= nf[j];
   const int64_t work = faces * (ipow(P, D) / P);
   const int64_t blocks = std::min<int64_t>((work + 255) / 256, 1 << 20);
-  face_kernel<D, P><<<(unsigned)blocks, 256, 0, st>>>(
-      traces, glo, ghi, dbar, axis, g->cells[0], D >= 2 ? g->cells[1] : 1,
+  auto kern = axis == 0 ? face_kernel<D, P, 0>
+                        : (axis == 1 ? face_kernel<D, P, (D > 1 ? 1 : 0)>
+                                     : face_kernel<D, P, (D > 2 ? 2 : 0)>);
+  kern<<<(unsigned)blocks, 256, 0, st>>>(
+      traces, glo, ghi, dbar, g->cells[0], D >= 2 ? g->cells[1] : 1,
       D == 3 ? g->cells[2] : 1, g->bc[axis][0], g->bc[axis][1], g->gamma);
 }
 

@@ -34,11 +34,18 @@ struct PredCfg {
   static constexpr int PD = ipow(P, D);      // spatial nodes
   static constexpr int PT = PD * P;          // space-time nodes
   static constexpr int TILE = PT * M;        // doubles in one space-time tile
-  static constexpr int NF = (D == 3) ? 2 : 1;
-  static constexpr int FREG_A = NF * TILE;
+  // flux planes exchanged between line threads: F_y (D>=2) and F_z (D=3),
+  // stored with the contraction index fastest and padded to an even count
+  // so a thread reads two nodes per 128-bit shared load
+  static constexpr int NF = (D == 3) ? 2 : (D == 2 ? 1 : 0);
+  static constexpr int PL = P + (P & 1);
+  static constexpr int PLANE = PD * M * PL;  // doubles per exchanged flux buffer
+  static constexpr int FREG_A = NF * PLANE;
   static constexpr int FREG_B = D * PD * M;
-  static constexpr int FREG = FREG_A > FREG_B ? FREG_A : FREG_B;
-  static constexpr int ELEM = TILE + FREG;   // doubles per element slab
+  static constexpr int FREG_AB = FREG_A > FREG_B ? FREG_A : FREG_B;
+  static constexpr int FREG = FREG_AB > TILE ? FREG_AB : TILE;  // also holds the rate
+  static constexpr int TILE_PAD = TILE + (TILE & 1);   // keeps F 16-byte aligned
+  static constexpr int ELEM = TILE_PAD + FREG + (FREG & 1);   // doubles per element slab
   static constexpr int BUDGET = 110 * 1024;  // bytes of tiles per CTA (>= 2 CTAs/SM)
   static constexpr int EPB_T = (256 / PD) > 0 ? (256 / PD) : 1;
   static constexpr int EPB_S = (BUDGET / (ELEM * 8)) > 0 ? (BUDGET / (ELEM * 8)) : 1;
@@ -46,7 +53,7 @@ struct PredCfg {
   static constexpr int NT = ((EPB * PD + 31) / 32) * 32;
   static constexpr int NW = NT / 32;
   // small shared data: scaled D (3 P^2), reduction partials (2 NT), flags
-  static constexpr int SMALL_DBL = 3 * P * P + 2 * NT;
+  static constexpr int SMALL_DBL = ((3 * P * P + 2 * NT + 1) / 2) * 2;
   static constexpr int FLAGS = 5 * EPB + 1;
   static constexpr size_t SMALL_BYTES = SMALL_DBL * 8 + ((FLAGS * 4 + 15) / 16) * 16;
   static constexpr size_t TILE_BYTES = (size_t)EPB * ELEM * 8;
@@ -83,6 +90,19 @@ __device__ __forceinline__ int node3(int i, int j, int k) {
   if (D == 3) return (i * P + j) * P + k;
   if (D == 2) return i * P + j;
   return i;
+}
+
+// exchanged flux planes: F_y plane (i, k, t) and F_z plane (i, j, t), each
+// holding v-rows of PL contiguous values along the contraction axis
+template <int D, int P>
+__device__ __forceinline__ int fy_idx(int i, int k, int t, int v) {
+  constexpr int M = D + 2, PL = P + (P & 1);
+  return D == 3 ? (((i * P + k) * P + t) * M + v) * PL : ((i * P + t) * M + v) * PL;
+}
+template <int P>
+__device__ __forceinline__ int fz_idx(int i, int j, int t, int v) {
+  constexpr int M = 5, PL = P + (P & 1);
+  return (((i * P + j) * P + t) * M + v) * PL;
 }
 
 // L(w) = -sum_j (D/dx_j) F_j(w) at one node from published per-node fluxes
@@ -146,25 +166,27 @@ predict_kernel(PredArgs a) {
 
   for (int x = tid; x < D * P * P; x += NT) {
     const int dir = x / (P * P);
-    Ds[x] = T.diff[x - dir * P * P] / a.dx[dir];
+    const double h = dir == 0 ? a.dx[0] : (dir == 1 ? a.dx[1] : a.dx[2]);
+    Ds[x] = T.diff[x - dir * P * P] / h;
   }
 
   // node-role coordinates
   const int ni = (D == 3) ? item / (P * P) : (D == 2 ? item / P : item);
   const int nj = (D == 3) ? (item / P) % P : (D == 2 ? item % P : 0);
   const int nk = (D == 3) ? item % P : 0;
-  // line-role coordinates: x-line (la, lb) at time lt
-  const int lt = item % P;
-  const int lrest = item / P;
-  const int la = (D == 3) ? lrest / P : (D == 2 ? lrest : 0);
-  const int lb = (D == 3) ? lrest % P : 0;
+  // line-role coordinates: x-line (la, lb) at time lt, la fastest so that
+  // the P lanes reading one F_y plane (same lb, lt) sit in one warp and the
+  // shared loads broadcast
+  const int la = (D >= 2) ? item % P : 0;
+  const int lb = (D == 3) ? (item / P) % P : 0;
+  const int lt = (D == 3) ? item / (P * P) : (D == 2 ? item / P : item);
 
   const int64_t ngroups = (a.n_elem + EPB - 1) / EPB;
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     const int64_t e = g * EPB + el;
     const bool valid = lane_ok && e < a.n_elem;
     double* Q = tiles + (lane_ok ? el : 0) * C::ELEM;
-    double* F = Q + TILE;
+    double* F = Q + C::TILE_PAD;
     __syncthreads();  // Ds ready / previous group finished with the tiles
     if (tid < EPB) {
       const bool ve = g * EPB + tid < a.n_elem;
@@ -234,31 +256,34 @@ predict_kernel(PredArgs a) {
       double rate[P][M];
       // phase 1: line role, x contraction in registers, publish F_y/F_z
       if (work) {
+        double ql[P][M];
+#pragma unroll
+        for (int l = 0; l < P; ++l)
+#pragma unroll
+          for (int v = 0; v < M; ++v) ql[l][v] = Q[qi<P, M>(node3<D, P>(l, la, lb), lt, v)];
 #pragma unroll
         for (int i = 0; i < P; ++i)
 #pragma unroll
           for (int v = 0; v < M; ++v) rate[i][v] = 0.0;
 #pragma unroll
         for (int l = 0; l < P; ++l) {
-          const int nd = node3<D, P>(l, la, lb);
-          double q[M];
-#pragma unroll
-          for (int v = 0; v < M; ++v) q[v] = Q[qi<P, M>(nd, lt, v)];
           double f[D][M];
-          flux_all<D>(q, gm1, f);
+          flux_all<D>(ql[l], gm1, f);
 #pragma unroll
           for (int i = 0; i < P; ++i) {
             const double dil = Ds[i * P + l];
 #pragma unroll
             for (int v = 0; v < M; ++v) rate[i][v] = fma(dil, f[0][v], rate[i][v]);
           }
+          // F_y at node (l, la, lb, lt) -> plane (i=l, k=lb, t=lt), slot j=la
           if (D >= 2) {
 #pragma unroll
-            for (int v = 0; v < M; ++v) F[qi<P, M>(nd, lt, v)] = f[1][v];
+            for (int v = 0; v < M; ++v) F[fy_idx<D, P>(l, lb, lt, v) + la] = f[1][v];
           }
+          // F_z -> plane (i=l, j=la, t=lt), slot k=lb
           if (D == 3) {
 #pragma unroll
-            for (int v = 0; v < M; ++v) F[TILE + qi<P, M>(nd, lt, v)] = f[2][v];
+            for (int v = 0; v < M; ++v) F[C::PLANE + fz_idx<P>(l, la, lt, v) + lb] = f[2][v];
           }
         }
 #pragma unroll
@@ -268,32 +293,43 @@ predict_kernel(PredArgs a) {
       }
       if (D >= 2) {
         __syncthreads();
-        // phase 2: y (and z) derivatives of the owned line from the planes
+        // phase 2: y (and z) derivatives of the owned line; the P lanes of a
+        // warp that share a plane read it by broadcast, two nodes per load
         if (work) {
-          double dr[P];
+          double dr[C::PL];
 #pragma unroll
-          for (int l = 0; l < P; ++l) dr[l] = Ds[P * P + la * P + l];
+          for (int l = 0; l < C::PL; ++l) dr[l] = l < P ? Ds[P * P + la * P + l] : 0.0;
 #pragma unroll
           for (int i = 0; i < P; ++i)
 #pragma unroll
             for (int v = 0; v < M; ++v) {
+              const double2* row =
+                  reinterpret_cast<const double2*>(F + fy_idx<D, P>(i, lb, lt, v));
               double s = 0.0;
 #pragma unroll
-              for (int l = 0; l < P; ++l)
-                s = fma(dr[l], F[qi<P, M>(node3<D, P>(i, l, lb), lt, v)], s);
+              for (int l2 = 0; l2 < C::PL / 2; ++l2) {
+                const double2 fv = row[l2];
+                s = fma(dr[2 * l2], fv.x, s);
+                if (2 * l2 + 1 < P) s = fma(dr[2 * l2 + 1], fv.y, s);
+              }
               rate[i][v] -= s;
             }
           if (D == 3) {
 #pragma unroll
-            for (int l = 0; l < P; ++l) dr[l] = Ds[2 * P * P + lb * P + l];
+            for (int l = 0; l < C::PL; ++l) dr[l] = l < P ? Ds[2 * P * P + lb * P + l] : 0.0;
 #pragma unroll
             for (int i = 0; i < P; ++i)
 #pragma unroll
               for (int v = 0; v < M; ++v) {
+                const double2* row =
+                    reinterpret_cast<const double2*>(F + C::PLANE + fz_idx<P>(i, la, lt, v));
                 double s = 0.0;
 #pragma unroll
-                for (int l = 0; l < P; ++l)
-                  s = fma(dr[l], F[TILE + qi<P, M>(node3<D, P>(i, la, l), lt, v)], s);
+                for (int l2 = 0; l2 < C::PL / 2; ++l2) {
+                  const double2 fv = row[l2];
+                  s = fma(dr[2 * l2], fv.x, s);
+                  if (2 * l2 + 1 < P) s = fma(dr[2 * l2 + 1], fv.y, s);
+                }
                 rate[i][v] -= s;
               }
           }

@@ -1,0 +1,169 @@
+"""CPU-side tests of the product host layer: C-ABI surface, tables, mesh,
+initial conditions, validation and the work model.  No GPU needed."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "aderdg_b200.h")
+
+
+def header_functions():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(adg_\w+)\(", txt, re.M)))
+
+
+def test_header_and_binding_agree():
+    from paper_1808_03788_b200 import _lib
+
+    assert header_functions() == sorted(_lib.EXPORTS)
+    assert set(_lib._SIGS) == set(_lib.EXPORTS)
+
+
+def test_library_loads_and_exports_every_symbol():
+    from paper_1808_03788_b200 import _lib
+
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libaderdg_b200.so not built (run __graft_entry__.build())")
+    lib = _lib.load()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    assert lib.adg_version() == 1
+    # ABI structs: the C compiler's layout equals the ctypes layout
+    src = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "aderdg_b200.h"
+int main(void){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(adg_grid), offsetof(adg_grid,cells),
+ offsetof(adg_grid,dx), offsetof(adg_grid,gamma), offsetof(adg_grid,bc), sizeof(adg_reduce));
+ return 0;}'''
+    exe = os.path.join(ROOT, "build", "abi_probe")
+    os.makedirs(os.path.dirname(exe), exist_ok=True)
+    c = exe + ".c"
+    with open(c, "w") as f:
+        f.write(src)
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+    got = [int(x) for x in subprocess.check_output([exe]).split()]
+    G = _lib.Grid
+    assert got == [ctypes.sizeof(G), G.cells.offset, G.dx.offset, G.gamma.offset, G.bc.offset,
+                   ctypes.sizeof(_lib.Reduce)]
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    from paper_1808_03788_b200 import _lib
+
+    saved = _lib._lib
+    try:
+        _lib._lib = None
+        with pytest.raises(_lib.LibraryMissing):
+            _lib.load(str(tmp_path / "nope.so"))
+    finally:
+        _lib._lib = saved
+
+
+@pytest.mark.parametrize("n", range(10))
+def test_product_tables_match_reference(golden, n):
+    from paper_1808_03788_b200.basis import basis_tables
+
+    g = golden("tables")
+    t = basis_tables(n)
+    for key, val in (("nodes", t.nodes), ("weights", t.weights), ("diff", t.diff),
+                     ("left", t.left_vals), ("right", t.right_vals),
+                     ("sub_project", t.sub_project), ("sub_recover", t.sub_recover),
+                     ("k1", t.k1), ("gw", t.gw), ("g0", t.g0), ("k1_opnorm", t.k1_opnorm)):
+        ref = g[f"N{n}_{key}"]
+        assert np.max(np.abs(np.asarray(val) - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))), key
+    blob = t.device_blob()
+    P, S = n + 1, 2 * n + 1
+    assert blob.size == 5 * P + 2 * P * P + 1 + 2 * S * P
+
+
+def test_mesh_matches_oracle():
+    from oracle.basis import oracle_tables
+    from oracle.sim import OracleMesh
+    from paper_1808_03788_b200 import CartesianMesh, basis_tables
+
+    ext, cells = [(-1.0, 2.0), (0.0, 1.0), (3.0, 4.5)], (3, 4, 2)
+    a = CartesianMesh(ext, cells)
+    b = OracleMesh(ext, cells)
+    np.testing.assert_allclose(a.node_coords(basis_tables(3)), b.node_coords(oracle_tables(3)),
+                               atol=1e-15)
+    for ax in range(3):
+        for s in (0, 1):
+            np.testing.assert_allclose(a.face_node_coords(basis_tables(2), ax, s),
+                                       b.face_node_coords(oracle_tables(2), ax, s), atol=1e-15)
+    with pytest.raises(ValueError):
+        CartesianMesh([(0, 1)], (0,))
+    with pytest.raises(ValueError):
+        CartesianMesh([(1, 0)], (3,))
+
+
+@pytest.mark.parametrize("case,problem", [("c1_vortex", "vortex"),
+                                          ("c2_wave_4", "density_wave"),
+                                          ("c4_explosion_16", "explosion")])
+def test_initial_conditions_match_golden(golden, case, problem):
+    from paper_1808_03788_b200 import CartesianMesh, basis_tables, build_problem, make_system
+
+    g = golden(case)
+    mesh = CartesianMesh([tuple(e) for e in g["extents"]], [int(c) for c in g["cells"]])
+    system = make_system("euler", mesh.dim)
+    ic, _ = build_problem(problem, system)
+    u = ic(mesh.node_coords(basis_tables(int(g["degree"]))))
+    if problem == "explosion":
+        # the golden u0 is after IC flattening (device side); compare cells kept intact
+        keep = np.all(np.isclose(u, g["u0"], rtol=0, atol=1e-14), axis=(2, 3, 4))
+        assert keep.mean() > 0.8
+    else:
+        np.testing.assert_allclose(u, g["u0"], rtol=0, atol=1e-14)
+
+
+def test_boundary_normalisation_and_validation():
+    from paper_1808_03788_b200.driver import normalize_boundary
+
+    assert normalize_boundary("outflow", 2) == {(0, 0): "outflow", (0, 1): "outflow",
+                                                (1, 0): "outflow", (1, 1): "outflow"}
+    t = normalize_boundary({0: ("wall", "outflow")}, 2)
+    assert t[(0, 0)] == "wall" and t[(0, 1)] == "outflow" and t[(1, 0)] == "periodic"
+    with pytest.raises(ValueError):
+        normalize_boundary({0: ("periodic", "wall")}, 1)
+    with pytest.raises(ValueError):
+        normalize_boundary("bogus", 1)
+    with pytest.raises(ValueError):
+        normalize_boundary(3, 1)
+
+
+def test_simulation_argument_errors_precede_device_use():
+    from paper_1808_03788_b200 import CartesianMesh, Simulation, make_system
+
+    mesh = CartesianMesh([(0, 1), (0, 1)], (4, 4))
+    e2 = make_system("euler", 2)
+    with pytest.raises(ValueError):
+        Simulation(mesh, e2, 3, 0.5)                 # cfl >= 1/(2N+1)
+    with pytest.raises(ValueError):
+        Simulation(mesh, make_system("euler", 3), 3, 0.05)
+    with pytest.raises(ValueError):
+        Simulation(mesh, e2, 3, 0.05, boundary="exact")
+    with pytest.raises(NotImplementedError):
+        Simulation(mesh, e2, 3, 0.05, predictor_mode="primitive")
+    with pytest.raises(NotImplementedError):
+        make_system("advection", 2)
+    import torch
+
+    if not torch.cuda.is_available():
+        with pytest.raises(RuntimeError, match="no CPU fallback"):
+            Simulation(mesh, e2, 3, 0.05)
+
+
+def test_work_model_matches_survey():
+    from paper_1808_03788_b200 import roofline
+
+    assert roofline.step_flops_per_dof(4, 3, 2) == 4782
+    assert roofline.step_bytes_per_dof(4, 3) == 560
+    assert roofline.step_flops_per_dof(3, 2, 4) == 3430
+    assert abs(roofline.roofline_dofs(4, 3, 2, 37e12, 6454.3e9) - 7.74e9) < 0.01e9
