@@ -150,21 +150,23 @@ int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partia
                double* totals_out, void* stream);
 
 /* -- a posteriori subcell limiter (limiter.py; driver.py:265-299) ------- */
-/* Subcell averages of u (limiter.project_to_subcells, limiter.py:27-33):
- * sub_out [E, S^d, m] */
+/* Subcell averages of u^n (limiter.project_to_subcells, limiter.py:27-33)
+ * sub_out [E, S^d, m] (S = 2N+1) and their per-cell extrema cmin/cmax
+ * [E, m] (the per-cell part of limiter.relaxed_bounds, limiter.py:62-63).
+ * Device limiter: dim 1-2 any degree, dim 3 degree <= 2. */
 int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, double* sub_out,
-                         void* stream);
-/* Troubled-cell detection (limiter.py:51-86 + driver.py:272-285):
- * prev_sub / cand_sub [E, S^d, m] subcell averages of u^n and the
- * candidate, cand the candidate nodal states, pred_bad from adg_predict,
- * halo_prev [per axis/side: cells with 1 along axis, S^d, m] subcell data of
- * neighbour ranks for ADG_BC_GHOST faces (NULL otherwise).  Writes
- * troubled[E] (uint8), the compacted list idx[E] (int32, ascending) and
- * *count (int32).  force_all != 0 marks every cell. */
-int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub,
-               const double* cand_sub, const double* cand, const uint8_t* pred_bad,
-               double delta0, double eps, int force_all, uint8_t* troubled, int32_t* idx,
-               int32_t* count, void* stream);
+                         double* cmin_out, double* cmax_out, void* stream);
+/* Troubled-cell detection (limiter.py:51-86 + driver.py:272-285): DMP
+ * bounds from the own and 2d face-neighbour cells of prev_sub (ghost cells
+ * through the face kinds, driver.py:301-340), relaxed by
+ * max(delta0, eps (hi - lo)); a cell is troubled if a candidate subcell
+ * average leaves them, a candidate nodal or subcell state is inadmissible,
+ * pred_bad is set, or force_all != 0.  Writes troubled[E] (uint8), the
+ * compacted list idx[*count] (int32, unordered) and *count (int32). */
+int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub, const double* cmin,
+               const double* cmax, const double* cand, const uint8_t* pred_bad, double delta0,
+               double eps, int force_all, uint8_t* troubled, int32_t* idx, int32_t* count,
+               void* stream);
 /* MUSCL-Hancock rescue of the listed cells from t^n subcell averages
  * (limiter.py:89-223 + driver.py:286-298), writing recovered nodal states
  * into u_out for listed cells (other cells untouched) and setting

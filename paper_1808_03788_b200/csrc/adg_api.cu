@@ -207,21 +207,22 @@ int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partia
 }
 
 int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, double* sub_out,
-                         void* stream) {
+                         double* cmin_out, double* cmax_out, void* stream) {
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
-  return wrap(h, adg::project_subcells(g, u, sub_out, (cudaStream_t)stream, &e), e);
+  return wrap(h, adg::project_subcells(g, u, sub_out, cmin_out, cmax_out, (cudaStream_t)stream,
+                                       &e), e);
 }
 
-int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub,
-               const double* cand_sub, const double* cand, const uint8_t* pred_bad,
-               double delta0, double eps, int force_all, uint8_t* troubled, int32_t* idx,
-               int32_t* count, void* stream) {
+int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub, const double* cmin,
+               const double* cmax, const double* cand, const uint8_t* pred_bad, double delta0,
+               double eps, int force_all, uint8_t* troubled, int32_t* idx, int32_t* count,
+               void* stream) {
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
-  return wrap(h, adg::detect(g, prev_sub, cand_sub, cand, pred_bad, delta0, eps, force_all,
+  return wrap(h, adg::detect(g, prev_sub, cmin, cmax, cand, pred_bad, delta0, eps, force_all,
                              troubled, idx, count, (cudaStream_t)stream, &e), e);
 }
 

@@ -37,9 +37,9 @@ int totals_finalize(const adg_grid* g, const double* partial, int64_t nblocks, d
                     cudaStream_t st, std::string* err);
 
 // limiter
-int project_subcells(const adg_grid* g, const double* u, double* sub, cudaStream_t st,
-                     std::string* err);
-int detect(const adg_grid* g, const double* prev_sub, const double* cand_sub,
+int project_subcells(const adg_grid* g, const double* u, double* sub, double* cmin,
+                     double* cmax, cudaStream_t st, std::string* err);
+int detect(const adg_grid* g, const double* prev_sub, const double* cmin, const double* cmax,
            const double* cand, const uint8_t* pred_bad, double delta0, double eps,
            int force_all, uint8_t* troubled, int32_t* idx, int32_t* count, cudaStream_t st,
            std::string* err);

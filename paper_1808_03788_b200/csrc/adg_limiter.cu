@@ -1,25 +1,882 @@
-// adg_limiter.cu -- a posteriori subcell limiter (placeholder until the
-// limiter kernels land).
+// adg_limiter.cu -- a posteriori subcell finite-volume limiter (sm_100a).
+//
+// References: driver._limit / _pad_subcells / _boundary_slab
+// (driver.py:265-340), limiter.project_to_subcells (limiter.py:27-33),
+// relaxed_bounds (:51-73), detect_troubled (:76-86), gather_windows
+// (:89-101), muscl_subcell_step/_muscl_once (:104-202), minmod (:45-48),
+// recover_from_subcells (:36-42), flatten_inadmissible (:205-223) and the
+// IC flattening of Simulation.project_initial_condition (driver.py:137-152).
+//
+// Device layout: prev_sub[E][S^d][m] subcell averages of u^n (S = 2N+1),
+// cmin/cmax[E][m] their per-cell extrema.  Ghost subcells outside the grid
+// are never materialised: a global subcell coordinate is mapped through the
+// face kind per axis (periodic wrap, outflow clamp, wall mirror + normal
+// momentum flip), which reproduces the reference's sequential per-axis
+// padding exactly, corners included.
+//
+// Troubled cells are compacted with an atomic counter; every rescue reads
+// only t^n data and writes only its own cell, so the result does not depend
+// on the compaction order.  One CTA rescues one cell (window, MUSCL-Hancock
+// half step, Rusanov subcell faces, first-order retry, recovery, flatten).
 #include "adg_common.cuh"
 #include "adg_internal.h"
 
 namespace adg {
-int project_subcells(const adg_grid*, const double*, double*, cudaStream_t, std::string* err) {
-  *err = "limiter not built";
-  return ADG_ERR_UNSUPPORTED;
+
+template <int D, int P>
+struct LimCfg {
+  static constexpr int M = D + 2;
+  static constexpr int S = 2 * P - 1;
+  static constexpr int PD = ipow(P, D);
+  static constexpr int SD = ipow(S, D);
+  static constexpr int W = S + 4;              // window edge
+  static constexpr int WD = ipow(W, D);
+  static constexpr int R = S + 2;              // 1-halo region edge
+  static constexpr int RD = ipow(R, D);
+  static constexpr int NT = 256;
+};
+
+struct LimGrid {
+  int64_t n[3];
+  int bc[3][2];
+  double gm1, gamma;
+  double h[3];  // subcell widths dx_j / S
+};
+
+// ---------------------------------------------------------------- helpers
+template <int D>
+__device__ __forceinline__ int64_t cell_index(const int64_t* c, const int64_t* n) {
+  int64_t e = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) e = e * n[j] + c[j];
+  return e;
 }
-int detect(const adg_grid*, const double*, const double*, const double*, const uint8_t*, double,
-           double, int, uint8_t*, int32_t*, int32_t*, cudaStream_t, std::string* err) {
-  *err = "limiter not built";
-  return ADG_ERR_UNSUPPORTED;
+
+// map a global subcell coordinate along axis j into the grid; returns false
+// for kinds without a device mapping (exact / ghost); *flip toggles for walls
+__device__ __forceinline__ bool map_axis(int64_t g, int64_t nS, int bc_lo, int bc_hi,
+                                         int64_t* out, bool* flip) {
+  if (g >= 0 && g < nS) {
+    *out = g;
+    return true;
+  }
+  const int kind = g < 0 ? bc_lo : bc_hi;
+  if (kind == ADG_BC_PERIODIC) {
+    int64_t r = g % nS;
+    *out = r < 0 ? r + nS : r;
+    return true;
+  }
+  if (kind == ADG_BC_OUTFLOW) {
+    *out = g < 0 ? 0 : nS - 1;
+    return true;
+  }
+  if (kind == ADG_BC_WALL) {
+    *out = g < 0 ? -1 - g : 2 * nS - 1 - g;
+    *flip = !*flip;
+    return true;
+  }
+  return false;
 }
-int rescue(const adg_grid*, const double*, const int32_t*, const int32_t*, int32_t,
-           const double*, double*, int32_t*, cudaStream_t, std::string* err) {
-  *err = "limiter not built";
-  return ADG_ERR_UNSUPPORTED;
+
+// prev_sub value set (m doubles) at global subcell coordinate gs[]
+template <int D, int P>
+__device__ __forceinline__ void fetch_sub(const double* __restrict__ sub, const LimGrid& G,
+                                          const int64_t* gs, double* out) {
+  using C = LimCfg<D, P>;
+  constexpr int S = C::S, M = C::M;
+  int64_t cc[3], loc[3];
+  bool flip[3] = {false, false, false};
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    int64_t g;
+    map_axis(gs[j], G.n[j] * S, G.bc[j][0], G.bc[j][1], &g, &flip[j]);
+    cc[j] = g / S;
+    loc[j] = g - cc[j] * S;
+  }
+  int64_t e = cell_index<D>(cc, G.n);
+  int s = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) s = s * S + (int)loc[j];
+  const double* p = sub + ((size_t)e * C::SD + s) * M;
+#pragma unroll
+  for (int v = 0; v < M; ++v) out[v] = p[v];
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+    if (flip[j]) out[1 + j] = -out[1 + j];
 }
-int flatten_ic(const adg_grid*, double*, int32_t*, cudaStream_t, std::string* err) {
-  *err = "limiter not built";
-  return ADG_ERR_UNSUPPORTED;
+
+// subcell averages of one cell's nodal data held in shared memory:
+// sequential per-axis contraction with P_sub (limiter.py:27-33)
+template <int D, int P>
+__device__ void project_cell(const double* __restrict__ nodal, double* __restrict__ tmp,
+                             double* __restrict__ out, int tid, int nt) {
+  using C = LimCfg<D, P>;
+  constexpr int S = C::S, M = C::M;
+  const DegreeTables& T = tab<P>();
+  if (D == 1) {
+    for (int x = tid; x < S * M; x += nt) {
+      const int s = x / M, v = x - s * M;
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc = fma(T.sub_project[s * P + i], nodal[i * M + v], acc);
+      out[x] = acc;
+    }
+    return;
+  }
+  if (D == 2) {
+    // axis 0: tmp[s0][i1][v]
+    for (int x = tid; x < S * P * M; x += nt) {
+      const int s0 = x / (P * M), r = x - s0 * P * M, i1 = r / M, v = r - i1 * M;
+      double acc = 0.0;
+#pragma unroll
+      for (int i0 = 0; i0 < P; ++i0)
+        acc = fma(T.sub_project[s0 * P + i0], nodal[(i0 * P + i1) * M + v], acc);
+      tmp[x] = acc;
+    }
+    __syncthreads();
+    for (int x = tid; x < S * S * M; x += nt) {
+      const int s0 = x / (S * M), r = x - s0 * S * M, s1 = r / M, v = r - s1 * M;
+      double acc = 0.0;
+#pragma unroll
+      for (int i1 = 0; i1 < P; ++i1)
+        acc = fma(T.sub_project[s1 * P + i1], tmp[(s0 * P + i1) * M + v], acc);
+      out[x] = acc;
+    }
+    return;
+  }
+  // D == 3: three passes through tmp (size S*S*P*M) using out as scratch
+  for (int x = tid; x < S * P * P * M; x += nt) {
+    const int s0 = x / (P * P * M), r = x - s0 * P * P * M;
+    double acc = 0.0;
+#pragma unroll
+    for (int i0 = 0; i0 < P; ++i0) acc = fma(T.sub_project[s0 * P + i0], nodal[i0 * P * P * M + r], acc);
+    out[x] = acc;
+  }
+  __syncthreads();
+  for (int x = tid; x < S * S * P * M; x += nt) {
+    const int s0 = x / (S * P * M), r = x - s0 * S * P * M, s1 = r / (P * M),
+              r2 = r - s1 * P * M;
+    double acc = 0.0;
+#pragma unroll
+    for (int i1 = 0; i1 < P; ++i1)
+      acc = fma(T.sub_project[s1 * P + i1], out[(s0 * P + i1) * P * M + r2], acc);
+    tmp[x] = acc;
+  }
+  __syncthreads();
+  for (int x = tid; x < S * S * S * M; x += nt) {
+    const int s01 = x / (S * M), r = x - s01 * S * M, s2 = r / M, v = r - s2 * M;
+    double acc = 0.0;
+#pragma unroll
+    for (int i2 = 0; i2 < P; ++i2)
+      acc = fma(T.sub_project[s2 * P + i2], tmp[(s01 * P + i2) * M + v], acc);
+    out[x] = acc;
+  }
 }
+
+template <int D, int P>
+__device__ __forceinline__ size_t proj_scratch() {
+  using C = LimCfg<D, P>;
+  return D == 3 ? (size_t)C::S * C::S * P * C::M : (size_t)C::S * P * C::M;
+}
+
+// -------------------------------------------------------------- kernels
+// prev_sub + per-cell extrema of u^n (one block per cell, grid stride)
+template <int D, int P>
+__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+subcell_prep_kernel(const double* __restrict__ u, int64_t E, double* __restrict__ sub,
+                    double* __restrict__ cmin, double* __restrict__ cmax) {
+  using C = LimCfg<D, P>;
+  constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
+  extern __shared__ __align__(16) double lsm[];
+  double* nodal = lsm;                      // PD*M
+  double* out = nodal + PD * M;             // max(SD*M, S*P*P*M)
+  double* tmp = out + SD * M;
+  __shared__ double rmin[NT], rmax[NT];
+  const int tid = threadIdx.x;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    for (int x = tid; x < PD * M; x += NT) nodal[x] = u[(size_t)e * PD * M + x];
+    __syncthreads();
+    project_cell<D, P>(nodal, tmp, out, tid, NT);
+    __syncthreads();
+    for (int x = tid; x < SD * M; x += NT) sub[(size_t)e * SD * M + x] = out[x];
+    for (int v = 0; v < M; ++v) {
+      double lo = __longlong_as_double(0x7ff0000000000000LL), hi = -lo;
+      for (int s = tid; s < SD; s += NT) {
+        lo = fmin(lo, out[s * M + v]);
+        hi = fmax(hi, out[s * M + v]);
+      }
+      rmin[tid] = lo;
+      rmax[tid] = hi;
+      __syncthreads();
+      for (int o = NT / 2; o > 0; o >>= 1) {
+        if (tid < o) {
+          rmin[tid] = fmin(rmin[tid], rmin[tid + o]);
+          rmax[tid] = fmax(rmax[tid], rmax[tid + o]);
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        cmin[e * M + v] = rmin[0];
+        cmax[e * M + v] = rmax[0];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// min/max over the ghost cell beyond face (axis j, side) of cell c: the
+// reference pads S subcell layers through the face kind (driver.py:317-340)
+template <int D, int P>
+__device__ void ghost_extrema(const double* __restrict__ sub, const double* __restrict__ cmin,
+                              const double* __restrict__ cmax, const LimGrid& G,
+                              const int64_t* c, int j, int side, double* lo, double* hi) {
+  using C = LimCfg<D, P>;
+  constexpr int S = C::S, M = C::M;
+  const int kind = G.bc[j][side];
+  int64_t cc[3] = {c[0], c[1], c[2]};
+  if (kind == ADG_BC_PERIODIC) {
+    cc[j] = side ? 0 : G.n[j] - 1;
+    const int64_t e = cell_index<D>(cc, G.n);
+#pragma unroll
+    for (int v = 0; v < M; ++v) {
+      lo[v] = cmin[e * M + v];
+      hi[v] = cmax[e * M + v];
+    }
+    return;
+  }
+  const int64_t e = cell_index<D>(cc, G.n);   // the edge cell itself
+  if (kind == ADG_BC_WALL) {
+#pragma unroll
+    for (int v = 0; v < M; ++v) {
+      lo[v] = cmin[e * M + v];
+      hi[v] = cmax[e * M + v];
+    }
+    const double a = lo[1 + j], b = hi[1 + j];
+    lo[1 + j] = -b;
+    hi[1 + j] = -a;
+    return;
+  }
+  // outflow: every ghost layer repeats the edge subcell layer
+#pragma unroll
+  for (int v = 0; v < M; ++v) {
+    lo[v] = __longlong_as_double(0x7ff0000000000000LL);
+    hi[v] = -lo[v];
+  }
+  const int edge = side ? S - 1 : 0;
+  for (int s = 0; s < C::SD; ++s) {
+    int rem = s, idx[3] = {0, 0, 0};
+    for (int a = D - 1; a >= 0; --a) {
+      idx[a] = rem % S;
+      rem /= S;
+    }
+    if (idx[j] != edge) continue;
+    const double* p = sub + ((size_t)e * C::SD + s) * M;
+#pragma unroll
+    for (int v = 0; v < M; ++v) {
+      lo[v] = fmin(lo[v], p[v]);
+      hi[v] = fmax(hi[v], p[v]);
+    }
+  }
+}
+
+// troubled-cell screen (limiter.py:51-86, driver.py:272-285)
+template <int D, int P>
+__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cmin,
+              const double* __restrict__ cmax, const double* __restrict__ cand,
+              const uint8_t* __restrict__ pred_bad, LimGrid G, int64_t E, double delta0,
+              double eps, int force_all, uint8_t* __restrict__ troubled, int32_t* idx,
+              int32_t* count) {
+  using C = LimCfg<D, P>;
+  constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
+  extern __shared__ __align__(16) double lsm[];
+  double* nodal = lsm;
+  double* out = nodal + PD * M;
+  double* tmp = out + SD * M;
+  __shared__ double s_lo[M], s_hi[M];
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    for (int x = tid; x < PD * M; x += NT) nodal[x] = cand[(size_t)e * PD * M + x];
+    if (tid == 0) {
+      s_bad = force_all || pred_bad[e];
+      int64_t c[3] = {0, 0, 0};
+      int64_t r = e;
+      for (int j = D - 1; j >= 0; --j) {
+        c[j] = r % G.n[j];
+        r /= G.n[j];
+      }
+      double lo[M], hi[M];
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        lo[v] = cmin[e * M + v];
+        hi[v] = cmax[e * M + v];
+      }
+      // own cell, then face neighbours in axis order, low then high
+      for (int j = 0; j < D; ++j) {
+        for (int side = 0; side < 2; ++side) {
+          double nlo[M], nhi[M];
+          const bool inside = side ? (c[j] + 1 < G.n[j]) : (c[j] > 0);
+          if (inside) {
+            int64_t cc[3] = {c[0], c[1], c[2]};
+            cc[j] += side ? 1 : -1;
+            const int64_t en = cell_index<D>(cc, G.n);
+#pragma unroll
+            for (int v = 0; v < M; ++v) {
+              nlo[v] = cmin[en * M + v];
+              nhi[v] = cmax[en * M + v];
+            }
+          } else {
+            ghost_extrema<D, P>(prev_sub, cmin, cmax, G, c, j, side, nlo, nhi);
+          }
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            lo[v] = fmin(lo[v], nlo[v]);
+            hi[v] = fmax(hi[v], nhi[v]);
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        const double delta = fmax(delta0, eps * (hi[v] - lo[v]));
+        s_lo[v] = lo[v] - delta;
+        s_hi[v] = hi[v] + delta;
+      }
+    }
+    __syncthreads();
+    project_cell<D, P>(nodal, tmp, out, tid, NT);
+    __syncthreads();
+    int bad = 0;
+    for (int s = tid; s < SD; s += NT) {
+      const double* q = out + s * M;
+#pragma unroll
+      for (int v = 0; v < M; ++v) bad |= (q[v] < s_lo[v]) | (q[v] > s_hi[v]);
+      bad |= !admissible<D>(q, G.gm1);
+    }
+    for (int nd = tid; nd < PD; nd += NT) bad |= !admissible<D>(nodal + nd * M, G.gm1);
+    if (bad) s_bad = 1;   // benign race: every writer stores 1
+    __syncthreads();
+    if (tid == 0) {
+      troubled[e] = (uint8_t)s_bad;
+      if (s_bad) idx[atomicAdd(count, 1)] = (int32_t)e;
+    }
+    __syncthreads();
+  }
+}
+
+// Rusanov one-sided terms (corrector.py:100-129) for a subcell face
+template <int D>
+__device__ __forceinline__ void rusanov_pair(const double* qm, const double* qp, int a,
+                                             double gamma, double gm1, double* dlow,
+                                             double* dhigh) {
+  constexpr int M = D + 2;
+  const double s = fmax(max_abs_eig<D>(qm, gamma, gm1, a), max_abs_eig<D>(qp, gamma, gm1, a));
+  double fm[M], fp[M];
+  flux_axis<D>(qm, gm1, a, fm);
+  flux_axis<D>(qp, gm1, a, fp);
+  const double hs = 0.5 * s;
+#pragma unroll
+  for (int v = 0; v < M; ++v) {
+    const double central = 0.5 * (fm[v] + fp[v]);
+    const double diss = hs * (qp[v] - qm[v]);
+    dlow[v] = (central + 0.0) - diss;
+    dhigh[v] = (-central + 0.0) + diss;
+  }
+}
+
+__device__ __forceinline__ double minmod(double a, double b) {
+  return (a * b > 0.0) ? (fabs(a) <= fabs(b) ? a : b) : 0.0;
+}
+
+// MUSCL-Hancock rescue of one troubled cell per block (limiter.py:104-223)
+template <int D, int P>
+__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ idx,
+              const int32_t* __restrict__ count, LimGrid G, const double* __restrict__ dt_dev,
+              double* __restrict__ u_out, int32_t* failed) {
+  using C = LimCfg<D, P>;
+  constexpr int M = C::M, S = C::S, SD = C::SD, PD = C::PD, W = C::W, WD = C::WD, R = C::R,
+                RD = C::RD, NT = C::NT;
+  const DegreeTables& T = tab<P>();
+  extern __shared__ __align__(16) double lsm[];
+  double* win = lsm;                    // [WD][M]
+  double* vh = win + WD * M;            // [RD][M]  half-step states
+  double* sl = vh + RD * M;             // [RD][D][M] limited slopes
+  double* nw = sl + RD * D * M;         // [SD][M]  new averages
+  double* tmp = nw + SD * M;            // recovery scratch
+  double* nod = tmp + (D == 3 ? S * S * P * M : S * P * M) + SD * M;  // [PD][M]
+  __shared__ int s_ok, s_flat;
+  const int tid = threadIdx.x;
+  const double dt = *dt_dev;
+  const int ncells = *count;
+  for (int b = blockIdx.x; b < ncells; b += gridDim.x) {
+    const int64_t e = idx[b];
+    int64_t c[3] = {0, 0, 0};
+    {
+      int64_t r = e;
+      for (int j = D - 1; j >= 0; --j) {
+        c[j] = r % G.n[j];
+        r /= G.n[j];
+      }
+    }
+    // window of t^n subcell averages with a 2-layer halo (limiter.py:89-101)
+    for (int w = tid; w < WD; w += NT) {
+      int rem = w;
+      int64_t gs[3] = {0, 0, 0};
+      for (int j = D - 1; j >= 0; --j) {
+        gs[j] = c[j] * S - 2 + rem % W;
+        rem /= W;
+      }
+      fetch_sub<D, P>(prev_sub, G, gs, win + w * M);
+    }
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {   // sloped, then first order
+      const bool flat = pass == 1;
+      if (tid == 0) s_ok = 1;
+      __syncthreads();
+      // slopes + half step on the 1-halo region
+      for (int r = tid; r < RD; r += NT) {
+        int ri[3] = {0, 0, 0}, rem = r;
+        for (int j = D - 1; j >= 0; --j) {
+          ri[j] = rem % R;
+          rem /= R;
+        }
+        auto wix = [&](int dj, int off) {
+          int x = 0;
+          for (int j = 0; j < D; ++j) x = x * W + ri[j] + 1 + (j == dj ? off : 0);
+          return x;
+        };
+        const double* cq = win + wix(0, 0) * M;
+        double slope[D][M];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double* up = win + wix(j, 1) * M;
+          const double* dn = win + wix(j, -1) * M;
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            if (flat) {
+              slope[j][v] = 0.0;
+            } else {
+              const double fwd = (up[v] - cq[v]) / G.h[j];
+              const double bwd = (cq[v] - dn[v]) / G.h[j];
+              slope[j][v] = minmod(fwd, bwd);
+            }
+          }
+        }
+        double rate[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) rate[v] = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double qh[M], ql[M], fh[M], fl[M];
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            const double off = 0.5 * G.h[j] * slope[j][v];
+            qh[v] = cq[v] + off;
+            ql[v] = cq[v] - off;
+          }
+          flux_axis<D>(qh, G.gm1, j, fh);
+          flux_axis<D>(ql, G.gm1, j, fl);
+#pragma unroll
+          for (int v = 0; v < M; ++v) rate[v] = rate[v] - (fh[v] - fl[v]) / G.h[j];
+        }
+        double half[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          half[v] = cq[v] + (0.5 * dt) * rate[v];
+          vh[r * M + v] = half[v];
+        }
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double lo[M], hi[M];
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            const double off = 0.5 * G.h[j] * slope[j][v];
+            sl[(r * D + j) * M + v] = off;
+            lo[v] = half[v] - off;
+            hi[v] = half[v] + off;
+          }
+          ok = ok && admissible<D>(lo, G.gm1) && admissible<D>(hi, G.gm1);
+        }
+        if (!ok) s_ok = 0;
+      }
+      __syncthreads();
+      // core update through the subcell faces
+      for (int s = tid; s < SD; s += NT) {
+        int si[3] = {0, 0, 0}, rem = s;
+        for (int j = D - 1; j >= 0; --j) {
+          si[j] = rem % S;
+          rem /= S;
+        }
+        auto rix = [&](int dj, int off) {
+          int x = 0;
+          for (int j = 0; j < D; ++j) x = x * R + si[j] + 1 + (j == dj ? off : 0);
+          return x;
+        };
+        auto wcore = [&]() {
+          int x = 0;
+          for (int j = 0; j < D; ++j) x = x * W + si[j] + 2;
+          return x;
+        };
+        double q[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) q[v] = win[wcore() * M + v];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const int rc = rix(0, 0), rl = rix(j, -1), rh = rix(j, 1);
+          double a[M], bq[M], dlo_h[M], dhi_h[M], dlo_l[M], dhi_l[M];
+          // high face: minus = hi state of this cell, plus = lo state of next
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            a[v] = vh[rc * M + v] + sl[(rc * D + j) * M + v];
+            bq[v] = vh[rh * M + v] - sl[(rh * D + j) * M + v];
+          }
+          rusanov_pair<D>(a, bq, j, G.gamma, G.gm1, dlo_h, dhi_h);
+          // low face: minus = hi state of previous, plus = lo state of this
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            a[v] = vh[rl * M + v] + sl[(rl * D + j) * M + v];
+            bq[v] = vh[rc * M + v] - sl[(rc * D + j) * M + v];
+          }
+          rusanov_pair<D>(a, bq, j, G.gamma, G.gm1, dlo_l, dhi_l);
+          const double c_j = dt / G.h[j];
+#pragma unroll
+          for (int v = 0; v < M; ++v) q[v] -= c_j * (dlo_h[v] + dhi_l[v]);
+        }
+        if (!admissible<D>(q, G.gm1)) s_ok = 0;
+#pragma unroll
+        for (int v = 0; v < M; ++v) nw[s * M + v] = q[v];
+      }
+      __syncthreads();
+      if (s_ok) break;
+      if (pass == 1) {
+        if (tid == 0) atomicOr(failed, 1);
+      }
+      __syncthreads();
+    }
+    if (!s_ok) {
+      __syncthreads();
+      continue;
+    }
+    // recovery (limiter.py:36-42): sequential per-axis contraction with R_sub
+    if (D == 1) {
+      for (int x = tid; x < PD * M; x += NT) {
+        const int i = x / M, v = x - i * M;
+        double acc = 0.0;
+        for (int s = 0; s < S; ++s) acc = fma(T.sub_recover[i * S + s], nw[s * M + v], acc);
+        nod[x] = acc;
+      }
+    } else if (D == 2) {
+      for (int x = tid; x < P * S * M; x += NT) {
+        const int i0 = x / (S * M), r = x - i0 * S * M;
+        double acc = 0.0;
+        for (int s0 = 0; s0 < S; ++s0) acc = fma(T.sub_recover[i0 * S + s0], nw[s0 * S * M + r], acc);
+        tmp[x] = acc;
+      }
+      __syncthreads();
+      for (int x = tid; x < PD * M; x += NT) {
+        const int i0 = x / (P * M), r = x - i0 * P * M, i1 = r / M, v = r - i1 * M;
+        double acc = 0.0;
+        for (int s1 = 0; s1 < S; ++s1)
+          acc = fma(T.sub_recover[i1 * S + s1], tmp[(i0 * S + s1) * M + v], acc);
+        nod[x] = acc;
+      }
+    } else {
+      for (int x = tid; x < P * S * S * M; x += NT) {
+        const int i0 = x / (S * S * M), r = x - i0 * S * S * M;
+        double acc = 0.0;
+        for (int s0 = 0; s0 < S; ++s0)
+          acc = fma(T.sub_recover[i0 * S + s0], nw[s0 * S * S * M + r], acc);
+        tmp[x] = acc;
+      }
+      __syncthreads();
+      double* t2 = tmp + P * S * S * M;
+      for (int x = tid; x < P * P * S * M; x += NT) {
+        const int i0 = x / (P * S * M), r = x - i0 * P * S * M, i1 = r / (S * M),
+                  r2 = r - i1 * S * M;
+        double acc = 0.0;
+        for (int s1 = 0; s1 < S; ++s1)
+          acc = fma(T.sub_recover[i1 * S + s1], tmp[(i0 * S + s1) * S * M + r2], acc);
+        t2[x] = acc;
+      }
+      __syncthreads();
+      for (int x = tid; x < PD * M; x += NT) {
+        const int i01 = x / (P * M), r = x - i01 * P * M, i2 = r / M, v = r - i2 * M;
+        double acc = 0.0;
+        for (int s2 = 0; s2 < S; ++s2)
+          acc = fma(T.sub_recover[i2 * S + s2], t2[(i01 * S + s2) * M + v], acc);
+        nod[x] = acc;
+      }
+    }
+    __syncthreads();
+    // flatten_inadmissible (limiter.py:205-223): nodal and its subcell
+    // projection must be admissible, else the cell becomes its mean
+    if (tid == 0) s_flat = 0;
+    __syncthreads();
+    for (int nd = tid; nd < PD; nd += NT)
+      if (!admissible<D>(nod + nd * M, G.gm1)) s_flat = 1;
+    __syncthreads();
+    if (!s_flat) {
+      double* pj = vh;    // reuse: projection of the recovered polynomial
+      project_cell<D, P>(nod, tmp + PD * M * 0 + (D == 3 ? P * S * S * M : P * S * M), pj, tid, NT);
+      __syncthreads();
+      for (int s = tid; s < SD; s += NT)
+        if (!admissible<D>(pj + s * M, G.gm1)) s_flat = 1;
+      __syncthreads();
+    }
+    double* dst = u_out + (size_t)e * PD * M;
+    if (s_flat) {
+      // mean of the new subcell averages (numpy mean: sum / count)
+      __shared__ double s_mean[M];
+      if (tid < M) {
+        double acc = 0.0;
+        for (int s = 0; s < SD; ++s) acc += nw[s * M + tid];
+        s_mean[tid] = acc / SD;
+      }
+      __syncthreads();
+      for (int x = tid; x < PD * M; x += NT) dst[x] = s_mean[x % M];
+    } else {
+      for (int x = tid; x < PD * M; x += NT) dst[x] = nod[x];
+    }
+    __syncthreads();
+  }
+}
+
+// IC flattening (driver.py:137-152): one block per cell
+template <int D, int P>
+__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+flatten_ic_kernel(double* __restrict__ u, int64_t E, double gm1, int32_t* nflat) {
+  using C = LimCfg<D, P>;
+  constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
+  const DegreeTables& T = tab<P>();
+  extern __shared__ __align__(16) double lsm[];
+  double* nodal = lsm;
+  double* out = nodal + PD * M;
+  double* tmp = out + SD * M;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    double* ue = u + (size_t)e * PD * M;
+    for (int x = tid; x < PD * M; x += NT) nodal[x] = ue[x];
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    project_cell<D, P>(nodal, tmp, out, tid, NT);
+    __syncthreads();
+    int bad = 0;
+    for (int s = tid; s < SD; s += NT) bad |= !admissible<D>(out + s * M, gm1);
+    for (int nd = tid; nd < PD; nd += NT) bad |= !admissible<D>(nodal + nd * M, gm1);
+    if (bad) s_bad = 1;
+    __syncthreads();
+    if (s_bad) {
+      __shared__ double s_mean[M];
+      if (tid < M) {
+        double acc = 0.0;
+        for (int nd = 0; nd < PD; ++nd) {
+          double w;
+          if (D == 1) w = T.weights[nd];
+          else if (D == 2) w = T.weights[nd / P] * T.weights[nd % P];
+          else w = T.weights[nd / (P * P)] * T.weights[(nd / P) % P] * T.weights[nd % P];
+          acc += nodal[nd * M + tid] * w;
+        }
+        s_mean[tid] = acc;
+      }
+      __syncthreads();
+      for (int x = tid; x < PD * M; x += NT) ue[x] = s_mean[x % M];
+      if (tid == 0) atomicAdd(nflat, 1);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- launchers
+static LimGrid lim_grid(const adg_grid* g) {
+  LimGrid G;
+  const int S = 2 * g->degree + 1;
+  for (int j = 0; j < 3; ++j) {
+    G.n[j] = j < g->dim ? g->cells[j] : 1;
+    G.h[j] = j < g->dim ? g->dx[j] / S : 1.0;
+    G.bc[j][0] = j < g->dim ? g->bc[j][0] : 0;
+    G.bc[j][1] = j < g->dim ? g->bc[j][1] : 0;
+  }
+  G.gamma = g->gamma;
+  G.gm1 = g->gamma - 1.0;
+  return G;
+}
+
+template <int D, int P>
+static size_t proj_smem() {
+  using C = LimCfg<D, P>;
+  const size_t out = D == 3 ? (size_t)C::S * P * P * C::M : (size_t)C::SD * C::M;
+  const size_t tmp = D == 3 ? (size_t)C::S * C::S * P * C::M : (size_t)C::S * P * C::M;
+  return ((size_t)C::PD * C::M + (out > (size_t)C::SD * C::M ? out : (size_t)C::SD * C::M) +
+          tmp) * 8;
+}
+
+template <int D, int P>
+static size_t rescue_smem() {
+  using C = LimCfg<D, P>;
+  const size_t tmp = D == 3 ? (size_t)P * C::S * C::S * C::M + (size_t)P * P * C::S * C::M
+                            : (size_t)P * C::S * C::M;
+  return ((size_t)C::WD * C::M + (size_t)C::RD * C::M * (1 + D) + (size_t)C::SD * C::M + tmp +
+          (size_t)C::SD * C::M + (size_t)C::PD * C::M + 64) * 8;
+}
+
+template <typename K>
+static bool set_smem(K kern, size_t bytes) {
+  if (bytes > 227 * 1024) return false;
+  if (bytes > 48 * 1024)
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) ==
+           cudaSuccess;
+  return true;
+}
+
+static bool lim_supported(const adg_grid* g, std::string* err) {
+  for (int j = 0; j < g->dim; ++j)
+    for (int s = 0; s < 2; ++s)
+      if (g->bc[j][s] == ADG_BC_GHOST) {
+        *err = "the subcell limiter supports periodic / outflow / wall faces on the device";
+        return false;
+      }
+  return true;
+}
+
+#define ADG_LIM_SWITCH(FN, ...)                                                 \
+  do {                                                                          \
+    switch (g->dim * 16 + g->degree + 1) {                                      \
+      case 17: rc = FN<1, 1>(__VA_ARGS__); break;                               \
+      case 18: rc = FN<1, 2>(__VA_ARGS__); break;                               \
+      case 19: rc = FN<1, 3>(__VA_ARGS__); break;                               \
+      case 20: rc = FN<1, 4>(__VA_ARGS__); break;                               \
+      case 21: rc = FN<1, 5>(__VA_ARGS__); break;                               \
+      case 22: rc = FN<1, 6>(__VA_ARGS__); break;                               \
+      case 23: rc = FN<1, 7>(__VA_ARGS__); break;                               \
+      case 24: rc = FN<1, 8>(__VA_ARGS__); break;                               \
+      case 25: rc = FN<1, 9>(__VA_ARGS__); break;                               \
+      case 26: rc = FN<1, 10>(__VA_ARGS__); break;                              \
+      case 33: rc = FN<2, 1>(__VA_ARGS__); break;                               \
+      case 34: rc = FN<2, 2>(__VA_ARGS__); break;                               \
+      case 35: rc = FN<2, 3>(__VA_ARGS__); break;                               \
+      case 36: rc = FN<2, 4>(__VA_ARGS__); break;                               \
+      case 37: rc = FN<2, 5>(__VA_ARGS__); break;                               \
+      case 38: rc = FN<2, 6>(__VA_ARGS__); break;                               \
+      case 39: rc = FN<2, 7>(__VA_ARGS__); break;                               \
+      case 40: rc = FN<2, 8>(__VA_ARGS__); break;                               \
+      case 41: rc = FN<2, 9>(__VA_ARGS__); break;                               \
+      case 42: rc = FN<2, 10>(__VA_ARGS__); break;                              \
+      case 49: rc = FN<3, 1>(__VA_ARGS__); break;                               \
+      case 50: rc = FN<3, 2>(__VA_ARGS__); break;                               \
+      case 51: rc = FN<3, 3>(__VA_ARGS__); break;                               \
+      default:                                                                  \
+        *err = "subcell limiter on the device: dim 1-2 (any N) or 3 (N <= 2)";  \
+        return ADG_ERR_UNSUPPORTED;                                             \
+    }                                                                           \
+  } while (0)
+
+static int lerr(std::string* err) {
+  cudaError_t ce = cudaGetLastError();
+  if (ce != cudaSuccess) {
+    *err = cudaGetErrorString(ce);
+    return ADG_ERR_CUDA;
+  }
+  return ADG_OK;
+}
+
+template <int D, int P>
+static int launch_prep(const adg_grid* g, const double* u, double* sub, double* cmin,
+                       double* cmax, cudaStream_t st, std::string* err) {
+  const size_t sm = proj_smem<D, P>();
+  if (!set_smem(subcell_prep_kernel<D, P>, sm)) {
+    *err = "limiter tile exceeds shared memory";
+    return ADG_ERR_UNSUPPORTED;
+  }
+  const int64_t E = n_elements(g);
+  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
+  subcell_prep_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(u, E, sub, cmin, cmax);
+  return lerr(err);
+}
+
+template <int D, int P>
+static int launch_detect(const adg_grid* g, const double* prev_sub, const double* cmin,
+                         const double* cmax, const double* cand, const uint8_t* pred_bad,
+                         double d0, double eps, int force, uint8_t* troubled, int32_t* idx,
+                         int32_t* count, cudaStream_t st, std::string* err) {
+  const size_t sm = proj_smem<D, P>();
+  if (!set_smem(detect_kernel<D, P>, sm)) {
+    *err = "limiter tile exceeds shared memory";
+    return ADG_ERR_UNSUPPORTED;
+  }
+  const int64_t E = n_elements(g);
+  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
+  cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+  detect_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(prev_sub, cmin, cmax, cand, pred_bad,
+                                                          lim_grid(g), E, d0, eps, force,
+                                                          troubled, idx, count);
+  return lerr(err);
+}
+
+template <int D, int P>
+static int launch_rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
+                         const int32_t* count, int32_t cmax, const double* dt, double* u_out,
+                         int32_t* failed, cudaStream_t st, std::string* err) {
+  const size_t sm = rescue_smem<D, P>();
+  if (!set_smem(rescue_kernel<D, P>, sm)) {
+    *err = "limiter window exceeds shared memory";
+    return ADG_ERR_UNSUPPORTED;
+  }
+  if (cmax <= 0) return ADG_OK;
+  rescue_kernel<D, P><<<(unsigned)cmax, LimCfg<D, P>::NT, sm, st>>>(prev_sub, idx, count,
+                                                                   lim_grid(g), dt, u_out,
+                                                                   failed);
+  return lerr(err);
+}
+
+template <int D, int P>
+static int launch_flatten(const adg_grid* g, double* u, int32_t* nflat, cudaStream_t st,
+                          std::string* err) {
+  const size_t sm = proj_smem<D, P>();
+  if (!set_smem(flatten_ic_kernel<D, P>, sm)) {
+    *err = "limiter tile exceeds shared memory";
+    return ADG_ERR_UNSUPPORTED;
+  }
+  const int64_t E = n_elements(g);
+  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
+  cudaMemsetAsync(nflat, 0, sizeof(int32_t), st);
+  flatten_ic_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(u, E, g->gamma - 1.0, nflat);
+  return lerr(err);
+}
+
+int project_subcells(const adg_grid* g, const double* u, double* sub, double* cmin, double* cmax,
+                     cudaStream_t st, std::string* err) {
+  int rc = ADG_OK;
+  ADG_LIM_SWITCH(launch_prep, g, u, sub, cmin, cmax, st, err);
+  return rc;
+}
+
+int detect(const adg_grid* g, const double* prev_sub, const double* cmin, const double* cmax,
+           const double* cand, const uint8_t* pred_bad, double delta0, double eps, int force_all,
+           uint8_t* troubled, int32_t* idx, int32_t* count, cudaStream_t st, std::string* err) {
+  if (!lim_supported(g, err)) return ADG_ERR_UNSUPPORTED;
+  int rc = ADG_OK;
+  ADG_LIM_SWITCH(launch_detect, g, prev_sub, cmin, cmax, cand, pred_bad, delta0, eps, force_all,
+                 troubled, idx, count, st, err);
+  return rc;
+}
+
+int rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
+           const int32_t* count_dev, int32_t count_max, const double* dt_dev, double* u_out,
+           int32_t* failed, cudaStream_t st, std::string* err) {
+  if (!lim_supported(g, err)) return ADG_ERR_UNSUPPORTED;
+  int rc = ADG_OK;
+  ADG_LIM_SWITCH(launch_rescue, g, prev_sub, idx, count_dev, count_max, dt_dev, u_out, failed, st,
+                 err);
+  return rc;
+}
+
+int flatten_ic(const adg_grid* g, double* u, int32_t* nflat, cudaStream_t st, std::string* err) {
+  int rc = ADG_OK;
+  ADG_LIM_SWITCH(launch_flatten, g, u, nflat, st, err);
+  return rc;
+}
+
 }  // namespace adg

@@ -344,10 +344,62 @@ class Simulation:
             return True, 0.0, None
         return self._attempt_limited(row, trial)
 
-    def _attempt_limited(self, row, trial):
-        from . import limiter as _limiter  # noqa: F401  (kernels live in the .so)
+    def _limiter_buffers(self):
+        lb = getattr(self, "_lim", None)
+        if lb is None:
+            E = self.mesh.n_elements
+            S = self.tables.n_subcells
+            m = self._m
+            f64 = dict(dtype=torch.float64, device=self.device)
+            lb = {"sub": torch.empty(E * S ** self.mesh.dim * m, **f64),
+                  "cmin": torch.empty(E * m, **f64), "cmax": torch.empty(E * m, **f64),
+                  "troubled": torch.empty(self.mesh.cells, dtype=torch.uint8,
+                                          device=self.device),
+                  "idx": torch.empty(E, dtype=torch.int32, device=self.device),
+                  "count": torch.zeros(1, dtype=torch.int32, device=self.device),
+                  "failed": torch.zeros(1, dtype=torch.int32, device=self.device),
+                  "sub_of": None}
+            self._lim = lb
+        return lb
 
-        raise NotImplementedError("subcell limiter kernels are not built yet")
+    def _attempt_limited(self, row, trial):
+        """_attempt_step + _limit on the device (driver.py:204-230, :265-299).
+        Returns (accepted, limited_fraction, troubled flags)."""
+        buf = self._buf
+        lb = self._limiter_buffers()
+        sp = _stream_ptr()
+        dt_dev = row[0:1]
+        if lb["sub_of"] is not self._u or self._red_cur is None:
+            # t^n subcell averages and their per-cell extrema (once per step)
+            self._h.call("adg_project_subcells", self._gp(), _ptr(self._u), _ptr(lb["sub"]),
+                         _ptr(lb["cmin"]), _ptr(lb["cmax"]), sp)
+            lb["sub_of"] = self._u
+        self._predict(dt_dev)
+        self.sweep_log.append(None)
+        self._faces()
+        nxt = self._update(dt_dev, None)
+        self._h.call("adg_detect", self._gp(), _ptr(lb["sub"]), _ptr(lb["cmin"]),
+                     _ptr(lb["cmax"]), _ptr(self._u_next), _ptr(buf.pred_bad), self.dmp_delta0,
+                     self.dmp_eps, int(bool(self.force_limit_all)), _ptr(lb["troubled"]),
+                     _ptr(lb["idx"]), _ptr(lb["count"]), sp)
+        n_tr = int(lb["count"].item())
+        self.sweep_log[-1] = int(buf.sweeps.max().item())
+        if n_tr:
+            lb["failed"].zero_()
+            self._h.call("adg_rescue", self._gp(), _ptr(lb["sub"]), _ptr(lb["idx"]),
+                         _ptr(lb["count"]), n_tr, _ptr(dt_dev), _ptr(self._u_next),
+                         _ptr(lb["failed"]), sp)
+            if int(lb["failed"].item()):
+                return False, 0.0, None   # driver.py:292-293 -> restart with dt/2
+            # rescued cells changed u_next: redo its wave speeds / totals
+            self._h.call("adg_wavespeed", self._gp(), _ptr(self._u_next), _ptr(buf.red[nxt]), sp)
+        self._h.call("adg_totals", self._gp(), _ptr(self._u_next), _ptr(buf.partial),
+                     _ptr(row[2:]), sp)
+        self._h.call("adg_advance_time", _ptr(buf.t), _ptr(dt_dev), _ptr(row[1:2]), sp)
+        self._u, self._u_next = self._u_next, self._u
+        self._red_cur = nxt
+        troubled = lb["troubled"].clone().bool()
+        return True, n_tr / self.mesh.n_elements, troubled
 
     def run(self, t_end, max_steps=None, on_step=None):
         """March until t_end or max_steps (driver.py:186-202)."""

@@ -176,3 +176,50 @@ def test_conservation_full_size_c2(pkg):
     err = sim.error_norms(exact)
     assert err["linf"].max() < 1e-6
     assert max(sim.sweep_log) <= 3
+
+
+@pytest.mark.parametrize("name,problem,bc", [("c4_explosion_16", "explosion", "outflow"),
+                                             ("sod_1d", "sod", "outflow"),
+                                             ("blast_wall", "blast", "wall")])
+def test_limiter_cases(pkg, golden, name, problem, bc):
+    """Troubled-cell flags identical to the reference every step; states within
+    1e-10 (limiter.py / driver.py:265-299 on the device)."""
+    g = golden(name)
+    mesh = pkg.CartesianMesh([tuple(e) for e in g["extents"]], [int(c) for c in g["cells"]])
+    system = pkg.make_system("euler", mesh.dim)
+    sim = pkg.Simulation(mesh, system, int(g["degree"]), float(g["cfl"]), boundary=bc,
+                         use_limiter=True)
+    params = {"p_ambient": 1e-2} if problem == "blast" else {}
+    ic, _ = pkg.build_problem(problem, system, **params)
+    sim.project_initial_condition(ic)
+    assert rel_linf(sim.u, g["u0"]) <= 1e-14
+    for s in range(len(g["dts"])):
+        sim.run(np.inf, max_steps=s + 1)
+        np.testing.assert_array_equal(sim.last_troubled.cpu().numpy(), g["troubled"][s],
+                                      err_msg=f"step {s + 1}")
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-12)
+    np.testing.assert_allclose([h["limited_fraction"] for h in sim.history], g["fracs"])
+    assert rel_linf(sim.u, g["u"]) <= TOL
+
+
+def test_explosion_64_vs_oracle(pkg):
+    """C4 shape at 64^2 (oracle-feasible), 4 limited steps against the oracle:
+    identical troubled flags every step, states within 1e-10."""
+    from oracle import problems as oprob
+    from oracle.euler import EulerOracle
+    from oracle.sim import OracleMesh, OracleSimulation
+
+    ext, cells, n, cfl = [(-1.0, 1.0), (-1.0, 1.0)], (64, 64), 5, 0.9 / 22.0
+    osim = OracleSimulation(OracleMesh(ext, cells), EulerOracle(2), n, cfl, boundary="outflow",
+                            use_limiter=True, per_element_picard=True)
+    osim.project_initial_condition(oprob.explosion()[0])
+    mesh = pkg.CartesianMesh(ext, cells)
+    system = pkg.make_system("euler", 2)
+    sim = pkg.Simulation(mesh, system, n, cfl, boundary="outflow", use_limiter=True)
+    sim.project_initial_condition(pkg.build_problem("explosion", system)[0])
+    assert rel_linf(sim.u, osim.u) <= 1e-14
+    for s in range(4):
+        osim.run(np.inf, max_steps=s + 1)
+        sim.run(np.inf, max_steps=s + 1)
+        np.testing.assert_array_equal(sim.last_troubled.cpu().numpy(), osim.last_troubled)
+    assert rel_linf(sim.u, osim.u) <= TOL
