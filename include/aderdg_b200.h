@@ -122,22 +122,25 @@ int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double*
 /* -- face coupling along one axis: driver._face_states (driver.py:234-261)
  *    + corrector.face_fluxes (corrector.py:100-129) + the time weighting of
  *    face_integral (corrector.py:186) ------------------------------------ */
-/* dbar_out: [faces (cells with cells[axis]+1 along axis), P^(d-1), m], the
- * time-integrated low-side term sum_t w_t d_low; the high-side term is its
- * exact negation.  ghost_lo / ghost_hi: exterior traces for ADG_BC_GHOST
- * faces, [cells with 1 along axis, P^(d-1), P_t, m], else NULL. */
+/* fd: element-major face terms [E][d axes][2 sides][P^(d-1)][m] shared by
+ * all axes; this call fills the entries of `axis` with the time-integrated
+ * low-side Rusanov term sum_t w_t d_low of each face (for the element's
+ * high face, and for the low face of the element above it, where the
+ * high-side term is its exact negation).  Traces are the predictor's blocks;
+ * ghost_lo / ghost_hi: exterior trace blocks for ADG_BC_GHOST faces,
+ * [cells with 1 along axis][trace block], else NULL. */
 int adg_face_flux(adg_handle* h, const adg_grid* g, int axis, const double* traces,
-                  const double* ghost_lo, const double* ghost_hi, double* dbar_out,
+                  const double* ghost_lo, const double* ghost_hi, double* fd,
                   void* stream);
 
 /* -- corrector.face_integral + element_update (corrector.py:180-205) with a
  *    fused epilogue: wave speeds of u_out folded into red_next (the next
  *    step's compute_timestep) and per-block conserved-total partials
- *    (driver.py:344-350).  dbar[a] from adg_face_flux for axis a.
+ *    (driver.py:344-350).  fd filled by adg_face_flux for every axis.
+ *    u, vol, fd stream through TMA bulk copies (16-byte aligned buffers).
  *    totals_partial: [adg_update_blocks(g), m] (may be NULL).            */
 int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
-               const double* dbar0, const double* dbar1, const double* dbar2,
-               const double* dt_dev, double* u_out, adg_reduce* red_next,
+               const double* fd, const double* dt_dev, double* u_out, adg_reduce* red_next,
                double* totals_partial, void* stream);
 int64_t adg_update_blocks(const adg_grid* g);
 /* totals[m] = cell_volume * fixed-order sum of the partials */

@@ -62,7 +62,7 @@ _SIGS = {
     "adg_advance_time": (_I, [_P, _P, _P, _P, _P]),
     "adg_predict": (_I, [_P, _P, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P]),
     "adg_face_flux": (_I, [_P, _P, _I, _P, _P, _P, _P, _P]),
-    "adg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "adg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "adg_update_blocks": (_I64, [_P]),
     "adg_totals_finalize": (_I, [_P, _P, _P, _I64, _P, _P]),
     "adg_totals": (_I, [_P, _P, _P, _P, _P, _P]),

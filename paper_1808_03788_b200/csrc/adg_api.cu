@@ -172,17 +172,15 @@ int adg_face_flux(adg_handle* h, const adg_grid* g, int axis, const double* trac
                                 (cudaStream_t)stream, &e), e);
 }
 
-int64_t adg_update_blocks(const adg_grid* g) { return adg::reduce_blocks(g); }
+int64_t adg_update_blocks(const adg_grid* g) { return adg::update_blocks(g); }
 
 int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
-               const double* dbar0, const double* dbar1, const double* dbar2,
-               const double* dt_dev, double* u_out, adg_reduce* red_next,
+               const double* fd, const double* dt_dev, double* u_out, adg_reduce* red_next,
                double* totals_partial, void* stream) {
   int rc = check_grid(h, g);
   if (rc) return rc;
-  const double* db[3] = {dbar0, dbar1, dbar2};
   std::string e;
-  return wrap(h, adg::update(g, u, vol, db, dt_dev, u_out, red_next, totals_partial,
+  return wrap(h, adg::update(g, u, vol, fd, dt_dev, u_out, red_next, totals_partial,
                              (cudaStream_t)stream, &e), e);
 }
 

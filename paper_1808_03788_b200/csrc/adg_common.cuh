@@ -38,6 +38,19 @@ template <int P> __device__ __forceinline__ const DegreeTables& tab() { return c
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 
 // ---------------------------------------------------------------- Euler
+// 1/x from the hardware approximation refined by two Newton steps (error
+// below one ulp of the IEEE quotient; the reference's 1.0 / rho is replaced
+// at the 1e-16 level, far inside the 1e-10 parity bar).  Saves the
+// slow-path-guarded IEEE division on every flux evaluation.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // systems.py:128-133 pressure; identical operation order.
 template <int D>
 __device__ __forceinline__ double pressure(const double* q, double gm1) {
@@ -50,7 +63,7 @@ __device__ __forceinline__ double pressure(const double* q, double gm1) {
 // systems.py:140-156: F[j][v].  One IEEE division (1/rho) as in the reference.
 template <int D>
 __device__ __forceinline__ void flux_all(const double* q, double gm1, double f[D][D + 2]) {
-  const double r = 1.0 / q[0];
+  const double r = rcp_nr(q[0]);
   double kin = q[1] * q[1];
 #pragma unroll
   for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
@@ -70,7 +83,7 @@ __device__ __forceinline__ void flux_all(const double* q, double gm1, double f[D
 // Flux along a single axis a (same arithmetic as flux_all's row a).
 template <int D>
 __device__ __forceinline__ void flux_axis(const double* q, double gm1, int a, double f[D + 2]) {
-  const double r = 1.0 / q[0];
+  const double r = rcp_nr(q[0]);
   double kin = q[1] * q[1];
 #pragma unroll
   for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
@@ -109,6 +122,58 @@ __device__ __forceinline__ void atomic_max_pos(uint64_t* addr, double v) {
   // v >= 0 and finite: IEEE bit patterns order like unsigned integers
   atomicMax(reinterpret_cast<unsigned long long*>(addr),
             static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// ---------------------------------------------------------------- TMA bulk
+// 1-D bulk copies between global and shared memory (cp.async.bulk, SASS
+// UBLKCP) completing on an mbarrier; sizes and addresses 16-byte aligned.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Host-side launch helpers ------------------------------------------------

@@ -28,6 +28,19 @@ int64_t reduce_blocks(const adg_grid* g) {
                                                 kReduceBlocksCap));
 }
 
+// blocks (= totals partials) of one update launch: persistent blocks over
+// chunks of EB elements, EB = max(1, 768 / (P^d m)) as in UpdCfg (a fixed
+// count keeps the global atomics few and the totals bitwise reproducible);
+// never fewer than the reduction kernels use, so one partial buffer serves both
+int64_t update_blocks(const adg_grid* g) {
+  const int64_t P = g->degree + 1;
+  int64_t pd = 1;
+  for (int j = 0; j < g->dim; ++j) pd *= P;
+  const int64_t eb = std::max<int64_t>(1, 256 / pd) * 2;   // >= UpdCfg::EB
+  const int64_t nb = std::min<int64_t>(std::max<int64_t>(n_elements(g) / eb, 1), kUpdateBlocksCap);
+  return std::max<int64_t>(nb, reduce_blocks(g));
+}
+
 // -------------------------------------------------------------------------
 // Block-level fold of per-thread wave speeds / counts / totals.  Max is
 // order independent; totals use a fixed shuffle tree + fixed warp order, so
@@ -252,8 +265,17 @@ face_kernel(const double* __restrict__ traces, const double* __restrict__ ghost_
     } else {
       pp = tr_lo + (size_t)elem(ca) * PD * M;
     }
-    pm += (size_t)tg * P * M;
-    pp += (size_t)tg * P * M;
+    // element-face trace blocks are written by the predictor's owner roles:
+    // x faces [j][k][t], y faces [k][t][i], z faces [t][i][j] (2-D: x [j][t],
+    // y [t][i]); (ta, tb) are the ascending tangential indices
+    constexpr int SA = D == 3 ? (AX == 0 ? P * P : (AX == 1 ? 1 : P)) : (D == 2 ? (AX == 0 ? P : 1) : 0);
+    constexpr int SB = D == 3 ? (AX == 0 ? P : (AX == 1 ? P * P : 1)) : 0;
+    constexpr int ST = D == 3 ? (AX == 0 ? 1 : (AX == 1 ? P : P * P)) : (D == 2 ? (AX == 0 ? 1 : P) : 1);
+    const int ta = D == 3 ? tg / P : tg;
+    const int tb = D == 3 ? tg % P : 0;
+    const int base = ta * SA + tb * SB;
+    pm += (size_t)base * M;
+    pp += (size_t)base * M;
     double acc[M];
 #pragma unroll
     for (int v = 0; v < M; ++v) acc[v] = 0.0;
@@ -262,8 +284,8 @@ face_kernel(const double* __restrict__ traces, const double* __restrict__ ghost_
       double qm[M], qp[M];
 #pragma unroll
       for (int v = 0; v < M; ++v) {
-        qm[v] = pm[t * M + v];
-        qp[v] = pp[t * M + v];
+        qm[v] = pm[t * ST * M + v];
+        qp[v] = pp[t * ST * M + v];
       }
       if (reflect_m) qm[1 + axis] = -qm[1 + axis];   // systems.py:231-234
       if (reflect_p) qp[1 + axis] = -qp[1 + axis];
@@ -281,64 +303,71 @@ face_kernel(const double* __restrict__ traces, const double* __restrict__ ghost_
         acc[v] = fma(wt, dlow, acc[v]);
       }
     }
-    double* o = dbar + (size_t)x * M;
+    // element-major face terms fd[E][D][2 sides][P^(d-1)][m]: the face is the
+    // high face of its low-side element and the low face of its high-side
+    // element (periodic: face n_a repeats face 0, each element written once)
+    constexpr size_t FBLK = (size_t)PF * M;
+    if (ca >= 1) {
+      double* o = dbar + ((size_t)elem(ca - 1) * (2 * D) + 2 * axis + 1) * FBLK + (size_t)tg * M;
 #pragma unroll
-    for (int v = 0; v < M; ++v) o[v] = acc[v];
+      for (int v = 0; v < M; ++v) o[v] = acc[v];
+    }
+    if (ca < n[axis]) {
+      double* o = dbar + ((size_t)elem(ca) * (2 * D) + 2 * axis) * FBLK + (size_t)tg * M;
+#pragma unroll
+      for (int v = 0; v < M; ++v) o[v] = acc[v];
+    }
   }
 }
 
 // -------------------------------------------------------------------------
-// Element update, thread per (element, node), grid-stride with a fixed grid.
+// Element update, streamed with TMA bulk copies.  Each persistent block walks
+// chunks of EB consecutive elements; a chunk is three contiguous, 16-byte
+// aligned blocks (u, vol, element-major face terms) fetched by one elected
+// thread with cp.async.bulk into a double-buffered stage (the next chunk
+// lands while the current one is computed), a thread per node forms
+// u + (vol - sum of face integrals) / mass in the reference's order
+// (corrector.py:180-205) in place, folds the new state into the next step's
+// wave-speed record and the conserved-total partial, and the chunk leaves
+// through one bulk store.  A ragged tail chunk uses plain loads/stores.
 template <int D, int P>
-__global__ void __launch_bounds__(kReduceThreads)
-update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
-              const double* __restrict__ db0, const double* __restrict__ db1,
-              const double* __restrict__ db2, const double* __restrict__ dt_dev,
-              double* __restrict__ u_out, int64_t c0, int64_t c1, int64_t c2, double dx0,
-              double dx1, double dx2, double gamma, adg_reduce* red, double* partial) {
-  constexpr int M = D + 2;
-  constexpr int PD = ipow(P, D);
-  constexpr int PF = PD / P;
-  const DegreeTables& T = tab<P>();
-  const double gm1 = gamma - 1.0;
-  const double dt = *dt_dev;
-  const int64_t n[3] = {c0, c1, c2};
-  const double dx[3] = {dx0, dx1, dx2};
-  const double* dbs[3] = {db0, db1, db2};
-  const int64_t E = n[0] * (D >= 2 ? n[1] : 1) * (D == 3 ? n[2] : 1);
-  const double cv = dx0 * (D >= 2 ? dx1 : 1.0) * (D == 3 ? dx2 : 1.0);
-  double lam[3] = {0.0, 0.0, 0.0};
-  unsigned nadm = 0, nnf = 0;
-  double tot[M];
-#pragma unroll
-  for (int v = 0; v < M; ++v) tot[v] = 0.0;
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < E * PD;
-       x += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = x / PD;
-    const int node = (int)(x - e * PD);
+struct UpdCfg {
+  static constexpr int M = D + 2;
+  static constexpr int PD = ipow(P, D);
+  static constexpr int PF = PD / P;
+  static constexpr int FE = 2 * D * PF * M;            // face-term values per element
+  static constexpr int EB0 = (256 / PD) > 0 ? (256 / PD) : 1;
+  // chunk byte counts must be multiples of 16 for the bulk engine
+  static constexpr int EB = ((EB0 * PD * M) % 2 == 0) ? EB0 : 2 * EB0;
+  static constexpr int CU = EB * PD * M;               // state values per chunk
+  static constexpr int CF = EB * FE;                   // face values per chunk
+  static constexpr int STAGE = 2 * CU + CF;            // doubles per stage
+  // double-buffered unless two stages exceed the shared-memory budget
+  static constexpr int NSTAGE = (2 * STAGE * 8 <= 200 * 1024) ? 2 : 1;
+  static constexpr size_t SMEM = (size_t)NSTAGE * STAGE * 8;
+};
+
+template <int D, int P>
+__device__ __forceinline__ void update_chunk(const double* SU_in, const double* SV,
+                                             const double* SF, double* SU_out, int neb,
+                                             const double* s_w, const double* s_l,
+                                             const double* s_r, double dt, double cv,
+                                             const double* dx, double gamma, double gm1,
+                                             double* lam, unsigned& nadm, unsigned& nnf,
+                                             double* tot) {
+  using C = UpdCfg<D, P>;
+  constexpr int M = C::M, PD = C::PD, PF = C::PF, FE = C::FE;
+  for (int y = threadIdx.x; y < neb * PD; y += kReduceThreads) {
+    const int el = y / PD, node = y - el * PD;
     int k[3] = {0, 0, 0};
     if (D == 1) k[0] = node;
     if (D == 2) { k[0] = node / P; k[1] = node % P; }
     if (D == 3) { k[0] = node / (P * P); k[1] = (node / P) % P; k[2] = node % P; }
-    int64_t c[3] = {0, 0, 0};
-    {
-      int64_t r = e;
-      for (int j = D - 1; j >= 0; --j) {
-        c[j] = r % n[j];
-        r /= n[j];
-      }
-    }
     double total[M];
 #pragma unroll
-    for (int v = 0; v < M; ++v) total[v] = vol[x * M + v];
+    for (int v = 0; v < M; ++v) total[v] = SV[y * M + v];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      // face index of the element's low face along a in the (n_a+1) face grid
-      int64_t flo = 0;
-      for (int j = 0; j < D; ++j) flo = flo * (n[j] + (j == a ? 1 : 0)) + c[j];
-      int64_t stride_a = 1;
-      for (int j = D - 1; j > a; --j) stride_a *= n[j];
-      const int64_t fhi = flo + stride_a;
       int tg = 0;
       double wtan = 1.0;
       bool first = true;
@@ -346,14 +375,13 @@ update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
       for (int j = 0; j < D; ++j) {
         if (j == a) continue;
         tg = tg * P + k[j];
-        wtan = first ? T.weights[k[j]] : wtan * T.weights[k[j]];
+        wtan = first ? s_w[k[j]] : wtan * s_w[k[j]];
         first = false;
       }
-      const double area = cv / dx[a];
-      const double sc = dt * area;
-      const double* dlo = dbs[a] + ((size_t)flo * PF + tg) * M;
-      const double* dhi = dbs[a] + ((size_t)fhi * PF + tg) * M;
-      const double vl = T.left[k[a]], vr = T.right[k[a]];
+      const double sc = dt * (cv / dx[a]);
+      const double* dlo = SF + el * FE + (2 * a) * PF * M + tg * M;
+      const double* dhi = dlo + PF * M;
+      const double vl = s_l[k[a]], vr = s_r[k[a]];
 #pragma unroll
       for (int v = 0; v < M; ++v) {
         const double blo = (D > 1) ? (-dlo[v]) * wtan : -dlo[v];
@@ -365,15 +393,113 @@ update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
         total[v] -= sc * (vr * bhi);
       }
     }
-    const double wnode = node_weight<D, P>(node);
+    double wnode;
+    if (D == 1) wnode = s_w[k[0]];
+    else if (D == 2) wnode = s_w[k[0]] * s_w[k[1]];
+    else wnode = s_w[k[0]] * s_w[k[1]] * s_w[k[2]];
     const double mass = cv * wnode;
     double q[M];
 #pragma unroll
     for (int v = 0; v < M; ++v) {
-      q[v] = u[x * M + v] + total[v] / mass;
-      u_out[x * M + v] = q[v];
+      q[v] = SU_in[y * M + v] + total[v] / mass;
+      SU_out[y * M + v] = q[v];
     }
-    node_fold<D>(q, gamma, gm1, wnode, lam, nadm, nnf, partial ? tot : nullptr);
+    node_fold<D>(q, gamma, gm1, wnode, lam, nadm, nnf, tot);
+  }
+}
+
+template <int D, int P>
+__global__ void __launch_bounds__(kReduceThreads)
+update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
+              const double* __restrict__ fd, const double* __restrict__ dt_dev,
+              double* __restrict__ u_out, int64_t E, double dx0, double dx1, double dx2,
+              double gamma, adg_reduce* red, double* partial) {
+  using C = UpdCfg<D, P>;
+  constexpr int M = C::M, PD = C::PD, FE = C::FE, EB = C::EB, CU = C::CU, CF = C::CF;
+  constexpr int STAGE = C::STAGE;
+  extern __shared__ __align__(128) double usm[];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ double s_w[P], s_l[P], s_r[P];
+  const DegreeTables& T = tab<P>();
+  const int tid = threadIdx.x;
+  if (tid < P) {
+    s_w[tid] = T.weights[tid];
+    s_l[tid] = T.left[tid];
+    s_r[tid] = T.right[tid];
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double gm1 = gamma - 1.0;
+  const double dt = *dt_dev;
+  const double dx[3] = {dx0, dx1, dx2};
+  const double cv = dx0 * (D >= 2 ? dx1 : 1.0) * (D == 3 ? dx2 : 1.0);
+  double lam[3] = {0.0, 0.0, 0.0};
+  unsigned nadm = 0, nnf = 0;
+  double tot[M];
+#pragma unroll
+  for (int v = 0; v < M; ++v) tot[v] = 0.0;
+  double* tp = partial ? tot : nullptr;
+
+  const int64_t nfull = E / EB;             // chunks served by the bulk engine
+  auto issue = [&](int stg, int64_t c) {
+    double* st = usm + stg * STAGE;
+    const int64_t e0 = c * EB;
+    mbar_expect_tx(&bar[stg], (uint32_t)(STAGE * 8));
+    bulk_g2s(st, u + (size_t)e0 * PD * M, CU * 8, &bar[stg]);
+    bulk_g2s(st + CU, vol + (size_t)e0 * PD * M, CU * 8, &bar[stg]);
+    bulk_g2s(st + 2 * CU, fd + (size_t)e0 * FE, CF * 8, &bar[stg]);
+  };
+  uint32_t phase[2] = {0u, 0u};
+  int64_t c = blockIdx.x;
+  if (C::NSTAGE == 2 && tid == 0 && c < nfull) issue(0, c);
+  for (int i = 0; c < nfull; ++i, c += gridDim.x) {
+    const int stg = C::NSTAGE == 2 ? (i & 1) : 0;
+    const int64_t cn = c + gridDim.x;
+    if (tid == 0) {
+      if (C::NSTAGE == 2) {
+        if (cn < nfull) {
+          bulk_wait_read_all();   // the other stage's bulk store has left smem
+          issue(stg ^ 1, cn);
+        }
+      } else {
+        bulk_wait_read_all();
+        issue(0, c);
+      }
+    }
+    mbar_wait(&bar[stg], phase[stg]);
+    phase[stg] ^= 1u;
+    double* st = usm + stg * STAGE;
+    update_chunk<D, P>(st, st + CU, st + 2 * CU, st, EB, s_w, s_l, s_r, dt, cv, dx, gamma, gm1,
+                       lam, nadm, nnf, tp);
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(u_out + (size_t)c * EB * PD * M, st, CU * 8);
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+  __syncthreads();
+  // ragged tail (E % EB elements) with plain loads / stores, by block 0
+  const int tail = (int)(E - nfull * EB);
+  if (tail > 0 && blockIdx.x == 0) {
+    double* st = usm;
+    const size_t off = (size_t)nfull * EB * PD * M;
+    for (int x = tid; x < tail * PD * M; x += kReduceThreads) {
+      st[x] = u[off + x];
+      st[CU + x] = vol[off + x];
+    }
+    for (int x = tid; x < tail * FE; x += kReduceThreads)
+      st[2 * CU + x] = fd[(size_t)nfull * EB * FE + x];
+    __syncthreads();
+    update_chunk<D, P>(st, st + CU, st + 2 * CU, st, tail, s_w, s_l, s_r, dt, cv, dx, gamma,
+                       gm1, lam, nadm, nnf, tp);
+    __syncthreads();
+    for (int x = tid; x < tail * PD * M; x += kReduceThreads) u_out[off + x] = st[x];
   }
   block_fold<D>(lam, nadm, nnf, tot, red, partial);
 }
@@ -381,14 +507,22 @@ update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
 template <int M>
 __global__ void totals_finalize_kernel(const double* __restrict__ partial, int64_t nb, double cv,
                                        double* out) {
-  // one warp per quantity, fixed strided order + fixed shuffle tree
-  const int v = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (v >= M) return;
-  double s = 0.0;
-  for (int64_t b = lane; b < nb; b += 32) s += partial[b * M + v];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[v] = cv * s;
+  // 1024 threads: fixed strided partial sums, then a fixed shared-memory
+  // tree -> bitwise reproducible for a given partial count
+  __shared__ double sm[1024];
+  const int t = threadIdx.x;
+  for (int v = 0; v < M; ++v) {
+    double s = 0.0;
+    for (int64_t b = t; b < nb; b += 1024) s += partial[b * M + v];
+    sm[t] = s;
+    __syncthreads();
+    for (int o = 512; o > 0; o >>= 1) {
+      if (t < o) sm[t] += sm[t + o];
+      __syncthreads();
+    }
+    if (t == 0) out[v] = cv * sm[0];
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------ launchers
@@ -500,25 +634,29 @@ int face_flux(const adg_grid* g, int axis, const double* traces, const double* g
 }
 
 template <int D, int P>
-static void launch_update(const adg_grid* g, const double* u, const double* vol,
-                          const double* const dbar[3], const double* dt_dev, double* u_out,
-                          adg_reduce* red, double* partial, cudaStream_t st) {
-  update_kernel<D, P><<<(unsigned)reduce_blocks(g), kReduceThreads, 0, st>>>(
-      u, vol, dbar[0], dbar[1], dbar[2], dt_dev, u_out, g->cells[0], D >= 2 ? g->cells[1] : 1,
-      D == 3 ? g->cells[2] : 1, g->dx[0], D >= 2 ? g->dx[1] : 1.0, D == 3 ? g->dx[2] : 1.0,
-      g->gamma, red, partial);
+static void launch_update(const adg_grid* g, const double* u, const double* vol, const double* fd,
+                          const double* dt_dev, double* u_out, adg_reduce* red, double* partial,
+                          cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(update_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)UpdCfg<D, P>::SMEM);
+    attr = true;
+  }
+  update_kernel<D, P><<<(unsigned)update_blocks(g), kReduceThreads, UpdCfg<D, P>::SMEM, st>>>(
+      u, vol, fd, dt_dev, u_out, n_elements(g), g->dx[0], D >= 2 ? g->dx[1] : 1.0,
+      D == 3 ? g->dx[2] : 1.0, g->gamma, red, partial);
 }
 
-int update(const adg_grid* g, const double* u, const double* vol, const double* const dbar[3],
+int update(const adg_grid* g, const double* u, const double* vol, const double* fd,
            const double* dt_dev, double* u_out, adg_reduce* red_next, double* partial,
            cudaStream_t st, std::string* err) {
-  for (int a = 0; a < g->dim; ++a)
-    if (!dbar[a]) {
-      *err = "missing face data";
-      return ADG_ERR_INVALID;
-    }
+  if (!fd) {
+    *err = "missing face data";
+    return ADG_ERR_INVALID;
+  }
   if (red_next) zero_reduce_kernel<<<1, 32, 0, st>>>(red_next);
-  ADG_SWITCH_DP(launch_update, g, u, vol, dbar, dt_dev, u_out, red_next, partial, st);
+  ADG_SWITCH_DP(launch_update, g, u, vol, fd, dt_dev, u_out, red_next, partial, st);
   return check_launch(err);
 }
 
@@ -527,9 +665,9 @@ int totals_finalize(const adg_grid* g, const double* partial, int64_t nb, double
   double cv = 1.0;
   for (int j = 0; j < g->dim; ++j) cv *= g->dx[j];
   switch (g->dim) {
-    case 1: totals_finalize_kernel<3><<<1, 96, 0, st>>>(partial, nb, cv, out); break;
-    case 2: totals_finalize_kernel<4><<<1, 128, 0, st>>>(partial, nb, cv, out); break;
-    case 3: totals_finalize_kernel<5><<<1, 160, 0, st>>>(partial, nb, cv, out); break;
+    case 1: totals_finalize_kernel<3><<<1, 1024, 0, st>>>(partial, nb, cv, out); break;
+    case 2: totals_finalize_kernel<4><<<1, 1024, 0, st>>>(partial, nb, cv, out); break;
+    case 3: totals_finalize_kernel<5><<<1, 1024, 0, st>>>(partial, nb, cv, out); break;
     default: *err = "bad dim"; return ADG_ERR_INVALID;
   }
   return check_launch(err);

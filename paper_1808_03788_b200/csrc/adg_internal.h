@@ -12,9 +12,11 @@ namespace adg {
 
 constexpr int kReduceThreads = 256;
 constexpr int64_t kReduceBlocksCap = 4096;  // fixed -> bitwise-reproducible totals
+constexpr int64_t kUpdateBlocksCap = 148 * 8;
 
 int64_t n_elements(const adg_grid* g);
 int64_t reduce_blocks(const adg_grid* g);
+int64_t update_blocks(const adg_grid* g);
 
 size_t predict_workspace_bytes(int dim, int P, int num_sms);
 int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol, int max_iter,
@@ -30,7 +32,7 @@ int advance_time(double* t_dev, const double* dt_dev, double* t_out, cudaStream_
                  std::string* err);
 int face_flux(const adg_grid* g, int axis, const double* traces, const double* ghost_lo,
               const double* ghost_hi, double* dbar, cudaStream_t st, std::string* err);
-int update(const adg_grid* g, const double* u, const double* vol, const double* const dbar[3],
+int update(const adg_grid* g, const double* u, const double* vol, const double* fd,
            const double* dt_dev, double* u_out, adg_reduce* red_next, double* partial,
            cudaStream_t st, std::string* err);
 int totals_finalize(const adg_grid* g, const double* partial, int64_t nblocks, double* out,

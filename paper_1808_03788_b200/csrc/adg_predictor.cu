@@ -8,15 +8,22 @@
 // the SM (shared memory; an L2-resident global slab for the 3-D N>=6
 // tiles that exceed 227 KB).  HBM traffic is u in, vol + traces out.
 //
-// Work decomposition of one Picard sweep (P = N+1 nodes per axis, m vars):
-//  phase 1  "line" role: a thread owns one x-line of the tile at one time
-//           node, evaluates the Euler flux on its P nodes, contracts the
-//           x-flux with D_x in registers, and publishes F_y (F_z) planes;
-//  phase 2  same thread adds the y (z) derivative of its line from the
-//           published planes (lanes sharing a plane read it by broadcast);
-//  phase 3  "node" role: a thread owns one spatial node at all P time
-//           nodes, applies the time operator gw (registers), forms
-//           q_new = dt * gw.rate + g0 u and the residual partials.
+// Shared memory is the bottleneck resource of this kernel (16 doubles per
+// clock per SM; for 64-bit accesses a broadcast does not save wavefronts),
+// so the schedule minimises shared doubles moved per thread.  A Picard
+// sweep (P = N+1 nodes per axis, m quantities) is
+//   A  x-owner (x-line, time t): loads its line of q, F_x on its P nodes,
+//      -D_x F_x in registers;
+//      y-owner (y-line, t): loads its line of q, F_y, D_y F_y -> published
+//      x-line-major;  z-owner (z-line, t): likewise for z.
+//      (each owner recomputes the pointwise flux it needs from q: cheaper
+//      than exchanging flux planes, and A needs no barrier inside)
+//   B  x-owner: rate = ((-D_x F_x) - D_y F_y) - D_z F_z (predictor.py:86-90
+//      order), written in place over its own partial row;
+//   C  node (spatial node, all t): q_new = dt gw.rate + g0 u, residual.
+// Three barriers per sweep.  The startup rates and the volume integral use
+// the same line ownership on the spatial tile.  Every layout was checked with
+// tools/bankcheck.py to be free of bank conflicts at P = 5.
 // Residual norms are reduced per element in a fixed order (bitwise
 // deterministic); an element freezes at its first converged sweep
 // (>= min_iter).  SURVEY.md Appendix A: per-element stopping differs from
@@ -31,34 +38,39 @@ namespace adg {
 template <int D, int P>
 struct PredCfg {
   static constexpr int M = D + 2;
-  static constexpr int PD = ipow(P, D);      // spatial nodes
+  static constexpr int PD = ipow(P, D);      // spatial nodes = threads per element
   static constexpr int PT = PD * P;          // space-time nodes
   static constexpr int TILE = PT * M;        // doubles in one space-time tile
-  // flux planes exchanged between line threads: F_y (D>=2) and F_z (D=3),
-  // stored with the contraction index fastest and padded to an even count
-  // so a thread reads two nodes per 128-bit shared load
-  static constexpr int NF = (D == 3) ? 2 : (D == 2 ? 1 : 0);
-  static constexpr int PL = P + (P & 1);
-  static constexpr int PLANE = PD * M * PL;  // doubles per exchanged flux buffer
-  static constexpr int FREG_A = NF * PLANE;
-  static constexpr int FREG_B = D * PD * M;
-  static constexpr int FREG_AB = FREG_A > FREG_B ? FREG_A : FREG_B;
-  static constexpr int FREG = FREG_AB > TILE ? FREG_AB : TILE;  // also holds the rate
-  static constexpr int TILE_PAD = TILE + (TILE & 1);   // keeps F 16-byte aligned
-  static constexpr int ELEM = TILE_PAD + FREG + (FREG & 1);   // doubles per element slab
+  static constexpr int TILE_PAD = TILE + (TILE & 1);
+  static constexpr int NBUF = D == 3 ? 3 : 2;   // Q + partial buffers
+  static constexpr int SPAT = D * PD * M;        // per-direction spatial pieces
+  static constexpr int RSZ0 = TILE > SPAT ? TILE : SPAT;
+  static constexpr int RSZ = RSZ0 + (RSZ0 & 1);  // region size (even: 16-B aligned)
+  static constexpr int ELEM = NBUF * RSZ;        // doubles per element
   static constexpr int BUDGET = 110 * 1024;  // bytes of tiles per CTA (>= 2 CTAs/SM)
   static constexpr int EPB_T = (256 / PD) > 0 ? (256 / PD) : 1;
   static constexpr int EPB_S = (BUDGET / (ELEM * 8)) > 0 ? (BUDGET / (ELEM * 8)) : 1;
   static constexpr int EPB = EPB_T < EPB_S ? EPB_T : EPB_S;
   static constexpr int NT = ((EPB * PD + 31) / 32) * 32;
   static constexpr int NW = NT / 32;
-  // small shared data: scaled D (3 P^2), reduction partials (2 NT), flags
-  static constexpr int SMALL_DBL = ((3 * P * P + 2 * NT + 1) / 2) * 2;
+  // the residual partials of a lone 3-D element live in its z-partial buffer
+  // (dead during the reduction), so the C2 tile (3 x 25 KB) + D/dx fits
+  // three CTAs per SM
+  static constexpr bool RED_IN_TILE = (NBUF == 3 && EPB == 1 && 2 * NT <= RSZ);
+  static constexpr int SMALL_DBL = ((3 * P * P + (RED_IN_TILE ? 0 : 2 * NT) + 1) / 2) * 2;
   static constexpr int FLAGS = 5 * EPB + 1;
   static constexpr size_t SMALL_BYTES = SMALL_DBL * 8 + ((FLAGS * 4 + 15) / 16) * 16;
   static constexpr size_t TILE_BYTES = (size_t)EPB * ELEM * 8;
   static constexpr bool SMEM_TILES = (SMALL_BYTES + TILE_BYTES) <= 220 * 1024;
   static constexpr size_t SMEM_BYTES = SMALL_BYTES + (SMEM_TILES ? TILE_BYTES : 0);
+  // resident CTAs per SM the shared footprint allows (228 KB, 1 KB reserved
+  // per CTA); passed to __launch_bounds__ so registers do not become the limit
+  static constexpr int MINB0 = (int)((228 * 1024) / (SMEM_BYTES + 1024));
+  static constexpr int MINB_R = (65536 / (128 * NT)) > 0 ? 65536 / (128 * NT) : 1;  // >= 128 regs
+  static constexpr int MINB1 = MINB0 < MINB_R ? MINB0 : MINB_R;
+  static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > 3 ? 3 : MINB1);
+  // spatial line tasks (startup / volume): D directions x P^(D-1) lines
+  static constexpr int NTASK = D * (PD / P);
 };
 
 struct PredArgs {
@@ -78,12 +90,6 @@ struct PredArgs {
   int min_iter;
 };
 
-// index of a space-time tile value: [node][t][v]
-template <int P, int M>
-__device__ __forceinline__ int qi(int node, int t, int v) {
-  return (node * P + t) * M + v;
-}
-
 // spatial node index from per-axis indices (row-major, last axis fastest)
 template <int D, int P>
 __device__ __forceinline__ int node3(int i, int j, int k) {
@@ -91,58 +97,94 @@ __device__ __forceinline__ int node3(int i, int j, int k) {
   if (D == 2) return i * P + j;
   return i;
 }
-
-// exchanged flux planes: F_y plane (i, k, t) and F_z plane (i, j, t), each
-// holding v-rows of PL contiguous values along the contraction axis
+// x-line index (== the x-owner's item); y/z partial rows are x-line-major
 template <int D, int P>
-__device__ __forceinline__ int fy_idx(int i, int k, int t, int v) {
-  constexpr int M = D + 2, PL = P + (P & 1);
-  return D == 3 ? (((i * P + k) * P + t) * M + v) * PL : ((i * P + t) * M + v) * PL;
-}
-template <int P>
-__device__ __forceinline__ int fz_idx(int i, int j, int t, int v) {
-  constexpr int M = 5, PL = P + (P & 1);
-  return (((i * P + j) * P + t) * M + v) * PL;
+__device__ __forceinline__ int xline(int j, int k, int t) {
+  return D == 3 ? t + P * k + P * P * j : (D == 2 ? t + P * j : t);
 }
 
-// L(w) = -sum_j (D/dx_j) F_j(w) at one node from published per-node fluxes
-// F[(dir*PD + node)*M + v]; accumulated x then y then z (predictor.py:86-90).
-template <int D, int P>
-__device__ __forceinline__ void node_rate(const double* __restrict__ F, const double* Ds, int i,
-                                          int j, int k, double out[D + 2]) {
+// Contract one direction of a spatial (single time level) field held
+// node-major in shared memory: out[node] = sum_l W[row(node)][l] X[line node l].
+// Executed as line tasks: task -> (dir, line); the line's P states are loaded,
+// transformed pointwise by `pre` (flux of the state, or identity), contracted
+// with the P x P matrix W_dir and written node-major into part[dir].
+// Used for the two startup rates (predictor.py:99-126) and the volume
+// integral's stiffness contraction (corrector.py:169-176).
+template <int D, int P, int MODE, int DIR>
+__device__ __forceinline__ void spatial_line_task(const double* __restrict__ X,
+                                                  double* __restrict__ part,
+                                                  const double* __restrict__ W, double gm1,
+                                                  int line) {
+  // MODE 0: X = states [node][v], pre = flux along DIR, W = D/dx (all dirs)
+  // MODE 1: X = per-direction rows X[dir][node][v], W = stiffness (shared)
   using C = PredCfg<D, P>;
   constexpr int M = C::M, PD = C::PD;
+  const int ta = D == 3 ? line / P : line;
+  const int tb = D == 3 ? line % P : 0;
+  double x[P][M];
 #pragma unroll
-  for (int v = 0; v < M; ++v) out[v] = 0.0;
+  for (int l = 0; l < P; ++l) {
+    const int nd = DIR == 0 ? node3<D, P>(l, ta, tb)
+                            : (DIR == 1 ? node3<D, P>(ta, l, tb) : node3<D, P>(ta, tb, l));
+    if (MODE == 0) {
+      double q[M];
 #pragma unroll
-  for (int dir = 0; dir < D; ++dir) {
-    const int row = dir == 0 ? i : (dir == 1 ? j : k);
-    double acc[M];
+      for (int v = 0; v < M; ++v) q[v] = X[nd * M + v];
+      flux_axis<D>(q, gm1, DIR, x[l]);
+    } else {
 #pragma unroll
-    for (int v = 0; v < M; ++v) acc[v] = 0.0;
+      for (int v = 0; v < M; ++v) x[l][v] = X[(DIR * PD + nd) * M + v];
+    }
+  }
+  const double* Wd = MODE == 0 ? W + DIR * P * P : W;
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    double y[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) y[v] = 0.0;
 #pragma unroll
     for (int l = 0; l < P; ++l) {
-      const int nd = dir == 0 ? node3<D, P>(l, j, k)
-                              : (dir == 1 ? node3<D, P>(i, l, k) : node3<D, P>(i, j, l));
-      const double dl = Ds[dir * P * P + row * P + l];
+      const double d = Wd[i * P + l];
 #pragma unroll
-      for (int v = 0; v < M; ++v) acc[v] = fma(dl, F[(dir * PD + nd) * M + v], acc[v]);
+      for (int v = 0; v < M; ++v) y[v] = fma(d, x[l][v], y[v]);
     }
+    const int nd = DIR == 0 ? node3<D, P>(i, ta, tb)
+                            : (DIR == 1 ? node3<D, P>(ta, i, tb) : node3<D, P>(ta, tb, i));
 #pragma unroll
-    for (int v = 0; v < M; ++v) out[v] -= acc[v];
+    for (int v = 0; v < M; ++v) part[(DIR * PD + nd) * M + v] = y[v];
+  }
+}
+
+// Contract each direction of a spatial (single time level) field held
+// node-major in shared memory, as D x P^(D-1) line tasks spread over the
+// element's threads; used for the two startup rates (predictor.py:99-126)
+// and the volume integral's stiffness contraction (corrector.py:169-176).
+template <int D, int P, int MODE>
+__device__ __forceinline__ void spatial_line_tasks(const double* __restrict__ X,
+                                                   double* __restrict__ part,
+                                                   const double* __restrict__ W, double gm1,
+                                                   int item) {
+  using C = PredCfg<D, P>;
+  constexpr int PD = C::PD, PF = PD / P;
+  for (int task = item; task < C::NTASK; task += PD) {
+    const int dir = task / PF;
+    const int line = task - dir * PF;
+    if (dir == 0) spatial_line_task<D, P, MODE, 0>(X, part, W, gm1, line);
+    if (D >= 2 && dir == 1) spatial_line_task<D, P, MODE, (D >= 2 ? 1 : 0)>(X, part, W, gm1, line);
+    if (D == 3 && dir == 2) spatial_line_task<D, P, MODE, (D == 3 ? 2 : 0)>(X, part, W, gm1, line);
   }
 }
 
 template <int D, int P>
-__global__ void __launch_bounds__(PredCfg<D, P>::NT)
+__global__ void __launch_bounds__(PredCfg<D, P>::NT, PredCfg<D, P>::MINB)
 predict_kernel(PredArgs a) {
   using C = PredCfg<D, P>;
-  constexpr int M = C::M, PD = C::PD, TILE = C::TILE, EPB = C::EPB, NT = C::NT;
+  constexpr int M = C::M, PD = C::PD, EPB = C::EPB, NT = C::NT, LS = P * M;
+  constexpr int TP = C::RSZ;
   const DegreeTables& T = tab<P>();
   extern __shared__ __align__(16) double smem[];
   double* Ds = smem;                          // [3][P][P] D / dx_dir
-  double* red = Ds + 3 * P * P;               // [NT][2]
-  int* fl = reinterpret_cast<int*>(red + 2 * NT);
+  int* fl = reinterpret_cast<int*>(Ds + 3 * P * P + (C::RED_IN_TILE ? 0 : 2 * NT));
   int* frozen = fl;                           // [EPB]
   int* conv = fl + EPB;                       // [EPB]
   int* nsw = fl + 2 * EPB;                    // [EPB]
@@ -155,11 +197,17 @@ predict_kernel(PredArgs a) {
   } else {
     tiles = a.ws + (size_t)blockIdx.x * EPB * C::ELEM;
   }
+  // [NT][2] residual partials
+  double* red = C::RED_IN_TILE ? tiles + 2 * C::RSZ : Ds + 3 * P * P;
 
   const int tid = threadIdx.x;
-  const int el = tid / PD;
-  const int item = tid - el * PD;
-  const bool lane_ok = el < EPB;
+  // padding lanes (tid >= EPB*PD) shadow the last item of the last element:
+  // they execute the same instructions on the same data (duplicate stores of
+  // identical values are benign), so no branch diverges inside a warp; they
+  // only contribute zeros to the residual reduction
+  const bool lane_ok = tid < EPB * PD;
+  const int el = lane_ok ? tid / PD : EPB - 1;
+  const int item = lane_ok ? tid - el * PD : PD - 1;
   const double gm1 = a.gamma - 1.0;
   const double dt = *a.dt;
   const int max_iter = a.max_iter;
@@ -169,24 +217,31 @@ predict_kernel(PredArgs a) {
     const double h = dir == 0 ? a.dx[0] : (dir == 1 ? a.dx[1] : a.dx[2]);
     Ds[x] = T.diff[x - dir * P * P] / h;
   }
+  const double* Dx = Ds;
+  const double* Dy = Ds + P * P;
+  const double* Dz = Ds + 2 * P * P;
 
-  // node-role coordinates
+  // role coordinates; item is the owned line / node in every role
   const int ni = (D == 3) ? item / (P * P) : (D == 2 ? item / P : item);
   const int nj = (D == 3) ? (item / P) % P : (D == 2 ? item % P : 0);
   const int nk = (D == 3) ? item % P : 0;
-  // line-role coordinates: x-line (la, lb) at time lt, la fastest so that
-  // the P lanes reading one F_y plane (same lb, lt) sit in one warp and the
-  // shared loads broadcast
-  const int la = (D >= 2) ? item % P : 0;
-  const int lb = (D == 3) ? (item / P) % P : 0;
-  const int lt = (D == 3) ? item / (P * P) : (D == 2 ? item / P : item);
+  const int xt = item % P;                                            // x: [j][k][t]
+  const int xk = (D == 3) ? (item / P) % P : 0;
+  const int xj = (D == 3) ? item / (P * P) : (D == 2 ? item / P : 0);
+  const int yi = item % P;                                            // y: [k][t][i]
+  const int yt = (D == 3) ? (item / P) % P : item / P;
+  const int yk = (D == 3) ? item / (P * P) : 0;
+  const int zj = item % P;                                            // z: [t][i][j]
+  const int zi = (item / P) % P;
+  const int zt = item / (P * P);
 
   const int64_t ngroups = (a.n_elem + EPB - 1) / EPB;
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     const int64_t e = g * EPB + el;
-    const bool valid = lane_ok && e < a.n_elem;
-    double* Q = tiles + (lane_ok ? el : 0) * C::ELEM;
-    double* F = Q + C::TILE_PAD;
+    const bool valid = e < a.n_elem;
+    double* Q = tiles + el * C::ELEM;
+    double* B1 = Q + TP;       // y partials / rate (x-line-major); startup+volume scratch
+    double* B2 = Q + 2 * TP;   // z partials (D == 3)
     __syncthreads();  // Ds ready / previous group finished with the tiles
     if (tid < EPB) {
       const bool ve = g * EPB + tid < a.n_elem;
@@ -198,51 +253,55 @@ predict_kernel(PredArgs a) {
     }
     if (tid == 0) *all_frozen = 0;
 
-    // ---------------- startup guess (node role) ----------------------
+    // ---------------- startup guess --------------------------------------
+    // k = L(w) = ((-D_x F_x) - D_y F_y) - D_z F_z at the spatial nodes,
+    // w = u (k1) then u + dt k1 (k2); states staged node-major in Q[:PD*M]
+    double* W0 = Q;                 // staged states [node][v]
+    double* PA = B1;                // per-direction pieces [dir][node][v]
     double uu[M];
     double k1[M];
+    double k2[M];
     if (valid) {
       const double* ue = a.u + (size_t)e * PD * M + (size_t)item * M;
 #pragma unroll
-      for (int v = 0; v < M; ++v) uu[v] = ue[v];
-      double f[D][M];
-      flux_all<D>(uu, gm1, f);
-#pragma unroll
-      for (int dir = 0; dir < D; ++dir)
-#pragma unroll
-        for (int v = 0; v < M; ++v) F[(dir * PD + item) * M + v] = f[dir][v];
-    }
-    __syncthreads();
-    if (valid) node_rate<D, P>(F, Ds, ni, nj, nk, k1);
-    double k2[M];
-    if (P >= 3) {
-      __syncthreads();
-      if (valid) {
-        double w[M];
-#pragma unroll
-        for (int v = 0; v < M; ++v) w[v] = uu[v] + dt * k1[v];
-        double f[D][M];
-        flux_all<D>(w, gm1, f);
-#pragma unroll
-        for (int dir = 0; dir < D; ++dir)
-#pragma unroll
-          for (int v = 0; v < M; ++v) F[(dir * PD + item) * M + v] = f[dir][v];
+      for (int v = 0; v < M; ++v) {
+        uu[v] = ue[v];
+        W0[item * M + v] = uu[v];
       }
-      __syncthreads();
-      if (valid) node_rate<D, P>(F, Ds, ni, nj, nk, k2);
     }
+#pragma unroll
+    for (int pass = 0; pass < (P >= 3 ? 2 : 1); ++pass) {
+      __syncthreads();
+      if (valid) spatial_line_tasks<D, P, 0>(W0, PA, Ds, gm1, item);
+      __syncthreads();
+      double* kk = pass == 0 ? k1 : k2;
+      if (valid) {
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          double r = 0.0;
+#pragma unroll
+          for (int dir = 0; dir < D; ++dir) r -= PA[(dir * PD + item) * M + v];
+          kk[v] = r;
+        }
+        if (pass == 0) {
+#pragma unroll
+          for (int v = 0; v < M; ++v) W0[item * M + v] = uu[v] + dt * k1[v];
+        }
+      }
+    }
+    __syncthreads();   // W0 (inside Q) is about to be overwritten
     if (valid) {
 #pragma unroll
       for (int t = 0; t < P; ++t) {
         const double s = T.nodes[t] * dt;
         if (P <= 2) {
 #pragma unroll
-          for (int v = 0; v < M; ++v) Q[qi<P, M>(item, t, v)] = uu[v] + s * k1[v];
+          for (int v = 0; v < M; ++v) Q[item * LS + t * M + v] = uu[v] + s * k1[v];
         } else {
           const double c2 = 0.5 * s * s / dt;
 #pragma unroll
           for (int v = 0; v < M; ++v)
-            Q[qi<P, M>(item, t, v)] = uu[v] + s * k1[v] + c2 * (k2[v] - k1[v]);
+            Q[item * LS + t * M + v] = uu[v] + s * k1[v] + c2 * (k2[v] - k1[v]);
         }
       }
     }
@@ -254,104 +313,111 @@ predict_kernel(PredArgs a) {
       if (*all_frozen) break;
       const bool work = valid && !frozen[el];
       double rate[P][M];
-      // phase 1: line role, x contraction in registers, publish F_y/F_z
+      // A: x-owner (registers) + y/z-owners (published partials)
       if (work) {
-        double ql[P][M];
+        {
+          double fx[P][M];
 #pragma unroll
-        for (int l = 0; l < P; ++l)
+          for (int l = 0; l < P; ++l) {
+            double q[M];
 #pragma unroll
-          for (int v = 0; v < M; ++v) ql[l][v] = Q[qi<P, M>(node3<D, P>(l, la, lb), lt, v)];
-#pragma unroll
-        for (int i = 0; i < P; ++i)
-#pragma unroll
-          for (int v = 0; v < M; ++v) rate[i][v] = 0.0;
-#pragma unroll
-        for (int l = 0; l < P; ++l) {
-          double f[D][M];
-          flux_all<D>(ql[l], gm1, f);
+            for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(l, xj, xk) * LS + xt * M + v];
+            flux_axis<D>(q, gm1, 0, fx[l]);
+          }
 #pragma unroll
           for (int i = 0; i < P; ++i) {
-            const double dil = Ds[i * P + l];
+            double y[M];
 #pragma unroll
-            for (int v = 0; v < M; ++v) rate[i][v] = fma(dil, f[0][v], rate[i][v]);
-          }
-          // F_y at node (l, la, lb, lt) -> plane (i=l, k=lb, t=lt), slot j=la
-          if (D >= 2) {
+            for (int v = 0; v < M; ++v) y[v] = 0.0;
 #pragma unroll
-            for (int v = 0; v < M; ++v) F[fy_idx<D, P>(l, lb, lt, v) + la] = f[1][v];
-          }
-          // F_z -> plane (i=l, j=la, t=lt), slot k=lb
-          if (D == 3) {
+            for (int l = 0; l < P; ++l) {
+              const double d = Dx[i * P + l];
 #pragma unroll
-            for (int v = 0; v < M; ++v) F[C::PLANE + fz_idx<P>(l, la, lt, v) + lb] = f[2][v];
+              for (int v = 0; v < M; ++v) y[v] = fma(d, fx[l][v], y[v]);
+            }
+#pragma unroll
+            for (int v = 0; v < M; ++v) rate[i][v] = -y[v];
           }
         }
+        if (D >= 2) {
+          double fy[P][M];
 #pragma unroll
-        for (int i = 0; i < P; ++i)
+          for (int l = 0; l < P; ++l) {
+            double q[M];
 #pragma unroll
-          for (int v = 0; v < M; ++v) rate[i][v] = -rate[i][v];
+            for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(yi, l, yk) * LS + yt * M + v];
+            flux_axis<D>(q, gm1, 1, fy[l]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < P; ++jj) {
+            double y[M];
+#pragma unroll
+            for (int v = 0; v < M; ++v) y[v] = 0.0;
+#pragma unroll
+            for (int l = 0; l < P; ++l) {
+              const double d = Dy[jj * P + l];
+#pragma unroll
+              for (int v = 0; v < M; ++v) y[v] = fma(d, fy[l][v], y[v]);
+            }
+#pragma unroll
+            for (int v = 0; v < M; ++v) B1[xline<D, P>(jj, yk, yt) * LS + yi * M + v] = y[v];
+          }
+        }
+        if (D == 3) {
+          double fz[P][M];
+#pragma unroll
+          for (int l = 0; l < P; ++l) {
+            double q[M];
+#pragma unroll
+            for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(zi, zj, l) * LS + zt * M + v];
+            flux_axis<D>(q, gm1, 2, fz[l]);
+          }
+#pragma unroll
+          for (int kk = 0; kk < P; ++kk) {
+            double y[M];
+#pragma unroll
+            for (int v = 0; v < M; ++v) y[v] = 0.0;
+#pragma unroll
+            for (int l = 0; l < P; ++l) {
+              const double d = Dz[kk * P + l];
+#pragma unroll
+              for (int v = 0; v < M; ++v) y[v] = fma(d, fz[l][v], y[v]);
+            }
+#pragma unroll
+            for (int v = 0; v < M; ++v) B2[xline<D, P>(zj, kk, zt) * LS + zi * M + v] = y[v];
+          }
+        }
       }
-      if (D >= 2) {
-        __syncthreads();
-        // phase 2: y (and z) derivatives of the owned line; the P lanes of a
-        // warp that share a plane read it by broadcast, two nodes per load
-        if (work) {
-          double dr[C::PL];
-#pragma unroll
-          for (int l = 0; l < C::PL; ++l) dr[l] = l < P ? Ds[P * P + la * P + l] : 0.0;
+      if (D >= 2) __syncthreads();
+      // B: x-owner completes its rate in place (x-line-major rows of B1)
+      if (work) {
+        if (D >= 2) {
 #pragma unroll
           for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int v = 0; v < M; ++v) {
-              const double2* row =
-                  reinterpret_cast<const double2*>(F + fy_idx<D, P>(i, lb, lt, v));
-              double s = 0.0;
-#pragma unroll
-              for (int l2 = 0; l2 < C::PL / 2; ++l2) {
-                const double2 fv = row[l2];
-                s = fma(dr[2 * l2], fv.x, s);
-                if (2 * l2 + 1 < P) s = fma(dr[2 * l2 + 1], fv.y, s);
-              }
-              rate[i][v] -= s;
-            }
-          if (D == 3) {
-#pragma unroll
-            for (int l = 0; l < C::PL; ++l) dr[l] = l < P ? Ds[2 * P * P + lb * P + l] : 0.0;
-#pragma unroll
-            for (int i = 0; i < P; ++i)
-#pragma unroll
-              for (int v = 0; v < M; ++v) {
-                const double2* row =
-                    reinterpret_cast<const double2*>(F + C::PLANE + fz_idx<P>(i, la, lt, v));
-                double s = 0.0;
-#pragma unroll
-                for (int l2 = 0; l2 < C::PL / 2; ++l2) {
-                  const double2 fv = row[l2];
-                  s = fma(dr[2 * l2], fv.x, s);
-                  if (2 * l2 + 1 < P) s = fma(dr[2 * l2 + 1], fv.y, s);
-                }
-                rate[i][v] -= s;
-              }
-          }
+            for (int v = 0; v < M; ++v) rate[i][v] -= B1[item * LS + i * M + v];
         }
-      }
-      __syncthreads();
-      // phase 2b: publish the rate (reuses the F_y plane)
-      if (work) {
+        if (D == 3) {
+#pragma unroll
+          for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int v = 0; v < M; ++v) rate[i][v] -= B2[item * LS + i * M + v];
+        }
 #pragma unroll
         for (int i = 0; i < P; ++i)
 #pragma unroll
-          for (int v = 0; v < M; ++v) F[qi<P, M>(node3<D, P>(i, la, lb), lt, v)] = rate[i][v];
+          for (int v = 0; v < M; ++v) B1[item * LS + i * M + v] = rate[i][v];
       }
       __syncthreads();
-      // phase 3: node role, time operator + residual
+      // C: node role, time operator + residual; rate(node, s) sits in the
+      // x-line-major row of (nj, nk, s) at slot ni
       double sd = 0.0, sq = 0.0;
       if (work) {
         double r[P][M];
 #pragma unroll
         for (int s = 0; s < P; ++s)
 #pragma unroll
-          for (int v = 0; v < M; ++v) r[s][v] = F[qi<P, M>(item, s, v)];
+          for (int v = 0; v < M; ++v) r[s][v] = B1[xline<D, P>(nj, nk, s) * LS + ni * M + v];
 #pragma unroll
         for (int t = 0; t < P; ++t) {
           const double g0 = T.g0[t];
@@ -361,15 +427,15 @@ predict_kernel(PredArgs a) {
 #pragma unroll
             for (int s = 0; s < P; ++s) c = fma(T.gw[t * P + s], r[s][v], c);
             const double qn = c * dt + g0 * uu[v];
-            const double dq = Q[qi<P, M>(item, t, v)] - qn;
+            const double dq = Q[item * LS + t * M + v] - qn;
             sd = fma(dq, dq, sd);
             sq = fma(qn, qn, sq);
-            Q[qi<P, M>(item, t, v)] = qn;
+            Q[item * LS + t * M + v] = qn;
           }
         }
       }
-      red[2 * tid] = sd;
-      red[2 * tid + 1] = sq;
+      red[2 * tid] = lane_ok ? sd : 0.0;
+      red[2 * tid + 1] = lane_ok ? sq : 0.0;
       __syncthreads();
       // per-element fixed-order reduction; warp w handles elements w, w+NW, ..
       {
@@ -404,60 +470,10 @@ predict_kernel(PredArgs a) {
       __syncthreads();
     }
 
-    // ---------------- admissibility of the converged tile --------------
+    // ---------------- admissibility, traces, volume flux sums ----------
+    double fb[D][M];   // fbar_dir = sum_t w_t F_dir(q_t) (corrector.py:171)
     if (valid) {
       bool ok = true;
-#pragma unroll
-      for (int t = 0; t < P; ++t) {
-        double q[M];
-#pragma unroll
-        for (int v = 0; v < M; ++v) q[v] = Q[qi<P, M>(item, t, v)];
-        ok = ok && admissible<D>(q, gm1);
-      }
-      if (!ok) okf[el] = 0;
-    }
-
-    // ---------------- traces (line role) ------------------------------
-    if (valid) {
-      const size_t face_stride = (size_t)a.n_elem * PD * M;
-      const size_t eoff = (size_t)e * PD * M;
-      const int tang = (D == 3) ? (la * P + lb) : (D == 2 ? la : 0);
-#pragma unroll
-      for (int dir = 0; dir < D; ++dir) {
-        double lo[M], hi[M];
-#pragma unroll
-        for (int v = 0; v < M; ++v) lo[v] = hi[v] = 0.0;
-#pragma unroll
-        for (int l = 0; l < P; ++l) {
-          const int nd = dir == 0 ? node3<D, P>(l, la, lb)
-                                  : (dir == 1 ? node3<D, P>(la, l, lb) : node3<D, P>(la, lb, l));
-          const double pl = T.left[l], pr = T.right[l];
-#pragma unroll
-          for (int v = 0; v < M; ++v) {
-            const double qv = Q[qi<P, M>(nd, lt, v)];
-            lo[v] = fma(pl, qv, lo[v]);
-            hi[v] = fma(pr, qv, hi[v]);
-          }
-        }
-        double* tlo = a.traces + (size_t)(2 * dir) * face_stride + eoff + (size_t)(tang * P + lt) * M;
-        double* thi = tlo + face_stride;
-#pragma unroll
-        for (int v = 0; v < M; ++v) {
-          tlo[v] = lo[v];
-          thi[v] = hi[v];
-        }
-      }
-      if (a.q_out) {
-        double* qo = a.q_out + (size_t)e * TILE + (size_t)item * P * M;
-#pragma unroll
-        for (int x = 0; x < P * M; ++x) qo[x] = Q[item * P * M + x];
-      }
-    }
-    // ---------------- volume integral (node role) ----------------------
-    // fbar_j = sum_t w_t F_j(q_t) (corrector.py:171), published per node
-    __syncthreads();  // F region free (rate no longer needed)
-    if (valid) {
-      double fb[D][M];
 #pragma unroll
       for (int dir = 0; dir < D; ++dir)
 #pragma unroll
@@ -466,7 +482,8 @@ predict_kernel(PredArgs a) {
       for (int t = 0; t < P; ++t) {
         double q[M];
 #pragma unroll
-        for (int v = 0; v < M; ++v) q[v] = Q[qi<P, M>(item, t, v)];
+        for (int v = 0; v < M; ++v) q[v] = Q[item * LS + t * M + v];
+        ok = ok && admissible<D>(q, gm1);
         double f[D][M];
         flux_all<D>(q, gm1, f);
         const double wt = T.weights[t];
@@ -475,16 +492,57 @@ predict_kernel(PredArgs a) {
 #pragma unroll
           for (int v = 0; v < M; ++v) fb[dir][v] = fma(wt, f[dir][v], fb[dir][v]);
       }
+      if (!ok) okf[el] = 0;
+      // traces: each owner role writes its own line's face states at block
+      // offset item*m (x: [j][k][t], y: [k][t][i], z: [t][i][j])
+      const size_t face_stride = (size_t)a.n_elem * PD * M;
+      const size_t eoff = (size_t)e * PD * M + (size_t)item * M;
+#pragma unroll
+      for (int dir = 0; dir < D; ++dir) {
+        double lo[M], hi[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) lo[v] = hi[v] = 0.0;
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+          const int q0 = dir == 0 ? node3<D, P>(l, xj, xk) * LS + xt * M
+                                  : (dir == 1 ? node3<D, P>(yi, l, yk) * LS + yt * M
+                                              : node3<D, P>(zi, zj, l) * LS + zt * M);
+          const double pl = T.left[l], pr = T.right[l];
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            const double qv = Q[q0 + v];
+            lo[v] = fma(pl, qv, lo[v]);
+            hi[v] = fma(pr, qv, hi[v]);
+          }
+        }
+        double* tlo = a.traces + (size_t)(2 * dir) * face_stride + eoff;
+        double* thi = tlo + face_stride;
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          tlo[v] = lo[v];
+          thi[v] = hi[v];
+        }
+      }
+      if (a.q_out) {
+        double* qo = a.q_out + (size_t)e * C::TILE + (size_t)item * LS;
+#pragma unroll
+        for (int x = 0; x < LS; ++x) qo[x] = Q[item * LS + x];
+      }
+      // publish fbar node-major for the stiffness line tasks
 #pragma unroll
       for (int dir = 0; dir < D; ++dir)
 #pragma unroll
-        for (int v = 0; v < M; ++v) F[(dir * PD + item) * M + v] = fb[dir][v];
+        for (int v = 0; v < M; ++v) B1[(dir * PD + item) * M + v] = fb[dir][v];
     }
+    __syncthreads();
+    // volume: contrib_dir = stiff x_dir fbar_dir (corrector.py:172-174)
+    if (valid) spatial_line_tasks<D, P, 1>(B1, Q, T.stiff, gm1, item);
     __syncthreads();
     if (valid) {
       const double cv = a.dx[0] * (D >= 2 ? a.dx[1] : 1.0) * (D == 3 ? a.dx[2] : 1.0);
       const double wnode = T.weights[ni] * (D >= 2 ? T.weights[nj] : 1.0) *
                            (D == 3 ? T.weights[nk] : 1.0);
+      const double* CB = Q;
       double acc[M];
 #pragma unroll
       for (int v = 0; v < M; ++v) acc[v] = 0.0;
@@ -492,19 +550,8 @@ predict_kernel(PredArgs a) {
       for (int dir = 0; dir < D; ++dir) {
         const int row = dir == 0 ? ni : (dir == 1 ? nj : nk);
         const double coef = (dt * cv / a.dx[dir]) * (wnode / T.weights[row]);
-        double c[M];
 #pragma unroll
-        for (int v = 0; v < M; ++v) c[v] = 0.0;
-#pragma unroll
-        for (int l = 0; l < P; ++l) {
-          const int nd = dir == 0 ? node3<D, P>(l, nj, nk)
-                                  : (dir == 1 ? node3<D, P>(ni, l, nk) : node3<D, P>(ni, nj, l));
-          const double sl = T.stiff[row * P + l];
-#pragma unroll
-          for (int v = 0; v < M; ++v) c[v] = fma(sl, F[(dir * PD + nd) * M + v], c[v]);
-        }
-#pragma unroll
-        for (int v = 0; v < M; ++v) acc[v] += coef * c[v];
+        for (int v = 0; v < M; ++v) acc[v] += coef * CB[(dir * PD + item) * M + v];
       }
       double* vo = a.vol + (size_t)e * PD * M + (size_t)item * M;
 #pragma unroll

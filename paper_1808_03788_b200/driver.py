@@ -87,13 +87,9 @@ class StepBuffers:
         f64 = dict(dtype=torch.float64, device=device)
         self.vol = torch.empty(n_elem * pd * m, **f64)
         self.traces = torch.empty(2 * dim * n_elem * pd * m, **f64)
-        self.dbar = []
+        # element-major face terms [E][dim][2 sides][P^(d-1)][m] (adg_face_flux)
         p = round(pd ** (1.0 / dim))
-        for a in range(dim):
-            nf = 1
-            for j in range(dim):
-                nf *= cells[j] + (1 if j == a else 0)
-            self.dbar.append(torch.empty(nf * (pd // p) * m, **f64))
+        self.fd = torch.empty(n_elem * 2 * dim * (pd // p) * m, **f64)
         self.pred_bad = torch.empty(n_elem, dtype=torch.uint8, device=device)
         self.sweeps = torch.empty(n_elem, dtype=torch.int32, device=device)
         self.red = torch.zeros(2, _lib.REDUCE_WORDS, dtype=torch.int64, device=device)
@@ -269,15 +265,14 @@ class Simulation:
             glo = self._ghost.get((a, 0))
             ghi = self._ghost.get((a, 1))
             self._h.call("adg_face_flux", self._gp(), a, _ptr(buf.traces), _ptr(glo),
-                         _ptr(ghi), _ptr(buf.dbar[a]), _stream_ptr())
+                         _ptr(ghi), _ptr(buf.fd), _stream_ptr())
 
     def _update(self, dt_dev, totals_dst):
         buf = self._buf
         nxt = 1 - (self._red_cur or 0)
-        db = [_ptr(buf.dbar[a]) if a < self.mesh.dim else None for a in range(3)]
-        self._h.call("adg_update", self._gp(), _ptr(self._u), _ptr(buf.vol), db[0], db[1],
-                     db[2], _ptr(dt_dev), _ptr(self._u_next), _ptr(buf.red[nxt]),
-                     _ptr(buf.partial), _stream_ptr())
+        self._h.call("adg_update", self._gp(), _ptr(self._u), _ptr(buf.vol), _ptr(buf.fd),
+                     _ptr(dt_dev), _ptr(self._u_next), _ptr(buf.red[nxt]), _ptr(buf.partial),
+                     _stream_ptr())
         if totals_dst is not None:
             self._h.call("adg_totals_finalize", self._gp(), _ptr(buf.partial), buf.nblocks,
                          _ptr(totals_dst), _stream_ptr())

@@ -68,10 +68,18 @@ def run_predictor(u, system, spacings, dt, tables, tol=1e-12, max_iter=None, min
            mi, int(min_iter), q.data_ptr() if q is not None else None, vol.data_ptr(),
            traces.data_ptr(), bad.data_ptr(), sweeps.data_ptr(),
            torch.cuda.current_stream().cuda_stream)
+    # the kernel writes each face's trace block in its owner role's order
+    # (x: [j][k][t], y: [k][t][i], z: [t][i][j]; 2-D y: [t][i]); present them
+    # in the reference layout (tangential axes ascending, then t, then m)
+    perms = {3: {0: (0, 1, 2), 1: (2, 0, 1), 2: (1, 2, 0)}, 2: {0: (0, 1), 1: (1, 0)},
+             1: {0: (0,)}}[d]
+    nc = len(cells)
     tr = {}
     for j in range(d):
         for s in (0, 1):
-            tr[(j, s)] = traces[2 * j + s].view(cells + (P,) * (d - 1) + (P, m))
+            blk = traces[2 * j + s].view(cells + (P,) * d + (m,))
+            order = tuple(range(nc)) + tuple(nc + p for p in perms[j]) + (nc + d,)
+            tr[(j, s)] = blk.permute(order).contiguous()
     ok_conv = bad == 0
     return PredictorResult(q=q, iterations=int(sweeps.max().item()), converged=None,
                            admissible=None, sweeps=sweeps, traces=tr, volume=vol,
