@@ -40,7 +40,11 @@ def local_mesh(global_mesh, world, rank):
     x0, x1 = global_mesh.extents[0]
     dx = (x1 - x0) / global_mesh.cells[0]
     ext = [(x0 + lo * dx, x0 + hi * dx)] + list(global_mesh.extents[1:])
-    return CartesianMesh(ext, (hi - lo,) + tuple(global_mesh.cells[1:]))
+    mesh = CartesianMesh(ext, (hi - lo,) + tuple(global_mesh.cells[1:]))
+    # the slab's element widths are the global ones bit for bit (recomputing
+    # them from the slab extents can differ by an ulp)
+    mesh.spacings = tuple(global_mesh.spacings)
+    return mesh
 
 
 def exchange_planes(send_lo, send_hi, recv_lo, recv_hi, group=None):
@@ -123,7 +127,9 @@ class SlabSimulation(Simulation):
 
     def _combine_rows(self, rows):
         if self.world > 1:
-            dist.all_reduce(rows[:, 2:], op=dist.ReduceOp.SUM, group=self.group)
+            tot = rows[:, 2:].contiguous()   # collectives need dense tensors
+            dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=self.group)
+            rows[:, 2:] = tot
 
     def _state_finite(self):
         if self.world > 1:

@@ -1,0 +1,84 @@
+"""Slab decomposition on one GPU, sequentially (no cross-waiting kernels):
+K slab Simulations exchange their x-trace planes by device copies and
+combine their wave-speed records exactly as decomp.SlabSimulation does over
+NCCL.  The assembled state must equal the single-domain run bitwise (same
+per-element arithmetic, identical dt)."""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_inprocess(pkg, gmesh, system, degree, cfl, u0, steps, nslabs):
+    from paper_1808_03788_b200.decomp import local_mesh
+    from paper_1808_03788_b200.driver import Simulation
+
+    sims = []
+    P = degree + 1
+    for r in range(nslabs):
+        mesh = local_mesh(gmesh, nslabs, r)
+        plane = int(np.prod(mesh.cells[1:])) * P ** mesh.dim * system.n_vars
+        ghost = {(0, 0): torch.empty(plane, dtype=torch.float64, device="cuda"),
+                 (0, 1): torch.empty(plane, dtype=torch.float64, device="cuda")}
+        sim = Simulation(mesh, system, degree, cfl, _ghost=ghost)
+        k = mesh.cells[0]
+        sim.set_state(u0[r * k:(r + 1) * k])   # the global projection, sliced
+        sims.append(sim)
+    m = system.n_vars
+    dts = []
+    for _ in range(steps):
+        for sim in sims:
+            if sim._red_cur is None:
+                sim._wavespeed()
+        reds = torch.stack([sim._buf.red[sim._red_cur] for sim in sims])
+        comb = reds[0].clone()
+        comb[0:3] = reds[:, 0:3].amax(dim=0)     # decomp.combine_reduce semantics
+        comb[3:5] = reds[:, 3:5].sum(dim=0)
+        rows = []
+        for sim in sims:
+            sim._buf.red[sim._red_cur].copy_(comb)
+            row = torch.zeros(2 + m, dtype=torch.float64, device="cuda")
+            st = torch.zeros(1, dtype=torch.int32, device="cuda")
+            sim._timestep_into(row[0:1], st, math.inf)
+            sim._predict(row[0:1])
+            rows.append(row)
+        for r, sim in enumerate(sims):
+            n = sim._ghost[(0, 0)].numel()
+            face = sim.mesh.n_elements * sim._pd * m
+            lo = sim._buf.traces[0:n]
+            hi = sim._buf.traces[2 * face - n:2 * face]
+            sims[(r - 1) % nslabs]._ghost[(0, 1)].copy_(lo)
+            sims[(r + 1) % nslabs]._ghost[(0, 0)].copy_(hi)
+        for sim, row in zip(sims, rows):
+            sim._faces()
+            nxt = sim._update(row[0:1], None)
+            sim._u, sim._u_next = sim._u_next, sim._u
+            sim._red_cur = nxt
+        dts.append(float(rows[0][0].item()))
+    return torch.cat([s.u for s in sims], dim=0), dts
+
+
+@pytest.mark.parametrize("nslabs,cells,degree", [(2, (4, 3, 2), 3), (4, (8, 2, 2), 4),
+                                                 (2, (6, 4), 5)])
+def test_slabs_equal_single_domain(nslabs, cells, degree):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1808_03788_b200 as pkg
+
+    d = len(cells)
+    gmesh = pkg.CartesianMesh([(0.0, float(nslabs))] + [(0.0, 1.0)] * (d - 1), cells)
+    system = pkg.make_system("euler", d)
+    cfl = 0.9 / (d * (2 * degree + 1))
+    ic, _ = pkg.build_problem("density_wave", system, velocity=[1.0, -0.5, 0.3][:d])
+    ref = pkg.Simulation(gmesh, system, degree, cfl)
+    ref.project_initial_condition(ic)
+    u0 = ref.u.clone()
+    ref.run(np.inf, max_steps=3)
+    u, dts = _run_inprocess(pkg, gmesh, system, degree, cfl, u0, 3, nslabs)
+    np.testing.assert_array_equal(dts, [h["dt"] for h in ref.history])
+    assert torch.equal(u, ref.u)
