@@ -112,7 +112,9 @@ int adg_advance_time(adg_handle* h, double* t_dev, const double* dt_dev, double*
  *           at its first converged sweep >= min_iter
  * q_out   : optional [E, P^d, P_t, m] space-time predictor (NULL to skip)
  * vol_out : [E, P^d, m] volume accumulator (true integral)
- * traces  : [d][2][E, P^(d-1), P_t, m] face traces (side 0 = low face)
+ * traces  : [d][2][E][adg_trace_block(g)] face traces (side 0 = low
+ *           face); the block holds P^(d-1) x P_t x m values ordered per
+ *           axis x: [j][k][t][v], y: [k][t][i][v], z: [t][i][j][v]
  * pred_bad: [E] uint8, !(converged && admissible)   (driver.py:212)
  * sweeps  : [E] int32 Picard sweeps taken                                 */
 int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double* dt_dev,
@@ -143,6 +145,10 @@ int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* 
                const double* fd, const double* dt_dev, double* u_out, adg_reduce* red_next,
                double* totals_partial, void* stream);
 int64_t adg_update_blocks(const adg_grid* g);
+/* doubles per element trace block: P^d m rounded up to even (16-byte
+ * multiple, so the face kernel moves each block with one TMA bulk copy);
+ * traces are [d][2][E][adg_trace_block(g)], ghost planes likewise */
+int64_t adg_trace_block(const adg_grid* g);
 /* totals[m] = cell_volume * fixed-order sum of the partials */
 int adg_totals_finalize(adg_handle* h, const adg_grid* g, const double* totals_partial,
                         int64_t nblocks, double* totals_out, void* stream);

@@ -27,7 +27,7 @@ STATUS_NONFINITE = 2
 EXPORTS = (
     "adg_create", "adg_destroy", "adg_last_error", "adg_version", "adg_set_tables",
     "adg_wavespeed", "adg_timestep", "adg_advance_time", "adg_predict", "adg_face_flux", "adg_update",
-    "adg_update_blocks", "adg_totals_finalize", "adg_totals", "adg_project_subcells",
+    "adg_update_blocks", "adg_trace_block", "adg_totals_finalize", "adg_totals", "adg_project_subcells",
     "adg_detect", "adg_rescue", "adg_flatten_ic",
 )
 
@@ -64,6 +64,7 @@ _SIGS = {
     "adg_face_flux": (_I, [_P, _P, _I, _P, _P, _P, _P, _P]),
     "adg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "adg_update_blocks": (_I64, [_P]),
+    "adg_trace_block": (_I64, [_P]),
     "adg_totals_finalize": (_I, [_P, _P, _P, _I64, _P, _P]),
     "adg_totals": (_I, [_P, _P, _P, _P, _P, _P]),
     "adg_project_subcells": (_I, [_P, _P, _P, _P, _P, _P, _P]),

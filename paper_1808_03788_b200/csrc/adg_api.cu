@@ -174,6 +174,13 @@ int adg_face_flux(adg_handle* h, const adg_grid* g, int axis, const double* trac
 
 int64_t adg_update_blocks(const adg_grid* g) { return adg::update_blocks(g); }
 
+int64_t adg_trace_block(const adg_grid* g) {
+  int64_t pd = 1;
+  for (int j = 0; j < g->dim; ++j) pd *= g->degree + 1;
+  const int64_t b = pd * (g->dim + 2);
+  return b + (b & 1);
+}
+
 int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
                const double* fd, const double* dt_dev, double* u_out, adg_reduce* red_next,
                double* totals_partial, void* stream) {

@@ -108,6 +108,29 @@ __device__ __forceinline__ double max_abs_eig(const double* q, double gamma, dou
   return fabs(un / q[0]) + sqrt(gamma * p / q[0]);
 }
 
+// Flux along axis a AND the max |eigenvalue| of the same state, sharing one
+// reciprocal of rho and one pressure (face kernel: corrector.py:58-62 +
+// systems.py:140-178).  Quotients become products with the Newton-refined
+// reciprocal (<= 1 ulp), so lam may differ from the reference's in the last
+// bit; it only scales the Rusanov dissipation.
+template <int D>
+__device__ __forceinline__ double flux_eig_axis(const double* q, double gamma, double gm1, int a,
+                                                double f[D + 2]) {
+  const double r = rcp_nr(q[0]);
+  double kin = q[1] * q[1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
+  const double p = gm1 * (q[D + 1] - 0.5 * kin * r);
+  const double ep = q[D + 1] + p;
+  const double va = q[1 + a] * r;
+  f[0] = q[1 + a];
+#pragma unroll
+  for (int i = 0; i < D; ++i) f[1 + i] = q[1 + i] * va;
+  f[1 + a] += p;
+  f[D + 1] = ep * va;
+  return fabs(va) + sqrt(gamma * p * r);
+}
+
 // systems.py:225-229: all finite, rho > 0, p > 0.
 template <int D>
 __device__ __forceinline__ bool admissible(const double* q, double gm1) {

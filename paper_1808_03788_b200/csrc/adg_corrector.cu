@@ -194,129 +194,183 @@ __global__ void advance_time_kernel(double* t, const double* dt, double* t_out) 
 }
 
 // -------------------------------------------------------------------------
-// Face coupling.  Thread per (face, tangential node); loops over the P time
-// nodes and integrates sum_t w_t d_low(t) (corrector.py:186).
+// Face coupling, streamed with TMA bulk copies.  A persistent block walks
+// chunks of FB consecutive faces of one axis; for every face the minus-side
+// and plus-side trace blocks (one element block each, padded to a 16-byte
+// multiple) are fetched by lanes of warp 0 with cp.async.bulk into a
+// double-buffered stage, and a thread per (face, tangential node) integrates
+// sum_t w_t d_low(t) (corrector.py:100-129, :186) from shared memory.  The
+// result is written element-major for both adjacent elements (coalesced).
+// Face states follow driver._face_states/_ghost_trace (driver.py:234-261):
+// periodic wrap, outflow copy, wall reflection, or caller ghost traces.
+template <int D, int P>
+struct FaceCfg {
+  static constexpr int M = D + 2;
+  static constexpr int PD = ipow(P, D);
+  static constexpr int PF = PD / P;                  // tangential nodes per face
+  static constexpr int TB = PD * M + ((PD * M) & 1); // trace element block (doubles)
+  static constexpr int FB = (128 / PF) > 0 ? (128 / PF) : 1;
+  static constexpr int NT = ((FB * PF + 31) / 32) * 32 < 64 ? 64 : ((FB * PF + 31) / 32) * 32;
+  static constexpr int STAGE = 2 * FB * TB;
+  // one stage per block: the kernel is latency bound, so four resident
+  // blocks (16 warps) per SM beat in-block double buffering
+  static constexpr int NSTAGE = 1;
+  static constexpr size_t SMEM = (size_t)NSTAGE * STAGE * 8;
+};
+
 template <int D, int P, int AX>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(FaceCfg<D, P>::NT)
 face_kernel(const double* __restrict__ traces, const double* __restrict__ ghost_lo,
-            const double* __restrict__ ghost_hi, double* __restrict__ dbar,
-            int64_t c0, int64_t c1, int64_t c2, int bc_lo, int bc_hi, double gamma) {
-  constexpr int axis = AX;  // compile-time: keeps the state arrays in registers
-  constexpr int M = D + 2;
-  constexpr int PD = ipow(P, D);
-  constexpr int PF = PD / P;  // tangential nodes per face
+            const double* __restrict__ ghost_hi, double* __restrict__ fd, int64_t c0,
+            int64_t c1, int64_t c2, int bc_lo, int bc_hi, double gamma) {
+  using C = FaceCfg<D, P>;
+  constexpr int axis = AX;
+  constexpr int M = C::M, PF = C::PF, TB = C::TB, FB = C::FB, STAGE = C::STAGE;
+  extern __shared__ __align__(128) double fsm[];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int s_ref[2][FB][2];           // wall reflection of minus / plus state
+  __shared__ int64_t s_dst[2][FB][2];       // element receiving the face as high / low face
   const DegreeTables& T = tab<P>();
   const double gm1 = gamma - 1.0;
-  int64_t n[3] = {c0, c1, c2};
+  const int tid = threadIdx.x;
+  const int64_t n[3] = {c0, c1, c2};
   int64_t nf[3] = {c0, c1, c2};
   nf[axis] += 1;
   const int64_t faces = nf[0] * (D >= 2 ? nf[1] : 1) * (D == 3 ? nf[2] : 1);
   const int64_t E = n[0] * (D >= 2 ? n[1] : 1) * (D == 3 ? n[2] : 1);
-  const size_t fstride = (size_t)E * PD * M;
+  const size_t fstride = (size_t)E * TB;
   const double* tr_lo = traces + (size_t)(2 * axis) * fstride;
   const double* tr_hi = tr_lo + fstride;
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < faces * PF;
-       x += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = x / PF;
-    const int tg = (int)(x - f * PF);
-    int64_t c[3] = {0, 0, 0};
-    {
-      int64_t r = f;
+  const int64_t nchunks = (faces + FB - 1) / FB;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // warp 0: lane 2f + side fetches the minus (side 0) / plus (side 1) state
+  // block of face f of chunk c into stage stg
+  auto issue = [&](int stg, int64_t c) {
+    const int64_t f0 = c * FB;
+    const int nfb = (int)((faces - f0) < FB ? (faces - f0) : FB);
+    if (tid == 0) mbar_expect_tx(&bar[stg], (uint32_t)(2 * nfb * TB * 8));
+    __syncwarp();
+    for (int lane = tid; lane < 2 * nfb; lane += 32) {
+      const int f = lane >> 1, side = lane & 1;
+      int64_t cc[3] = {0, 0, 0};
+      int64_t r = f0 + f;
       for (int j = D - 1; j >= 0; --j) {
-        c[j] = r % nf[j];
+        cc[j] = r % nf[j];
         r /= nf[j];
       }
-    }
-    const int64_t ca = c[axis];
-    auto elem = [&](int64_t caxis) {
-      int64_t cc[3] = {c[0], c[1], c[2]};
-      cc[axis] = caxis;
-      int64_t e = 0;
-      for (int j = 0; j < D; ++j) e = e * n[j] + cc[j];
-      return e;
-    };
-    auto plane = [&]() {  // index within the boundary plane (axis removed)
-      int64_t e = 0;
+      const int64_t ca = cc[axis];
+      auto elem = [&](int64_t caxis) {
+        int64_t e = 0;
+        for (int j = 0; j < D; ++j) e = e * n[j] + (j == axis ? caxis : cc[j]);
+        return e;
+      };
+      int64_t plane = 0;
       for (int j = 0; j < D; ++j)
-        if (j != axis) e = e * n[j] + c[j];
-      return e;
-    };
-    // minus state source (low side), plus state source (high side)
-    const double* pm;
-    const double* pp;
-    bool reflect_m = false, reflect_p = false;
-    if (ca == 0) {
-      if (bc_lo == ADG_BC_PERIODIC) pm = tr_hi + (size_t)elem(n[axis] - 1) * PD * M;
-      else if (bc_lo == ADG_BC_GHOST) pm = ghost_lo + (size_t)plane() * PD * M;
-      else {
-        pm = tr_lo + (size_t)elem(0) * PD * M;
-        reflect_m = bc_lo == ADG_BC_WALL;
+        if (j != axis) plane = plane * n[j] + cc[j];
+      const double* src;
+      int refl = 0;
+      if (side == 0) {   // minus state: high trace of the low-side element
+        if (ca == 0) {
+          if (bc_lo == ADG_BC_PERIODIC) src = tr_hi + (size_t)elem(n[axis] - 1) * TB;
+          else if (bc_lo == ADG_BC_GHOST) src = ghost_lo + (size_t)plane * TB;
+          else { src = tr_lo + (size_t)elem(0) * TB; refl = bc_lo == ADG_BC_WALL; }
+        } else {
+          src = tr_hi + (size_t)elem(ca - 1) * TB;
+        }
+        s_dst[stg][f][0] = ca >= 1 ? elem(ca - 1) : -1;
+      } else {           // plus state: low trace of the high-side element
+        if (ca == n[axis]) {
+          if (bc_hi == ADG_BC_PERIODIC) src = tr_lo + (size_t)elem(0) * TB;
+          else if (bc_hi == ADG_BC_GHOST) src = ghost_hi + (size_t)plane * TB;
+          else { src = tr_hi + (size_t)elem(n[axis] - 1) * TB; refl = bc_hi == ADG_BC_WALL; }
+        } else {
+          src = tr_lo + (size_t)elem(ca) * TB;
+        }
+        s_dst[stg][f][1] = ca < n[axis] ? elem(ca) : -1;
       }
-    } else {
-      pm = tr_hi + (size_t)elem(ca - 1) * PD * M;
+      s_ref[stg][f][side] = refl;
+      bulk_g2s(fsm + stg * STAGE + (size_t)lane * TB, src, TB * 8, &bar[stg]);
     }
-    if (ca == n[axis]) {
-      if (bc_hi == ADG_BC_PERIODIC) pp = tr_lo + (size_t)elem(0) * PD * M;
-      else if (bc_hi == ADG_BC_GHOST) pp = ghost_hi + (size_t)plane() * PD * M;
-      else {
-        pp = tr_hi + (size_t)elem(n[axis] - 1) * PD * M;
-        reflect_p = bc_hi == ADG_BC_WALL;
+  };
+
+  uint32_t phase[2] = {0u, 0u};
+  int64_t c = blockIdx.x;
+  if (tid < 32 && c < nchunks) issue(0, c);
+  __syncthreads();
+  // element-face trace blocks are written by the predictor's owner roles:
+  // x faces [j][k][t], y faces [k][t][i], z faces [t][i][j] (2-D: x [j][t],
+  // y [t][i]); (ta, tb) are the ascending tangential indices
+  constexpr int SA = D == 3 ? (AX == 0 ? P * P : (AX == 1 ? 1 : P)) : (D == 2 ? (AX == 0 ? P : 1) : 0);
+  constexpr int SB = D == 3 ? (AX == 0 ? P : (AX == 1 ? P * P : 1)) : 0;
+  constexpr int ST = D == 3 ? (AX == 0 ? 1 : (AX == 1 ? P : P * P)) : (D == 2 ? (AX == 0 ? 1 : P) : 1);
+  for (int i = 0; c < nchunks; ++i, c += gridDim.x) {
+    const int stg = C::NSTAGE == 2 ? (i & 1) : 0;
+    const int64_t cn = c + gridDim.x;
+    if (C::NSTAGE == 2 && tid < 32 && cn < nchunks) issue(stg ^ 1, cn);
+    if (C::NSTAGE == 1 && i > 0) {
+      if (tid < 32) issue(0, c);
+      __syncthreads();
+    }
+    mbar_wait(&bar[stg], phase[stg]);
+    phase[stg] ^= 1u;
+    const int64_t f0 = c * FB;
+    const int nfb = (int)((faces - f0) < FB ? (faces - f0) : FB);
+    if (tid < nfb * PF) {
+      const int f = tid / PF, tg = tid - f * PF;
+      const int ta = D == 3 ? tg / P : tg;
+      const int tb = D == 3 ? tg % P : 0;
+      const int base = ta * SA + tb * SB;
+      const double* pm = fsm + stg * STAGE + (size_t)(2 * f) * TB + base * M;
+      const double* pp = pm + TB;
+      const bool rm = s_ref[stg][f][0], rp = s_ref[stg][f][1];
+      double acc[M];
+#pragma unroll
+      for (int v = 0; v < M; ++v) acc[v] = 0.0;
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        double qm[M], qp[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          qm[v] = pm[t * ST * M + v];
+          qp[v] = pp[t * ST * M + v];
+        }
+        if (rm) qm[1 + axis] = -qm[1 + axis];   // systems.py:231-234
+        if (rp) qp[1 + axis] = -qp[1 + axis];
+        double fm[M], fp[M];
+        const double s = fmax(flux_eig_axis<D>(qm, gamma, gm1, axis, fm),
+                              flux_eig_axis<D>(qp, gamma, gm1, axis, fp));
+        const double hs = 0.5 * s;
+        const double wt = T.weights[t];
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          const double central = 0.5 * (fm[v] + fp[v]);
+          const double dlow = (central + 0.0) - hs * (qp[v] - qm[v]);
+          acc[v] = fma(wt, dlow, acc[v]);
+        }
       }
-    } else {
-      pp = tr_lo + (size_t)elem(ca) * PD * M;
-    }
-    // element-face trace blocks are written by the predictor's owner roles:
-    // x faces [j][k][t], y faces [k][t][i], z faces [t][i][j] (2-D: x [j][t],
-    // y [t][i]); (ta, tb) are the ascending tangential indices
-    constexpr int SA = D == 3 ? (AX == 0 ? P * P : (AX == 1 ? 1 : P)) : (D == 2 ? (AX == 0 ? P : 1) : 0);
-    constexpr int SB = D == 3 ? (AX == 0 ? P : (AX == 1 ? P * P : 1)) : 0;
-    constexpr int ST = D == 3 ? (AX == 0 ? 1 : (AX == 1 ? P : P * P)) : (D == 2 ? (AX == 0 ? 1 : P) : 1);
-    const int ta = D == 3 ? tg / P : tg;
-    const int tb = D == 3 ? tg % P : 0;
-    const int base = ta * SA + tb * SB;
-    pm += (size_t)base * M;
-    pp += (size_t)base * M;
-    double acc[M];
+      // element-major face terms fd[E][D][2 sides][P^(d-1)][m]: the face is
+      // the high face of its low-side element and the low face of its
+      // high-side element (periodic: face n_a repeats face 0)
+      constexpr size_t FBLK = (size_t)PF * M;
+      const int64_t eL = s_dst[stg][f][0], eR = s_dst[stg][f][1];
+      if (eL >= 0) {
+        double* o = fd + ((size_t)eL * (2 * D) + 2 * axis + 1) * FBLK + (size_t)tg * M;
 #pragma unroll
-    for (int v = 0; v < M; ++v) acc[v] = 0.0;
-#pragma unroll
-    for (int t = 0; t < P; ++t) {
-      double qm[M], qp[M];
-#pragma unroll
-      for (int v = 0; v < M; ++v) {
-        qm[v] = pm[t * ST * M + v];
-        qp[v] = pp[t * ST * M + v];
+        for (int v = 0; v < M; ++v) o[v] = acc[v];
       }
-      if (reflect_m) qm[1 + axis] = -qm[1 + axis];   // systems.py:231-234
-      if (reflect_p) qp[1 + axis] = -qp[1 + axis];
-      const double s = fmax(max_abs_eig<D>(qm, gamma, gm1, axis),
-                            max_abs_eig<D>(qp, gamma, gm1, axis));
-      double fm[M], fp[M];
-      flux_axis<D>(qm, gm1, axis, fm);
-      flux_axis<D>(qp, gm1, axis, fp);
-      const double hs = 0.5 * s;
-      const double wt = T.weights[t];
+      if (eR >= 0) {
+        double* o = fd + ((size_t)eR * (2 * D) + 2 * axis) * FBLK + (size_t)tg * M;
 #pragma unroll
-      for (int v = 0; v < M; ++v) {
-        const double central = 0.5 * (fm[v] + fp[v]);
-        const double dlow = (central + 0.0) - hs * (qp[v] - qm[v]);
-        acc[v] = fma(wt, dlow, acc[v]);
+        for (int v = 0; v < M; ++v) o[v] = acc[v];
       }
     }
-    // element-major face terms fd[E][D][2 sides][P^(d-1)][m]: the face is the
-    // high face of its low-side element and the low face of its high-side
-    // element (periodic: face n_a repeats face 0, each element written once)
-    constexpr size_t FBLK = (size_t)PF * M;
-    if (ca >= 1) {
-      double* o = dbar + ((size_t)elem(ca - 1) * (2 * D) + 2 * axis + 1) * FBLK + (size_t)tg * M;
-#pragma unroll
-      for (int v = 0; v < M; ++v) o[v] = acc[v];
-    }
-    if (ca < n[axis]) {
-      double* o = dbar + ((size_t)elem(ca) * (2 * D) + 2 * axis) * FBLK + (size_t)tg * M;
-#pragma unroll
-      for (int v = 0; v < M; ++v) o[v] = acc[v];
-    }
+    __syncthreads();   // stage and face metadata free for the next prefetch
   }
 }
 
@@ -603,19 +657,25 @@ int advance_time(double* t_dev, const double* dt_dev, double* t_out, cudaStream_
 
 template <int D, int P>
 static void launch_face(const adg_grid* g, int axis, const double* traces, const double* glo,
-                        const double* ghi, double* dbar, cudaStream_t st) {
+                        const double* ghi, double* fd, cudaStream_t st) {
+  using C = FaceCfg<D, P>;
   int64_t nf[3] = {g->cells[0], g->cells[1], g->cells[2]};
   nf[axis] += 1;
   int64_t faces = 1;
   for (int j = 0; j < D; ++j) faces *= nf[j];
-  const int64_t work = faces * (ipow(P, D) / P);
-  const int64_t blocks = std::min<int64_t>((work + 255) / 256, 1 << 20);
+  const int64_t chunks = (faces + C::FB - 1) / C::FB;
   auto kern = axis == 0 ? face_kernel<D, P, 0>
                         : (axis == 1 ? face_kernel<D, P, (D > 1 ? 1 : 0)>
                                      : face_kernel<D, P, (D > 2 ? 2 : 0)>);
-  kern<<<(unsigned)blocks, 256, 0, st>>>(
-      traces, glo, ghi, dbar, g->cells[0], D >= 2 ? g->cells[1] : 1,
-      D == 3 ? g->cells[2] : 1, g->bc[axis][0], g->bc[axis][1], g->gamma);
+  static bool attr[3] = {false, false, false};
+  if (!attr[axis]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr[axis] = true;
+  }
+  const int64_t blocks = std::min<int64_t>(chunks, 148 * 8);
+  kern<<<(unsigned)blocks, C::NT, C::SMEM, st>>>(
+      traces, glo, ghi, fd, g->cells[0], D >= 2 ? g->cells[1] : 1, D == 3 ? g->cells[2] : 1,
+      g->bc[axis][0], g->bc[axis][1], g->gamma);
 }
 
 int face_flux(const adg_grid* g, int axis, const double* traces, const double* ghost_lo,

@@ -495,8 +495,10 @@ predict_kernel(PredArgs a) {
       if (!ok) okf[el] = 0;
       // traces: each owner role writes its own line's face states at block
       // offset item*m (x: [j][k][t], y: [k][t][i], z: [t][i][j])
-      const size_t face_stride = (size_t)a.n_elem * PD * M;
-      const size_t eoff = (size_t)e * PD * M + (size_t)item * M;
+      // element trace blocks padded to a 16-byte multiple (TMA in the face kernel)
+      constexpr int TB = PD * M + ((PD * M) & 1);
+      const size_t face_stride = (size_t)a.n_elem * TB;
+      const size_t eoff = (size_t)e * TB + (size_t)item * M;
 #pragma unroll
       for (int dir = 0; dir < D; ++dir) {
         double lo[M], hi[M];

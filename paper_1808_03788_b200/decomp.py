@@ -100,7 +100,8 @@ class SlabSimulation(Simulation):
             plane = 1
             for c in mesh.cells[1:]:
                 plane *= c
-            n = plane * P ** mesh.dim * system.n_vars
+            blk = P ** mesh.dim * system.n_vars
+            n = plane * (blk + (blk & 1))   # trace blocks are padded (adg_trace_block)
             dev = kw.get("device")
             dev = torch.device("cuda", torch.cuda.current_device() if dev is None else int(dev))
             ghost = {(0, 0): torch.empty(n, dtype=torch.float64, device=dev),
@@ -112,7 +113,7 @@ class SlabSimulation(Simulation):
     def _swap_halos(self):
         buf = self._buf
         n = self._ghost[(0, 0)].numel()
-        face = self.mesh.n_elements * self._pd * self._m
+        face = self.mesh.n_elements * buf.tb
         lo_plane = buf.traces[0:n]                       # axis 0, side 0, first layer
         hi_plane = buf.traces[2 * face - n:2 * face]     # axis 0, side 1, last layer
         exchange_planes(lo_plane, hi_plane, self._ghost[(0, 0)], self._ghost[(0, 1)],

@@ -86,7 +86,9 @@ class StepBuffers:
     def __init__(self, grid, n_elem, pd, m, dim, device, cells, limiter=False):
         f64 = dict(dtype=torch.float64, device=device)
         self.vol = torch.empty(n_elem * pd * m, **f64)
-        self.traces = torch.empty(2 * dim * n_elem * pd * m, **f64)
+        # trace element blocks padded to a 16-byte multiple (adg_trace_block)
+        self.tb = int(_lib.load().adg_trace_block(_lib.ctypes.byref(grid)))
+        self.traces = torch.empty(2 * dim * n_elem * self.tb, **f64)
         # element-major face terms [E][dim][2 sides][P^(d-1)][m] (adg_face_flux)
         p = round(pd ** (1.0 / dim))
         self.fd = torch.empty(n_elem * 2 * dim * (pd // p) * m, **f64)

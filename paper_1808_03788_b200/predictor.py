@@ -59,7 +59,8 @@ def run_predictor(u, system, spacings, dt, tables, tol=1e-12, max_iter=None, min
     f64 = dict(dtype=torch.float64, device=dev)
     q = torch.empty(cells + (P,) * d + (P, m), **f64) if want_q else None
     vol = torch.empty(u.shape, **f64)
-    traces = torch.empty(2 * d, E * pd * m, **f64)
+    tb = pd * m + ((pd * m) & 1)   # padded trace element block (adg_trace_block)
+    traces = torch.empty(2 * d, E, tb, **f64)
     bad = torch.empty(cells, dtype=torch.uint8, device=dev)
     sweeps = torch.empty(cells, dtype=torch.int32, device=dev)
     dt_dev = torch.full((1,), float(dt), **f64)
@@ -77,7 +78,7 @@ def run_predictor(u, system, spacings, dt, tables, tol=1e-12, max_iter=None, min
     tr = {}
     for j in range(d):
         for s in (0, 1):
-            blk = traces[2 * j + s].view(cells + (P,) * d + (m,))
+            blk = traces[2 * j + s][:, :pd * m].reshape(cells + (P,) * d + (m,))
             order = tuple(range(nc)) + tuple(nc + p for p in perms[j]) + (nc + d,)
             tr[(j, s)] = blk.permute(order).contiguous()
     ok_conv = bad == 0

@@ -22,7 +22,8 @@ def _run_inprocess(pkg, gmesh, system, degree, cfl, u0, steps, nslabs):
     P = degree + 1
     for r in range(nslabs):
         mesh = local_mesh(gmesh, nslabs, r)
-        plane = int(np.prod(mesh.cells[1:])) * P ** mesh.dim * system.n_vars
+        blk = P ** mesh.dim * system.n_vars
+        plane = int(np.prod(mesh.cells[1:])) * (blk + (blk & 1))
         ghost = {(0, 0): torch.empty(plane, dtype=torch.float64, device="cuda"),
                  (0, 1): torch.empty(plane, dtype=torch.float64, device="cuda")}
         sim = Simulation(mesh, system, degree, cfl, _ghost=ghost)
@@ -49,7 +50,7 @@ def _run_inprocess(pkg, gmesh, system, degree, cfl, u0, steps, nslabs):
             rows.append(row)
         for r, sim in enumerate(sims):
             n = sim._ghost[(0, 0)].numel()
-            face = sim.mesh.n_elements * sim._pd * m
+            face = sim.mesh.n_elements * sim._buf.tb
             lo = sim._buf.traces[0:n]
             hi = sim._buf.traces[2 * face - n:2 * face]
             sims[(r - 1) % nslabs]._ghost[(0, 1)].copy_(lo)
