@@ -42,7 +42,11 @@ struct PredCfg {
   static constexpr int PT = PD * P;          // space-time nodes
   static constexpr int TILE = PT * M;        // doubles in one space-time tile
   static constexpr int TILE_PAD = TILE + (TILE & 1);
-  static constexpr int NBUF = D == 3 ? 3 : 2;   // Q + partial buffers
+  // 3-D tiles from N=5 up exchange the y and z partials one after the other
+  // through a single buffer, so N=5/6 tiles fit two CTAs and N=6 one CTA of
+  // shared memory (instead of the L2 slab); N<=4 keeps both in flight
+  static constexpr bool SEQ_YZ = (D == 3 && P >= 6);
+  static constexpr int NBUF = D == 3 ? (SEQ_YZ ? 2 : 3) : 2;   // Q + partial buffers
   static constexpr int SPAT = D * PD * M;        // per-direction spatial pieces
   static constexpr int RSZ0 = TILE > SPAT ? TILE : SPAT;
   static constexpr int RSZ = RSZ0 + (RSZ0 & 1);  // region size (even: 16-B aligned)
@@ -313,6 +317,31 @@ predict_kernel(PredArgs a) {
       if (*all_frozen) break;
       const bool work = valid && !frozen[el];
       double rate[P][M];
+      // z-owner: own z-line -> D_z partials, x-line-major rows of dst
+      auto zpass = [&](double* dst) {
+          double fz[P][M];
+#pragma unroll
+          for (int l = 0; l < P; ++l) {
+            double q[M];
+#pragma unroll
+            for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(zi, zj, l) * LS + zt * M + v];
+            flux_axis<D>(q, gm1, 2, fz[l]);
+          }
+#pragma unroll
+          for (int kk = 0; kk < P; ++kk) {
+            double y[M];
+#pragma unroll
+            for (int v = 0; v < M; ++v) y[v] = 0.0;
+#pragma unroll
+            for (int l = 0; l < P; ++l) {
+              const double d = Dz[kk * P + l];
+#pragma unroll
+              for (int v = 0; v < M; ++v) y[v] = fma(d, fz[l][v], y[v]);
+            }
+#pragma unroll
+            for (int v = 0; v < M; ++v) dst[xline<D, P>(zj, kk, zt) * LS + zi * M + v] = y[v];
+          }
+      };
       // A: x-owner (registers) + y/z-owners (published partials)
       if (work) {
         {
@@ -363,45 +392,35 @@ predict_kernel(PredArgs a) {
             for (int v = 0; v < M; ++v) B1[xline<D, P>(jj, yk, yt) * LS + yi * M + v] = y[v];
           }
         }
-        if (D == 3) {
-          double fz[P][M];
-#pragma unroll
-          for (int l = 0; l < P; ++l) {
-            double q[M];
-#pragma unroll
-            for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(zi, zj, l) * LS + zt * M + v];
-            flux_axis<D>(q, gm1, 2, fz[l]);
-          }
-#pragma unroll
-          for (int kk = 0; kk < P; ++kk) {
-            double y[M];
-#pragma unroll
-            for (int v = 0; v < M; ++v) y[v] = 0.0;
-#pragma unroll
-            for (int l = 0; l < P; ++l) {
-              const double d = Dz[kk * P + l];
-#pragma unroll
-              for (int v = 0; v < M; ++v) y[v] = fma(d, fz[l][v], y[v]);
-            }
-#pragma unroll
-            for (int v = 0; v < M; ++v) B2[xline<D, P>(zj, kk, zt) * LS + zi * M + v] = y[v];
-          }
-        }
+        if (D == 3 && !C::SEQ_YZ) zpass(B2);
       }
       if (D >= 2) __syncthreads();
+      if (C::SEQ_YZ) {
+        // y partials consumed, then the z partials take the same buffer
+        if (work) {
+#pragma unroll
+          for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int v = 0; v < M; ++v) rate[i][v] -= B1[item * LS + i * M + v];
+        }
+        __syncthreads();
+        if (work) zpass(B1);
+        __syncthreads();
+      }
       // B: x-owner completes its rate in place (x-line-major rows of B1)
       if (work) {
-        if (D >= 2) {
+        if (D >= 2 && !C::SEQ_YZ) {
 #pragma unroll
           for (int i = 0; i < P; ++i)
 #pragma unroll
             for (int v = 0; v < M; ++v) rate[i][v] -= B1[item * LS + i * M + v];
         }
         if (D == 3) {
+          const double* PZ = C::SEQ_YZ ? B1 : B2;
 #pragma unroll
           for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int v = 0; v < M; ++v) rate[i][v] -= B2[item * LS + i * M + v];
+            for (int v = 0; v < M; ++v) rate[i][v] -= PZ[item * LS + i * M + v];
         }
 #pragma unroll
         for (int i = 0; i < P; ++i)

@@ -1,0 +1,92 @@
+#!/usr/bin/env python
+"""Throughput of every BASELINE config shape on one B200 (supplement to
+bench.py, whose single JSON line is C2).  Prints one JSON object per case:
+
+  C1  2-D vortex 32^2, N=3, 10 steps
+  C2  3-D density wave 64^3, N=4, 20 steps
+  C3  3-D density wave 32^3, N=2..9, 10 steps each
+  C4  2-D circular explosion 512^2, N=5, limiter, first K steps (--c4-steps)
+
+DOF-updates/s = E (N+1)^d steps / t, t from CUDA events around
+Simulation.run (the bench-tdu scope, cli.py:79-91), after 2 warm-up steps.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_1808_03788_b200 as pkg  # noqa: E402
+from paper_1808_03788_b200 import roofline  # noqa: E402
+
+
+def run_case(name, ext, cells, degree, cfl, problem, steps, boundary="periodic",
+             limiter=False, warmup=2, t_end=np.inf):
+    d = len(cells)
+    system = pkg.make_system("euler", d)
+    sim = pkg.Simulation(pkg.CartesianMesh(ext, cells), system, degree, cfl,
+                         boundary=boundary, use_limiter=limiter)
+    sim.project_initial_condition(pkg.build_problem(problem, system)[0])
+    sim.run(t_end, max_steps=warmup)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    a.record()
+    sim.run(t_end, max_steps=warmup + steps)
+    b.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    ms = a.elapsed_time(b)
+    n = sim.step_count - warmup
+    dofs = sim.mesh.n_elements * (degree + 1) ** d * n
+    sweeps = [s for s in sim.sweep_log[warmup:] if s is not None]
+    out = {"case": name, "cells": list(cells), "degree": degree, "steps": n,
+           "ms_per_step": ms / n, "dof_per_s": dofs / (ms * 1e-3),
+           "wall_dof_per_s": dofs / wall, "picard_sweeps_max": max(sweeps) if sweeps else None}
+    if limiter:
+        fr = [h["limited_fraction"] for h in sim.history[warmup:]]
+        out["limited_fraction_mean"] = float(np.mean(fr))
+        out["t"] = sim.t
+    else:
+        s = float(np.mean(sweeps))
+        fl = roofline.step_flops_per_dof(degree, d, s)
+        by = roofline.step_bytes_per_dof(degree, d)
+        out["flop_per_dof"] = fl
+        out["flop_per_byte"] = fl / by
+        out["step_roofline_dof_per_s"] = roofline.roofline_dofs(degree, d, s, 33.635e12,
+                                                                6454.3e9)
+        out["step_roofline_frac"] = out["dof_per_s"] / out["step_roofline_dof_per_s"]
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="C1,C2,C3,C4")
+    ap.add_argument("--c4-steps", type=int, default=100)
+    ap.add_argument("--c3-cells", type=int, default=32)
+    args = ap.parse_args()
+    which = set(args.only.split(","))
+    if "C1" in which:
+        run_case("C1", [(0.0, 10.0), (0.0, 10.0)], (32, 32), 3, 0.9 / 14.0, "vortex", 10)
+    if "C2" in which:
+        run_case("C2", [(0.0, 1.0)] * 3, (64, 64, 64), 4, 0.9 / 27.0, "density_wave", 20)
+    if "C3" in which:
+        n3 = args.c3_cells
+        for n in range(2, 10):
+            run_case(f"C3_N{n}", [(0.0, 1.0)] * 3, (n3,) * 3, n, 0.9 / (3 * (2 * n + 1)),
+                     "density_wave", 10)
+    if "C4" in which:
+        run_case("C4", [(-1.0, 1.0), (-1.0, 1.0)], (512, 512), 5, 0.9 / 22.0, "explosion",
+                 args.c4_steps, boundary="outflow", limiter=True, t_end=0.25)
+
+
+if __name__ == "__main__":
+    main()
