@@ -51,12 +51,18 @@ typedef struct adg_handle adg_handle;
 
 /* Grid descriptor (POD).  cells are the LOCAL element counts of this rank;
  * dx are the element widths (mesh.py:32).  dim in 1..3, degree in 0..9,
- * nvars = dim + 2 (Euler). */
+ * nvars = dim + 2 (Euler).  mode = predictor_mode (driver.py:45-48):
+ * ADG_MODE_CONSERVATIVE evolves the predictor and the MUSCL-Hancock half
+ * step in conservative variables, ADG_MODE_PRIMITIVE in primitive ones
+ * (predictor.py:94-96, :165-189; limiter.py:127-177). */
+#define ADG_MODE_CONSERVATIVE 0
+#define ADG_MODE_PRIMITIVE 1
+
 typedef struct adg_grid {
   int32_t dim;
   int32_t degree;
   int32_t nvars;
-  int32_t reserved;
+  int32_t mode;
   int64_t cells[3];
   double dx[3];
   double gamma;

@@ -35,20 +35,36 @@ def dg_rate(q, phys, spacings, tab):
     return out
 
 
+def prim_rate(v, phys, spacings, tab):
+    """primitive_rhs(v, grad v) with nodal gradients (predictor.py:65-71, :94-96)."""
+    d = phys.dim
+    first = v.ndim - 2 - d
+    g = np.empty(v.shape[:-1] + (d, v.shape[-1]))
+    for j in range(d):
+        g[..., j, :] = contract(tab.diff / spacings[j], v, first + j)
+    return phys.primitive_rhs(v, g)
+
+
 def _with_time(u, n):
     return np.repeat(u[..., None, :], n, axis=-2)
 
 
-def startup_guess(u, phys, spacings, dt, tab):
-    """Initial space-time iterate (predictor.py:99-126), conservative mode."""
+def startup_guess(u, phys, spacings, dt, tab, mode="conservative"):
+    """Initial space-time iterate (predictor.py:99-126).  In primitive mode
+    u is converted first and the guess is built in primitive variables."""
     n = tab.degree
-    k1 = dg_rate(_with_time(u, 1), phys, spacings, tab)[..., 0, :]
+    if mode == "primitive":
+        u = phys.cons_to_prim(u)
+        rate = lambda w: prim_rate(w, phys, spacings, tab)  # noqa: E731
+    else:
+        rate = lambda w: dg_rate(w, phys, spacings, tab)  # noqa: E731
+    k1 = rate(_with_time(u, 1))[..., 0, :]
     q = np.empty(u.shape[:-1] + (n + 1, u.shape[-1]))
     if n <= 1:
         for t in range(n + 1):
             q[..., t, :] = u + (tab.nodes[t] * dt) * k1
         return q
-    k2 = dg_rate(_with_time(u + dt * k1, 1), phys, spacings, tab)[..., 0, :]
+    k2 = rate(_with_time(u + dt * k1, 1))[..., 0, :]
     for t in range(n + 1):
         s = tab.nodes[t] * dt
         q[..., t, :] = u + s * k1 + (0.5 * s * s / dt) * (k2 - k1)
@@ -65,7 +81,7 @@ class PicardOut:
 
 
 def picard_solve(u, phys, spacings, dt, tab, tol=1e-12, max_iter=None,
-                 initial=None, per_element=False):
+                 initial=None, per_element=False, mode="conservative"):
     """Space-time Picard fixed point (predictor.py:135-191).
 
     per_element=False reproduces the reference's global stopping rule
@@ -76,8 +92,10 @@ def picard_solve(u, phys, spacings, dt, tab, tol=1e-12, max_iter=None,
     d = phys.dim
     if max_iter is None:
         max_iter = 2 * tab.degree + 2
-    q = startup_guess(u, phys, spacings, dt, tab) if initial is None \
+    prim = mode == "primitive"
+    q = startup_guess(u, phys, spacings, dt, tab, mode) if initial is None \
         else np.array(initial, dtype=float)
+    u_it = phys.cons_to_prim(u) if prim else u
     red = tuple(range(u.ndim - 1 - d, q.ndim))
     grid_shape = u.shape[:-1 - d]
     converged = np.zeros(grid_shape, dtype=bool)
@@ -85,10 +103,10 @@ def picard_solve(u, phys, spacings, dt, tab, tol=1e-12, max_iter=None,
     frozen = np.zeros(grid_shape, dtype=bool)
     it = 0
     for _ in range(max_iter):
-        rate = dg_rate(q, phys, spacings, tab)
+        rate = prim_rate(q, phys, spacings, tab) if prim else dg_rate(q, phys, spacings, tab)
         q_new = contract(tab.gw, rate, -2)
         q_new *= dt
-        q_new += tab.g0[:, None] * u[..., None, :]
+        q_new += tab.g0[:, None] * u_it[..., None, :]
         it += 1
         delta = q - q_new
         res = tab.k1_opnorm * np.sqrt(np.sum(delta * delta, axis=red))
@@ -109,6 +127,8 @@ def picard_solve(u, phys, spacings, dt, tab, tol=1e-12, max_iter=None,
             first_conv[(first_conv == 0) & conv_now] = it
             if np.all(converged):
                 break
+    if prim:
+        q = phys.prim_to_cons(q)
     ok = np.all(phys.admissible(q), axis=tuple(range(len(grid_shape), q.ndim - 1)))
     return PicardOut(q=q, iterations=it, converged=converged, admissible=ok,
                      sweeps=first_conv)

@@ -90,3 +90,27 @@ class EulerOracle:
             q[..., 1 + j] = rho * v[..., 1 + j]
         q[..., -1] = v[..., -1] / (self.gamma - 1.0) + 0.5 * rho * kin
         return q
+
+    # systems.py:200-223: quasi-linear primitive time derivative
+    def primitive_rhs(self, v, grad):
+        d = self.dim
+        rho = v[..., 0]
+        p = v[..., -1]
+        div = grad[..., 0, 1]
+        for j in range(1, d):
+            div = div + grad[..., j, 1 + j]
+        out = np.empty_like(v)
+        arho = v[..., 1] * grad[..., 0, 0]
+        ap = v[..., 1] * grad[..., 0, d + 1]
+        for j in range(1, d):
+            arho = arho + v[..., 1 + j] * grad[..., j, 0]
+            ap = ap + v[..., 1 + j] * grad[..., j, d + 1]
+        out[..., 0] = -(arho + rho * div)
+        for i in range(d):
+            av = v[..., 1] * grad[..., 0, 1 + i]
+            for j in range(1, d):
+                av = av + v[..., 1 + j] * grad[..., j, 1 + i]
+            out[..., 1 + i] = -(av + grad[..., i, d + 1] / rho)
+        out[..., d + 1] = -(ap + self.gamma * p * div)
+        return out
+

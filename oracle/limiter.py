@@ -80,10 +80,14 @@ def windows(padded, starts, size, dim):
     return padded[tuple(idx)]
 
 
-def _hancock(win, phys, h, dt, flat):
-    """One MUSCL-Hancock pass over windows (limiter.py:124-202), conservative."""
+def _hancock(win, phys, h, dt, flat, mode="conservative"):
+    """One MUSCL-Hancock pass over windows (limiter.py:124-202)."""
     d = phys.dim
     m = phys.n_vars
+    prim = mode == "primitive"
+    cons = win
+    if prim:
+        win = phys.cons_to_prim(win)
 
     def g(sls):
         return (slice(None),) + sls + (slice(None),)
@@ -98,24 +102,29 @@ def _hancock(win, phys, h, dt, flat):
             fwd = (win[g(up)] - c) / h[j]
             bwd = (c - win[g(dn)]) / h[j]
             slope[..., j, :] = minmod(fwd, bwd)
-    rate = np.zeros_like(c)
-    for j in range(d):
-        off = 0.5 * h[j] * slope[..., j, :]
-        fh = phys.flux(c + off)[..., j, :]
-        fl = phys.flux(c - off)[..., j, :]
-        rate = rate - (fh - fl) / h[j]
-    half = c + (0.5 * dt) * rate
+    if prim:
+        half = c + (0.5 * dt) * phys.primitive_rhs(c, slope)
+    else:
+        rate = np.zeros_like(c)
+        for j in range(d):
+            off = 0.5 * h[j] * slope[..., j, :]
+            fh = phys.flux(c + off)[..., j, :]
+            fl = phys.flux(c - off)[..., j, :]
+            rate = rate - (fh - fl) / h[j]
+        half = c + (0.5 * dt) * rate
     ok = np.ones(win.shape[0], dtype=bool)
     lo_f, hi_f = [], []
     axes = tuple(range(1, 1 + d))
     for j in range(d):
         off = 0.5 * h[j] * slope[..., j, :]
         lo_q, hi_q = half - off, half + off
+        if prim:
+            lo_q, hi_q = phys.prim_to_cons(lo_q), phys.prim_to_cons(hi_q)
         lo_f.append(lo_q)
         hi_f.append(hi_q)
         ok &= np.all(phys.admissible(lo_q), axis=axes)
         ok &= np.all(phys.admissible(hi_q), axis=axes)
-    new = win[g(tuple(slice(2, -2) for _ in range(d)))].copy()
+    new = cons[g(tuple(slice(2, -2) for _ in range(d)))].copy()
     for j in range(d):
         qm_sl = tuple(slice(None, -1) if i == j else slice(1, -1) for i in range(d))
         qp_sl = tuple(slice(1, None) if i == j else slice(1, -1) for i in range(d))
@@ -127,12 +136,12 @@ def _hancock(win, phys, h, dt, flat):
     return new, ~ok
 
 
-def muscl_step(win, phys, h, dt):
+def muscl_step(win, phys, h, dt, mode="conservative"):
     """MUSCL-Hancock with first-order retry (limiter.py:104-121)."""
-    new, bad = _hancock(win, phys, h, dt, flat=False)
+    new, bad = _hancock(win, phys, h, dt, flat=False, mode=mode)
     failed = np.zeros(win.shape[0], dtype=bool)
     if np.any(bad):
-        redo, still = _hancock(win[bad], phys, h, dt, flat=True)
+        redo, still = _hancock(win[bad], phys, h, dt, flat=True, mode=mode)
         new[bad] = redo
         failed[np.flatnonzero(bad)[still]] = True
     return new, failed

@@ -19,6 +19,7 @@ ADG_ERR_CUDA = 3
 ADG_ERR_UNSUPPORTED = 4
 
 BC_CODES = {"periodic": 0, "outflow": 1, "wall": 2, "exact": 3, "ghost": 3}
+MODE_CODES = {"conservative": 0, "primitive": 1}   # adg_grid.mode (ADG_MODE_*)
 
 STATUS_NO_ADMISSIBLE = 1
 STATUS_NONFINITE = 2
@@ -34,7 +35,7 @@ EXPORTS = (
 
 class Grid(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int32), ("degree", ctypes.c_int32),
-                ("nvars", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("nvars", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("cells", ctypes.c_int64 * 3), ("dx", ctypes.c_double * 3),
                 ("gamma", ctypes.c_double), ("bc", (ctypes.c_int32 * 2) * 3)]
 

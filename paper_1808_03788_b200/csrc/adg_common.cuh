@@ -131,6 +131,53 @@ __device__ __forceinline__ double flux_eig_axis(const double* q, double gamma, d
   return fabs(va) + sqrt(gamma * p * r);
 }
 
+// systems.py:180-198 conservative <-> primitive (rho, v_1..d, p)
+template <int D>
+__device__ __forceinline__ void cons_to_prim(const double* q, double gm1, double* v) {
+  v[0] = q[0];
+#pragma unroll
+  for (int j = 0; j < D; ++j) v[1 + j] = q[1 + j] / q[0];
+  v[D + 1] = pressure<D>(q, gm1);
+}
+template <int D>
+__device__ __forceinline__ void prim_to_cons(const double* v, double gm1, double* q) {
+  const double rho = v[0];
+  double kin = v[1] * v[1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) kin = kin + v[1 + j] * v[1 + j];
+  q[0] = rho;
+#pragma unroll
+  for (int j = 0; j < D; ++j) q[1 + j] = rho * v[1 + j];
+  q[D + 1] = v[D + 1] / gm1 + 0.5 * rho * kin;
+}
+
+// systems.py:200-223: quasi-linear primitive time derivative; g[j][w] is
+// the j-derivative of primitive quantity w
+template <int D>
+__device__ __forceinline__ void primitive_rhs(const double* v, const double g[D][D + 2],
+                                              double gamma, double* out) {
+  const double rho = v[0], p = v[D + 1];
+  double div = g[0][1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) div = div + g[j][1 + j];
+  double arho = v[1] * g[0][0];
+  double ap = v[1] * g[0][D + 1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) {
+    arho = arho + v[1 + j] * g[j][0];
+    ap = ap + v[1 + j] * g[j][D + 1];
+  }
+  out[0] = -(arho + rho * div);
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double av = v[1] * g[0][1 + i];
+#pragma unroll
+    for (int j = 1; j < D; ++j) av = av + v[1 + j] * g[j][1 + i];
+    out[1 + i] = -(av + g[i][D + 1] / rho);
+  }
+  out[D + 1] = -(ap + gamma * p * div);
+}
+
 // systems.py:225-229: all finite, rho > 0, p > 0.
 template <int D>
 __device__ __forceinline__ bool admissible(const double* q, double gm1) {

@@ -41,6 +41,7 @@ struct LimGrid {
   int bc[3][2];
   double gm1, gamma;
   double h[3];  // subcell widths dx_j / S
+  int prim;     // predictor_mode == "primitive": MUSCL-Hancock in primitive variables
 };
 
 // ---------------------------------------------------------------- helpers
@@ -388,6 +389,20 @@ __device__ __forceinline__ double minmod(double a, double b) {
   return (a * b > 0.0) ? (fabs(a) <= fabs(b) ? a : b) : 0.0;
 }
 
+// face states of the primitive-mode half step back to conservative
+// (limiter.py:160-171)
+template <int D>
+__device__ __forceinline__ void to_cons2(double* a, double* b, double gm1) {
+  constexpr int M = D + 2;
+  double t[M];
+  prim_to_cons<D>(a, gm1, t);
+#pragma unroll
+  for (int v = 0; v < M; ++v) a[v] = t[v];
+  prim_to_cons<D>(b, gm1, t);
+#pragma unroll
+  for (int v = 0; v < M; ++v) b[v] = t[v];
+}
+
 // MUSCL-Hancock rescue of one troubled cell per block (limiter.py:104-223)
 template <int D, int P>
 __global__ void __launch_bounds__(LimCfg<D, P>::NT)
@@ -428,6 +443,12 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
         rem /= W;
       }
       fetch_sub<D, P>(prev_sub, G, gs, win + w * M);
+      if (G.prim) {   // limiter.py:127-128: the window in primitive variables
+        double vv[M];
+        cons_to_prim<D>(win + w * M, G.gm1, vv);
+#pragma unroll
+        for (int v = 0; v < M; ++v) win[w * M + v] = vv[v];
+      }
     }
     __syncthreads();
     for (int pass = 0; pass < 2; ++pass) {   // sloped, then first order
@@ -466,6 +487,10 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
         double rate[M];
 #pragma unroll
         for (int v = 0; v < M; ++v) rate[v] = 0.0;
+        if (G.prim) {
+          // limiter.py:146-147: half = c + dt/2 primitive_rhs(c, slopes)
+          primitive_rhs<D>(cq, slope, G.gamma, rate);
+        } else {
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           double qh[M], ql[M], fh[M], fl[M];
@@ -479,6 +504,7 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
           flux_axis<D>(ql, G.gm1, j, fl);
 #pragma unroll
           for (int v = 0; v < M; ++v) rate[v] = rate[v] - (fh[v] - fl[v]) / G.h[j];
+        }
         }
         double half[M];
 #pragma unroll
@@ -496,6 +522,15 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
             sl[(r * D + j) * M + v] = off;
             lo[v] = half[v] - off;
             hi[v] = half[v] + off;
+          }
+          if (G.prim) {
+            double tq[M];
+            prim_to_cons<D>(lo, G.gm1, tq);
+#pragma unroll
+            for (int v = 0; v < M; ++v) lo[v] = tq[v];
+            prim_to_cons<D>(hi, G.gm1, tq);
+#pragma unroll
+            for (int v = 0; v < M; ++v) hi[v] = tq[v];
           }
           ok = ok && admissible<D>(lo, G.gm1) && admissible<D>(hi, G.gm1);
         }
@@ -520,8 +555,14 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
           return x;
         };
         double q[M];
+        if (G.prim) {   // conservative core average (limiter.py:178)
+          int64_t gs[3] = {0, 0, 0};
+          for (int j = 0; j < D; ++j) gs[j] = c[j] * S + si[j];
+          fetch_sub<D, P>(prev_sub, G, gs, q);
+        } else {
 #pragma unroll
-        for (int v = 0; v < M; ++v) q[v] = win[wcore() * M + v];
+          for (int v = 0; v < M; ++v) q[v] = win[wcore() * M + v];
+        }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           const int rc = rix(0, 0), rl = rix(j, -1), rh = rix(j, 1);
@@ -532,6 +573,7 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
             a[v] = vh[rc * M + v] + sl[(rc * D + j) * M + v];
             bq[v] = vh[rh * M + v] - sl[(rh * D + j) * M + v];
           }
+          if (G.prim) to_cons2<D>(a, bq, G.gm1);
           rusanov_pair<D>(a, bq, j, G.gamma, G.gm1, dlo_h, dhi_h);
           // low face: minus = hi state of previous, plus = lo state of this
 #pragma unroll
@@ -539,6 +581,7 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
             a[v] = vh[rl * M + v] + sl[(rl * D + j) * M + v];
             bq[v] = vh[rc * M + v] - sl[(rc * D + j) * M + v];
           }
+          if (G.prim) to_cons2<D>(a, bq, G.gm1);
           rusanov_pair<D>(a, bq, j, G.gamma, G.gm1, dlo_l, dhi_l);
           const double c_j = dt / G.h[j];
 #pragma unroll
@@ -701,6 +744,7 @@ static LimGrid lim_grid(const adg_grid* g) {
   }
   G.gamma = g->gamma;
   G.gm1 = g->gamma - 1.0;
+  G.prim = g->mode == ADG_MODE_PRIMITIVE ? 1 : 0;
   return G;
 }
 

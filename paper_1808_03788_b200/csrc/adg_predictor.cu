@@ -92,6 +92,7 @@ struct PredArgs {
   double tol;
   int max_iter;
   int min_iter;
+  int prim;            // predictor_mode: 0 conservative, 1 primitive
 };
 
 // spatial node index from per-axis indices (row-major, last axis fastest)
@@ -121,6 +122,7 @@ __device__ __forceinline__ void spatial_line_task(const double* __restrict__ X,
                                                   int line) {
   // MODE 0: X = states [node][v], pre = flux along DIR, W = D/dx (all dirs)
   // MODE 1: X = per-direction rows X[dir][node][v], W = stiffness (shared)
+  // MODE 2: X = primitive states [node][v], no pre (gradients), W = D/dx
   using C = PredCfg<D, P>;
   constexpr int M = C::M, PD = C::PD;
   const int ta = D == 3 ? line / P : line;
@@ -135,12 +137,15 @@ __device__ __forceinline__ void spatial_line_task(const double* __restrict__ X,
 #pragma unroll
       for (int v = 0; v < M; ++v) q[v] = X[nd * M + v];
       flux_axis<D>(q, gm1, DIR, x[l]);
+    } else if (MODE == 2) {
+#pragma unroll
+      for (int v = 0; v < M; ++v) x[l][v] = X[nd * M + v];
     } else {
 #pragma unroll
       for (int v = 0; v < M; ++v) x[l][v] = X[(DIR * PD + nd) * M + v];
     }
   }
-  const double* Wd = MODE == 0 ? W + DIR * P * P : W;
+  const double* Wd = MODE != 1 ? W + DIR * P * P : W;
 #pragma unroll
   for (int i = 0; i < P; ++i) {
     double y[M];
@@ -179,7 +184,12 @@ __device__ __forceinline__ void spatial_line_tasks(const double* __restrict__ X,
   }
 }
 
-template <int D, int P>
+// PRIM = 1: predictor_mode="primitive" (predictor.py:94-96, :109-112,
+// :165-189): the startup guess and the Picard iterate live in primitive
+// variables and the rate is primitive_rhs(v, grad v); gradients travel
+// through the same owner passes as the conservative flux derivatives; the
+// converged tile is converted back before the admissibility screen.
+template <int D, int P, int PRIM>
 __global__ void __launch_bounds__(PredCfg<D, P>::NT, PredCfg<D, P>::MINB)
 predict_kernel(PredArgs a) {
   using C = PredCfg<D, P>;
@@ -262,30 +272,46 @@ predict_kernel(PredArgs a) {
     // w = u (k1) then u + dt k1 (k2); states staged node-major in Q[:PD*M]
     double* W0 = Q;                 // staged states [node][v]
     double* PA = B1;                // per-direction pieces [dir][node][v]
-    double uu[M];
+    double uu[M];   // u^n (conservative), or its primitive state (PRIM)
     double k1[M];
     double k2[M];
     if (valid) {
       const double* ue = a.u + (size_t)e * PD * M + (size_t)item * M;
 #pragma unroll
-      for (int v = 0; v < M; ++v) {
-        uu[v] = ue[v];
-        W0[item * M + v] = uu[v];
+      for (int v = 0; v < M; ++v) uu[v] = ue[v];
+      if (PRIM) {
+        double vv[M];
+        cons_to_prim<D>(uu, gm1, vv);
+#pragma unroll
+        for (int v = 0; v < M; ++v) uu[v] = vv[v];
       }
+#pragma unroll
+      for (int v = 0; v < M; ++v) W0[item * M + v] = uu[v];
     }
 #pragma unroll
     for (int pass = 0; pass < (P >= 3 ? 2 : 1); ++pass) {
       __syncthreads();
-      if (valid) spatial_line_tasks<D, P, 0>(W0, PA, Ds, gm1, item);
+      if (valid) spatial_line_tasks<D, P, PRIM ? 2 : 0>(W0, PA, Ds, gm1, item);
       __syncthreads();
       double* kk = pass == 0 ? k1 : k2;
       if (valid) {
+        if (PRIM) {
+          double gr[D][M], w[M];   // w: the staged state (u, then u + dt k1)
 #pragma unroll
-        for (int v = 0; v < M; ++v) {
-          double r = 0.0;
+          for (int dir = 0; dir < D; ++dir)
 #pragma unroll
-          for (int dir = 0; dir < D; ++dir) r -= PA[(dir * PD + item) * M + v];
-          kk[v] = r;
+            for (int v = 0; v < M; ++v) gr[dir][v] = PA[(dir * PD + item) * M + v];
+#pragma unroll
+          for (int v = 0; v < M; ++v) w[v] = W0[item * M + v];
+          primitive_rhs<D>(w, gr, a.gamma, kk);
+        } else {
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            double r = 0.0;
+#pragma unroll
+            for (int dir = 0; dir < D; ++dir) r -= PA[(dir * PD + item) * M + v];
+            kk[v] = r;
+          }
         }
         if (pass == 0) {
 #pragma unroll
@@ -316,7 +342,19 @@ predict_kernel(PredArgs a) {
     for (; it < max_iter; ++it) {
       if (*all_frozen) break;
       const bool work = valid && !frozen[el];
-      double rate[P][M];
+      double rate[P][M];             // conservative: the rate; PRIM: first the x-gradient
+      double ql[PRIM ? P : 1][M];    // PRIM: the x-owner's primitive states
+      double gyr[(PRIM && C::SEQ_YZ) ? P : 1][M];
+      // pointwise pre-transform of a line state: directional flux, or the
+      // primitive state itself (gradients)
+      auto pre = [&](const double* q, int dir, double* out) {
+        if (PRIM) {
+#pragma unroll
+          for (int v = 0; v < M; ++v) out[v] = q[v];
+        } else {
+          flux_axis<D>(q, gm1, dir, out);
+        }
+      };
       // z-owner: own z-line -> D_z partials, x-line-major rows of dst
       auto zpass = [&](double* dst) {
           double fz[P][M];
@@ -325,7 +363,7 @@ predict_kernel(PredArgs a) {
             double q[M];
 #pragma unroll
             for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(zi, zj, l) * LS + zt * M + v];
-            flux_axis<D>(q, gm1, 2, fz[l]);
+            pre(q, 2, fz[l]);
           }
 #pragma unroll
           for (int kk = 0; kk < P; ++kk) {
@@ -351,7 +389,11 @@ predict_kernel(PredArgs a) {
             double q[M];
 #pragma unroll
             for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(l, xj, xk) * LS + xt * M + v];
-            flux_axis<D>(q, gm1, 0, fx[l]);
+            pre(q, 0, fx[l]);
+            if (PRIM) {
+#pragma unroll
+              for (int v = 0; v < M; ++v) ql[PRIM ? l : 0][v] = q[v];
+            }
           }
 #pragma unroll
           for (int i = 0; i < P; ++i) {
@@ -365,7 +407,7 @@ predict_kernel(PredArgs a) {
               for (int v = 0; v < M; ++v) y[v] = fma(d, fx[l][v], y[v]);
             }
 #pragma unroll
-            for (int v = 0; v < M; ++v) rate[i][v] = -y[v];
+            for (int v = 0; v < M; ++v) rate[i][v] = PRIM ? y[v] : -y[v];
           }
         }
         if (D >= 2) {
@@ -375,7 +417,7 @@ predict_kernel(PredArgs a) {
             double q[M];
 #pragma unroll
             for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(yi, l, yk) * LS + yt * M + v];
-            flux_axis<D>(q, gm1, 1, fy[l]);
+            pre(q, 1, fy[l]);
           }
 #pragma unroll
           for (int jj = 0; jj < P; ++jj) {
@@ -401,21 +443,40 @@ predict_kernel(PredArgs a) {
 #pragma unroll
           for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int v = 0; v < M; ++v) rate[i][v] -= B1[item * LS + i * M + v];
+            for (int v = 0; v < M; ++v) {
+              if (PRIM) gyr[PRIM ? i : 0][v] = B1[item * LS + i * M + v];
+              else rate[i][v] -= B1[item * LS + i * M + v];
+            }
         }
         __syncthreads();
         if (work) zpass(B1);
         __syncthreads();
       }
+      if (PRIM && work) {
+        // rate = primitive_rhs(v, (grad_x, grad_y, grad_z)) at the x-line's nodes
+        const double* PZ = C::SEQ_YZ ? B1 : B2;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          double gr[D][M];
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            gr[0][v] = rate[i][v];
+            if (D >= 2) gr[D >= 2 ? 1 : 0][v] = C::SEQ_YZ ? gyr[(PRIM && C::SEQ_YZ) ? i : 0][v]
+                                                           : B1[item * LS + i * M + v];
+            if (D == 3) gr[D == 3 ? 2 : 0][v] = PZ[item * LS + i * M + v];
+          }
+          primitive_rhs<D>(ql[PRIM ? i : 0], gr, a.gamma, rate[i]);
+        }
+      }
       // B: x-owner completes its rate in place (x-line-major rows of B1)
       if (work) {
-        if (D >= 2 && !C::SEQ_YZ) {
+        if (!PRIM && D >= 2 && !C::SEQ_YZ) {
 #pragma unroll
           for (int i = 0; i < P; ++i)
 #pragma unroll
             for (int v = 0; v < M; ++v) rate[i][v] -= B1[item * LS + i * M + v];
         }
-        if (D == 3) {
+        if (!PRIM && D == 3) {
           const double* PZ = C::SEQ_YZ ? B1 : B2;
 #pragma unroll
           for (int i = 0; i < P; ++i)
@@ -489,6 +550,21 @@ predict_kernel(PredArgs a) {
       __syncthreads();
     }
 
+    if (PRIM) {
+      // q_cons = prim_to_cons(q) (predictor.py:188), each node thread its own
+      if (valid) {
+#pragma unroll
+        for (int t = 0; t < P; ++t) {
+          double v[M], q[M];
+#pragma unroll
+          for (int w = 0; w < M; ++w) v[w] = Q[item * LS + t * M + w];
+          prim_to_cons<D>(v, gm1, q);
+#pragma unroll
+          for (int w = 0; w < M; ++w) Q[item * LS + t * M + w] = q[w];
+        }
+      }
+      __syncthreads();
+    }
     // ---------------- admissibility, traces, volume flux sums ----------
     double fb[D][M];   // fbar_dir = sum_t w_t F_dir(q_t) (corrector.py:171)
     if (valid) {
@@ -591,9 +667,9 @@ template <int D, int P>
 static int launch_predict(const PredArgs& a0, cudaStream_t st, int num_sms, double* ws_pool,
                           size_t ws_bytes, std::string* err) {
   using C = PredCfg<D, P>;
-  auto kern = predict_kernel<D, P>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  auto kern = a0.prim ? predict_kernel<D, P, 1> : predict_kernel<D, P, 0>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[a0.prim ? 1 : 0]) {
     if (C::SMEM_BYTES > 48 * 1024) {
       cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)C::SMEM_BYTES);
@@ -602,7 +678,7 @@ static int launch_predict(const PredArgs& a0, cudaStream_t st, int num_sms, doub
         return ADG_ERR_CUDA;
       }
     }
-    attr_set = true;
+    attr_set[a0.prim ? 1 : 0] = true;
   }
   PredArgs a = a0;
   const int64_t ngroups = (a.n_elem + C::EPB - 1) / C::EPB;
@@ -678,6 +754,7 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   a.tol = tol;
   a.max_iter = max_iter > 0 ? max_iter : 2 * g->degree + 2;
   a.min_iter = min_iter;
+  a.prim = g->mode == ADG_MODE_PRIMITIVE ? 1 : 0;
   const int P = g->degree + 1;
   if (g->dim == 1) { ADG_DISPATCH_P(1, launch_predict, a, st, num_sms, ws, ws_bytes, err) }
   if (g->dim == 2) { ADG_DISPATCH_P(2, launch_predict, a, st, num_sms, ws, ws_bytes, err) }

@@ -124,8 +124,6 @@ class Simulation:
                 f"system '{getattr(system, 'name', system)}' has no B200 kernels (Euler only)")
         if predictor_mode not in ("conservative", "primitive"):
             raise ValueError(f"unknown predictor mode {predictor_mode!r}")
-        if predictor_mode == "primitive":
-            raise NotImplementedError("primitive-variable predictor is not on the B200 path yet")
         self.mesh = mesh
         self.system = system
         self.tables = basis_tables(degree)
@@ -177,6 +175,7 @@ class Simulation:
         g.dim = d
         g.degree = self.tables.degree
         g.nvars = self.system.n_vars
+        g.mode = _lib.MODE_CODES[self.predictor_mode]
         for j in range(3):
             g.cells[j] = int(cells[j]) if j < d else 1
             g.dx[j] = float(spacings[j]) if j < d else 1.0

@@ -24,10 +24,11 @@ class PredictorResult:
     volume: torch.Tensor = None
 
 
-def _grid(system, cells, spacings, degree, boundary_codes=None):
+def _grid(system, cells, spacings, degree, boundary_codes=None, mode="conservative"):
     g = _lib.Grid()
     d = system.dim
     g.dim, g.degree, g.nvars = d, degree, system.n_vars
+    g.mode = _lib.MODE_CODES[mode]
     for j in range(3):
         g.cells[j] = int(cells[j]) if j < d else 1
         g.dx[j] = float(spacings[j]) if j < d else 1.0
@@ -39,7 +40,7 @@ def _grid(system, cells, spacings, degree, boundary_codes=None):
 
 
 def run_predictor(u, system, spacings, dt, tables, tol=1e-12, max_iter=None, min_iter=1,
-                  want_q=True):
+                  want_q=True, mode="conservative"):
     """Fused predictor on u (cells.., P.., m); returns PredictorResult with q,
     traces {(j, side): (cells.., P^(d-1) tangential.., P_t, m)} and the volume
     accumulator of corrector.volume_integral (corrector.py:141-177)."""
@@ -52,7 +53,7 @@ def run_predictor(u, system, spacings, dt, tables, tol=1e-12, max_iter=None, min
         raise ValueError(f"u has shape {tuple(u.shape)}; expected (cells..,{P}^{d},{m})")
     h = _lib.Handle.get(u.device.index)
     h.ensure_tables(tables)
-    g = _grid(system, cells, spacings, tables.degree)
+    g = _grid(system, cells, spacings, tables.degree, mode=mode)
     E = int(np.prod(cells))
     pd = P ** d
     dev = u.device
@@ -92,11 +93,12 @@ def picard_solve(u, system, spacings, dt, tables, tol=1e-12, max_iter=None,
     """Device picard_solve.  `converged & admissible` is exact; the two flags
     are reported jointly (the kernel's pred_bad, driver.py:212) -- converged
     carries the joint flag and admissible is all-true where it holds."""
-    if mode != "conservative":
-        raise NotImplementedError("primitive mode is not on the B200 path")
+    if mode not in _lib.MODE_CODES:
+        raise ValueError(f"unknown predictor mode {mode!r}")
     if initial is not None:
         raise NotImplementedError("custom initial iterates are not supported on the B200 path")
-    res, good = run_predictor(u, system, spacings, dt, tables, tol, max_iter, min_iter)
+    res, good = run_predictor(u, system, spacings, dt, tables, tol, max_iter, min_iter,
+                              mode=mode)
     res.converged = good
     res.admissible = torch.ones_like(good)
     return res

@@ -134,9 +134,9 @@ def gen_predictor():
 
 
 def run_case(name, mesh, sysd, degree, cfl, ic, steps, boundary="periodic",
-             use_limiter=False, store_first=False):
+             use_limiter=False, store_first=False, predictor_mode="conservative"):
     sim = aderdg.Simulation(mesh, sysd, degree, cfl, boundary=boundary,
-                            use_limiter=use_limiter)
+                            use_limiter=use_limiter, predictor_mode=predictor_mode)
     u0 = sim.project_initial_condition(ic).copy()
     dts, iters, flags, fracs, lam = [], [], [], [], []
     orig = predictor.picard_solve
@@ -206,8 +206,29 @@ def gen_cases():
              0.15, icb, 4, boundary="wall", use_limiter=True)
 
 
+def gen_primitive():
+    """predictor_mode="primitive" (predictor.py:94-96, :109-112, :165-189;
+    limiter.py:127-177): smooth, limited and near-vacuum cases."""
+    e2 = CompressibleEuler(2, gamma=GAMMA)
+    e1 = CompressibleEuler(1, gamma=GAMMA)
+    e3 = CompressibleEuler(3, gamma=GAMMA)
+    ic, _ = problems.vortex()
+    run_case("prim_vortex", aderdg.CartesianMesh([(0, 10), (0, 10)], (16, 16)), e2, 3,
+             0.9 / 14.0, ic, 4, predictor_mode="primitive")
+    ic3, _ = problems.density_wave()
+    run_case("prim_wave3d", wave_mesh((3, 3, 3)), e3, 4, 0.9 / 27.0, ic3, 2,
+             predictor_mode="primitive")
+    ics, _ = problems.sod()
+    run_case("prim_sod", aderdg.CartesianMesh([(0, 1)], (40,)), e1, 3, 0.09, ics, 10,
+             boundary="outflow", use_limiter=True, predictor_mode="primitive")
+    # the reference's near-vacuum blast (test_acceptance.py:164-197 setup)
+    icb, _ = problems.blast()
+    run_case("prim_blast", aderdg.CartesianMesh([(-1, 1), (-1, 1)], (16, 16)), e2, 2, 0.15,
+             icb, 4, boundary="wall", use_limiter=True, predictor_mode="primitive")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tables", "pointwise", "predictor", "cases"]
+    which = sys.argv[1:] or ["tables", "pointwise", "predictor", "cases", "primitive"]
     if "tables" in which:
         gen_tables()
     if "pointwise" in which:
@@ -216,3 +237,5 @@ if __name__ == "__main__":
         gen_predictor()
     if "cases" in which:
         gen_cases()
+    if "primitive" in which:
+        gen_primitive()

@@ -149,8 +149,8 @@ def test_simulation_argument_errors_precede_device_use():
         Simulation(mesh, make_system("euler", 3), 3, 0.05)
     with pytest.raises(ValueError):
         Simulation(mesh, e2, 3, 0.05, boundary="exact")
-    with pytest.raises(NotImplementedError):
-        Simulation(mesh, e2, 3, 0.05, predictor_mode="primitive")
+    with pytest.raises(ValueError):
+        Simulation(mesh, e2, 3, 0.05, predictor_mode="characteristic")
     with pytest.raises(NotImplementedError):
         make_system("advection", 2)
     import torch

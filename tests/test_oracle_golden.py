@@ -130,11 +130,12 @@ def _mesh_from(g):
     return OracleMesh([tuple(e) for e in g["extents"]], tuple(int(c) for c in g["cells"]))
 
 
-def _run_case(g, ic, boundary="periodic", use_limiter=False, steps=None):
+def _run_case(g, ic, boundary="periodic", use_limiter=False, steps=None,
+              mode="conservative"):
     mesh = _mesh_from(g)
     e = EulerOracle(mesh.dim)
     sim = OracleSimulation(mesh, e, int(g["degree"]), float(g["cfl"]), boundary=boundary,
-                           use_limiter=use_limiter)
+                           use_limiter=use_limiter, predictor_mode=mode)
     u0 = sim.project_initial_condition(ic)
     np.testing.assert_allclose(u0, g["u0"], rtol=0, atol=1e-14)
     n = len(g["dts"]) if steps is None else steps
@@ -183,4 +184,20 @@ def test_case_limiter(golden, name, icname, bc):
     sim, flags = _run_case(g, ic, boundary=bc, use_limiter=True)
     np.testing.assert_array_equal(np.stack(flags), g["troubled"])
     np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-13)
+    assert _rel(sim.u, g["u"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name,icname,bc,limited", [
+    ("prim_vortex", "vortex", "periodic", False), ("prim_wave3d", "wave", "periodic", False),
+    ("prim_sod", "sod", "outflow", True), ("prim_blast", "blast", "wall", True)])
+def test_case_primitive_mode(golden, name, icname, bc, limited):
+    """predictor_mode="primitive" (predictor.py:94-96, :165-189; limiter.py:127-177)."""
+    g = golden(name)
+    ic = {"vortex": problems.vortex, "wave": problems.density_wave, "sod": problems.sod,
+          "blast": problems.blast}[icname]()[0]
+    sim, flags = _run_case(g, ic, boundary=bc, use_limiter=limited, mode="primitive")
+    if limited:
+        np.testing.assert_array_equal(np.stack(flags), g["troubled"])
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-13)
+    assert sim.sweep_log == list(g["iters"])
     assert _rel(sim.u, g["u"]) <= 1e-12
