@@ -9,6 +9,7 @@
 
 namespace adg {
 __constant__ DegreeTables c_tab[kMaxP];
+DegreeTables h_tab[kMaxP];
 
 void upload_tables(int degree, const double* blob, int64_t n, std::string* err, int* rc) {
   const int P = degree + 1, S = 2 * degree + 1;
@@ -36,6 +37,7 @@ void upload_tables(int degree, const double* blob, int64_t n, std::string* err, 
   for (int k = 0; k < P; ++k)
     for (int l = 0; l < P; ++l) t.stiff[k * P + l] = t.diff[l * P + k] * t.weights[l];
   t.loaded = 1;
+  h_tab[degree] = t;
   cudaError_t ce = cudaMemcpyToSymbol(c_tab, &t, sizeof(t), sizeof(t) * degree);
   if (ce != cudaSuccess) {
     *err = cudaGetErrorString(ce);

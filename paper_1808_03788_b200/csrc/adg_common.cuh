@@ -32,6 +32,7 @@ struct DegreeTables {
 };
 
 extern __constant__ DegreeTables c_tab[kMaxP];
+extern DegreeTables h_tab[kMaxP];   // host copy (adg_set_tables)
 
 template <int P> __device__ __forceinline__ const DegreeTables& tab() { return c_tab[P - 1]; }
 

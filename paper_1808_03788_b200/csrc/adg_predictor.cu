@@ -93,6 +93,11 @@ struct PredArgs {
   int max_iter;
   int min_iter;
   int prim;            // predictor_mode: 0 conservative, 1 primitive
+  // D / dx_dir for the three directions, [dir][P][P] (rows packed with the
+  // launch's P).  Kernel parameters live in the constant bank, so every
+  // contraction coefficient is a DFMA constant operand: no shared-memory
+  // wavefronts for the uniform matrices
+  double dd[3 * kMaxP * kMaxP];
 };
 
 // spatial node index from per-axis indices (row-major, last axis fastest)
@@ -191,7 +196,7 @@ __device__ __forceinline__ void spatial_line_tasks(const double* __restrict__ X,
 // converged tile is converted back before the admissibility screen.
 template <int D, int P, int PRIM>
 __global__ void __launch_bounds__(PredCfg<D, P>::NT, PredCfg<D, P>::MINB)
-predict_kernel(PredArgs a) {
+predict_kernel(const __grid_constant__ PredArgs a) {
   using C = PredCfg<D, P>;
   constexpr int M = C::M, PD = C::PD, EPB = C::EPB, NT = C::NT, LS = P * M;
   constexpr int TP = C::RSZ;
@@ -226,14 +231,9 @@ predict_kernel(PredArgs a) {
   const double dt = *a.dt;
   const int max_iter = a.max_iter;
 
-  for (int x = tid; x < D * P * P; x += NT) {
-    const int dir = x / (P * P);
-    const double h = dir == 0 ? a.dx[0] : (dir == 1 ? a.dx[1] : a.dx[2]);
-    Ds[x] = T.diff[x - dir * P * P] / h;
-  }
-  const double* Dx = Ds;
-  const double* Dy = Ds + P * P;
-  const double* Dz = Ds + 2 * P * P;
+  const double* Dx = a.dd;
+  const double* Dy = a.dd + P * P;
+  const double* Dz = a.dd + 2 * P * P;
 
   // role coordinates; item is the owned line / node in every role
   const int ni = (D == 3) ? item / (P * P) : (D == 2 ? item / P : item);
@@ -291,7 +291,7 @@ predict_kernel(PredArgs a) {
 #pragma unroll
     for (int pass = 0; pass < (P >= 3 ? 2 : 1); ++pass) {
       __syncthreads();
-      if (valid) spatial_line_tasks<D, P, PRIM ? 2 : 0>(W0, PA, Ds, gm1, item);
+      if (valid) spatial_line_tasks<D, P, PRIM ? 2 : 0>(W0, PA, a.dd, gm1, item);
       __syncthreads();
       double* kk = pass == 0 ? k1 : k2;
       if (valid) {
@@ -755,6 +755,14 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   a.max_iter = max_iter > 0 ? max_iter : 2 * g->degree + 2;
   a.min_iter = min_iter;
   a.prim = g->mode == ADG_MODE_PRIMITIVE ? 1 : 0;
+  {
+    // D / dx exactly as the reference forms it (diff / spacing, one IEEE
+    // division per entry, basis.py diff; predictor.py:65-71)
+    const int Pl = g->degree + 1;
+    for (int dir = 0; dir < 3; ++dir)
+      for (int x = 0; x < Pl * Pl; ++x)
+        a.dd[dir * Pl * Pl + x] = dir < g->dim ? h_tab[g->degree].diff[x] / g->dx[dir] : 0.0;
+  }
   const int P = g->degree + 1;
   if (g->dim == 1) { ADG_DISPATCH_P(1, launch_predict, a, st, num_sms, ws, ws_bytes, err) }
   if (g->dim == 2) { ADG_DISPATCH_P(2, launch_predict, a, st, num_sms, ws, ws_bytes, err) }
