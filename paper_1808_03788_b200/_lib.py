@@ -10,7 +10,7 @@ import ctypes
 import os
 
 LIB_NAME = "libaderdg_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("ADG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 ADG_OK = 0
 ADG_ERR_INVALID = 1

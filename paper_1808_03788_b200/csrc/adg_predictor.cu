@@ -45,13 +45,19 @@ struct PredCfg {
   // 3-D tiles from N=5 up exchange the y and z partials one after the other
   // through a single buffer, so N=5/6 tiles fit two CTAs and N=6 one CTA of
   // shared memory (instead of the L2 slab); N<=4 keeps both in flight
-  static constexpr bool SEQ_YZ = (D == 3 && P >= 6);
+#ifndef ADG_SEQ_YZ_MINP
+#define ADG_SEQ_YZ_MINP 6
+#endif
+  static constexpr bool SEQ_YZ = (D == 3 && P >= ADG_SEQ_YZ_MINP);
   static constexpr int NBUF = D == 3 ? (SEQ_YZ ? 2 : 3) : 2;   // Q + partial buffers
   static constexpr int SPAT = D * PD * M;        // per-direction spatial pieces
   static constexpr int RSZ0 = TILE > SPAT ? TILE : SPAT;
   static constexpr int RSZ = RSZ0 + (RSZ0 & 1);  // region size (even: 16-B aligned)
   static constexpr int ELEM = NBUF * RSZ;        // doubles per element
-  static constexpr int BUDGET = 110 * 1024;  // bytes of tiles per CTA (>= 2 CTAs/SM)
+#ifndef ADG_TILE_BUDGET_KB
+#define ADG_TILE_BUDGET_KB 110
+#endif
+  static constexpr int BUDGET = ADG_TILE_BUDGET_KB * 1024;  // bytes of tiles per CTA (>= 2 CTAs/SM)
   static constexpr int EPB_T = (256 / PD) > 0 ? (256 / PD) : 1;
   static constexpr int EPB_S = (BUDGET / (ELEM * 8)) > 0 ? (BUDGET / (ELEM * 8)) : 1;
   static constexpr int EPB = EPB_T < EPB_S ? EPB_T : EPB_S;
@@ -72,7 +78,10 @@ struct PredCfg {
   static constexpr int MINB0 = (int)((228 * 1024) / (SMEM_BYTES + 1024));
   static constexpr int MINB_R = (65536 / (128 * NT)) > 0 ? 65536 / (128 * NT) : 1;  // >= 128 regs
   static constexpr int MINB1 = MINB0 < MINB_R ? MINB0 : MINB_R;
-  static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > 3 ? 3 : MINB1);
+#ifndef ADG_MINB_CAP
+#define ADG_MINB_CAP 3
+#endif
+  static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > ADG_MINB_CAP ? ADG_MINB_CAP : MINB1);
   // spatial line tasks (startup / volume): D directions x P^(D-1) lines
   static constexpr int NTASK = D * (PD / P);
 };
@@ -355,86 +364,61 @@ predict_kernel(const __grid_constant__ PredArgs a) {
           flux_axis<D>(q, gm1, dir, out);
         }
       };
-      // z-owner: own z-line -> D_z partials, x-line-major rows of dst
-      auto zpass = [&](double* dst) {
-          double fz[P][M];
+      // Line contraction, l-outer: each line state is loaded, transformed by
+      // `pre` and folded into all P outputs at once (acc[i] += W[i][l] f_l;
+      // same per-output fma order as a row-by-row mat-vec, but only one
+      // transformed state is live instead of P)
+      auto line_pass = [&](auto&& qaddr, int dir, const double* W, double sgn,
+                           double (&acc)[P][M]) {
 #pragma unroll
-          for (int l = 0; l < P; ++l) {
-            double q[M];
+        for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(zi, zj, l) * LS + zt * M + v];
-            pre(q, 2, fz[l]);
-          }
+          for (int v = 0; v < M; ++v) acc[i][v] = 0.0;
 #pragma unroll
-          for (int kk = 0; kk < P; ++kk) {
-            double y[M];
+        for (int l = 0; l < P; ++l) {
+          double q[M], f[M];
+          const double* src = Q + qaddr(l);
 #pragma unroll
-            for (int v = 0; v < M; ++v) y[v] = 0.0;
+          for (int v = 0; v < M; ++v) q[v] = src[v];
+          pre(q, dir, f);
+          if (PRIM && dir == 0) {
 #pragma unroll
-            for (int l = 0; l < P; ++l) {
-              const double d = Dz[kk * P + l];
-#pragma unroll
-              for (int v = 0; v < M; ++v) y[v] = fma(d, fz[l][v], y[v]);
-            }
-#pragma unroll
-            for (int v = 0; v < M; ++v) dst[xline<D, P>(zj, kk, zt) * LS + zi * M + v] = y[v];
-          }
-      };
-      // A: x-owner (registers) + y/z-owners (published partials)
-      if (work) {
-        {
-          double fx[P][M];
-#pragma unroll
-          for (int l = 0; l < P; ++l) {
-            double q[M];
-#pragma unroll
-            for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(l, xj, xk) * LS + xt * M + v];
-            pre(q, 0, fx[l]);
-            if (PRIM) {
-#pragma unroll
-              for (int v = 0; v < M; ++v) ql[PRIM ? l : 0][v] = q[v];
-            }
+            for (int v = 0; v < M; ++v) ql[PRIM ? l : 0][v] = q[v];
           }
 #pragma unroll
           for (int i = 0; i < P; ++i) {
-            double y[M];
+            const double d = sgn * W[i * P + l];
 #pragma unroll
-            for (int v = 0; v < M; ++v) y[v] = 0.0;
-#pragma unroll
-            for (int l = 0; l < P; ++l) {
-              const double d = Dx[i * P + l];
-#pragma unroll
-              for (int v = 0; v < M; ++v) y[v] = fma(d, fx[l][v], y[v]);
-            }
-#pragma unroll
-            for (int v = 0; v < M; ++v) rate[i][v] = PRIM ? y[v] : -y[v];
+            for (int v = 0; v < M; ++v) acc[i][v] = fma(d, f[v], acc[i][v]);
           }
         }
-        if (D >= 2) {
-          double fy[P][M];
+      };
+      // z-owner: own z-line -> D_z partials, x-line-major rows of dst
+      auto zpass = [&](double* dst) {
+        double acc[P][M];
+        line_pass([&](int l) { return node3<D, P>(zi, zj, l) * LS + zt * M; }, 2, Dz, 1.0, acc);
 #pragma unroll
-          for (int l = 0; l < P; ++l) {
-            double q[M];
+        for (int kk = 0; kk < P; ++kk)
 #pragma unroll
-            for (int v = 0; v < M; ++v) q[v] = Q[node3<D, P>(yi, l, yk) * LS + yt * M + v];
-            pre(q, 1, fy[l]);
-          }
+          for (int v = 0; v < M; ++v) dst[xline<D, P>(zj, kk, zt) * LS + zi * M + v] = acc[kk][v];
+      };
+      // y-owner: own y-line -> D_y partials, x-line-major rows of dst
+      auto ypass = [&](double* dst) {
+        double acc[P][M];
+        line_pass([&](int l) { return node3<D, P>(yi, l, yk) * LS + yt * M; }, 1, Dy, 1.0, acc);
 #pragma unroll
-          for (int jj = 0; jj < P; ++jj) {
-            double y[M];
+        for (int jj = 0; jj < P; ++jj)
 #pragma unroll
-            for (int v = 0; v < M; ++v) y[v] = 0.0;
-#pragma unroll
-            for (int l = 0; l < P; ++l) {
-              const double d = Dy[jj * P + l];
-#pragma unroll
-              for (int v = 0; v < M; ++v) y[v] = fma(d, fy[l][v], y[v]);
-            }
-#pragma unroll
-            for (int v = 0; v < M; ++v) B1[xline<D, P>(jj, yk, yt) * LS + yi * M + v] = y[v];
-          }
-        }
+          for (int v = 0; v < M; ++v) dst[xline<D, P>(jj, yk, yt) * LS + yi * M + v] = acc[jj][v];
+      };
+      // A: y/z-owners publish their partials first, then the x-owner's
+      // -D_x F_x (PRIM: +D_x v) accumulates straight into `rate`, so only
+      // one P x M block is live at a time
+      if (work) {
         if (D == 3 && !C::SEQ_YZ) zpass(B2);
+        if (D >= 2) ypass(B1);
+        line_pass([&](int l) { return node3<D, P>(l, xj, xk) * LS + xt * M; }, 0, Dx,
+                  PRIM ? 1.0 : -1.0, rate);
       }
       if (D >= 2) __syncthreads();
       if (C::SEQ_YZ) {
