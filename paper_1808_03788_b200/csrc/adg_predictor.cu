@@ -84,6 +84,14 @@ struct PredCfg {
   static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > ADG_MINB_CAP ? ADG_MINB_CAP : MINB1);
   // spatial line tasks (startup / volume): D directions x P^(D-1) lines
   static constexpr int NTASK = D * (PD / P);
+  // face-trace staging: the 2D trace blocks of an element are assembled in
+  // shared memory behind the published fbar and leave with cp.async.bulk
+  // (one 16-byte-aligned bulk store per face) instead of 40-byte-strided
+  // per-thread stores
+  static constexpr int TB = PD * M + ((PD * M) & 1);
+  static constexpr int FBAR = D * PD * M;
+  static constexpr int ST_OFF = FBAR + (FBAR & 1);
+  static constexpr bool TR_STAGE = SMEM_TILES && ((NBUF - 1) * RSZ >= ST_OFF + 2 * D * TB);
 };
 
 struct PredArgs {
@@ -284,18 +292,32 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     double uu[M];   // u^n (conservative), or its primitive state (PRIM)
     double k1[M];
     double k2[M];
+    // u^n of the group's elements: coalesced cooperative copy into each
+    // element's W0 (consecutive threads, consecutive doubles), then every
+    // node thread takes its own state from shared memory
+    for (int x = tid; x < EPB * PD * M; x += NT) {
+      const int ee = x / (PD * M);
+      const int off = x - ee * (PD * M);
+      if (g * EPB + ee < a.n_elem)
+        tiles[ee * C::ELEM + off] = a.u[(size_t)(g * EPB + ee) * PD * M + off];
+    }
+    __syncthreads();
     if (valid) {
-      const double* ue = a.u + (size_t)e * PD * M + (size_t)item * M;
 #pragma unroll
-      for (int v = 0; v < M; ++v) uu[v] = ue[v];
+      for (int v = 0; v < M; ++v) uu[v] = W0[item * M + v];
       if (PRIM) {
         double vv[M];
         cons_to_prim<D>(uu, gm1, vv);
 #pragma unroll
         for (int v = 0; v < M; ++v) uu[v] = vv[v];
       }
+    }
+    if (PRIM) {
+      __syncthreads();   // every lane has read its raw state (padding lanes share one)
+      if (valid && lane_ok) {
 #pragma unroll
-      for (int v = 0; v < M; ++v) W0[item * M + v] = uu[v];
+        for (int v = 0; v < M; ++v) W0[item * M + v] = uu[v];
+      }
     }
 #pragma unroll
     for (int pass = 0; pass < (P >= 3 ? 2 : 1); ++pass) {
@@ -344,6 +366,9 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         }
       }
     }
+    // the previous group's staged traces must be read out before the sweeps
+    // reuse B1 / B2
+    if (C::TR_STAGE && tid < EPB) bulk_wait_read_all();
     __syncthreads();
 
     // ---------------- Picard sweeps -----------------------------------
@@ -575,9 +600,10 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       // traces: each owner role writes its own line's face states at block
       // offset item*m (x: [j][k][t], y: [k][t][i], z: [t][i][j])
       // element trace blocks padded to a 16-byte multiple (TMA in the face kernel)
-      constexpr int TB = PD * M + ((PD * M) & 1);
+      constexpr int TB = C::TB;
       const size_t face_stride = (size_t)a.n_elem * TB;
       const size_t eoff = (size_t)e * TB + (size_t)item * M;
+      double* stage = B1 + C::ST_OFF;
 #pragma unroll
       for (int dir = 0; dir < D; ++dir) {
         double lo[M], hi[M];
@@ -596,14 +622,24 @@ predict_kernel(const __grid_constant__ PredArgs a) {
             hi[v] = fma(pr, qv, hi[v]);
           }
         }
-        double* tlo = a.traces + (size_t)(2 * dir) * face_stride + eoff;
-        double* thi = tlo + face_stride;
+        if (C::TR_STAGE) {
+          double* slo = stage + (2 * dir) * TB + item * M;
 #pragma unroll
-        for (int v = 0; v < M; ++v) {
-          tlo[v] = lo[v];
-          thi[v] = hi[v];
+          for (int v = 0; v < M; ++v) {
+            slo[v] = lo[v];
+            slo[TB + v] = hi[v];
+          }
+        } else {
+          double* tlo = a.traces + (size_t)(2 * dir) * face_stride + eoff;
+          double* thi = tlo + face_stride;
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            tlo[v] = lo[v];
+            thi[v] = hi[v];
+          }
         }
       }
+      if (C::TR_STAGE) fence_proxy_async_smem();   // staged traces -> async proxy
       if (a.q_out) {
         double* qo = a.q_out + (size_t)e * C::TILE + (size_t)item * LS;
 #pragma unroll
@@ -616,6 +652,15 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         for (int v = 0; v < M; ++v) B1[(dir * PD + item) * M + v] = fb[dir][v];
     }
     __syncthreads();
+    if (C::TR_STAGE && tid < EPB && valid_e[tid]) {
+      const size_t face_stride = (size_t)a.n_elem * C::TB;
+      const double* st = tiles + tid * C::ELEM + TP + C::ST_OFF;
+      double* dst = a.traces + (size_t)(g * EPB + tid) * C::TB;
+#pragma unroll
+      for (int f = 0; f < 2 * D; ++f)
+        bulk_s2g(dst + (size_t)f * face_stride, st + f * C::TB, C::TB * 8);
+      bulk_commit();
+    }
     // volume: contrib_dir = stiff x_dir fbar_dir (corrector.py:172-174)
     if (valid) spatial_line_tasks<D, P, 1>(B1, Q, T.stiff, gm1, item);
     __syncthreads();
@@ -634,17 +679,27 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #pragma unroll
         for (int v = 0; v < M; ++v) acc[v] += coef * CB[(dir * PD + item) * M + v];
       }
-      double* vo = a.vol + (size_t)e * PD * M + (size_t)item * M;
+      // own row of the dir-0 block is no longer read by anyone: stage there
+      if (lane_ok) {
 #pragma unroll
-      for (int v = 0; v < M; ++v) vo[v] = acc[v];
+        for (int v = 0; v < M; ++v) Q[item * M + v] = acc[v];
+      }
     }
     __syncthreads();
+    // coalesced copy of the group's volume blocks to HBM
+    for (int x = tid; x < EPB * PD * M; x += NT) {
+      const int ee = x / (PD * M);
+      const int off = x - ee * (PD * M);
+      if (g * EPB + ee < a.n_elem)
+        a.vol[(size_t)(g * EPB + ee) * PD * M + off] = tiles[ee * C::ELEM + off];
+    }
     if (tid < EPB && valid_e[tid]) {
       const int64_t ee = g * EPB + tid;
       a.pred_bad[ee] = !(conv[tid] && okf[tid]);
       a.sweeps[ee] = nsw[tid] ? nsw[tid] : it;
     }
   }
+  if (C::TR_STAGE && tid < EPB) bulk_wait_all();
 }
 
 template <int D, int P>
