@@ -165,6 +165,19 @@ int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partia
                double* totals_out, void* stream);
 
 /* -- a posteriori subcell limiter (limiter.py; driver.py:265-299) ------- */
+/* Exterior subcell averages for ADG_BC_GHOST ("exact") faces, the
+ * reference's _boundary_slab (driver.py:317-340) evaluated by the caller at
+ * t_n: slab[j][s] (device, NULL for other faces) holds `layers` subcell layers
+ * beyond face (j, s) as [len_0]..[len_{d-1}][m], len_i = n_i S + 2 layers
+ * for i < j (the axes padded before j, corners included), layers for i = j
+ * (outward order: index 0 is the farthest layer on side 0, the nearest on
+ * side 1), n_i S for i > j; layers >= max(S, 2). */
+typedef struct adg_subcell_ghosts {
+  const double* slab[3][2];
+  int32_t layers;
+  int32_t reserved;
+} adg_subcell_ghosts;
+
 /* Subcell averages of u^n (limiter.project_to_subcells, limiter.py:27-33)
  * sub_out [E, S^d, m] (S = 2N+1) and their per-cell extrema cmin/cmax
  * [E, m] (the per-cell part of limiter.relaxed_bounds, limiter.py:62-63).
@@ -177,11 +190,12 @@ int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, doub
  * max(delta0, eps (hi - lo)); a cell is troubled if a candidate subcell
  * average leaves them, a candidate nodal or subcell state is inadmissible,
  * pred_bad is set, or force_all != 0.  Writes troubled[E] (uint8), the
- * compacted list idx[*count] (int32, unordered) and *count (int32). */
+ * compacted list idx[*count] (int32, unordered) and *count (int32).
+ * ghosts: exterior slabs of ADG_BC_GHOST faces (NULL if there are none). */
 int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub, const double* cmin,
                const double* cmax, const double* cand, const uint8_t* pred_bad, double delta0,
-               double eps, int force_all, uint8_t* troubled, int32_t* idx, int32_t* count,
-               void* stream);
+               double eps, int force_all, const adg_subcell_ghosts* ghosts, uint8_t* troubled,
+               int32_t* idx, int32_t* count, void* stream);
 /* MUSCL-Hancock rescue of the listed cells from t^n subcell averages
  * (limiter.py:89-223 + driver.py:286-298), writing recovered nodal states
  * into u_out for listed cells (other cells untouched) and setting
@@ -189,7 +203,8 @@ int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub, const d
  * (driver.py:292-293 restart). */
 int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const int32_t* idx,
                const int32_t* count_dev, int32_t count_host_max, const double* dt_dev,
-               double* u_out, int32_t* failed_dev, void* stream);
+               const adg_subcell_ghosts* ghosts, double* u_out, int32_t* failed_dev,
+               void* stream);
 /* IC flattening (driver.py:137-152): cells whose nodal or subcell states are
  * inadmissible are replaced by their weighted mean; *nflat = count */
 int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat,

@@ -45,6 +45,12 @@ class Reduce(ctypes.Structure):
                 ("n_nonfinite", ctypes.c_uint64), ("reserved", ctypes.c_uint64 * 3)]
 
 
+class SubcellGhosts(ctypes.Structure):
+    """adg_subcell_ghosts: exterior subcell slabs of exact faces."""
+    _fields_ = [("slab", (ctypes.c_void_p * 2) * 3), ("layers", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
 REDUCE_WORDS = ctypes.sizeof(Reduce) // 8
 
 _P = ctypes.c_void_p
@@ -69,8 +75,8 @@ _SIGS = {
     "adg_totals_finalize": (_I, [_P, _P, _P, _I64, _P, _P]),
     "adg_totals": (_I, [_P, _P, _P, _P, _P, _P]),
     "adg_project_subcells": (_I, [_P, _P, _P, _P, _P, _P, _P]),
-    "adg_detect": (_I, [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _P, _P, _P, _P]),
-    "adg_rescue": (_I, [_P, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P]),
+    "adg_detect": (_I, [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _P]),
+    "adg_rescue": (_I, [_P, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P, _P]),
     "adg_flatten_ic": (_I, [_P, _P, _P, _P, _P]),
 }
 

@@ -42,6 +42,10 @@ struct LimGrid {
   double gm1, gamma;
   double h[3];  // subcell widths dx_j / S
   int prim;     // predictor_mode == "primitive": MUSCL-Hancock in primitive variables
+  // ADG_BC_GHOST ("exact") faces: caller-evaluated exterior subcell slabs
+  // (adg_subcell_ghosts); L = their layer count
+  const double* slab[3][2];
+  int L;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -79,26 +83,64 @@ __device__ __forceinline__ bool map_axis(int64_t g, int64_t nS, int bc_lo, int b
   return false;
 }
 
-// prev_sub value set (m doubles) at global subcell coordinate gs[]
+// prev_sub value set (m doubles) at global subcell coordinate gs[] of the
+// padded field.  The reference pads axis 0 first, then axis 1 on the padded
+// field, then axis 2 (driver.py:301-315), so the axes are resolved from the
+// last padded one down: periodic / outflow / wall map the coordinate into
+// the grid (wall: mirror + normal-momentum flip); an exact face reads the
+// caller's slab, which was evaluated at the raw coordinates of the axes
+// padded before it (corners included) and the mapped ones of those after.
 template <int D, int P>
 __device__ __forceinline__ void fetch_sub(const double* __restrict__ sub, const LimGrid& G,
                                           const int64_t* gs, double* out) {
   using C = LimCfg<D, P>;
   constexpr int S = C::S, M = C::M;
-  int64_t cc[3], loc[3];
+  int64_t g[3] = {0, 0, 0};
   bool flip[3] = {false, false, false};
 #pragma unroll
-  for (int j = 0; j < D; ++j) {
-    int64_t g;
-    map_axis(gs[j], G.n[j] * S, G.bc[j][0], G.bc[j][1], &g, &flip[j]);
-    cc[j] = g / S;
-    loc[j] = g - cc[j] * S;
-  }
-  int64_t e = cell_index<D>(cc, G.n);
-  int s = 0;
+  for (int j = 0; j < D; ++j) g[j] = gs[j];
+  const double* p = nullptr;
 #pragma unroll
-  for (int j = 0; j < D; ++j) s = s * S + (int)loc[j];
-  const double* p = sub + ((size_t)e * C::SD + s) * M;
+  for (int j = D - 1; j >= 0; --j) {
+    const int64_t nS = G.n[j] * S;
+    if (g[j] >= 0 && g[j] < nS) continue;
+    const int side = g[j] >= nS ? 1 : 0;
+    if (G.bc[j][side] == ADG_BC_GHOST) {
+      int64_t off = 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const int64_t ni = G.n[i] * S;
+        int64_t len, idx;
+        if (i < j) {
+          len = ni + 2 * G.L;
+          idx = g[i] + G.L;
+        } else if (i == j) {
+          len = G.L;
+          idx = side ? g[i] - ni : g[i] + G.L;
+        } else {
+          len = ni;
+          idx = g[i];
+        }
+        off = off * len + idx;
+      }
+      p = G.slab[j][side] + (size_t)off * M;
+      break;
+    }
+    map_axis(g[j], nS, G.bc[j][0], G.bc[j][1], &g[j], &flip[j]);
+  }
+  if (!p) {
+    int64_t cc[3], loc[3];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      cc[j] = g[j] / S;
+      loc[j] = g[j] - cc[j] * S;
+    }
+    const int64_t e = cell_index<D>(cc, G.n);
+    int s = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) s = s * S + (int)loc[j];
+    p = sub + ((size_t)e * C::SD + s) * M;
+  }
 #pragma unroll
   for (int v = 0; v < M; ++v) out[v] = p[v];
 #pragma unroll
@@ -242,6 +284,31 @@ __device__ void ghost_extrema(const double* __restrict__ sub, const double* __re
     for (int v = 0; v < M; ++v) {
       lo[v] = cmin[e * M + v];
       hi[v] = cmax[e * M + v];
+    }
+    return;
+  }
+  if (kind == ADG_BC_GHOST) {
+    // exact: the S^d caller-evaluated subcells of the ghost cell
+#pragma unroll
+    for (int v = 0; v < M; ++v) {
+      lo[v] = __longlong_as_double(0x7ff0000000000000LL);
+      hi[v] = -lo[v];
+    }
+    for (int s = 0; s < C::SD; ++s) {
+      int rem = s;
+      int64_t gs[3] = {0, 0, 0};
+      for (int a = D - 1; a >= 0; --a) {
+        const int ia = rem % S;
+        rem /= S;
+        gs[a] = a == j ? (side ? G.n[j] * S + ia : ia - S) : c[a] * S + ia;
+      }
+      double q[M];
+      fetch_sub<D, P>(sub, G, gs, q);
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        lo[v] = fmin(lo[v], q[v]);
+        hi[v] = fmax(hi[v], q[v]);
+      }
     }
     return;
   }
@@ -733,8 +800,11 @@ flatten_ic_kernel(double* __restrict__ u, int64_t E, double gm1, int32_t* nflat)
 }
 
 // ------------------------------------------------------------- launchers
-static LimGrid lim_grid(const adg_grid* g) {
+static LimGrid lim_grid(const adg_grid* g, const adg_subcell_ghosts* gh = nullptr) {
   LimGrid G;
+  for (int j = 0; j < 3; ++j)
+    for (int s = 0; s < 2; ++s) G.slab[j][s] = gh ? gh->slab[j][s] : nullptr;
+  G.L = gh ? gh->layers : 0;
   const int S = 2 * g->degree + 1;
   for (int j = 0; j < 3; ++j) {
     G.n[j] = j < g->dim ? g->cells[j] : 1;
@@ -775,11 +845,12 @@ static bool set_smem(K kern, size_t bytes) {
   return true;
 }
 
-static bool lim_supported(const adg_grid* g, std::string* err) {
+static bool lim_supported(const adg_grid* g, const adg_subcell_ghosts* gh, std::string* err) {
+  const int need = 2 * g->degree + 1 > 2 ? 2 * g->degree + 1 : 2;
   for (int j = 0; j < g->dim; ++j)
     for (int s = 0; s < 2; ++s)
-      if (g->bc[j][s] == ADG_BC_GHOST) {
-        *err = "the subcell limiter supports periodic / outflow / wall faces on the device";
+      if (g->bc[j][s] == ADG_BC_GHOST && (!gh || !gh->slab[j][s] || gh->layers < need)) {
+        *err = "ghost (exact) face without an exterior subcell slab of >= max(S, 2) layers";
         return false;
       }
   return true;
@@ -843,8 +914,9 @@ static int launch_prep(const adg_grid* g, const double* u, double* sub, double* 
 template <int D, int P>
 static int launch_detect(const adg_grid* g, const double* prev_sub, const double* cmin,
                          const double* cmax, const double* cand, const uint8_t* pred_bad,
-                         double d0, double eps, int force, uint8_t* troubled, int32_t* idx,
-                         int32_t* count, cudaStream_t st, std::string* err) {
+                         double d0, double eps, int force, const adg_subcell_ghosts* gh,
+                         uint8_t* troubled, int32_t* idx, int32_t* count, cudaStream_t st,
+                         std::string* err) {
   const size_t sm = proj_smem<D, P>();
   if (!set_smem(detect_kernel<D, P>, sm)) {
     *err = "limiter tile exceeds shared memory";
@@ -854,15 +926,16 @@ static int launch_detect(const adg_grid* g, const double* prev_sub, const double
   const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
   cudaMemsetAsync(count, 0, sizeof(int32_t), st);
   detect_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(prev_sub, cmin, cmax, cand, pred_bad,
-                                                          lim_grid(g), E, d0, eps, force,
+                                                          lim_grid(g, gh), E, d0, eps, force,
                                                           troubled, idx, count);
   return lerr(err);
 }
 
 template <int D, int P>
 static int launch_rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
-                         const int32_t* count, int32_t cmax, const double* dt, double* u_out,
-                         int32_t* failed, cudaStream_t st, std::string* err) {
+                         const int32_t* count, int32_t cmax, const double* dt,
+                         const adg_subcell_ghosts* gh, double* u_out, int32_t* failed,
+                         cudaStream_t st, std::string* err) {
   const size_t sm = rescue_smem<D, P>();
   if (!set_smem(rescue_kernel<D, P>, sm)) {
     *err = "limiter window exceeds shared memory";
@@ -870,7 +943,7 @@ static int launch_rescue(const adg_grid* g, const double* prev_sub, const int32_
   }
   if (cmax <= 0) return ADG_OK;
   rescue_kernel<D, P><<<(unsigned)cmax, LimCfg<D, P>::NT, sm, st>>>(prev_sub, idx, count,
-                                                                   lim_grid(g), dt, u_out,
+                                                                   lim_grid(g, gh), dt, u_out,
                                                                    failed);
   return lerr(err);
 }
@@ -899,21 +972,23 @@ int project_subcells(const adg_grid* g, const double* u, double* sub, double* cm
 
 int detect(const adg_grid* g, const double* prev_sub, const double* cmin, const double* cmax,
            const double* cand, const uint8_t* pred_bad, double delta0, double eps, int force_all,
-           uint8_t* troubled, int32_t* idx, int32_t* count, cudaStream_t st, std::string* err) {
-  if (!lim_supported(g, err)) return ADG_ERR_UNSUPPORTED;
+           const adg_subcell_ghosts* gh, uint8_t* troubled, int32_t* idx, int32_t* count,
+           cudaStream_t st, std::string* err) {
+  if (!lim_supported(g, gh, err)) return ADG_ERR_UNSUPPORTED;
   int rc = ADG_OK;
   ADG_LIM_SWITCH(launch_detect, g, prev_sub, cmin, cmax, cand, pred_bad, delta0, eps, force_all,
-                 troubled, idx, count, st, err);
+                 gh, troubled, idx, count, st, err);
   return rc;
 }
 
 int rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
-           const int32_t* count_dev, int32_t count_max, const double* dt_dev, double* u_out,
-           int32_t* failed, cudaStream_t st, std::string* err) {
-  if (!lim_supported(g, err)) return ADG_ERR_UNSUPPORTED;
+           const int32_t* count_dev, int32_t count_max, const double* dt_dev,
+           const adg_subcell_ghosts* gh, double* u_out, int32_t* failed, cudaStream_t st,
+           std::string* err) {
+  if (!lim_supported(g, gh, err)) return ADG_ERR_UNSUPPORTED;
   int rc = ADG_OK;
-  ADG_LIM_SWITCH(launch_rescue, g, prev_sub, idx, count_dev, count_max, dt_dev, u_out, failed, st,
-                 err);
+  ADG_LIM_SWITCH(launch_rescue, g, prev_sub, idx, count_dev, count_max, dt_dev, gh, u_out, failed,
+                 st, err);
   return rc;
 }
 

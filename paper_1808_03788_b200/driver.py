@@ -149,6 +149,12 @@ class Simulation:
         self._h = _lib.Handle.get(self.device.index)
         self._h.ensure_tables(self.tables)
         self._ghost = _ghost or {}
+        # "exact" faces: exterior traces / subcell slabs evaluated from
+        # exact_solution on the host each step (driver.py:250-261, :317-340)
+        # and handed to the kernels as ADG_BC_GHOST data
+        self._exact_faces = [k for k, v in self.boundary.items()
+                             if v == "exact" and k not in self._ghost]
+        self._exact_trace = {}
         d = mesh.dim
         self._P = degree + 1
         self._m = system.n_vars
@@ -260,11 +266,85 @@ class Simulation:
                      0, self.min_picard_iter, _ptr(q_out), _ptr(buf.vol), _ptr(buf.traces),
                      _ptr(buf.pred_bad), _ptr(buf.sweeps), _stream_ptr())
 
+    # -- exact faces ----------------------------------------------------
+    def _trace_strides(self, axis):
+        """(tangential strides..., time stride) of a face trace block in units
+        of m (the predictor's owner-role order, adg_predict)."""
+        P = self._P
+        d = self.mesh.dim
+        if d == 3:
+            return {0: ((P * P, P), 1), 1: ((1, P * P), P), 2: ((P, 1), P * P)}[axis]
+        if d == 2:
+            return {0: ((P,), 1), 1: ((1,), P)}[axis]
+        return ((), 1)
+
+    def _fill_exact_traces(self, dt):
+        """Exterior space-time traces of the exact faces for a step of dt
+        (driver._ghost_trace, driver.py:250-261), in trace-block layout."""
+        if not self._exact_faces:
+            return
+        buf = self._buf
+        P, m, d = self._P, self._m, self.mesh.dim
+        for (axis, side) in self._exact_faces:
+            pts = self.mesh.face_node_coords(self.tables, axis, side)
+            vals = np.stack([np.asarray(self.exact_solution(pts, self.t + tau * dt), dtype=float)
+                             for tau in self.tables.nodes], axis=-2)
+            nplanes = self.mesh.n_elements // self.mesh.cells[axis]
+            vals = vals.reshape((nplanes,) + (P,) * (d - 1) + (P, m))
+            tang, st = self._trace_strides(axis)
+            pos = np.zeros((P,) * (d - 1) + (P,), dtype=np.int64)
+            for k, stride in enumerate(tang):
+                sh = [1] * d
+                sh[k] = P
+                pos = pos + stride * np.arange(P).reshape(sh)
+            sh = [1] * d
+            sh[d - 1] = P
+            pos = pos + st * np.arange(P).reshape(sh)
+            block = np.zeros((nplanes, buf.tb))
+            cols = (pos[..., None] * m + np.arange(m)).reshape(-1)
+            block[:, cols] = vals.reshape(nplanes, -1)
+            dst = self._exact_trace.get((axis, side))
+            if dst is None:
+                dst = torch.empty(nplanes * buf.tb, dtype=torch.float64, device=self.device)
+                self._exact_trace[(axis, side)] = dst
+            dst.copy_(torch.from_numpy(block.reshape(-1)))
+
+    def _exact_subcell_ghosts(self):
+        """adg_subcell_ghosts for the exact faces at t_n (driver._boundary_slab,
+        driver.py:317-340): slab (j, s) spans the axes padded before j with
+        their ghost layers, its own `layers` ghost layers, and the interior of
+        the later axes."""
+        if not self._exact_faces:
+            return None
+        d = self.mesh.dim
+        S = self.tables.n_subcells
+        L = max(S, 2)
+        gh = _lib.SubcellGhosts()
+        gh.layers = L
+        keep = []
+        for (axis, side) in self._exact_faces:
+            coords = []
+            for i in range(d):
+                if i < axis:
+                    coords.append(self.mesh.subcell_axis_coords(i, S, L))
+                elif i == axis:
+                    full = self.mesh.subcell_axis_coords(i, S, L)
+                    coords.append(full[:L] if side == 0 else full[-L:])
+                else:
+                    coords.append(self.mesh.subcell_axis_coords(i, S, 0))
+            pts = np.stack(np.meshgrid(*coords, indexing="ij"), axis=-1)
+            vals = np.ascontiguousarray(np.asarray(self.exact_solution(pts, self.t), dtype=float))
+            dev = torch.from_numpy(vals.reshape(-1)).to(self.device)
+            keep.append(dev)
+            gh.slab[axis][side] = dev.data_ptr()
+        self._exact_slabs = keep   # keep the device copies alive
+        return gh
+
     def _faces(self):
         buf = self._buf
         for a in range(self.mesh.dim):
-            glo = self._ghost.get((a, 0))
-            ghi = self._ghost.get((a, 1))
+            glo = self._ghost.get((a, 0), self._exact_trace.get((a, 0)))
+            ghi = self._ghost.get((a, 1), self._exact_trace.get((a, 1)))
             self._h.call("adg_face_flux", self._gp(), a, _ptr(buf.traces), _ptr(glo),
                          _ptr(ghi), _ptr(buf.fd), _stream_ptr())
 
@@ -334,6 +414,7 @@ class Simulation:
     def _attempt(self, row, trial):
         buf = self._buf
         dt_dev = row[0:1]
+        self._fill_exact_traces(trial)
         if not self.use_limiter:
             self._enqueue_unlimited(dt_dev, row[2:], row[1:2])
             self.sweep_log.append(int(buf.sweeps.max().item()))
@@ -374,16 +455,18 @@ class Simulation:
         self.sweep_log.append(None)
         self._faces()
         nxt = self._update(dt_dev, None)
+        gh = self._exact_subcell_ghosts()
+        ghp = _lib.ctypes.byref(gh) if gh is not None else None
         self._h.call("adg_detect", self._gp(), _ptr(lb["sub"]), _ptr(lb["cmin"]),
                      _ptr(lb["cmax"]), _ptr(self._u_next), _ptr(buf.pred_bad), self.dmp_delta0,
-                     self.dmp_eps, int(bool(self.force_limit_all)), _ptr(lb["troubled"]),
+                     self.dmp_eps, int(bool(self.force_limit_all)), ghp, _ptr(lb["troubled"]),
                      _ptr(lb["idx"]), _ptr(lb["count"]), sp)
         n_tr = int(lb["count"].item())
         self.sweep_log[-1] = int(buf.sweeps.max().item())
         if n_tr:
             lb["failed"].zero_()
             self._h.call("adg_rescue", self._gp(), _ptr(lb["sub"]), _ptr(lb["idx"]),
-                         _ptr(lb["count"]), n_tr, _ptr(dt_dev), _ptr(self._u_next),
+                         _ptr(lb["count"]), n_tr, _ptr(dt_dev), ghp, _ptr(self._u_next),
                          _ptr(lb["failed"]), sp)
             if int(lb["failed"].item()):
                 return False, 0.0, None   # driver.py:292-293 -> restart with dt/2
@@ -405,7 +488,7 @@ class Simulation:
         scale = abs(t_end) if np.isfinite(t_end) else 1.0
         tiny = 1e-12 * max(1.0, scale)
         fast = (on_step is None and not self.use_limiter and not np.isfinite(t_end)
-                and max_steps is not None)
+                and max_steps is not None and not self._exact_faces)
         if fast:
             self._run_batch(max(0, max_steps - self.step_count))
             return self.step_count

@@ -227,8 +227,74 @@ def gen_primitive():
              icb, 4, boundary="wall", use_limiter=True, predictor_mode="primitive")
 
 
+def gen_output():
+    """Diagnostics / snapshot text of the reference writers (output.py) for a
+    small Sod run (the determinism acceptance case, test_acceptance.py:354-366,
+    at fewer steps) and a 2-D vortex state: formatting parity fixtures."""
+    from aderdg import output
+    e1 = CompressibleEuler(1, gamma=GAMMA)
+    ics, _ = problems.sod()
+    sim = aderdg.Simulation(aderdg.CartesianMesh([(0, 1)], (50,)), e1, 2, 0.15,
+                            boundary="outflow", use_limiter=True)
+    sim.project_initial_condition(ics)
+    sim.run(np.inf, max_steps=8)
+    hist = sim.history
+    arrays = dict(
+        steps=np.array([h["step"] for h in hist]), times=np.array([h["time"] for h in hist]),
+        dts=np.array([h["dt"] for h in hist]), totals=np.array([h["totals"] for h in hist]),
+        fracs=np.array([h["limited_fraction"] for h in hist]),
+        diag_csv=np.array(output.diagnostics_csv(hist, e1.quantity_names)),
+        u=sim.u, t=np.array(sim.t), step_count=np.array(sim.step_count),
+        fields_csv=np.array(output.fields_csv(sim)), fields_vtk=np.array(output.fields_vtk(sim)),
+        names=np.array(e1.quantity_names))
+    e2 = CompressibleEuler(2, gamma=GAMMA)
+    ic, _ = problems.vortex()
+    sim2 = aderdg.Simulation(aderdg.CartesianMesh([(0, 10), (0, 10)], (4, 3)), e2, 2, 0.1)
+    sim2.project_initial_condition(ic)
+    sim2.run(np.inf, max_steps=1)
+    arrays.update(u2=sim2.u, t2=np.array(sim2.t), vtk2=np.array(output.fields_vtk(sim2)),
+                  csv2=np.array(output.fields_csv(sim2)),
+                  tdu=np.array(aderdg.kernels.throughput_per_dof(1.25, 4096, 20, 4, 3)))
+    save("output_sod", **arrays)
+
+
+def static_exact(ic):
+    """A time-independent "exact" solution (Dirichlet data = the IC)."""
+    return lambda x, t: ic(x)
+
+
+def gen_exact():
+    """"exact" faces (driver.py:250-261, :317-340): a 2-D density wave with
+    its true translating solution on every face (unlimited), and a limited
+    explosion whose Dirichlet data is the static IC, mixed with outflow and
+    wall faces so ghost corners combine exact with other kinds."""
+    e2 = CompressibleEuler(2, gamma=GAMMA)
+    ic, ex = problems.density_wave(vel=(1.0, 0.5))
+    sim = aderdg.Simulation(aderdg.CartesianMesh([(0, 1), (0, 1)], (8, 6)), e2, 3, 0.9 / 14.0,
+                            boundary="exact", exact_solution=ex)
+    u0 = sim.project_initial_condition(ic).copy()
+    sim.run(np.inf, max_steps=5)
+    save("exact_wave2d", u0=u0, u=sim.u, dts=np.array([h["dt"] for h in sim.history]),
+         degree=np.array(3), cfl=np.array(0.9 / 14.0), cells=np.array(sim.mesh.cells),
+         extents=np.array(sim.mesh.extents))
+    ic4, _ = problems.explosion()
+    bnd = {0: ("exact", "outflow"), 1: ("wall", "exact")}
+    sim = aderdg.Simulation(aderdg.CartesianMesh([(-0.8, 0.8), (-0.8, 0.8)], (12, 12)), e2, 2,
+                            0.15, boundary=bnd, use_limiter=True,
+                            exact_solution=static_exact(ic4))
+    u0 = sim.project_initial_condition(ic4).copy()
+    flags = []
+    for _ in range(8):
+        sim.run(np.inf, max_steps=sim.step_count + 1)
+        flags.append(np.asarray(sim.last_troubled, dtype=bool))
+    save("exact_explosion", u0=u0, u=sim.u, dts=np.array([h["dt"] for h in sim.history]),
+         troubled=np.stack(flags), degree=np.array(2), cfl=np.array(0.15),
+         cells=np.array(sim.mesh.cells), extents=np.array(sim.mesh.extents))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tables", "pointwise", "predictor", "cases", "primitive"]
+    which = sys.argv[1:] or ["tables", "pointwise", "predictor", "cases", "primitive", "output",
+                             "exact"]
     if "tables" in which:
         gen_tables()
     if "pointwise" in which:
@@ -239,3 +305,7 @@ if __name__ == "__main__":
         gen_cases()
     if "primitive" in which:
         gen_primitive()
+    if "output" in which:
+        gen_output()
+    if "exact" in which:
+        gen_exact()

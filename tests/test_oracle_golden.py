@@ -201,3 +201,37 @@ def test_case_primitive_mode(golden, name, icname, bc, limited):
     np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-13)
     assert sim.sweep_log == list(g["iters"])
     assert _rel(sim.u, g["u"]) <= 1e-12
+
+
+def test_case_exact_faces(golden):
+    """"exact" faces (driver.py:250-261, :317-340): translating density wave
+    with its exact solution on every face, unlimited."""
+    g = golden("exact_wave2d")
+    ic, ex = problems.density_wave(vel=(1.0, 0.5))
+    mesh = _mesh_from(g)
+    sim = OracleSimulation(mesh, EulerOracle(2), int(g["degree"]), float(g["cfl"]),
+                           boundary="exact", exact_solution=ex)
+    sim.project_initial_condition(ic)
+    np.testing.assert_allclose(sim.u, g["u0"], rtol=0, atol=1e-14)
+    sim.run(np.inf, max_steps=len(g["dts"]))
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-13)
+    assert _rel(sim.u, g["u"]) <= 1e-12
+
+
+def test_case_exact_faces_limited(golden):
+    """Limited explosion with static Dirichlet ("exact") data mixed with
+    outflow / wall faces: exact ghost subcells incl. corners."""
+    g = golden("exact_explosion")
+    ic, _ = problems.explosion()
+    mesh = _mesh_from(g)
+    sim = OracleSimulation(mesh, EulerOracle(2), int(g["degree"]), float(g["cfl"]),
+                           boundary={0: ("exact", "outflow"), 1: ("wall", "exact")},
+                           use_limiter=True, exact_solution=lambda x, t: ic(x))
+    sim.project_initial_condition(ic)
+    flags = []
+    for _ in range(len(g["dts"])):
+        sim.run(np.inf, max_steps=sim.step_count + 1)
+        flags.append(sim.last_troubled.copy())
+    np.testing.assert_array_equal(np.stack(flags), g["troubled"])
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-13)
+    assert _rel(sim.u, g["u"]) <= 1e-12
