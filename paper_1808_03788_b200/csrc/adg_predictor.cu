@@ -439,6 +439,38 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       // A: y/z-owners publish their partials first, then the x-owner's
       // -D_x F_x (PRIM: +D_x v) accumulates straight into `rate`, so only
       // one P x M block is live at a time
+      // y-owner, accumulating: dst += D_y F_y (RMW schedule below)
+      auto ypass_add = [&](double* dst) {
+        double acc[P][M];
+        line_pass([&](int l) { return node3<D, P>(yi, l, yk) * LS + yt * M; }, 1, Dy, 1.0, acc);
+#pragma unroll
+        for (int jj = 0; jj < P; ++jj)
+#pragma unroll
+          for (int v = 0; v < M; ++v) dst[xline<D, P>(jj, yk, yt) * LS + yi * M + v] += acc[jj][v];
+      };
+      // Two-buffer 3-D schedule (conservative mode): the z partials go to B1,
+      // the y-owners add theirs in place, and the x-owner subtracts the sum
+      // from its own -D_x F_x: rate = -D_x F_x - (D_z F_z + D_y F_y).  Same
+      // shared traffic as three buffers, one more barrier, 2/3 of the shared
+      // footprint and only one P x M block live per phase.
+      constexpr bool RMW = C::SEQ_YZ && !PRIM;
+      if constexpr (RMW) {
+        if (work) zpass(B1);
+        __syncthreads();
+        if (work) ypass_add(B1);
+        __syncthreads();
+        if (work) {
+          line_pass([&](int l) { return node3<D, P>(l, xj, xk) * LS + xt * M; }, 0, Dx, -1.0,
+                    rate);
+#pragma unroll
+          for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int v = 0; v < M; ++v) {
+              const double r = rate[i][v] - B1[item * LS + i * M + v];
+              B1[item * LS + i * M + v] = r;
+            }
+        }
+      } else {
       if (work) {
         if (D == 3 && !C::SEQ_YZ) zpass(B2);
         if (D >= 2) ypass(B1);
@@ -496,6 +528,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         for (int i = 0; i < P; ++i)
 #pragma unroll
           for (int v = 0; v < M; ++v) B1[item * LS + i * M + v] = rate[i][v];
+      }
       }
       __syncthreads();
       // C: node role, time operator + residual; rate(node, s) sits in the
