@@ -510,20 +510,77 @@ class Simulation:
         red = self._buf.red[self._red_cur]
         return int(red[4].item()) == 0
 
+    def _step_into(self, rows, status, sweeps, s):
+        """Enqueue one unlimited step writing its history row / status /
+        sweep count into slot s of the given device buffers."""
+        self._timestep_into(rows[s, 0:1], status[s:s + 1], math.inf)
+        self._enqueue_unlimited(rows[s, 0:1], rows[s, 2:], rows[s, 1:2])
+        torch.amax(self._buf.sweeps, dim=0, keepdim=True, out=sweeps[s:s + 1])
+
+    # CUDA graph of two consecutive steps (the u / u_next and wave-speed
+    # double buffers return to their starting roles after two steps), replayed
+    # with a device-side slot counter; removes the per-launch host cost that
+    # bounds small grids (C1: ~8 launches per step)
+    graphs_enabled = True
+
+    def _batch_buffers(self, k):
+        bb = getattr(self, "_bb", None)
+        if bb is None or bb["cap"] < k:
+            cap = max(k, 64)
+            dev = self.device
+            bb = {"cap": cap,
+                  "rows": torch.zeros(cap, 2 + self._m, dtype=torch.float64, device=dev),
+                  "status": torch.zeros(cap, dtype=torch.int32, device=dev),
+                  "sweeps": torch.zeros(cap, dtype=torch.int32, device=dev),
+                  "cnt": torch.zeros(1, dtype=torch.int64, device=dev),
+                  "srow": torch.zeros(2, 2 + self._m, dtype=torch.float64, device=dev),
+                  "sst": torch.zeros(2, dtype=torch.int32, device=dev),
+                  "ssw": torch.zeros(2, dtype=torch.int32, device=dev),
+                  "graphs": {}}
+            self._bb = bb
+        return bb
+
+    def _pair_graph(self, bb):
+        key = (self._u.data_ptr(), self._red_cur)
+        g = bb["graphs"].get(key)
+        if g is not None:
+            return g
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for j in range(2):
+                self._step_into(bb["srow"], bb["sst"], bb["ssw"], j)
+                bb["rows"].index_copy_(0, bb["cnt"], bb["srow"][j:j + 1])
+                bb["status"].index_copy_(0, bb["cnt"], bb["sst"][j:j + 1])
+                bb["sweeps"].index_copy_(0, bb["cnt"], bb["ssw"][j:j + 1])
+                bb["cnt"].add_(1)
+        # capture only recorded the launches: state is back where it started
+        bb["graphs"][key] = g
+        return g
+
     def _run_batch(self, k):
         """k device-resident steps with one host synchronisation at the end."""
         if k <= 0:
             return
         buf = self._buf
         m = self._m
-        rows = torch.zeros(k, 2 + m, dtype=torch.float64, device=self.device)
-        status = torch.zeros(k, dtype=torch.int32, device=self.device)
-        sweeps = torch.zeros(k, dtype=torch.int32, device=self.device)
+        bb = self._batch_buffers(k)
+        rows, status, sweeps = bb["rows"][:k], bb["status"][:k], bb["sweeps"][:k]
+        rows.zero_()
+        status.zero_()
         buf.t.fill_(self.t)
-        for s in range(k):
-            self._timestep_into(rows[s, 0:1], status[s:s + 1], math.inf)
-            self._enqueue_unlimited(rows[s, 0:1], rows[s, 2:], rows[s, 1:2])
-            torch.amax(buf.sweeps, dim=0, keepdim=True, out=sweeps[s:s + 1])
+        use_graph = self.graphs_enabled and self._exchange is None
+        s = 0
+        while s < k:
+            if use_graph and self._red_cur is not None and k - s >= 2:
+                g = self._pair_graph(bb)
+                bb["cnt"].fill_(s)
+                while k - s >= 2:
+                    g.replay()
+                    s += 2
+                continue
+            self._step_into(bb["rows"], bb["status"], bb["sweeps"], s)
+            s += 1
         self._combine_rows(rows)
         host = rows.cpu().numpy()
         st = status.cpu().numpy()

@@ -27,7 +27,7 @@ from paper_1808_03788_b200 import roofline  # noqa: E402
 
 
 def run_case(name, ext, cells, degree, cfl, problem, steps, boundary="periodic",
-             limiter=False, warmup=2, t_end=np.inf):
+             limiter=False, warmup=3, t_end=np.inf):
     d = len(cells)
     system = pkg.make_system("euler", d)
     sim = pkg.Simulation(pkg.CartesianMesh(ext, cells), system, degree, cfl,
