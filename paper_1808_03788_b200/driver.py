@@ -32,6 +32,7 @@ BOUNDARY_KINDS = ("periodic", "outflow", "wall", "exact")
 
 DMP_DELTA0 = 1e-3   # limiter.py:22
 DMP_EPS = 1e-3      # limiter.py:23
+GRAPH_MAX_DOFS = 1 << 21   # batched steps replay a CUDA graph below this size
 MAX_HALVINGS = 3    # limiter.py:24
 
 DEFAULT_CFL = {0: 0.9, 1: 0.30, 2: 0.15, 3: 0.09, 4: 0.062, 5: 0.044,
@@ -569,7 +570,10 @@ class Simulation:
         rows.zero_()
         status.zero_()
         buf.t.fill_(self.t)
-        use_graph = self.graphs_enabled and self._exchange is None
+        # only launch-bound grids gain from the graph (capture + instantiate
+        # costs tens of ms once; a C2-size step is ~16 ms of GPU work)
+        use_graph = (self.graphs_enabled and self._exchange is None
+                     and self.mesh.n_elements * self._pd <= GRAPH_MAX_DOFS)
         s = 0
         while s < k:
             if use_graph and self._red_cur is not None and k - s >= 2:
