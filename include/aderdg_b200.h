@@ -210,6 +210,41 @@ int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const i
 int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat,
                    void* stream);
 
+/* -- module-level pieces: the reference's corrector / limiter functions on
+ *    arrays in the reference layouts (element grid flattened: E = product
+ *    of g->cells), for callers of the module API rather than Simulation.
+ *    dt_dev is a device scalar.  -------------------------------------------- */
+/* corrector.face_fluxes (corrector.py:100-129): n point pairs [n][m] ->
+ * d_low, d_high [n][m] across a face with normal +e_axis */
+int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const double* q_minus,
+                    const double* q_plus, double* d_low, double* d_high, void* stream);
+/* corrector.volume_integral (corrector.py:141-177): q [E][P^d][P_t][m] ->
+ * vol [E][P^d][m] */
+int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const double* dt_dev,
+                        double* vol_out, void* stream);
+/* corrector.face_integral (corrector.py:180-196): d_values
+ * [E][P^(d-1) tangential][P_t][m] of face (axis, side) -> [E][P^d][m] */
+int adg_face_integral(adg_handle* h, const adg_grid* g, int axis, int side,
+                      const double* d_values, const double* dt_dev, double* out, void* stream);
+/* corrector.element_update (corrector.py:199-205): u + (vol - acc_0 - ..)
+ * / mass; accs is a host array of n_acc (<= 6) device pointers */
+int adg_element_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
+                       const double* const* accs, int n_acc, double* u_out, void* stream);
+/* limiter.muscl_subcell_step (limiter.py:104-121) on caller windows
+ * [T][(S+4)^d][m] (count_dev: device int32 holding T): new averages
+ * [T][S^d][m], failed[T] (uint8).  Here g->dx are the SUBCELL widths and
+ * g->mode selects the conservative / primitive half step. */
+int adg_muscl_windows(adg_handle* h, const adg_grid* g, const double* windows, int64_t n_windows,
+                      const int32_t* count_dev, const double* dt_dev, double* avg_out,
+                      uint8_t* failed, void* stream);
+/* limiter.recover_from_subcells (limiter.py:36-42): [E][S^d][m] -> [E][P^d][m] */
+int adg_recover_subcells(adg_handle* h, const adg_grid* g, const double* ubar, double* u_out,
+                         void* stream);
+/* limiter.flatten_inadmissible (limiter.py:205-223), in place on nodal
+ * [E][P^d][m] with the cells' averages [E][S^d][m]; *nflat = cells flattened */
+int adg_flatten_cells(adg_handle* h, const adg_grid* g, double* nodal, const double* averages,
+                      int32_t* nflat, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,7 +29,9 @@ EXPORTS = (
     "adg_create", "adg_destroy", "adg_last_error", "adg_version", "adg_set_tables",
     "adg_wavespeed", "adg_timestep", "adg_advance_time", "adg_predict", "adg_face_flux", "adg_update",
     "adg_update_blocks", "adg_trace_block", "adg_totals_finalize", "adg_totals", "adg_project_subcells",
-    "adg_detect", "adg_rescue", "adg_flatten_ic",
+    "adg_detect", "adg_rescue", "adg_flatten_ic", "adg_face_fluxes", "adg_volume_integral",
+    "adg_face_integral", "adg_element_update", "adg_muscl_windows", "adg_recover_subcells",
+    "adg_flatten_cells",
 )
 
 
@@ -78,6 +80,13 @@ _SIGS = {
     "adg_detect": (_I, [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _P]),
     "adg_rescue": (_I, [_P, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P, _P]),
     "adg_flatten_ic": (_I, [_P, _P, _P, _P, _P]),
+    "adg_face_fluxes": (_I, [_P, _P, _I, _I64, _P, _P, _P, _P, _P]),
+    "adg_volume_integral": (_I, [_P, _P, _P, _P, _P, _P]),
+    "adg_face_integral": (_I, [_P, _P, _I, _I, _P, _P, _P, _P]),
+    "adg_element_update": (_I, [_P, _P, _P, _P, _P, _I, _P, _P]),
+    "adg_muscl_windows": (_I, [_P, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    "adg_recover_subcells": (_I, [_P, _P, _P, _P, _P]),
+    "adg_flatten_cells": (_I, [_P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

@@ -244,6 +244,71 @@ int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const i
                              failed_dev, (cudaStream_t)stream, &e), e);
 }
 
+int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const double* q_minus,
+                    const double* q_plus, double* d_low, double* d_high, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (axis < 0 || axis >= g->dim) return fail(h, ADG_ERR_INVALID, "axis out of range");
+  std::string e;
+  return wrap(h, adg::face_points(g, axis, n, q_minus, q_plus, d_low, d_high,
+                                  (cudaStream_t)stream, &e), e);
+}
+
+int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const double* dt_dev,
+                        double* vol_out, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::volume_integral(g, q, dt_dev, vol_out, (cudaStream_t)stream, &e), e);
+}
+
+int adg_face_integral(adg_handle* h, const adg_grid* g, int axis, int side,
+                      const double* d_values, const double* dt_dev, double* out, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (axis < 0 || axis >= g->dim || side < 0 || side > 1)
+    return fail(h, ADG_ERR_INVALID, "axis / side out of range");
+  std::string e;
+  return wrap(h, adg::face_integral(g, axis, side, d_values, dt_dev, out, (cudaStream_t)stream,
+                                    &e), e);
+}
+
+int adg_element_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
+                       const double* const* accs, int n_acc, double* u_out, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (n_acc < 0 || n_acc > 6 || (n_acc > 0 && !accs))
+    return fail(h, ADG_ERR_INVALID, "0..6 face accumulators");
+  std::string e;
+  return wrap(h, adg::element_update(g, u, vol, accs, n_acc, u_out, (cudaStream_t)stream, &e), e);
+}
+
+int adg_muscl_windows(adg_handle* h, const adg_grid* g, const double* windows, int64_t n_windows,
+                      const int32_t* count_dev, const double* dt_dev, double* avg_out,
+                      uint8_t* failed, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::muscl_windows(g, windows, n_windows, count_dev, dt_dev, avg_out, failed,
+                                    (cudaStream_t)stream, &e), e);
+}
+
+int adg_recover_subcells(adg_handle* h, const adg_grid* g, const double* ubar, double* u_out,
+                         void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::recover_subcells(g, ubar, u_out, (cudaStream_t)stream, &e), e);
+}
+
+int adg_flatten_cells(adg_handle* h, const adg_grid* g, double* nodal, const double* averages,
+                      int32_t* nflat, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  std::string e;
+  return wrap(h, adg::flatten_cells(g, nodal, averages, nflat, (cudaStream_t)stream, &e), e);
+}
+
 int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat, void* stream) {
   int rc = check_grid(h, g);
   if (rc) return rc;

@@ -189,6 +189,30 @@ __device__ __forceinline__ bool admissible(const double* q, double gm1) {
   return fin && (q[0] > 0.0) && (p > 0.0);
 }
 
+// Rusanov one-sided terms (corrector.py:100-129) for a subcell face
+template <int D>
+__device__ __forceinline__ void rusanov_pair(const double* qm, const double* qp, int a,
+                                             double gamma, double gm1, double* dlow,
+                                             double* dhigh) {
+  constexpr int M = D + 2;
+  const double s = fmax(max_abs_eig<D>(qm, gamma, gm1, a), max_abs_eig<D>(qp, gamma, gm1, a));
+  double fm[M], fp[M];
+  flux_axis<D>(qm, gm1, a, fm);
+  flux_axis<D>(qp, gm1, a, fp);
+  const double hs = 0.5 * s;
+#pragma unroll
+  for (int v = 0; v < M; ++v) {
+    const double central = 0.5 * (fm[v] + fp[v]);
+    const double diss = hs * (qp[v] - qm[v]);
+    dlow[v] = (central + 0.0) - diss;
+    dhigh[v] = (-central + 0.0) + diss;
+  }
+}
+
+__device__ __forceinline__ double minmod(double a, double b) {
+  return (a * b > 0.0) ? (fabs(a) <= fabs(b) ? a : b) : 0.0;
+}
+
 __device__ __forceinline__ void atomic_max_pos(uint64_t* addr, double v) {
   // v >= 0 and finite: IEEE bit patterns order like unsigned integers
   atomicMax(reinterpret_cast<unsigned long long*>(addr),

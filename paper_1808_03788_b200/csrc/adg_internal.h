@@ -52,6 +52,25 @@ int rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
 int flatten_ic(const adg_grid* g, double* u, int32_t* nflat, cudaStream_t st,
                std::string* err);
 
+int muscl_windows(const adg_grid* g, const double* windows, int64_t nwin,
+                  const int32_t* count_dev, const double* dt_dev, double* avg_out,
+                  uint8_t* fail_each, cudaStream_t st, std::string* err);
+int recover_subcells(const adg_grid* g, const double* ubar, double* out, cudaStream_t st,
+                     std::string* err);
+int flatten_cells(const adg_grid* g, double* nodal, const double* averages, int32_t* nflat,
+                  cudaStream_t st, std::string* err);
+
+// corrector module pieces (adg_pieces.cu)
+int face_points(const adg_grid* g, int axis, int64_t n, const double* qm, const double* qp,
+                double* dlow, double* dhigh, cudaStream_t st, std::string* err);
+int volume_integral(const adg_grid* g, const double* q, const double* dt_dev, double* vol,
+                    cudaStream_t st, std::string* err);
+int face_integral(const adg_grid* g, int axis, int side, const double* d_values,
+                  const double* dt_dev, double* out, cudaStream_t st, std::string* err);
+int element_update(const adg_grid* g, const double* u, const double* vol,
+                   const double* const* accs, int nacc, double* out, cudaStream_t st,
+                   std::string* err);
+
 void upload_tables(int degree, const double* blob, int64_t n, std::string* err, int* rc);
 
 }  // namespace adg

@@ -432,30 +432,6 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
   }
 }
 
-// Rusanov one-sided terms (corrector.py:100-129) for a subcell face
-template <int D>
-__device__ __forceinline__ void rusanov_pair(const double* qm, const double* qp, int a,
-                                             double gamma, double gm1, double* dlow,
-                                             double* dhigh) {
-  constexpr int M = D + 2;
-  const double s = fmax(max_abs_eig<D>(qm, gamma, gm1, a), max_abs_eig<D>(qp, gamma, gm1, a));
-  double fm[M], fp[M];
-  flux_axis<D>(qm, gm1, a, fm);
-  flux_axis<D>(qp, gm1, a, fp);
-  const double hs = 0.5 * s;
-#pragma unroll
-  for (int v = 0; v < M; ++v) {
-    const double central = 0.5 * (fm[v] + fp[v]);
-    const double diss = hs * (qp[v] - qm[v]);
-    dlow[v] = (central + 0.0) - diss;
-    dhigh[v] = (-central + 0.0) + diss;
-  }
-}
-
-__device__ __forceinline__ double minmod(double a, double b) {
-  return (a * b > 0.0) ? (fabs(a) <= fabs(b) ? a : b) : 0.0;
-}
-
 // face states of the primitive-mode half step back to conservative
 // (limiter.py:160-171)
 template <int D>
@@ -470,12 +446,78 @@ __device__ __forceinline__ void to_cons2(double* a, double* b, double gm1) {
   for (int v = 0; v < M; ++v) b[v] = t[v];
 }
 
-// MUSCL-Hancock rescue of one troubled cell per block (limiter.py:104-223)
+// nodal polynomial of one cell from its S^d subcell averages
+// (recover_from_subcells, limiter.py:36-42): sequential per-axis
+// contraction with R_sub; tmp needs P S^(D-1) m (+ P^2 S m for D = 3) doubles
 template <int D, int P>
+__device__ void recover_cell(const double* __restrict__ nw, double* __restrict__ tmp,
+                             double* __restrict__ nod, int tid, int NT) {
+  using C = LimCfg<D, P>;
+  constexpr int M = C::M, S = C::S, PD = C::PD;
+  const DegreeTables& T = tab<P>();
+    if (D == 1) {
+      for (int x = tid; x < PD * M; x += NT) {
+        const int i = x / M, v = x - i * M;
+        double acc = 0.0;
+        for (int s = 0; s < S; ++s) acc = fma(T.sub_recover[i * S + s], nw[s * M + v], acc);
+        nod[x] = acc;
+      }
+    } else if (D == 2) {
+      for (int x = tid; x < P * S * M; x += NT) {
+        const int i0 = x / (S * M), r = x - i0 * S * M;
+        double acc = 0.0;
+        for (int s0 = 0; s0 < S; ++s0) acc = fma(T.sub_recover[i0 * S + s0], nw[s0 * S * M + r], acc);
+        tmp[x] = acc;
+      }
+      __syncthreads();
+      for (int x = tid; x < PD * M; x += NT) {
+        const int i0 = x / (P * M), r = x - i0 * P * M, i1 = r / M, v = r - i1 * M;
+        double acc = 0.0;
+        for (int s1 = 0; s1 < S; ++s1)
+          acc = fma(T.sub_recover[i1 * S + s1], tmp[(i0 * S + s1) * M + v], acc);
+        nod[x] = acc;
+      }
+    } else {
+      for (int x = tid; x < P * S * S * M; x += NT) {
+        const int i0 = x / (S * S * M), r = x - i0 * S * S * M;
+        double acc = 0.0;
+        for (int s0 = 0; s0 < S; ++s0)
+          acc = fma(T.sub_recover[i0 * S + s0], nw[s0 * S * S * M + r], acc);
+        tmp[x] = acc;
+      }
+      __syncthreads();
+      double* t2 = tmp + P * S * S * M;
+      for (int x = tid; x < P * P * S * M; x += NT) {
+        const int i0 = x / (P * S * M), r = x - i0 * P * S * M, i1 = r / (S * M),
+                  r2 = r - i1 * S * M;
+        double acc = 0.0;
+        for (int s1 = 0; s1 < S; ++s1)
+          acc = fma(T.sub_recover[i1 * S + s1], tmp[(i0 * S + s1) * S * M + r2], acc);
+        t2[x] = acc;
+      }
+      __syncthreads();
+      for (int x = tid; x < PD * M; x += NT) {
+        const int i01 = x / (P * M), r = x - i01 * P * M, i2 = r / M, v = r - i2 * M;
+        double acc = 0.0;
+        for (int s2 = 0; s2 < S; ++s2)
+          acc = fma(T.sub_recover[i2 * S + s2], t2[(i01 * S + s2) * M + v], acc);
+        nod[x] = acc;
+      }
+    }
+}
+
+// MUSCL-Hancock rescue of one troubled cell per block (limiter.py:104-223).
+// WIN = 0: the cell's window is gathered from the t^n subcell field (the
+// driver path); recovery + flattening write u_out and a failure raises
+// *failed.  WIN = 1: muscl_subcell_step on caller windows (limiter.py:104-121):
+// window b is windows[b], the new averages go to avg_out[b] and the
+// per-window failure flag to fail_each[b].
+template <int D, int P, int WIN>
 __global__ void __launch_bounds__(LimCfg<D, P>::NT)
 rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ idx,
               const int32_t* __restrict__ count, LimGrid G, const double* __restrict__ dt_dev,
-              double* __restrict__ u_out, int32_t* failed) {
+              double* __restrict__ u_out, int32_t* failed, const double* __restrict__ windows,
+              double* __restrict__ avg_out, uint8_t* __restrict__ fail_each) {
   using C = LimCfg<D, P>;
   constexpr int M = C::M, S = C::S, SD = C::SD, PD = C::PD, W = C::W, WD = C::WD, R = C::R,
                 RD = C::RD, NT = C::NT;
@@ -492,9 +534,9 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
   const double dt = *dt_dev;
   const int ncells = *count;
   for (int b = blockIdx.x; b < ncells; b += gridDim.x) {
-    const int64_t e = idx[b];
+    const int64_t e = WIN ? b : idx[b];
     int64_t c[3] = {0, 0, 0};
-    {
+    if (!WIN) {
       int64_t r = e;
       for (int j = D - 1; j >= 0; --j) {
         c[j] = r % G.n[j];
@@ -503,13 +545,18 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
     }
     // window of t^n subcell averages with a 2-layer halo (limiter.py:89-101)
     for (int w = tid; w < WD; w += NT) {
-      int rem = w;
-      int64_t gs[3] = {0, 0, 0};
-      for (int j = D - 1; j >= 0; --j) {
-        gs[j] = c[j] * S - 2 + rem % W;
-        rem /= W;
+      if (WIN) {
+#pragma unroll
+        for (int v = 0; v < M; ++v) win[w * M + v] = windows[((size_t)b * WD + w) * M + v];
+      } else {
+        int rem = w;
+        int64_t gs[3] = {0, 0, 0};
+        for (int j = D - 1; j >= 0; --j) {
+          gs[j] = c[j] * S - 2 + rem % W;
+          rem /= W;
+        }
+        fetch_sub<D, P>(prev_sub, G, gs, win + w * M);
       }
-      fetch_sub<D, P>(prev_sub, G, gs, win + w * M);
       if (G.prim) {   // limiter.py:127-128: the window in primitive variables
         double vv[M];
         cons_to_prim<D>(win + w * M, G.gm1, vv);
@@ -622,7 +669,10 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
           return x;
         };
         double q[M];
-        if (G.prim) {   // conservative core average (limiter.py:178)
+        if (G.prim && WIN) {   // conservative core average (limiter.py:178)
+#pragma unroll
+          for (int v = 0; v < M; ++v) q[v] = windows[((size_t)b * WD + wcore()) * M + v];
+        } else if (G.prim) {
           int64_t gs[3] = {0, 0, 0};
           for (int j = 0; j < D; ++j) gs[j] = c[j] * S + si[j];
           fetch_sub<D, P>(prev_sub, G, gs, q);
@@ -660,65 +710,22 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
       }
       __syncthreads();
       if (s_ok) break;
-      if (pass == 1) {
+      if (pass == 1 && !WIN) {
         if (tid == 0) atomicOr(failed, 1);
       }
       __syncthreads();
+    }
+    if (WIN) {
+      for (int x = tid; x < SD * M; x += NT) avg_out[(size_t)b * SD * M + x] = nw[x];
+      if (tid == 0) fail_each[b] = !s_ok;
+      __syncthreads();
+      continue;
     }
     if (!s_ok) {
       __syncthreads();
       continue;
     }
-    // recovery (limiter.py:36-42): sequential per-axis contraction with R_sub
-    if (D == 1) {
-      for (int x = tid; x < PD * M; x += NT) {
-        const int i = x / M, v = x - i * M;
-        double acc = 0.0;
-        for (int s = 0; s < S; ++s) acc = fma(T.sub_recover[i * S + s], nw[s * M + v], acc);
-        nod[x] = acc;
-      }
-    } else if (D == 2) {
-      for (int x = tid; x < P * S * M; x += NT) {
-        const int i0 = x / (S * M), r = x - i0 * S * M;
-        double acc = 0.0;
-        for (int s0 = 0; s0 < S; ++s0) acc = fma(T.sub_recover[i0 * S + s0], nw[s0 * S * M + r], acc);
-        tmp[x] = acc;
-      }
-      __syncthreads();
-      for (int x = tid; x < PD * M; x += NT) {
-        const int i0 = x / (P * M), r = x - i0 * P * M, i1 = r / M, v = r - i1 * M;
-        double acc = 0.0;
-        for (int s1 = 0; s1 < S; ++s1)
-          acc = fma(T.sub_recover[i1 * S + s1], tmp[(i0 * S + s1) * M + v], acc);
-        nod[x] = acc;
-      }
-    } else {
-      for (int x = tid; x < P * S * S * M; x += NT) {
-        const int i0 = x / (S * S * M), r = x - i0 * S * S * M;
-        double acc = 0.0;
-        for (int s0 = 0; s0 < S; ++s0)
-          acc = fma(T.sub_recover[i0 * S + s0], nw[s0 * S * S * M + r], acc);
-        tmp[x] = acc;
-      }
-      __syncthreads();
-      double* t2 = tmp + P * S * S * M;
-      for (int x = tid; x < P * P * S * M; x += NT) {
-        const int i0 = x / (P * S * M), r = x - i0 * P * S * M, i1 = r / (S * M),
-                  r2 = r - i1 * S * M;
-        double acc = 0.0;
-        for (int s1 = 0; s1 < S; ++s1)
-          acc = fma(T.sub_recover[i1 * S + s1], tmp[(i0 * S + s1) * S * M + r2], acc);
-        t2[x] = acc;
-      }
-      __syncthreads();
-      for (int x = tid; x < PD * M; x += NT) {
-        const int i01 = x / (P * M), r = x - i01 * P * M, i2 = r / M, v = r - i2 * M;
-        double acc = 0.0;
-        for (int s2 = 0; s2 < S; ++s2)
-          acc = fma(T.sub_recover[i2 * S + s2], t2[(i01 * S + s2) * M + v], acc);
-        nod[x] = acc;
-      }
-    }
+    recover_cell<D, P>(nw, tmp, nod, tid, NT);
     __syncthreads();
     // flatten_inadmissible (limiter.py:205-223): nodal and its subcell
     // projection must be admissible, else the cell becomes its mean
@@ -748,6 +755,70 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
       for (int x = tid; x < PD * M; x += NT) dst[x] = s_mean[x % M];
     } else {
       for (int x = tid; x < PD * M; x += NT) dst[x] = nod[x];
+    }
+    __syncthreads();
+  }
+}
+
+// recover_from_subcells (limiter.py:36-42) on E cells: ubar [E][S^d][m] ->
+// nodal [E][P^d][m]
+template <int D, int P>
+__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+recover_kernel(const double* __restrict__ ubar, int64_t E, double* __restrict__ out) {
+  using C = LimCfg<D, P>;
+  constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
+  extern __shared__ __align__(16) double lsm[];
+  double* nw = lsm;
+  double* nod = nw + SD * M;
+  double* tmp = nod + PD * M;
+  const int tid = threadIdx.x;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    for (int x = tid; x < SD * M; x += NT) nw[x] = ubar[(size_t)e * SD * M + x];
+    __syncthreads();
+    recover_cell<D, P>(nw, tmp, nod, tid, NT);
+    __syncthreads();
+    for (int x = tid; x < PD * M; x += NT) out[(size_t)e * PD * M + x] = nod[x];
+    __syncthreads();
+  }
+}
+
+// flatten_inadmissible (limiter.py:205-223) on E cells, in place on nodal:
+// a cell whose nodal states or their subcell projection are inadmissible
+// becomes the mean of its subcell averages; *nflat counts them
+template <int D, int P>
+__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+flatten_cells_kernel(double* __restrict__ nodal, const double* __restrict__ averages, int64_t E,
+                     double gm1, int32_t* nflat) {
+  using C = LimCfg<D, P>;
+  constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
+  extern __shared__ __align__(16) double lsm[];
+  double* nod = lsm;
+  double* pj = nod + PD * M;
+  double* tmp = pj + SD * M;
+  __shared__ int s_flat;
+  __shared__ double s_mean[M];
+  const int tid = threadIdx.x;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    double* ne = nodal + (size_t)e * PD * M;
+    for (int x = tid; x < PD * M; x += NT) nod[x] = ne[x];
+    if (tid == 0) s_flat = 0;
+    __syncthreads();
+    project_cell<D, P>(nod, tmp, pj, tid, NT);
+    __syncthreads();
+    int bad = 0;
+    for (int nd = tid; nd < PD; nd += NT) bad |= !admissible<D>(nod + nd * M, gm1);
+    for (int x = tid; x < SD; x += NT) bad |= !admissible<D>(pj + x * M, gm1);
+    if (bad) s_flat = 1;
+    __syncthreads();
+    if (s_flat) {
+      if (tid < M) {
+        double acc = 0.0;
+        for (int x = 0; x < SD; ++x) acc += averages[((size_t)e * SD + x) * M + tid];
+        s_mean[tid] = acc / SD;
+      }
+      __syncthreads();
+      for (int x = tid; x < PD * M; x += NT) ne[x] = s_mean[x % M];
+      if (tid == 0) atomicAdd(nflat, 1);
     }
     __syncthreads();
   }
@@ -937,14 +1008,64 @@ static int launch_rescue(const adg_grid* g, const double* prev_sub, const int32_
                          const adg_subcell_ghosts* gh, double* u_out, int32_t* failed,
                          cudaStream_t st, std::string* err) {
   const size_t sm = rescue_smem<D, P>();
-  if (!set_smem(rescue_kernel<D, P>, sm)) {
+  if (!set_smem(rescue_kernel<D, P, 0>, sm)) {
     *err = "limiter window exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   if (cmax <= 0) return ADG_OK;
-  rescue_kernel<D, P><<<(unsigned)cmax, LimCfg<D, P>::NT, sm, st>>>(prev_sub, idx, count,
-                                                                   lim_grid(g, gh), dt, u_out,
-                                                                   failed);
+  rescue_kernel<D, P, 0><<<(unsigned)cmax, LimCfg<D, P>::NT, sm, st>>>(
+      prev_sub, idx, count, lim_grid(g, gh), dt, u_out, failed, nullptr, nullptr, nullptr);
+  return lerr(err);
+}
+
+template <int D, int P>
+static int launch_muscl_windows(const adg_grid* g, const double* windows, int64_t nwin,
+                                const int32_t* count_dev, const double* dt, double* avg_out,
+                                uint8_t* fail_each, cudaStream_t st, std::string* err) {
+  const size_t sm = rescue_smem<D, P>();
+  if (!set_smem(rescue_kernel<D, P, 1>, sm)) {
+    *err = "limiter window exceeds shared memory";
+    return ADG_ERR_UNSUPPORTED;
+  }
+  if (nwin <= 0) return ADG_OK;
+  const unsigned grid = (unsigned)(nwin < 65535 * 8 ? nwin : 65535 * 8);
+  LimGrid G = lim_grid(g);
+  for (int j = 0; j < 3; ++j) G.h[j] = j < g->dim ? g->dx[j] : 1.0;   // dx = subcell widths here
+  rescue_kernel<D, P, 1><<<grid, LimCfg<D, P>::NT, sm, st>>>(
+      nullptr, nullptr, count_dev, G, dt, nullptr, nullptr, windows, avg_out, fail_each);
+  return lerr(err);
+}
+
+template <int D, int P>
+static int launch_recover(const adg_grid* g, const double* ubar, double* out, cudaStream_t st,
+                          std::string* err) {
+  using C = LimCfg<D, P>;
+  const size_t tmp = D == 3 ? (size_t)P * C::S * C::S * C::M + (size_t)P * P * C::S * C::M
+                            : (size_t)P * C::S * C::M;
+  const size_t sm = ((size_t)C::SD * C::M + (size_t)C::PD * C::M + tmp) * 8;
+  if (!set_smem(recover_kernel<D, P>, sm)) {
+    *err = "limiter tile exceeds shared memory";
+    return ADG_ERR_UNSUPPORTED;
+  }
+  const int64_t E = n_elements(g);
+  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
+  recover_kernel<D, P><<<grid, C::NT, sm, st>>>(ubar, E, out);
+  return lerr(err);
+}
+
+template <int D, int P>
+static int launch_flatten_cells(const adg_grid* g, double* nodal, const double* averages,
+                                int32_t* nflat, cudaStream_t st, std::string* err) {
+  const size_t sm = proj_smem<D, P>();
+  if (!set_smem(flatten_cells_kernel<D, P>, sm)) {
+    *err = "limiter tile exceeds shared memory";
+    return ADG_ERR_UNSUPPORTED;
+  }
+  const int64_t E = n_elements(g);
+  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
+  cudaMemsetAsync(nflat, 0, sizeof(int32_t), st);
+  flatten_cells_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(nodal, averages, E,
+                                                                 g->gamma - 1.0, nflat);
   return lerr(err);
 }
 
@@ -989,6 +1110,29 @@ int rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
   int rc = ADG_OK;
   ADG_LIM_SWITCH(launch_rescue, g, prev_sub, idx, count_dev, count_max, dt_dev, gh, u_out, failed,
                  st, err);
+  return rc;
+}
+
+int muscl_windows(const adg_grid* g, const double* windows, int64_t nwin,
+                  const int32_t* count_dev, const double* dt_dev, double* avg_out,
+                  uint8_t* fail_each, cudaStream_t st, std::string* err) {
+  int rc = ADG_OK;
+  ADG_LIM_SWITCH(launch_muscl_windows, g, windows, nwin, count_dev, dt_dev, avg_out, fail_each, st,
+                 err);
+  return rc;
+}
+
+int recover_subcells(const adg_grid* g, const double* ubar, double* out, cudaStream_t st,
+                     std::string* err) {
+  int rc = ADG_OK;
+  ADG_LIM_SWITCH(launch_recover, g, ubar, out, st, err);
+  return rc;
+}
+
+int flatten_cells(const adg_grid* g, double* nodal, const double* averages, int32_t* nflat,
+                  cudaStream_t st, std::string* err) {
+  int rc = ADG_OK;
+  ADG_LIM_SWITCH(launch_flatten_cells, g, nodal, averages, nflat, st, err);
   return rc;
 }
 

@@ -167,3 +167,19 @@ def test_work_model_matches_survey():
     assert roofline.step_bytes_per_dof(4, 3) == 560
     assert roofline.step_flops_per_dof(3, 2, 4) == 3430
     assert abs(roofline.roofline_dofs(4, 3, 2, 37e12, 6454.3e9) - 7.74e9) < 0.01e9
+
+
+def test_module_shims_have_no_cpu_fallback():
+    """corrector / limiter module functions run only on the device."""
+    import torch
+
+    from paper_1808_03788_b200 import corrector, limiter, make_system
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    q = np.ones((4, 4))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        corrector.face_fluxes(q, q, 0, make_system("euler", 2))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        limiter.minmod(q, q)
+    assert corrector.max_cfl_number(4) == 1.0 / 9.0
