@@ -191,20 +191,26 @@ int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, doub
  * average leaves them, a candidate nodal or subcell state is inadmissible,
  * pred_bad is set, or force_all != 0.  Writes troubled[E] (uint8), the
  * compacted list idx[*count] (int32, unordered) and *count (int32).
- * ghosts: exterior slabs of ADG_BC_GHOST faces (NULL if there are none). */
+ * ghosts: exterior slabs of ADG_BC_GHOST faces (NULL if there are none).
+ * cand_sub_out / cand_cmin_out / cand_cmax_out (may be NULL): the
+ * candidate's subcell averages and extrema; for every cell the rescue
+ * leaves alone they are the next step's prev_sub / cmin / cmax. */
 int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub, const double* cmin,
                const double* cmax, const double* cand, const uint8_t* pred_bad, double delta0,
                double eps, int force_all, const adg_subcell_ghosts* ghosts, uint8_t* troubled,
-               int32_t* idx, int32_t* count, void* stream);
+               int32_t* idx, int32_t* count, double* cand_sub_out, double* cand_cmin_out,
+               double* cand_cmax_out, void* stream);
 /* MUSCL-Hancock rescue of the listed cells from t^n subcell averages
  * (limiter.py:89-223 + driver.py:286-298), writing recovered nodal states
  * into u_out for listed cells (other cells untouched) and setting
  * *failed_dev != 0 if any cell failed after the first-order retry
- * (driver.py:292-293 restart). */
+ * (driver.py:292-293 restart).  sub_next / cmin_next / cmax_next (may be
+ * NULL) receive the rescued cells' subcell averages and extrema, completing
+ * adg_detect's candidate outputs into the next step's prev_sub. */
 int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const int32_t* idx,
                const int32_t* count_dev, int32_t count_host_max, const double* dt_dev,
                const adg_subcell_ghosts* ghosts, double* u_out, int32_t* failed_dev,
-               void* stream);
+               double* sub_next, double* cmin_next, double* cmax_next, void* stream);
 /* IC flattening (driver.py:137-152): cells whose nodal or subcell states are
  * inadmissible are replaced by their weighted mean; *nflat = count */
 int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat,

@@ -77,8 +77,9 @@ _SIGS = {
     "adg_totals_finalize": (_I, [_P, _P, _P, _I64, _P, _P]),
     "adg_totals": (_I, [_P, _P, _P, _P, _P, _P]),
     "adg_project_subcells": (_I, [_P, _P, _P, _P, _P, _P, _P]),
-    "adg_detect": (_I, [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _P]),
-    "adg_rescue": (_I, [_P, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P, _P]),
+    "adg_detect": (_I, [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _P, _P, _P,
+                        _P]),
+    "adg_rescue": (_I, [_P, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "adg_flatten_ic": (_I, [_P, _P, _P, _P, _P]),
     "adg_face_fluxes": (_I, [_P, _P, _I, _I64, _P, _P, _P, _P, _P]),
     "adg_volume_integral": (_I, [_P, _P, _P, _P, _P, _P]),

@@ -225,23 +225,26 @@ int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, doub
 int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub, const double* cmin,
                const double* cmax, const double* cand, const uint8_t* pred_bad, double delta0,
                double eps, int force_all, const adg_subcell_ghosts* ghosts, uint8_t* troubled,
-               int32_t* idx, int32_t* count, void* stream) {
+               int32_t* idx, int32_t* count, double* cand_sub_out, double* cand_cmin_out,
+               double* cand_cmax_out, void* stream) {
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::detect(g, prev_sub, cmin, cmax, cand, pred_bad, delta0, eps, force_all,
-                             ghosts, troubled, idx, count, (cudaStream_t)stream, &e), e);
+                             ghosts, troubled, idx, count, cand_sub_out, cand_cmin_out,
+                             cand_cmax_out, (cudaStream_t)stream, &e), e);
 }
 
 int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const int32_t* idx,
                const int32_t* count_dev, int32_t count_host_max, const double* dt_dev,
                const adg_subcell_ghosts* ghosts, double* u_out, int32_t* failed_dev,
-               void* stream) {
+               double* sub_next, double* cmin_next, double* cmax_next, void* stream) {
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::rescue(g, prev_sub, idx, count_dev, count_host_max, dt_dev, ghosts, u_out,
-                             failed_dev, (cudaStream_t)stream, &e), e);
+                             failed_dev, sub_next, cmin_next, cmax_next, (cudaStream_t)stream,
+                             &e), e);
 }
 
 int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const double* q_minus,

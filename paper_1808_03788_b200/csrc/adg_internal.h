@@ -44,11 +44,12 @@ int project_subcells(const adg_grid* g, const double* u, double* sub, double* cm
 int detect(const adg_grid* g, const double* prev_sub, const double* cmin, const double* cmax,
            const double* cand, const uint8_t* pred_bad, double delta0, double eps,
            int force_all, const adg_subcell_ghosts* gh, uint8_t* troubled, int32_t* idx,
-           int32_t* count, cudaStream_t st, std::string* err);
+           int32_t* count, double* sub_out, double* cmin_out, double* cmax_out, cudaStream_t st,
+           std::string* err);
 int rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
            const int32_t* count_dev, int32_t count_max, const double* dt_dev,
-           const adg_subcell_ghosts* gh, double* u_out, int32_t* failed, cudaStream_t st,
-           std::string* err);
+           const adg_subcell_ghosts* gh, double* u_out, int32_t* failed, double* sub_next,
+           double* cmin_next, double* cmax_next, cudaStream_t st, std::string* err);
 int flatten_ic(const adg_grid* g, double* u, int32_t* nflat, cudaStream_t st,
                std::string* err);
 

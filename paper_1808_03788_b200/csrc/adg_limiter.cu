@@ -150,7 +150,8 @@ __device__ __forceinline__ void fetch_sub(const double* __restrict__ sub, const 
 
 // subcell averages of one cell's nodal data held in shared memory:
 // sequential per-axis contraction with P_sub (limiter.py:27-33)
-template <int D, int P>
+// WARP = true: the calling warp alone does the cell (tid = lane, nt = 32)
+template <int D, int P, bool WARP = false>
 __device__ void project_cell(const double* __restrict__ nodal, double* __restrict__ tmp,
                              double* __restrict__ out, int tid, int nt) {
   using C = LimCfg<D, P>;
@@ -176,7 +177,7 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
         acc = fma(T.sub_project[s0 * P + i0], nodal[(i0 * P + i1) * M + v], acc);
       tmp[x] = acc;
     }
-    __syncthreads();
+    if (WARP) __syncwarp(); else __syncthreads();
     for (int x = tid; x < S * S * M; x += nt) {
       const int s0 = x / (S * M), r = x - s0 * S * M, s1 = r / M, v = r - s1 * M;
       double acc = 0.0;
@@ -195,7 +196,7 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
     for (int i0 = 0; i0 < P; ++i0) acc = fma(T.sub_project[s0 * P + i0], nodal[i0 * P * P * M + r], acc);
     out[x] = acc;
   }
-  __syncthreads();
+  if (WARP) __syncwarp(); else __syncthreads();
   for (int x = tid; x < S * S * P * M; x += nt) {
     const int s0 = x / (S * P * M), r = x - s0 * S * P * M, s1 = r / (P * M),
               r2 = r - s1 * P * M;
@@ -205,7 +206,7 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
       acc = fma(T.sub_project[s1 * P + i1], out[(s0 * P + i1) * P * M + r2], acc);
     tmp[x] = acc;
   }
-  __syncthreads();
+  if (WARP) __syncwarp(); else __syncthreads();
   for (int x = tid; x < S * S * S * M; x += nt) {
     const int s01 = x / (S * M), r = x - s01 * S * M, s2 = r / M, v = r - s2 * M;
     double acc = 0.0;
@@ -223,47 +224,72 @@ __device__ __forceinline__ size_t proj_scratch() {
 }
 
 // -------------------------------------------------------------- kernels
-// prev_sub + per-cell extrema of u^n (one block per cell, grid stride)
+// Limiter screening is one warp per cell: a cell's projection is a few
+// hundred short dot products, so a warp keeps all lanes busy without
+// block-wide barriers, and 8 cells share a CTA.
 template <int D, int P>
-__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+struct WarpCfg {
+  using C = LimCfg<D, P>;
+  static constexpr int SCR = D == 3 ? C::S * C::S * P * C::M : C::S * P * C::M;
+  static constexpr int OUT = (D == 3 ? C::S * P * P * C::M : 0) > C::SD * C::M
+                                 ? C::S * P * P * C::M : C::SD * C::M;
+  static constexpr int PER_WARP = C::PD * C::M + OUT + SCR + 2 * C::M;   // doubles
+  static constexpr int W0 = (200 * 1024) / (PER_WARP * 8);
+  static constexpr int WPB = W0 >= 8 ? 8 : (W0 >= 1 ? W0 : 1);   // warps (cells) per CTA
+  static constexpr size_t SMEM = (size_t)WPB * PER_WARP * 8;
+};
+
+// per-cell subcell averages + extrema of nodal data staged in a warp's
+// shared slice; writes sub / cmin / cmax of cell e when they are non-null
+template <int D, int P>
+__device__ __forceinline__ void warp_project_store(double* nodal, double* out, double* tmp,
+                                                   int lane, int64_t e, double* sub,
+                                                   double* cmin, double* cmax) {
+  using C = LimCfg<D, P>;
+  constexpr int M = C::M, SD = C::SD;
+  project_cell<D, P, true>(nodal, tmp, out, lane, 32);
+  __syncwarp();
+  if (sub)
+    for (int x = lane; x < SD * M; x += 32) sub[(size_t)e * SD * M + x] = out[x];
+  if (cmin) {
+#pragma unroll
+    for (int v = 0; v < M; ++v) {
+      double lo = __longlong_as_double(0x7ff0000000000000LL), hi = -lo;
+      for (int x = lane; x < SD; x += 32) {
+        lo = fmin(lo, out[x * M + v]);
+        hi = fmax(hi, out[x * M + v]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if (lane == 0) {
+        cmin[e * M + v] = lo;
+        cmax[e * M + v] = hi;
+      }
+    }
+  }
+}
+
+// prev_sub + per-cell extrema of u^n
+template <int D, int P>
+__global__ void __launch_bounds__(WarpCfg<D, P>::WPB * 32)
 subcell_prep_kernel(const double* __restrict__ u, int64_t E, double* __restrict__ sub,
                     double* __restrict__ cmin, double* __restrict__ cmax) {
   using C = LimCfg<D, P>;
-  constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
+  using W = WarpCfg<D, P>;
+  constexpr int M = C::M, PD = C::PD;
   extern __shared__ __align__(16) double lsm[];
-  double* nodal = lsm;                      // PD*M
-  double* out = nodal + PD * M;             // max(SD*M, S*P*P*M)
-  double* tmp = out + SD * M;
-  __shared__ double rmin[NT], rmax[NT];
-  const int tid = threadIdx.x;
-  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
-    for (int x = tid; x < PD * M; x += NT) nodal[x] = u[(size_t)e * PD * M + x];
-    __syncthreads();
-    project_cell<D, P>(nodal, tmp, out, tid, NT);
-    __syncthreads();
-    for (int x = tid; x < SD * M; x += NT) sub[(size_t)e * SD * M + x] = out[x];
-    for (int v = 0; v < M; ++v) {
-      double lo = __longlong_as_double(0x7ff0000000000000LL), hi = -lo;
-      for (int s = tid; s < SD; s += NT) {
-        lo = fmin(lo, out[s * M + v]);
-        hi = fmax(hi, out[s * M + v]);
-      }
-      rmin[tid] = lo;
-      rmax[tid] = hi;
-      __syncthreads();
-      for (int o = NT / 2; o > 0; o >>= 1) {
-        if (tid < o) {
-          rmin[tid] = fmin(rmin[tid], rmin[tid + o]);
-          rmax[tid] = fmax(rmax[tid], rmax[tid + o]);
-        }
-        __syncthreads();
-      }
-      if (tid == 0) {
-        cmin[e * M + v] = rmin[0];
-        cmax[e * M + v] = rmax[0];
-      }
-      __syncthreads();
-    }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* nodal = lsm + warp * W::PER_WARP;
+  double* out = nodal + PD * M;
+  double* tmp = out + W::OUT;
+  for (int64_t e = (int64_t)blockIdx.x * W::WPB + warp; e < E; e += (int64_t)gridDim.x * W::WPB) {
+    for (int x = lane; x < PD * M; x += 32) nodal[x] = u[(size_t)e * PD * M + x];
+    __syncwarp();
+    warp_project_store<D, P>(nodal, out, tmp, lane, e, sub, cmin, cmax);
+    __syncwarp();
   }
 }
 
@@ -347,27 +373,32 @@ __device__ void ghost_extrema(const double* __restrict__ sub, const double* __re
   }
 }
 
-// troubled-cell screen (limiter.py:51-86, driver.py:272-285)
+// troubled-cell screen (limiter.py:51-86, driver.py:272-285), one warp per
+// cell.  The candidate's subcell averages and extrema are written to
+// sub_out / cmin_out / cmax_out (when non-null): for every cell the rescue
+// leaves alone they are exactly the next step's prev_sub, so the driver
+// skips the separate projection of u^(n+1).
 template <int D, int P>
-__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+__global__ void __launch_bounds__(WarpCfg<D, P>::WPB * 32)
 detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cmin,
               const double* __restrict__ cmax, const double* __restrict__ cand,
               const uint8_t* __restrict__ pred_bad, LimGrid G, int64_t E, double delta0,
               double eps, int force_all, uint8_t* __restrict__ troubled, int32_t* idx,
-              int32_t* count) {
+              int32_t* count, double* __restrict__ sub_out, double* __restrict__ cmin_out,
+              double* __restrict__ cmax_out) {
   using C = LimCfg<D, P>;
-  constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
+  using W = WarpCfg<D, P>;
+  constexpr int M = C::M, SD = C::SD, PD = C::PD;
   extern __shared__ __align__(16) double lsm[];
-  double* nodal = lsm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* nodal = lsm + warp * W::PER_WARP;
   double* out = nodal + PD * M;
-  double* tmp = out + SD * M;
-  __shared__ double s_lo[M], s_hi[M];
-  __shared__ int s_bad;
-  const int tid = threadIdx.x;
-  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
-    for (int x = tid; x < PD * M; x += NT) nodal[x] = cand[(size_t)e * PD * M + x];
-    if (tid == 0) {
-      s_bad = force_all || pred_bad[e];
+  double* tmp = out + W::OUT;
+  double* s_lo = tmp + W::SCR;
+  double* s_hi = s_lo + M;
+  for (int64_t e = (int64_t)blockIdx.x * W::WPB + warp; e < E; e += (int64_t)gridDim.x * W::WPB) {
+    for (int x = lane; x < PD * M; x += 32) nodal[x] = cand[(size_t)e * PD * M + x];
+    if (lane == 0) {
       int64_t c[3] = {0, 0, 0};
       int64_t r = e;
       for (int j = D - 1; j >= 0; --j) {
@@ -411,27 +442,26 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
         s_hi[v] = hi[v] + delta;
       }
     }
-    __syncthreads();
-    project_cell<D, P>(nodal, tmp, out, tid, NT);
-    __syncthreads();
-    int bad = 0;
-    for (int s = tid; s < SD; s += NT) {
-      const double* q = out + s * M;
+    __syncwarp();
+    warp_project_store<D, P>(nodal, out, tmp, lane, e, sub_out, cmin_out, cmax_out);
+    int bad = lane == 0 ? (force_all || pred_bad[e]) : 0;
+    for (int x = lane; x < SD; x += 32) {
+      const double* q = out + x * M;
 #pragma unroll
       for (int v = 0; v < M; ++v) bad |= (q[v] < s_lo[v]) | (q[v] > s_hi[v]);
       bad |= !admissible<D>(q, G.gm1);
     }
-    for (int nd = tid; nd < PD; nd += NT) bad |= !admissible<D>(nodal + nd * M, G.gm1);
-    if (bad) s_bad = 1;   // benign race: every writer stores 1
-    __syncthreads();
-    if (tid == 0) {
-      troubled[e] = (uint8_t)s_bad;
-      if (s_bad) idx[atomicAdd(count, 1)] = (int32_t)e;
+    for (int nd = lane; nd < PD; nd += 32) bad |= !admissible<D>(nodal + nd * M, G.gm1);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      troubled[e] = (uint8_t)bad;
+      if (bad) idx[atomicAdd(count, 1)] = (int32_t)e;
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
+// Rusanov one-sided terms (corrector.py:100-129) live in adg_common.cuh
 // face states of the primitive-mode half step back to conservative
 // (limiter.py:160-171)
 template <int D>
@@ -517,7 +547,9 @@ __global__ void __launch_bounds__(LimCfg<D, P>::NT)
 rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ idx,
               const int32_t* __restrict__ count, LimGrid G, const double* __restrict__ dt_dev,
               double* __restrict__ u_out, int32_t* failed, const double* __restrict__ windows,
-              double* __restrict__ avg_out, uint8_t* __restrict__ fail_each) {
+              double* __restrict__ avg_out, uint8_t* __restrict__ fail_each,
+              double* __restrict__ sub_next, double* __restrict__ cmin_next,
+              double* __restrict__ cmax_next) {
   using C = LimCfg<D, P>;
   constexpr int M = C::M, S = C::S, SD = C::SD, PD = C::PD, W = C::W, WD = C::WD, R = C::R,
                 RD = C::RD, NT = C::NT;
@@ -752,9 +784,36 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
         s_mean[tid] = acc / SD;
       }
       __syncthreads();
-      for (int x = tid; x < PD * M; x += NT) dst[x] = s_mean[x % M];
-    } else {
-      for (int x = tid; x < PD * M; x += NT) dst[x] = nod[x];
+      for (int x = tid; x < PD * M; x += NT) nod[x] = s_mean[x % M];
+    }
+    for (int x = tid; x < PD * M; x += NT) dst[x] = nod[x];
+    if (!WIN && sub_next) {
+      // the rescued cell's subcell averages / extrema for the next step
+      // (same arithmetic as the screen's projection of unrescued cells)
+      __syncthreads();
+      double* pj = vh;
+      project_cell<D, P>(nod, tmp + (D == 3 ? P * S * S * M : P * S * M), pj, tid, NT);
+      __syncthreads();
+      for (int x = tid; x < SD * M; x += NT) sub_next[(size_t)e * SD * M + x] = pj[x];
+      if (tid < 32) {
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          double lo = __longlong_as_double(0x7ff0000000000000LL), hi = -lo;
+          for (int x = tid; x < SD; x += 32) {
+            lo = fmin(lo, pj[x * M + v]);
+            hi = fmax(hi, pj[x * M + v]);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+          }
+          if (tid == 0) {
+            cmin_next[e * M + v] = lo;
+            cmax_next[e * M + v] = hi;
+          }
+        }
+      }
     }
     __syncthreads();
   }
@@ -971,14 +1030,15 @@ static int lerr(std::string* err) {
 template <int D, int P>
 static int launch_prep(const adg_grid* g, const double* u, double* sub, double* cmin,
                        double* cmax, cudaStream_t st, std::string* err) {
-  const size_t sm = proj_smem<D, P>();
-  if (!set_smem(subcell_prep_kernel<D, P>, sm)) {
+  using W = WarpCfg<D, P>;
+  if (!set_smem(subcell_prep_kernel<D, P>, W::SMEM)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   const int64_t E = n_elements(g);
-  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
-  subcell_prep_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(u, E, sub, cmin, cmax);
+  const int64_t nb = (E + W::WPB - 1) / W::WPB;
+  const unsigned grid = (unsigned)(nb < 148 * 64 ? nb : 148 * 64);
+  subcell_prep_kernel<D, P><<<grid, W::WPB * 32, W::SMEM, st>>>(u, E, sub, cmin, cmax);
   return lerr(err);
 }
 
@@ -986,19 +1046,20 @@ template <int D, int P>
 static int launch_detect(const adg_grid* g, const double* prev_sub, const double* cmin,
                          const double* cmax, const double* cand, const uint8_t* pred_bad,
                          double d0, double eps, int force, const adg_subcell_ghosts* gh,
-                         uint8_t* troubled, int32_t* idx, int32_t* count, cudaStream_t st,
-                         std::string* err) {
-  const size_t sm = proj_smem<D, P>();
-  if (!set_smem(detect_kernel<D, P>, sm)) {
+                         uint8_t* troubled, int32_t* idx, int32_t* count, double* sub_out,
+                         double* cmin_out, double* cmax_out, cudaStream_t st, std::string* err) {
+  using W = WarpCfg<D, P>;
+  if (!set_smem(detect_kernel<D, P>, W::SMEM)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   const int64_t E = n_elements(g);
-  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
+  const int64_t nb = (E + W::WPB - 1) / W::WPB;
+  const unsigned grid = (unsigned)(nb < 148 * 64 ? nb : 148 * 64);
   cudaMemsetAsync(count, 0, sizeof(int32_t), st);
-  detect_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(prev_sub, cmin, cmax, cand, pred_bad,
-                                                          lim_grid(g, gh), E, d0, eps, force,
-                                                          troubled, idx, count);
+  detect_kernel<D, P><<<grid, W::WPB * 32, W::SMEM, st>>>(
+      prev_sub, cmin, cmax, cand, pred_bad, lim_grid(g, gh), E, d0, eps, force, troubled, idx,
+      count, sub_out, cmin_out, cmax_out);
   return lerr(err);
 }
 
@@ -1006,6 +1067,7 @@ template <int D, int P>
 static int launch_rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
                          const int32_t* count, int32_t cmax, const double* dt,
                          const adg_subcell_ghosts* gh, double* u_out, int32_t* failed,
+                         double* sub_next, double* cmin_next, double* cmax_next,
                          cudaStream_t st, std::string* err) {
   const size_t sm = rescue_smem<D, P>();
   if (!set_smem(rescue_kernel<D, P, 0>, sm)) {
@@ -1014,7 +1076,8 @@ static int launch_rescue(const adg_grid* g, const double* prev_sub, const int32_
   }
   if (cmax <= 0) return ADG_OK;
   rescue_kernel<D, P, 0><<<(unsigned)cmax, LimCfg<D, P>::NT, sm, st>>>(
-      prev_sub, idx, count, lim_grid(g, gh), dt, u_out, failed, nullptr, nullptr, nullptr);
+      prev_sub, idx, count, lim_grid(g, gh), dt, u_out, failed, nullptr, nullptr, nullptr,
+      sub_next, cmin_next, cmax_next);
   return lerr(err);
 }
 
@@ -1032,7 +1095,8 @@ static int launch_muscl_windows(const adg_grid* g, const double* windows, int64_
   LimGrid G = lim_grid(g);
   for (int j = 0; j < 3; ++j) G.h[j] = j < g->dim ? g->dx[j] : 1.0;   // dx = subcell widths here
   rescue_kernel<D, P, 1><<<grid, LimCfg<D, P>::NT, sm, st>>>(
-      nullptr, nullptr, count_dev, G, dt, nullptr, nullptr, windows, avg_out, fail_each);
+      nullptr, nullptr, count_dev, G, dt, nullptr, nullptr, windows, avg_out, fail_each, nullptr,
+      nullptr, nullptr);
   return lerr(err);
 }
 
@@ -1094,22 +1158,23 @@ int project_subcells(const adg_grid* g, const double* u, double* sub, double* cm
 int detect(const adg_grid* g, const double* prev_sub, const double* cmin, const double* cmax,
            const double* cand, const uint8_t* pred_bad, double delta0, double eps, int force_all,
            const adg_subcell_ghosts* gh, uint8_t* troubled, int32_t* idx, int32_t* count,
-           cudaStream_t st, std::string* err) {
+           double* sub_out, double* cmin_out, double* cmax_out, cudaStream_t st,
+           std::string* err) {
   if (!lim_supported(g, gh, err)) return ADG_ERR_UNSUPPORTED;
   int rc = ADG_OK;
   ADG_LIM_SWITCH(launch_detect, g, prev_sub, cmin, cmax, cand, pred_bad, delta0, eps, force_all,
-                 gh, troubled, idx, count, st, err);
+                 gh, troubled, idx, count, sub_out, cmin_out, cmax_out, st, err);
   return rc;
 }
 
 int rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
            const int32_t* count_dev, int32_t count_max, const double* dt_dev,
-           const adg_subcell_ghosts* gh, double* u_out, int32_t* failed, cudaStream_t st,
-           std::string* err) {
+           const adg_subcell_ghosts* gh, double* u_out, int32_t* failed, double* sub_next,
+           double* cmin_next, double* cmax_next, cudaStream_t st, std::string* err) {
   if (!lim_supported(g, gh, err)) return ADG_ERR_UNSUPPORTED;
   int rc = ADG_OK;
   ADG_LIM_SWITCH(launch_rescue, g, prev_sub, idx, count_dev, count_max, dt_dev, gh, u_out, failed,
-                 st, err);
+                 sub_next, cmin_next, cmax_next, st, err);
   return rc;
 }
 

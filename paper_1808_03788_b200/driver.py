@@ -429,8 +429,12 @@ class Simulation:
             S = self.tables.n_subcells
             m = self._m
             f64 = dict(dtype=torch.float64, device=self.device)
+            # t^n subcell averages / extrema and the next step's, swapped on
+            # acceptance (adg_detect + adg_rescue write the next ones)
             lb = {"sub": torch.empty(E * S ** self.mesh.dim * m, **f64),
                   "cmin": torch.empty(E * m, **f64), "cmax": torch.empty(E * m, **f64),
+                  "sub_n": torch.empty(E * S ** self.mesh.dim * m, **f64),
+                  "cmin_n": torch.empty(E * m, **f64), "cmax_n": torch.empty(E * m, **f64),
                   "troubled": torch.empty(self.mesh.cells, dtype=torch.uint8,
                                           device=self.device),
                   "idx": torch.empty(E, dtype=torch.int32, device=self.device),
@@ -461,14 +465,16 @@ class Simulation:
         self._h.call("adg_detect", self._gp(), _ptr(lb["sub"]), _ptr(lb["cmin"]),
                      _ptr(lb["cmax"]), _ptr(self._u_next), _ptr(buf.pred_bad), self.dmp_delta0,
                      self.dmp_eps, int(bool(self.force_limit_all)), ghp, _ptr(lb["troubled"]),
-                     _ptr(lb["idx"]), _ptr(lb["count"]), sp)
+                     _ptr(lb["idx"]), _ptr(lb["count"]), _ptr(lb["sub_n"]), _ptr(lb["cmin_n"]),
+                     _ptr(lb["cmax_n"]), sp)
         n_tr = int(lb["count"].item())
         self.sweep_log[-1] = int(buf.sweeps.max().item())
         if n_tr:
             lb["failed"].zero_()
             self._h.call("adg_rescue", self._gp(), _ptr(lb["sub"]), _ptr(lb["idx"]),
                          _ptr(lb["count"]), n_tr, _ptr(dt_dev), ghp, _ptr(self._u_next),
-                         _ptr(lb["failed"]), sp)
+                         _ptr(lb["failed"]), _ptr(lb["sub_n"]), _ptr(lb["cmin_n"]),
+                         _ptr(lb["cmax_n"]), sp)
             if int(lb["failed"].item()):
                 return False, 0.0, None   # driver.py:292-293 -> restart with dt/2
             # rescued cells changed u_next: redo its wave speeds / totals
@@ -478,6 +484,10 @@ class Simulation:
         self._h.call("adg_advance_time", _ptr(buf.t), _ptr(dt_dev), _ptr(row[1:2]), sp)
         self._u, self._u_next = self._u_next, self._u
         self._red_cur = nxt
+        # the candidate's projection (rescued cells re-projected) is u^(n+1)'s
+        for k in ("sub", "cmin", "cmax"):
+            lb[k], lb[k + "_n"] = lb[k + "_n"], lb[k]
+        lb["sub_of"] = self._u
         troubled = lb["troubled"].clone().bool()
         return True, n_tr / self.mesh.n_elements, troubled
 

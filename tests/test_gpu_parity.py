@@ -223,3 +223,27 @@ def test_explosion_64_vs_oracle(pkg):
         sim.run(np.inf, max_steps=s + 1)
         np.testing.assert_array_equal(sim.last_troubled.cpu().numpy(), osim.last_troubled)
     assert rel_linf(sim.u, osim.u) <= TOL
+
+
+def test_fused_subcell_reuse_is_bitwise(pkg):
+    """The screen's candidate projection (plus the rescue's re-projection of
+    rescued cells) replaces the next step's projection of u^(n+1): the run
+    must be bitwise identical to re-projecting every step."""
+    ext, cells, n, cfl = [(-1.0, 1.0), (-1.0, 1.0)], (40, 40), 4, 0.9 / 18.0
+    outs, flags = [], []
+    for fused in (True, False):
+        mesh = pkg.CartesianMesh(ext, cells)
+        system = pkg.make_system("euler", 2)
+        sim = pkg.Simulation(mesh, system, n, cfl, boundary="outflow", use_limiter=True)
+        sim.project_initial_condition(pkg.build_problem("explosion", system)[0])
+        fl = []
+        for s in range(6):
+            if not fused and getattr(sim, "_lim", None) is not None:
+                sim._lim["sub_of"] = None      # force the separate projection
+            sim.run(np.inf, max_steps=s + 1)
+            fl.append(sim.last_troubled.clone())
+        outs.append(sim.u.clone())
+        flags.append(torch.stack(fl))
+    assert torch.equal(flags[0], flags[1])
+    assert flags[0].any()
+    assert torch.equal(outs[0], outs[1])
