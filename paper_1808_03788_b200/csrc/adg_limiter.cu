@@ -398,48 +398,44 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
   double* s_hi = s_lo + M;
   for (int64_t e = (int64_t)blockIdx.x * W::WPB + warp; e < E; e += (int64_t)gridDim.x * W::WPB) {
     for (int x = lane; x < PD * M; x += 32) nodal[x] = cand[(size_t)e * PD * M + x];
-    if (lane == 0) {
-      int64_t c[3] = {0, 0, 0};
+    // DMP bounds: lane v < M owns quantity v; own cell, then the face
+    // neighbours in axis order, low then high (min / max are order-free)
+    int64_t c[3] = {0, 0, 0};
+    {
       int64_t r = e;
+#pragma unroll
       for (int j = D - 1; j >= 0; --j) {
         c[j] = r % G.n[j];
         r /= G.n[j];
       }
-      double lo[M], hi[M];
+    }
+    const int vq = lane < M ? lane : 0;
+    double lo = cmin[e * M + vq], hi = cmax[e * M + vq];
 #pragma unroll
-      for (int v = 0; v < M; ++v) {
-        lo[v] = cmin[e * M + v];
-        hi[v] = cmax[e * M + v];
-      }
-      // own cell, then face neighbours in axis order, low then high
-      for (int j = 0; j < D; ++j) {
-        for (int side = 0; side < 2; ++side) {
-          double nlo[M], nhi[M];
-          const bool inside = side ? (c[j] + 1 < G.n[j]) : (c[j] > 0);
-          if (inside) {
-            int64_t cc[3] = {c[0], c[1], c[2]};
-            cc[j] += side ? 1 : -1;
-            const int64_t en = cell_index<D>(cc, G.n);
+    for (int j = 0; j < D; ++j) {
 #pragma unroll
-            for (int v = 0; v < M; ++v) {
-              nlo[v] = cmin[en * M + v];
-              nhi[v] = cmax[en * M + v];
-            }
-          } else {
-            ghost_extrema<D, P>(prev_sub, cmin, cmax, G, c, j, side, nlo, nhi);
-          }
+      for (int side = 0; side < 2; ++side) {
+        const bool inside = side ? (c[j] + 1 < G.n[j]) : (c[j] > 0);
+        if (inside) {
+          int64_t en = 0;
 #pragma unroll
-          for (int v = 0; v < M; ++v) {
-            lo[v] = fmin(lo[v], nlo[v]);
-            hi[v] = fmax(hi[v], nhi[v]);
-          }
+          for (int a = 0; a < D; ++a) en = en * G.n[a] + c[a] + (a == j ? (side ? 1 : -1) : 0);
+          lo = fmin(lo, cmin[en * M + vq]);
+          hi = fmax(hi, cmax[en * M + vq]);
+        } else {   // warp-uniform: a boundary face of this cell
+          if (lane == 0) ghost_extrema<D, P>(prev_sub, cmin, cmax, G, c, j, side, s_lo, s_hi);
+          __syncwarp();
+          lo = fmin(lo, s_lo[vq]);
+          hi = fmax(hi, s_hi[vq]);
+          __syncwarp();
         }
       }
-#pragma unroll
-      for (int v = 0; v < M; ++v) {
-        const double delta = fmax(delta0, eps * (hi[v] - lo[v]));
-        s_lo[v] = lo[v] - delta;
-        s_hi[v] = hi[v] + delta;
+    }
+    {
+      const double delta = fmax(delta0, eps * (hi - lo));
+      if (lane < M) {
+        s_lo[lane] = lo - delta;
+        s_hi[lane] = hi + delta;
       }
     }
     __syncwarp();

@@ -248,9 +248,17 @@ predict_kernel(const __grid_constant__ PredArgs a) {
   const double dt = *a.dt;
   const int max_iter = a.max_iter;
 
-  const double* Dx = a.dd;
-  const double* Dy = a.dd + P * P;
-  const double* Dz = a.dd + 2 * P * P;
+  // D / dx per direction: 3-D reads them as uniform constant-bank operands
+  // (no shared wavefronts on the bottleneck pipe); 1-D / 2-D stage them in
+  // shared memory, where ptxas otherwise hoists the constants into registers
+  // and spills
+  if constexpr (D < 3) {
+    for (int x = tid; x < D * P * P; x += NT) Ds[x] = a.dd[x];
+  }
+  const double* DD = D == 3 ? a.dd : Ds;
+  const double* Dx = DD;
+  const double* Dy = DD + P * P;
+  const double* Dz = DD + 2 * P * P;
 
   // role coordinates; item is the owned line / node in every role
   const int ni = (D == 3) ? item / (P * P) : (D == 2 ? item / P : item);
@@ -322,7 +330,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #pragma unroll
     for (int pass = 0; pass < (P >= 3 ? 2 : 1); ++pass) {
       __syncthreads();
-      if (valid) spatial_line_tasks<D, P, PRIM ? 2 : 0>(W0, PA, a.dd, gm1, item);
+      if (valid) spatial_line_tasks<D, P, PRIM ? 2 : 0>(W0, PA, DD, gm1, item);
       __syncthreads();
       double* kk = pass == 0 ? k1 : k2;
       if (valid) {
@@ -393,8 +401,41 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       // `pre` and folded into all P outputs at once (acc[i] += W[i][l] f_l;
       // same per-output fma order as a row-by-row mat-vec, but only one
       // transformed state is live instead of P)
+      // (3-D: l-outer; 1-D / 2-D keep the transformed line and contract row
+      // by row, which ptxas allocates with fewer spills there; both give
+      // each output the same fma order)
       auto line_pass = [&](auto&& qaddr, int dir, const double* W, double sgn,
                            double (&acc)[P][M]) {
+        if constexpr (D < 3) {
+          double fl[P][M];
+#pragma unroll
+          for (int l = 0; l < P; ++l) {
+            double q[M];
+            const double* src = Q + qaddr(l);
+#pragma unroll
+            for (int v = 0; v < M; ++v) q[v] = src[v];
+            pre(q, dir, fl[l]);
+            if (PRIM && dir == 0) {
+#pragma unroll
+              for (int v = 0; v < M; ++v) ql[PRIM ? l : 0][v] = q[v];
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            double y[M];
+#pragma unroll
+            for (int v = 0; v < M; ++v) y[v] = 0.0;
+#pragma unroll
+            for (int l = 0; l < P; ++l) {
+              const double d = sgn * W[i * P + l];
+#pragma unroll
+              for (int v = 0; v < M; ++v) y[v] = fma(d, fl[l][v], y[v]);
+            }
+#pragma unroll
+            for (int v = 0; v < M; ++v) acc[i][v] = y[v];
+          }
+          return;
+        }
 #pragma unroll
         for (int i = 0; i < P; ++i)
 #pragma unroll
