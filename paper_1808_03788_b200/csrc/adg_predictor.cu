@@ -52,13 +52,33 @@ struct PredCfg {
   static constexpr int NBUF = D == 3 ? (SEQ_YZ ? 2 : 3) : 2;   // Q + partial buffers
   static constexpr int SPAT = D * PD * M;        // per-direction spatial pieces
   static constexpr int RSZ0 = TILE > SPAT ? TILE : SPAT;
-  static constexpr int RSZ = RSZ0 + (RSZ0 & 1);  // region size (even: 16-B aligned)
-  static constexpr int ELEM = NBUF * RSZ;        // doubles per element
 #ifndef ADG_TILE_BUDGET_KB
 #define ADG_TILE_BUDGET_KB 110
 #endif
   static constexpr int BUDGET = ADG_TILE_BUDGET_KB * 1024;  // bytes of tiles per CTA (>= 2 CTAs/SM)
   static constexpr int EPB_T = (256 / PD) > 0 ? (256 / PD) : 1;
+  static constexpr int EPB_S0 = (BUDGET / (NBUF * RSZ0 * 8)) > 0 ? (BUDGET / (NBUF * RSZ0 * 8)) : 1;
+  // face-trace staging: the 2D trace blocks of an element are assembled in
+  // shared memory behind the published fbar and leave with cp.async.bulk
+  // (one 16-byte-aligned bulk store per face) instead of 40-byte-strided
+  // per-thread stores
+  static constexpr int TB = PD * M + ((PD * M) & 1);
+  static constexpr int FBAR = D * PD * M;
+  static constexpr int ST_OFF = FBAR + (FBAR & 1);
+  // u^n of the CTA's next element is prefetched (cp.async) into the tail of
+  // the z-partial buffer, which is dead from the end of the sweeps until the
+  // next element's sweeps (the staged traces run from B1 into its head); the
+  // startup stages its states there.  Lone 3-D elements with three buffers
+  // (C2: N=4); the regions grow by the few doubles the tail needs
+#ifndef ADG_PREFETCH_U
+#define ADG_PREFETCH_U 1
+#endif
+  static constexpr bool PREFETCH = ADG_PREFETCH_U && NBUF == 3 && (EPB_T < EPB_S0 ? EPB_T : EPB_S0) == 1;
+  static constexpr int PF_NEED = (ST_OFF + 2 * D * TB + PD * M + 1) / 2;
+  static constexpr int RSZ1 = (PREFETCH && PF_NEED > RSZ0) ? PF_NEED : RSZ0;
+  static constexpr int RSZ = RSZ1 + (RSZ1 & 1);  // region size (even: 16-B aligned)
+  static constexpr int ELEM = NBUF * RSZ;        // doubles per element
+  static constexpr int PF_OFF = RSZ - PD * M;    // prefetch slot inside B2
   static constexpr int EPB_S = (BUDGET / (ELEM * 8)) > 0 ? (BUDGET / (ELEM * 8)) : 1;
   static constexpr int EPB = EPB_T < EPB_S ? EPB_T : EPB_S;
   static constexpr int NT = ((EPB * PD + 31) / 32) * 32;
@@ -84,14 +104,8 @@ struct PredCfg {
   static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > ADG_MINB_CAP ? ADG_MINB_CAP : MINB1);
   // spatial line tasks (startup / volume): D directions x P^(D-1) lines
   static constexpr int NTASK = D * (PD / P);
-  // face-trace staging: the 2D trace blocks of an element are assembled in
-  // shared memory behind the published fbar and leave with cp.async.bulk
-  // (one 16-byte-aligned bulk store per face) instead of 40-byte-strided
-  // per-thread stores
-  static constexpr int TB = PD * M + ((PD * M) & 1);
-  static constexpr int FBAR = D * PD * M;
-  static constexpr int ST_OFF = FBAR + (FBAR & 1);
   static constexpr bool TR_STAGE = SMEM_TILES && ((NBUF - 1) * RSZ >= ST_OFF + 2 * D * TB);
+  static_assert(!PREFETCH || (EPB == 1 && SMEM_TILES && TR_STAGE), "prefetch layout");
 };
 
 struct PredArgs {
@@ -275,6 +289,14 @@ predict_kernel(const __grid_constant__ PredArgs a) {
   const int zt = item / (P * P);
 
   const int64_t ngroups = (a.n_elem + EPB - 1) / EPB;
+  // asynchronous copy of element ge's u^n block into dst (PREFETCH layout)
+  auto prefetch_u = [&](int64_t ge, double* dst) {
+    const double* src = a.u + (size_t)ge * PD * M;
+    for (int x = tid; x < PD * M; x += NT) cp_async8(dst + x, src + x);
+    cp_async_commit();
+  };
+  if (C::PREFETCH && (int64_t)blockIdx.x < ngroups)
+    prefetch_u(blockIdx.x, tiles + 2 * C::RSZ + C::PF_OFF);
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     const int64_t e = g * EPB + el;
     const bool valid = e < a.n_elem;
@@ -295,7 +317,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     // ---------------- startup guess --------------------------------------
     // k = L(w) = ((-D_x F_x) - D_y F_y) - D_z F_z at the spatial nodes,
     // w = u (k1) then u + dt k1 (k2); states staged node-major in Q[:PD*M]
-    double* W0 = Q;                 // staged states [node][v]
+    double* W0 = C::PREFETCH ? B2 + C::PF_OFF : Q;   // staged states [node][v]
     double* PA = B1;                // per-direction pieces [dir][node][v]
     double uu[M];   // u^n (conservative), or its primitive state (PRIM)
     double k1[M];
@@ -303,11 +325,15 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     // u^n of the group's elements: coalesced cooperative copy into each
     // element's W0 (consecutive threads, consecutive doubles), then every
     // node thread takes its own state from shared memory
-    for (int x = tid; x < EPB * PD * M; x += NT) {
-      const int ee = x / (PD * M);
-      const int off = x - ee * (PD * M);
-      if (g * EPB + ee < a.n_elem)
-        tiles[ee * C::ELEM + off] = a.u[(size_t)(g * EPB + ee) * PD * M + off];
+    if constexpr (C::PREFETCH) {
+      cp_async_wait_all();   // this thread's part of u^n has landed in W0
+    } else {
+      for (int x = tid; x < EPB * PD * M; x += NT) {
+        const int ee = x / (PD * M);
+        const int off = x - ee * (PD * M);
+        if (g * EPB + ee < a.n_elem)
+          tiles[ee * C::ELEM + off] = a.u[(size_t)(g * EPB + ee) * PD * M + off];
+      }
     }
     __syncthreads();
     if (valid) {
@@ -633,6 +659,8 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       __syncthreads();
     }
 
+    // B2 is dead until the next element's sweeps: start fetching its u^n
+    if (C::PREFETCH && g + gridDim.x < ngroups) prefetch_u(g + gridDim.x, B2 + C::PF_OFF);
     if (PRIM) {
       // q_cons = prim_to_cons(q) (predictor.py:188), each node thread its own
       if (valid) {
