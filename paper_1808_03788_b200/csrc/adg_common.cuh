@@ -98,6 +98,28 @@ __device__ __forceinline__ void flux_axis(const double* q, double gm1, int a, do
   f[D + 1] = ep * va;
 }
 
+// flux_axis with a runtime axis (one instruction stream for every axis):
+// the normal momentum is selected, and the pressure enters its row through
+// the fma addend (zero elsewhere: fma(q, v, 0) is the rounded product)
+template <int D>
+__device__ __forceinline__ void flux_axis_dyn(const double* q, double gm1, int a,
+                                              double f[D + 2]) {
+  const double r = rcp_nr(q[0]);
+  double kin = q[1] * q[1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
+  const double p = gm1 * (q[D + 1] - 0.5 * kin * r);
+  const double ep = q[D + 1] + p;
+  double ma = q[1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) ma = a == j ? q[1 + j] : ma;
+  const double va = ma * r;
+  f[0] = ma;
+#pragma unroll
+  for (int i = 0; i < D; ++i) f[1 + i] = fma(q[1 + i], va, a == i ? p : 0.0);
+  f[D + 1] = ep * va;
+}
+
 // systems.py:173-178 with normal e_a: |u_n / rho| + sqrt(gamma p / rho),
 // u_n accumulated as 0 + sum_j q_j n_j exactly like the reference.
 template <int D>

@@ -35,6 +35,11 @@
 
 namespace adg {
 
+#ifndef ADG_PASS_UNROLL
+#define ADG_PASS_UNROLL 2
+#endif
+constexpr int kPassUnroll = ADG_PASS_UNROLL;
+
 template <int D, int P>
 struct PredCfg {
   static constexpr int M = D + 2;
@@ -149,39 +154,52 @@ __device__ __forceinline__ int xline(int j, int k, int t) {
 // Executed as line tasks: task -> (dir, line); the line's P states are loaded,
 // transformed pointwise by `pre` (flux of the state, or identity), contracted
 // with the P x P matrix W_dir and written node-major into part[dir].
+// The direction is a runtime value (strides, flux normal, matrix offset), so
+// lanes of different directions run one instruction stream: no divergence
+// and one copy of the code per call site.
 // Used for the two startup rates (predictor.py:99-126) and the volume
 // integral's stiffness contraction (corrector.py:169-176).
-template <int D, int P, int MODE, int DIR>
+template <int D, int P, int MODE>
 __device__ __forceinline__ void spatial_line_task(const double* __restrict__ X,
                                                   double* __restrict__ part,
                                                   const double* __restrict__ W, double gm1,
-                                                  int line) {
-  // MODE 0: X = states [node][v], pre = flux along DIR, W = D/dx (all dirs)
+                                                  int dir, int line) {
+  // MODE 0: X = states [node][v], pre = flux along dir, W = D/dx (all dirs)
   // MODE 1: X = per-direction rows X[dir][node][v], W = stiffness (shared)
   // MODE 2: X = primitive states [node][v], no pre (gradients), W = D/dx
   using C = PredCfg<D, P>;
   constexpr int M = C::M, PD = C::PD;
   const int ta = D == 3 ? line / P : line;
   const int tb = D == 3 ? line % P : 0;
+  // first node and node stride of the line (row-major, last axis fastest)
+  int base, stride;
+  if (D == 3) {
+    base = dir == 0 ? ta * P + tb : (dir == 1 ? ta * P * P + tb : ta * P * P + tb * P);
+    stride = dir == 0 ? P * P : (dir == 1 ? P : 1);
+  } else if (D == 2) {
+    base = dir == 0 ? ta : ta * P;
+    stride = dir == 0 ? P : 1;
+  } else {
+    base = 0;
+    stride = 1;
+  }
+  const double* Xd = MODE == 1 ? X + dir * PD * M : X;
   double x[P][M];
 #pragma unroll
   for (int l = 0; l < P; ++l) {
-    const int nd = DIR == 0 ? node3<D, P>(l, ta, tb)
-                            : (DIR == 1 ? node3<D, P>(ta, l, tb) : node3<D, P>(ta, tb, l));
+    const int nd = base + l * stride;
     if (MODE == 0) {
       double q[M];
 #pragma unroll
-      for (int v = 0; v < M; ++v) q[v] = X[nd * M + v];
-      flux_axis<D>(q, gm1, DIR, x[l]);
-    } else if (MODE == 2) {
-#pragma unroll
-      for (int v = 0; v < M; ++v) x[l][v] = X[nd * M + v];
+      for (int v = 0; v < M; ++v) q[v] = Xd[nd * M + v];
+      flux_axis_dyn<D>(q, gm1, dir, x[l]);
     } else {
 #pragma unroll
-      for (int v = 0; v < M; ++v) x[l][v] = X[(DIR * PD + nd) * M + v];
+      for (int v = 0; v < M; ++v) x[l][v] = Xd[nd * M + v];
     }
   }
-  const double* Wd = MODE != 1 ? W + DIR * P * P : W;
+  const double* Wd = MODE != 1 ? W + dir * P * P : W;
+  double* pd = part + dir * PD * M;
 #pragma unroll
   for (int i = 0; i < P; ++i) {
     double y[M];
@@ -193,10 +211,9 @@ __device__ __forceinline__ void spatial_line_task(const double* __restrict__ X,
 #pragma unroll
       for (int v = 0; v < M; ++v) y[v] = fma(d, x[l][v], y[v]);
     }
-    const int nd = DIR == 0 ? node3<D, P>(i, ta, tb)
-                            : (DIR == 1 ? node3<D, P>(ta, i, tb) : node3<D, P>(ta, tb, i));
+    const int nd = base + i * stride;
 #pragma unroll
-    for (int v = 0; v < M; ++v) part[(DIR * PD + nd) * M + v] = y[v];
+    for (int v = 0; v < M; ++v) pd[nd * M + v] = y[v];
   }
 }
 
@@ -211,12 +228,19 @@ __device__ __forceinline__ void spatial_line_tasks(const double* __restrict__ X,
                                                    int item) {
   using C = PredCfg<D, P>;
   constexpr int PD = C::PD, PF = PD / P;
+  // a lone element whose direction groups fit in whole warps: warp-aligned
+  // tasks (dir = tid / WPD): the matrix offset is warp-uniform
+  constexpr int WPD = ((PF + 31) / 32) * 32;
+  if constexpr (C::EPB == 1 && D * WPD <= C::NT) {
+    const int tid = threadIdx.x;
+    const int dir = tid / WPD;
+    const int line = tid - dir * WPD;
+    if (line < PF && dir < D) spatial_line_task<D, P, MODE>(X, part, W, gm1, dir, line);
+    return;
+  }
   for (int task = item; task < C::NTASK; task += PD) {
     const int dir = task / PF;
-    const int line = task - dir * PF;
-    if (dir == 0) spatial_line_task<D, P, MODE, 0>(X, part, W, gm1, line);
-    if (D >= 2 && dir == 1) spatial_line_task<D, P, MODE, (D >= 2 ? 1 : 0)>(X, part, W, gm1, line);
-    if (D == 3 && dir == 2) spatial_line_task<D, P, MODE, (D == 3 ? 2 : 0)>(X, part, W, gm1, line);
+    spatial_line_task<D, P, MODE>(X, part, W, gm1, dir, task - dir * PF);
   }
 }
 
@@ -353,7 +377,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         for (int v = 0; v < M; ++v) W0[item * M + v] = uu[v];
       }
     }
-#pragma unroll
+#pragma unroll kPassUnroll
     for (int pass = 0; pass < (P >= 3 ? 2 : 1); ++pass) {
       __syncthreads();
       if (valid) spatial_line_tasks<D, P, PRIM ? 2 : 0>(W0, PA, DD, gm1, item);
