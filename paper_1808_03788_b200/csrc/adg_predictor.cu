@@ -91,8 +91,13 @@ struct PredCfg {
   // the residual partials of a lone 3-D element live in its z-partial buffer
   // (dead during the reduction), so the C2 tile (3 x 25 KB) + D/dx fits
   // three CTAs per SM
-  static constexpr bool RED_IN_TILE = (NBUF == 3 && EPB == 1 && 2 * NT <= RSZ);
-  static constexpr int SMALL_DBL = ((3 * P * P + (RED_IN_TILE ? 0 : 2 * NT) + 1) / 2) * 2;
+  // a lone element reduces its residual norms warp by warp (xor shuffles)
+  // and every thread folds the NW warp partials itself, in warp order:
+  // one barrier per sweep for the residual instead of three
+  static constexpr bool WARP_RED = (EPB == 1);
+  static constexpr bool RED_IN_TILE = (!WARP_RED && NBUF == 3 && EPB == 1 && 2 * NT <= RSZ);
+  static constexpr int RED_DBL = WARP_RED ? 2 * NW : (RED_IN_TILE ? 0 : 2 * NT);
+  static constexpr int SMALL_DBL = ((3 * P * P + RED_DBL + 1) / 2) * 2;
   static constexpr int FLAGS = 5 * EPB + 1;
   static constexpr size_t SMALL_BYTES = SMALL_DBL * 8 + ((FLAGS * 4 + 15) / 16) * 16;
   static constexpr size_t TILE_BYTES = (size_t)EPB * ELEM * 8;
@@ -258,7 +263,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
   const DegreeTables& T = tab<P>();
   extern __shared__ __align__(16) double smem[];
   double* Ds = smem;                          // [3][P][P] D / dx_dir
-  int* fl = reinterpret_cast<int*>(Ds + 3 * P * P + (C::RED_IN_TILE ? 0 : 2 * NT));
+  int* fl = reinterpret_cast<int*>(Ds + 3 * P * P + C::RED_DBL);
   int* frozen = fl;                           // [EPB]
   int* conv = fl + EPB;                       // [EPB]
   int* nsw = fl + 2 * EPB;                    // [EPB]
@@ -431,9 +436,10 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 
     // ---------------- Picard sweeps -----------------------------------
     int it = 0;
+    bool fz = !valid;   // WARP_RED: the lone element's frozen flag, same in every thread
     for (; it < max_iter; ++it) {
-      if (*all_frozen) break;
-      const bool work = valid && !frozen[el];
+      if (C::WARP_RED ? fz : *all_frozen) break;
+      const bool work = valid && !(C::WARP_RED ? fz : frozen[el]);
       double rate[P][M];             // conservative: the rate; PRIM: first the x-gradient
       double ql[PRIM ? P : 1][M];    // PRIM: the x-owner's primitive states
       double gyr[(PRIM && C::SEQ_YZ) ? P : 1][M];
@@ -545,6 +551,10 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       // shared traffic as three buffers, one more barrier, 2/3 of the shared
       // footprint and only one P x M block live per phase.
       constexpr bool RMW = C::SEQ_YZ && !PRIM;
+#ifndef ADG_DYN_YZ
+#define ADG_DYN_YZ 1
+#endif
+      constexpr bool DYN_YZ = ADG_DYN_YZ && D == 3 && !PRIM && !C::SEQ_YZ;
       if constexpr (RMW) {
         if (work) zpass(B1);
         __syncthreads();
@@ -563,8 +573,49 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         }
       } else {
       if (work) {
-        if (D == 3 && !C::SEQ_YZ) zpass(B2);
-        if (D >= 2) ypass(B1);
+        if constexpr (DYN_YZ) {
+          // z then y owner through one instruction stream (runtime axis):
+          // line nodes base + l * nstride at time slot tt; the P outputs land
+          // in the x-line-major rows dbase + kk * dstride, slot `slot`
+#pragma unroll 1
+          for (int dd = 2; dd >= 1; --dd) {
+            const bool zz = dd == 2;
+            const int nbase = zz ? zi * P * P + zj * P : yi * P * P + yk;
+            const int nstride = zz ? 1 : P;
+            const int tt = zz ? zt : yt;
+            const int dbase = zz ? zt + P * P * zj : yt + P * yk;
+            const int dstride = zz ? P : P * P;
+            const int slot = zz ? zi : yi;
+            double* dst = zz ? B2 : B1;
+            const double* W = DD + dd * P * P;
+            double acc[P][M];
+#pragma unroll
+            for (int i = 0; i < P; ++i)
+#pragma unroll
+              for (int v = 0; v < M; ++v) acc[i][v] = 0.0;
+#pragma unroll
+            for (int l = 0; l < P; ++l) {
+              double q[M], f[M];
+              const double* src = Q + (nbase + l * nstride) * LS + tt * M;
+#pragma unroll
+              for (int v = 0; v < M; ++v) q[v] = src[v];
+              flux_axis_dyn<D>(q, gm1, dd, f);
+#pragma unroll
+              for (int i = 0; i < P; ++i) {
+                const double d = W[i * P + l];
+#pragma unroll
+                for (int v = 0; v < M; ++v) acc[i][v] = fma(d, f[v], acc[i][v]);
+              }
+            }
+#pragma unroll
+            for (int kk = 0; kk < P; ++kk)
+#pragma unroll
+              for (int v = 0; v < M; ++v) dst[(dbase + kk * dstride) * LS + slot * M + v] = acc[kk][v];
+          }
+        } else {
+          if (D == 3 && !C::SEQ_YZ) zpass(B2);
+          if (D >= 2) ypass(B1);
+        }
         line_pass([&](int l) { return node3<D, P>(l, xj, xk) * LS + xt * M; }, 0, Dx,
                   PRIM ? 1.0 : -1.0, rate);
       }
@@ -646,6 +697,38 @@ predict_kernel(const __grid_constant__ PredArgs a) {
             Q[item * LS + t * M + v] = qn;
           }
         }
+      }
+      if constexpr (C::WARP_RED) {
+        const int warp = tid >> 5, lane = tid & 31;
+        double s1 = lane_ok ? sd : 0.0, s2 = lane_ok ? sq : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (lane == 0) {
+          red[2 * warp] = s1;
+          red[2 * warp + 1] = s2;
+        }
+        __syncthreads();
+        if (!fz) {
+          double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+          for (int w = 0; w < C::NW; ++w) {
+            t1 += red[2 * w];
+            t2 += red[2 * w + 1];
+          }
+          const double res = T.k1_opnorm * sqrt(t1);
+          const double scale = 1.0 + sqrt(t2);
+          const int c = res <= a.tol * scale;
+          if (c && it + 1 >= a.min_iter) fz = true;
+          if (tid == 0) {
+            conv[0] = c;
+            nsw[0] = it + 1;
+          }
+        }
+        // red is rewritten only after the next sweep's two barriers
+        continue;
       }
       red[2 * tid] = lane_ok ? sd : 0.0;
       red[2 * tid + 1] = lane_ok ? sq : 0.0;
