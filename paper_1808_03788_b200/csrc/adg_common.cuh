@@ -211,6 +211,39 @@ __device__ __forceinline__ bool admissible(const double* q, double gm1) {
   return fin && (q[0] > 0.0) && (p > 0.0);
 }
 
+// flux_all and admissible of one state sharing the reciprocal of rho: the
+// sign of p = gm1 (E - 0.5 kin / rho) is read from the reciprocal-based
+// E - 0.5 kin r, which is within a few ulp of the reference's quotient; only
+// within 1e-12 of cancellation is the reference's IEEE division evaluated,
+// so the verdict is exactly systems.py:225-229's.
+template <int D>
+__device__ __forceinline__ bool flux_all_adm(const double* q, double gm1, double f[D][D + 2]) {
+  const double r = rcp_nr(q[0]);
+  double kin = q[1] * q[1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
+  const double x = 0.5 * kin * r;
+  const double dd = q[D + 1] - x;
+  const double p = gm1 * dd;
+  const double ep = q[D + 1] + p;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double vj = q[1 + j] * r;
+    f[j][0] = q[1 + j];
+#pragma unroll
+    for (int i = 0; i < D; ++i) f[j][1 + i] = q[1 + i] * vj;
+    f[j][1 + j] += p;
+    f[j][D + 1] = ep * vj;
+  }
+  bool fin = true;
+#pragma unroll
+  for (int v = 0; v < D + 2; ++v) fin = fin && isfinite(q[v]);
+  bool ppos;
+  if (fabs(dd) > 1e-12 * (fabs(q[D + 1]) + fabs(x))) ppos = dd > 0.0;
+  else ppos = pressure<D>(q, gm1) > 0.0;
+  return fin && (q[0] > 0.0) && ppos;
+}
+
 // Rusanov one-sided terms (corrector.py:100-129) for a subcell face
 template <int D>
 __device__ __forceinline__ void rusanov_pair(const double* qm, const double* qp, int a,

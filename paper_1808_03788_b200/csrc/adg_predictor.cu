@@ -317,6 +317,32 @@ predict_kernel(const __grid_constant__ PredArgs a) {
   const int zi = (item / P) % P;
   const int zt = item / (P * P);
 
+  // volume-integral scale of this thread's node per direction,
+  // (dt |Omega| / dx_j) (w_tensor / w_row) as corrector.py:172-176 forms it;
+  // element-independent, so formed once
+  double vcoef[D];
+  {
+    const double cv = a.dx[0] * (D >= 2 ? a.dx[1] : 1.0) * (D == 3 ? a.dx[2] : 1.0);
+    const double wnode = T.weights[ni] * (D >= 2 ? T.weights[nj] : 1.0) *
+                         (D == 3 ? T.weights[nk] : 1.0);
+#pragma unroll
+    for (int dir = 0; dir < D; ++dir) {
+      const int row = dir == 0 ? ni : (dir == 1 ? nj : nk);
+      vcoef[dir] = (dt * cv / a.dx[dir]) * (wnode / T.weights[row]);
+    }
+  }
+  // a lone element's volume block leaves straight from registers (strided
+  // 8-byte stores; L2 merges the sectors) instead of through shared memory
+  // and a barrier
+#ifndef ADG_VOL_DIRECT
+#define ADG_VOL_DIRECT 1
+#endif
+  constexpr bool VOL_DIRECT = ADG_VOL_DIRECT && EPB == 1;
+#ifndef ADG_VOL_NODE
+#define ADG_VOL_NODE 0
+#endif
+  constexpr bool VOL_NODE = ADG_VOL_NODE && VOL_DIRECT;
+
   const int64_t ngroups = (a.n_elem + EPB - 1) / EPB;
   // asynchronous copy of element ge's u^n block into dst (PREFETCH layout)
   auto prefetch_u = [&](int64_t ge, double* dst) {
@@ -384,7 +410,9 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     }
 #pragma unroll kPassUnroll
     for (int pass = 0; pass < (P >= 3 ? 2 : 1); ++pass) {
-      __syncthreads();
+      // pass 0 reads the u^n staged before the barrier above (PRIM
+      // rewrites it with primitive states first)
+      if (pass > 0 || PRIM) __syncthreads();
       if (valid) spatial_line_tasks<D, P, PRIM ? 2 : 0>(W0, PA, DD, gm1, item);
       __syncthreads();
       double* kk = pass == 0 ? k1 : k2;
@@ -413,7 +441,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         }
       }
     }
-    __syncthreads();   // W0 (inside Q) is about to be overwritten
+    if (!C::PREFETCH) __syncthreads();   // W0 (inside Q) is about to be overwritten
     if (valid) {
 #pragma unroll
       for (int t = 0; t < P; ++t) {
@@ -796,9 +824,8 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         double q[M];
 #pragma unroll
         for (int v = 0; v < M; ++v) q[v] = Q[item * LS + t * M + v];
-        ok = ok && admissible<D>(q, gm1);
         double f[D][M];
-        flux_all<D>(q, gm1, f);
+        ok = flux_all_adm<D>(q, gm1, f) && ok;
         const double wt = T.weights[t];
 #pragma unroll
         for (int dir = 0; dir < D; ++dir)
@@ -871,36 +898,70 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       bulk_commit();
     }
     // volume: contrib_dir = stiff x_dir fbar_dir (corrector.py:172-174)
+    if constexpr (VOL_NODE) {
+      // node form: each node thread contracts the D fbar lines through it
+      // (same per-output fma order as the line tasks), scales and stores
+      if (valid && lane_ok) {
+        double acc[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) acc[v] = 0.0;
+#pragma unroll
+        for (int dir = 0; dir < D; ++dir) {
+          const int row = dir == 0 ? ni : (dir == 1 ? nj : nk);
+          const int stride = D == 3 ? (dir == 0 ? P * P : (dir == 1 ? P : 1))
+                                    : (D == 2 ? (dir == 0 ? P : 1) : 1);
+          const double* fl = B1 + (dir * PD + item - row * stride) * M;
+          double y[M];
+#pragma unroll
+          for (int v = 0; v < M; ++v) y[v] = 0.0;
+#pragma unroll
+          for (int l = 0; l < P; ++l) {
+            const double d = T.stiff[row * P + l];
+#pragma unroll
+            for (int v = 0; v < M; ++v) y[v] = fma(d, fl[l * stride * M + v], y[v]);
+          }
+#pragma unroll
+          for (int v = 0; v < M; ++v) acc[v] += vcoef[dir] * y[v];
+        }
+        double* vo = a.vol + ((size_t)e * PD + item) * M;
+#pragma unroll
+        for (int v = 0; v < M; ++v) vo[v] = acc[v];
+      }
+    } else {
     if (valid) spatial_line_tasks<D, P, 1>(B1, Q, T.stiff, gm1, item);
     __syncthreads();
     if (valid) {
-      const double cv = a.dx[0] * (D >= 2 ? a.dx[1] : 1.0) * (D == 3 ? a.dx[2] : 1.0);
-      const double wnode = T.weights[ni] * (D >= 2 ? T.weights[nj] : 1.0) *
-                           (D == 3 ? T.weights[nk] : 1.0);
       const double* CB = Q;
       double acc[M];
 #pragma unroll
       for (int v = 0; v < M; ++v) acc[v] = 0.0;
 #pragma unroll
       for (int dir = 0; dir < D; ++dir) {
-        const int row = dir == 0 ? ni : (dir == 1 ? nj : nk);
-        const double coef = (dt * cv / a.dx[dir]) * (wnode / T.weights[row]);
 #pragma unroll
-        for (int v = 0; v < M; ++v) acc[v] += coef * CB[(dir * PD + item) * M + v];
+        for (int v = 0; v < M; ++v) acc[v] += vcoef[dir] * CB[(dir * PD + item) * M + v];
       }
-      // own row of the dir-0 block is no longer read by anyone: stage there
-      if (lane_ok) {
+      if constexpr (VOL_DIRECT) {
+        if (lane_ok) {
+          double* vo = a.vol + ((size_t)e * PD + item) * M;
+#pragma unroll
+          for (int v = 0; v < M; ++v) vo[v] = acc[v];
+        }
+      } else if (lane_ok) {
+        // own row of the dir-0 block is no longer read by anyone: stage there
 #pragma unroll
         for (int v = 0; v < M; ++v) Q[item * M + v] = acc[v];
       }
     }
-    __syncthreads();
-    // coalesced copy of the group's volume blocks to HBM
-    for (int x = tid; x < EPB * PD * M; x += NT) {
-      const int ee = x / (PD * M);
-      const int off = x - ee * (PD * M);
-      if (g * EPB + ee < a.n_elem)
-        a.vol[(size_t)(g * EPB + ee) * PD * M + off] = tiles[ee * C::ELEM + off];
+    if constexpr (!VOL_DIRECT) {
+      __syncthreads();
+      // coalesced copy of the group's volume blocks to HBM
+      for (int x = tid; x < EPB * PD * M; x += NT) {
+        const int ee = x / (PD * M);
+        const int off = x - ee * (PD * M);
+        if (g * EPB + ee < a.n_elem)
+          a.vol[(size_t)(g * EPB + ee) * PD * M + off] = tiles[ee * C::ELEM + off];
+      }
+    }
     }
     if (tid < EPB && valid_e[tid]) {
       const int64_t ee = g * EPB + tid;
