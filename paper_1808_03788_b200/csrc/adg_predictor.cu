@@ -1048,6 +1048,13 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
             int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
             int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
             std::string* err) {
+#ifndef ADG_NO_CLUSTER
+  // 3-D tiles beyond one SM's shared memory: thread-block cluster, one time
+  // slice per CTA (adg_predictor_cluster.cu)
+  if (predict_cluster_supported(g))
+    return predict_cluster(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
+                           sweeps, st, num_sms, err);
+#endif
   PredArgs a{};
   a.u = u;
   a.dt = dt_dev;

@@ -247,3 +247,43 @@ def test_fused_subcell_reuse_is_bitwise(pkg):
     assert torch.equal(flags[0], flags[1])
     assert flags[0].any()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n", [6, 7, 8, 9])
+def test_large_tile_predictor_matches_oracle(pkg, n):
+    """3-D N>=7 tiles run as a thread-block cluster (one time slice per CTA,
+    time operator over DSMEM): q, traces, volume and sweep counts against the
+    oracle's per-element Picard on seeded, anisotropic data (N=6 is the
+    single-CTA shared-memory kernel, for comparison)."""
+    from oracle import dg
+    from oracle.basis import oracle_tables
+    from oracle.euler import EulerOracle
+    from paper_1808_03788_b200.predictor import run_predictor
+
+    rng = np.random.default_rng(n)
+    cells = (3, 2, 1)
+    P = n + 1
+    x = rng.uniform(0, 1, cells + (P,) * 3)
+    y = rng.uniform(0, 1, cells + (P,) * 3)
+    u = np.empty(cells + (P,) * 3 + (5,))
+    rho = 1.0 + 0.3 * np.sin(2 * np.pi * x)
+    u[..., 0] = rho
+    u[..., 1] = rho * (0.7 + 0.2 * y)
+    u[..., 2] = rho * -0.4
+    u[..., 3] = rho * (0.2 - 0.1 * y)
+    u[..., 4] = 2.5 + 0.5 * rho * (0.81 + 0.16 + 0.09)
+    sp = (0.1, 0.2, 0.15)
+    dt = 5e-4
+    tabs = oracle_tables(n)
+    ref = dg.picard_solve(u, EulerOracle(3), sp, dt, tabs, per_element=True)
+    res, good = run_predictor(torch.as_tensor(u).cuda(), pkg.make_system("euler", 3), sp, dt,
+                              pkg.basis_tables(n))
+    assert bool(good.all())
+    assert rel_linf(res.q, ref.q) <= 1e-12
+    np.testing.assert_array_equal(res.sweeps.cpu().numpy(), ref.sweeps)
+    tr = dg.extract_traces(ref.q, tabs, 3)
+    for j in range(3):
+        for s in (0, 1):
+            assert rel_linf(res.traces[(j, s)], tr[(j, s)]) <= 1e-12
+    vol = dg.volume_integral(ref.q, EulerOracle(3), sp, dt, tabs)
+    assert rel_linf(res.volume, vol) <= 1e-11
