@@ -46,6 +46,16 @@ struct PredCfg {
   static constexpr int PD = ipow(P, D);      // spatial nodes = threads per element
   static constexpr int PT = PD * P;          // space-time nodes
   static constexpr int TILE = PT * M;        // doubles in one space-time tile
+  // space-time tile and x-line-major partial rows share padded strides: a
+  // node's (or a row's) P x m block is contiguous (LS doubles); 3-D P = 4
+  // pads the middle axis by one double (power-of-two strides would put
+  // every owner role's lanes on a few banks; tools/bankcheck.py)
+  static constexpr int LS = P * M;
+  static constexpr int QPAD = (D == 3 && P == 4) ? 1 : 0;
+  static constexpr int QK = LS;
+  static constexpr int QJ = P * QK + QPAD;
+  static constexpr int QI = P * QJ;
+  static constexpr int TILEP = D == 3 ? P * QI : TILE;
   static constexpr int TILE_PAD = TILE + (TILE & 1);
   // 3-D tiles from N=5 up exchange the y and z partials one after the other
   // through a single buffer, so N=5/6 tiles fit two CTAs and N=6 one CTA of
@@ -56,12 +66,18 @@ struct PredCfg {
   static constexpr bool SEQ_YZ = (D == 3 && P >= ADG_SEQ_YZ_MINP);
   static constexpr int NBUF = D == 3 ? (SEQ_YZ ? 2 : 3) : 2;   // Q + partial buffers
   static constexpr int SPAT = D * PD * M;        // per-direction spatial pieces
-  static constexpr int RSZ0 = TILE > SPAT ? TILE : SPAT;
+  static constexpr int RSZ0 = TILEP > SPAT ? TILEP : SPAT;
 #ifndef ADG_TILE_BUDGET_KB
 #define ADG_TILE_BUDGET_KB 110
 #endif
   static constexpr int BUDGET = ADG_TILE_BUDGET_KB * 1024;  // bytes of tiles per CTA (>= 2 CTAs/SM)
-  static constexpr int EPB_T = (256 / PD) > 0 ? (256 / PD) : 1;
+  // elements per CTA by thread count; 3-D tiles from P = ADG_LONE_MINP up
+  // run one element per CTA (the lone-element schedule: prefetch, warp
+  // residual reduction, direct volume stores)
+#ifndef ADG_LONE_MINP
+#define ADG_LONE_MINP 3
+#endif
+  static constexpr int EPB_T = (D == 3 && P >= ADG_LONE_MINP) ? 1 : ((256 / PD) > 0 ? (256 / PD) : 1);
   static constexpr int EPB_S0 = (BUDGET / (NBUF * RSZ0 * 8)) > 0 ? (BUDGET / (NBUF * RSZ0 * 8)) : 1;
   // face-trace staging: the 2D trace blocks of an element are assembled in
   // shared memory behind the published fbar and leave with cp.async.bulk
@@ -111,7 +127,9 @@ struct PredCfg {
 #ifndef ADG_MINB_CAP
 #define ADG_MINB_CAP 3
 #endif
-  static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > ADG_MINB_CAP ? ADG_MINB_CAP : MINB1);
+  // at least 12 warps per SM worth of CTAs before registers may grow past 170
+  static constexpr int MINB_CAP = (384 / NT) > ADG_MINB_CAP ? (384 / NT) : ADG_MINB_CAP;
+  static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > MINB_CAP ? MINB_CAP : MINB1);
   // spatial line tasks (startup / volume): D directions x P^(D-1) lines
   static constexpr int NTASK = D * (PD / P);
   static constexpr bool TR_STAGE = SMEM_TILES && ((NBUF - 1) * RSZ >= ST_OFF + 2 * D * TB);
@@ -152,6 +170,21 @@ __device__ __forceinline__ int node3(int i, int j, int k) {
 template <int D, int P>
 __device__ __forceinline__ int xline(int j, int k, int t) {
   return D == 3 ? t + P * k + P * P * j : (D == 2 ? t + P * j : t);
+}
+
+// offset of spatial node (i, j, k)'s P x m block in the padded tile, and of
+// x-line row (j, k, t) in the padded partial buffers
+template <int D, int P>
+__device__ __forceinline__ int noff(int i, int j, int k) {
+  using C = PredCfg<D, P>;
+  if (D == 3) return i * C::QI + j * C::QJ + k * C::QK;
+  return node3<D, P>(i, j, k) * C::LS;
+}
+template <int D, int P>
+__device__ __forceinline__ int roff(int j, int k, int t) {
+  using C = PredCfg<D, P>;
+  if (D == 3) return j * C::QI + k * C::QJ + t * C::QK;
+  return xline<D, P>(j, k, t) * C::LS;
 }
 
 // Contract one direction of a spatial (single time level) field held
@@ -258,7 +291,7 @@ template <int D, int P, int PRIM>
 __global__ void __launch_bounds__(PredCfg<D, P>::NT, PredCfg<D, P>::MINB)
 predict_kernel(const __grid_constant__ PredArgs a) {
   using C = PredCfg<D, P>;
-  constexpr int M = C::M, PD = C::PD, EPB = C::EPB, NT = C::NT, LS = P * M;
+  constexpr int M = C::M, PD = C::PD, EPB = C::EPB, NT = C::NT, LS = C::LS;
   constexpr int TP = C::RSZ;
   const DegreeTables& T = tab<P>();
   extern __shared__ __align__(16) double smem[];
@@ -316,6 +349,8 @@ predict_kernel(const __grid_constant__ PredArgs a) {
   const int zj = item % P;                                            // z: [t][i][j]
   const int zi = (item / P) % P;
   const int zt = item / (P * P);
+  const int qn0 = noff<D, P>(ni, nj, nk);   // node role: own node block in the tile
+  const int xr0 = roff<D, P>(xj, xk, xt);   // x-owner: own row in the partial buffers
 
   // volume-integral scale of this thread's node per direction,
   // (dt |Omega| / dx_j) (w_tensor / w_row) as corrector.py:172-176 forms it;
@@ -448,12 +483,12 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         const double s = T.nodes[t] * dt;
         if (P <= 2) {
 #pragma unroll
-          for (int v = 0; v < M; ++v) Q[item * LS + t * M + v] = uu[v] + s * k1[v];
+          for (int v = 0; v < M; ++v) Q[qn0 + t * M + v] = uu[v] + s * k1[v];
         } else {
           const double c2 = 0.5 * s * s / dt;
 #pragma unroll
           for (int v = 0; v < M; ++v)
-            Q[item * LS + t * M + v] = uu[v] + s * k1[v] + c2 * (k2[v] - k1[v]);
+            Q[qn0 + t * M + v] = uu[v] + s * k1[v] + c2 * (k2[v] - k1[v]);
         }
       }
     }
@@ -546,20 +581,20 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       // z-owner: own z-line -> D_z partials, x-line-major rows of dst
       auto zpass = [&](double* dst) {
         double acc[P][M];
-        line_pass([&](int l) { return node3<D, P>(zi, zj, l) * LS + zt * M; }, 2, Dz, 1.0, acc);
+        line_pass([&](int l) { return noff<D, P>(zi, zj, l) + zt * M; }, 2, Dz, 1.0, acc);
 #pragma unroll
         for (int kk = 0; kk < P; ++kk)
 #pragma unroll
-          for (int v = 0; v < M; ++v) dst[xline<D, P>(zj, kk, zt) * LS + zi * M + v] = acc[kk][v];
+          for (int v = 0; v < M; ++v) dst[roff<D, P>(zj, kk, zt) + zi * M + v] = acc[kk][v];
       };
       // y-owner: own y-line -> D_y partials, x-line-major rows of dst
       auto ypass = [&](double* dst) {
         double acc[P][M];
-        line_pass([&](int l) { return node3<D, P>(yi, l, yk) * LS + yt * M; }, 1, Dy, 1.0, acc);
+        line_pass([&](int l) { return noff<D, P>(yi, l, yk) + yt * M; }, 1, Dy, 1.0, acc);
 #pragma unroll
         for (int jj = 0; jj < P; ++jj)
 #pragma unroll
-          for (int v = 0; v < M; ++v) dst[xline<D, P>(jj, yk, yt) * LS + yi * M + v] = acc[jj][v];
+          for (int v = 0; v < M; ++v) dst[roff<D, P>(jj, yk, yt) + yi * M + v] = acc[jj][v];
       };
       // A: y/z-owners publish their partials first, then the x-owner's
       // -D_x F_x (PRIM: +D_x v) accumulates straight into `rate`, so only
@@ -567,11 +602,11 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       // y-owner, accumulating: dst += D_y F_y (RMW schedule below)
       auto ypass_add = [&](double* dst) {
         double acc[P][M];
-        line_pass([&](int l) { return node3<D, P>(yi, l, yk) * LS + yt * M; }, 1, Dy, 1.0, acc);
+        line_pass([&](int l) { return noff<D, P>(yi, l, yk) + yt * M; }, 1, Dy, 1.0, acc);
 #pragma unroll
         for (int jj = 0; jj < P; ++jj)
 #pragma unroll
-          for (int v = 0; v < M; ++v) dst[xline<D, P>(jj, yk, yt) * LS + yi * M + v] += acc[jj][v];
+          for (int v = 0; v < M; ++v) dst[roff<D, P>(jj, yk, yt) + yi * M + v] += acc[jj][v];
       };
       // Two-buffer 3-D schedule (conservative mode): the z partials go to B1,
       // the y-owners add theirs in place, and the x-owner subtracts the sum
@@ -589,14 +624,14 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         if (work) ypass_add(B1);
         __syncthreads();
         if (work) {
-          line_pass([&](int l) { return node3<D, P>(l, xj, xk) * LS + xt * M; }, 0, Dx, -1.0,
+          line_pass([&](int l) { return noff<D, P>(l, xj, xk) + xt * M; }, 0, Dx, -1.0,
                     rate);
 #pragma unroll
           for (int i = 0; i < P; ++i)
 #pragma unroll
             for (int v = 0; v < M; ++v) {
-              const double r = rate[i][v] - B1[item * LS + i * M + v];
-              B1[item * LS + i * M + v] = r;
+              const double r = rate[i][v] - B1[xr0 + i * M + v];
+              B1[xr0 + i * M + v] = r;
             }
         }
       } else {
@@ -608,11 +643,11 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #pragma unroll 1
           for (int dd = 2; dd >= 1; --dd) {
             const bool zz = dd == 2;
-            const int nbase = zz ? zi * P * P + zj * P : yi * P * P + yk;
-            const int nstride = zz ? 1 : P;
+            const int nbase = zz ? zi * C::QI + zj * C::QJ : yi * C::QI + yk * C::QK;
+            const int nstride = zz ? C::QK : C::QJ;
             const int tt = zz ? zt : yt;
-            const int dbase = zz ? zt + P * P * zj : yt + P * yk;
-            const int dstride = zz ? P : P * P;
+            const int dbase = zz ? zj * C::QI + zt * C::QK : yk * C::QJ + yt * C::QK;
+            const int dstride = zz ? C::QJ : C::QI;
             const int slot = zz ? zi : yi;
             double* dst = zz ? B2 : B1;
             const double* W = DD + dd * P * P;
@@ -624,7 +659,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #pragma unroll
             for (int l = 0; l < P; ++l) {
               double q[M], f[M];
-              const double* src = Q + (nbase + l * nstride) * LS + tt * M;
+              const double* src = Q + nbase + l * nstride + tt * M;
 #pragma unroll
               for (int v = 0; v < M; ++v) q[v] = src[v];
               flux_axis_dyn<D>(q, gm1, dd, f);
@@ -638,13 +673,13 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #pragma unroll
             for (int kk = 0; kk < P; ++kk)
 #pragma unroll
-              for (int v = 0; v < M; ++v) dst[(dbase + kk * dstride) * LS + slot * M + v] = acc[kk][v];
+              for (int v = 0; v < M; ++v) dst[dbase + kk * dstride + slot * M + v] = acc[kk][v];
           }
         } else {
           if (D == 3 && !C::SEQ_YZ) zpass(B2);
           if (D >= 2) ypass(B1);
         }
-        line_pass([&](int l) { return node3<D, P>(l, xj, xk) * LS + xt * M; }, 0, Dx,
+        line_pass([&](int l) { return noff<D, P>(l, xj, xk) + xt * M; }, 0, Dx,
                   PRIM ? 1.0 : -1.0, rate);
       }
       if (D >= 2) __syncthreads();
@@ -655,8 +690,8 @@ predict_kernel(const __grid_constant__ PredArgs a) {
           for (int i = 0; i < P; ++i)
 #pragma unroll
             for (int v = 0; v < M; ++v) {
-              if (PRIM) gyr[PRIM ? i : 0][v] = B1[item * LS + i * M + v];
-              else rate[i][v] -= B1[item * LS + i * M + v];
+              if (PRIM) gyr[PRIM ? i : 0][v] = B1[xr0 + i * M + v];
+              else rate[i][v] -= B1[xr0 + i * M + v];
             }
         }
         __syncthreads();
@@ -673,8 +708,8 @@ predict_kernel(const __grid_constant__ PredArgs a) {
           for (int v = 0; v < M; ++v) {
             gr[0][v] = rate[i][v];
             if (D >= 2) gr[D >= 2 ? 1 : 0][v] = C::SEQ_YZ ? gyr[(PRIM && C::SEQ_YZ) ? i : 0][v]
-                                                           : B1[item * LS + i * M + v];
-            if (D == 3) gr[D == 3 ? 2 : 0][v] = PZ[item * LS + i * M + v];
+                                                           : B1[xr0 + i * M + v];
+            if (D == 3) gr[D == 3 ? 2 : 0][v] = PZ[xr0 + i * M + v];
           }
           primitive_rhs<D>(ql[PRIM ? i : 0], gr, a.gamma, rate[i]);
         }
@@ -685,19 +720,19 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #pragma unroll
           for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int v = 0; v < M; ++v) rate[i][v] -= B1[item * LS + i * M + v];
+            for (int v = 0; v < M; ++v) rate[i][v] -= B1[xr0 + i * M + v];
         }
         if (!PRIM && D == 3) {
           const double* PZ = C::SEQ_YZ ? B1 : B2;
 #pragma unroll
           for (int i = 0; i < P; ++i)
 #pragma unroll
-            for (int v = 0; v < M; ++v) rate[i][v] -= PZ[item * LS + i * M + v];
+            for (int v = 0; v < M; ++v) rate[i][v] -= PZ[xr0 + i * M + v];
         }
 #pragma unroll
         for (int i = 0; i < P; ++i)
 #pragma unroll
-          for (int v = 0; v < M; ++v) B1[item * LS + i * M + v] = rate[i][v];
+          for (int v = 0; v < M; ++v) B1[xr0 + i * M + v] = rate[i][v];
       }
       }
       __syncthreads();
@@ -709,7 +744,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #pragma unroll
         for (int s = 0; s < P; ++s)
 #pragma unroll
-          for (int v = 0; v < M; ++v) r[s][v] = B1[xline<D, P>(nj, nk, s) * LS + ni * M + v];
+          for (int v = 0; v < M; ++v) r[s][v] = B1[roff<D, P>(nj, nk, s) + ni * M + v];
 #pragma unroll
         for (int t = 0; t < P; ++t) {
           const double g0 = T.g0[t];
@@ -719,10 +754,10 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #pragma unroll
             for (int s = 0; s < P; ++s) c = fma(T.gw[t * P + s], r[s][v], c);
             const double qn = c * dt + g0 * uu[v];
-            const double dq = Q[item * LS + t * M + v] - qn;
+            const double dq = Q[qn0 + t * M + v] - qn;
             sd = fma(dq, dq, sd);
             sq = fma(qn, qn, sq);
-            Q[item * LS + t * M + v] = qn;
+            Q[qn0 + t * M + v] = qn;
           }
         }
       }
@@ -803,10 +838,10 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         for (int t = 0; t < P; ++t) {
           double v[M], q[M];
 #pragma unroll
-          for (int w = 0; w < M; ++w) v[w] = Q[item * LS + t * M + w];
+          for (int w = 0; w < M; ++w) v[w] = Q[qn0 + t * M + w];
           prim_to_cons<D>(v, gm1, q);
 #pragma unroll
-          for (int w = 0; w < M; ++w) Q[item * LS + t * M + w] = q[w];
+          for (int w = 0; w < M; ++w) Q[qn0 + t * M + w] = q[w];
         }
       }
       __syncthreads();
@@ -823,7 +858,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       for (int t = 0; t < P; ++t) {
         double q[M];
 #pragma unroll
-        for (int v = 0; v < M; ++v) q[v] = Q[item * LS + t * M + v];
+        for (int v = 0; v < M; ++v) q[v] = Q[qn0 + t * M + v];
         double f[D][M];
         ok = flux_all_adm<D>(q, gm1, f) && ok;
         const double wt = T.weights[t];
@@ -847,9 +882,9 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         for (int v = 0; v < M; ++v) lo[v] = hi[v] = 0.0;
 #pragma unroll
         for (int l = 0; l < P; ++l) {
-          const int q0 = dir == 0 ? node3<D, P>(l, xj, xk) * LS + xt * M
-                                  : (dir == 1 ? node3<D, P>(yi, l, yk) * LS + yt * M
-                                              : node3<D, P>(zi, zj, l) * LS + zt * M);
+          const int q0 = dir == 0 ? noff<D, P>(l, xj, xk) + xt * M
+                                  : (dir == 1 ? noff<D, P>(yi, l, yk) + yt * M
+                                              : noff<D, P>(zi, zj, l) + zt * M);
           const double pl = T.left[l], pr = T.right[l];
 #pragma unroll
           for (int v = 0; v < M; ++v) {
@@ -877,9 +912,9 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       }
       if (C::TR_STAGE) fence_proxy_async_smem();   // staged traces -> async proxy
       if (a.q_out) {
-        double* qo = a.q_out + (size_t)e * C::TILE + (size_t)item * LS;
+        double* qo = a.q_out + (size_t)e * C::TILE + (size_t)item * LS;   // unpadded
 #pragma unroll
-        for (int x = 0; x < LS; ++x) qo[x] = Q[item * LS + x];
+        for (int x = 0; x < LS; ++x) qo[x] = Q[qn0 + x];
       }
       // publish fbar node-major for the stiffness line tasks
 #pragma unroll
