@@ -51,11 +51,13 @@ struct PredCfg {
   // pads the middle axis by one double (power-of-two strides would put
   // every owner role's lanes on a few banks; tools/bankcheck.py)
   static constexpr int LS = P * M;
+  // 2-D: node stride LS + 1 and an element stride chosen mod 16 doubles
+  // (element tiles of a CTA would otherwise start on the same bank)
   static constexpr int QPAD = (D == 3 && P == 4) ? 1 : 0;
-  static constexpr int QK = LS;
+  static constexpr int QK = LS + ((D == 2 && P >= 3) ? 1 : 0);
   static constexpr int QJ = P * QK + QPAD;
   static constexpr int QI = P * QJ;
-  static constexpr int TILEP = D == 3 ? P * QI : TILE;
+  static constexpr int TILEP = D == 3 ? P * QI : (D == 2 ? P * P * QK : TILE);
   static constexpr int TILE_PAD = TILE + (TILE & 1);
   // 3-D tiles from N=5 up exchange the y and z partials one after the other
   // through a single buffer, so N=5/6 tiles fit two CTAs and N=6 one CTA of
@@ -98,7 +100,10 @@ struct PredCfg {
   static constexpr int PF_NEED = (ST_OFF + 2 * D * TB + PD * M + 1) / 2;
   static constexpr int RSZ1 = (PREFETCH && PF_NEED > RSZ0) ? PF_NEED : RSZ0;
   static constexpr int RSZ = RSZ1 + (RSZ1 & 1);  // region size (even: 16-B aligned)
-  static constexpr int ELEM = NBUF * RSZ;        // doubles per element
+  static constexpr int EB = D != 2 ? 0 : (P == 3 ? 2 : (P == 5 ? 8 : ((P == 6 || P == 7) ? 2 : 0)));
+  static constexpr int ELEM0 = NBUF * RSZ;
+  static constexpr int ELEM = D == 2 ? ELEM0 + (((2 * TILEP + EB - ELEM0) % 16) + 16) % 16
+                                     : ELEM0;          // doubles per element
   static constexpr int PF_OFF = RSZ - PD * M;    // prefetch slot inside B2
   static constexpr int EPB_S = (BUDGET / (ELEM * 8)) > 0 ? (BUDGET / (ELEM * 8)) : 1;
   static constexpr int EPB = EPB_T < EPB_S ? EPB_T : EPB_S;
@@ -178,13 +183,13 @@ template <int D, int P>
 __device__ __forceinline__ int noff(int i, int j, int k) {
   using C = PredCfg<D, P>;
   if (D == 3) return i * C::QI + j * C::QJ + k * C::QK;
-  return node3<D, P>(i, j, k) * C::LS;
+  return node3<D, P>(i, j, k) * C::QK;
 }
 template <int D, int P>
 __device__ __forceinline__ int roff(int j, int k, int t) {
   using C = PredCfg<D, P>;
   if (D == 3) return j * C::QI + k * C::QJ + t * C::QK;
-  return xline<D, P>(j, k, t) * C::LS;
+  return xline<D, P>(j, k, t) * C::QK;
 }
 
 // Contract one direction of a spatial (single time level) field held
