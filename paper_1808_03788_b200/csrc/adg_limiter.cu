@@ -151,18 +151,23 @@ __device__ __forceinline__ void fetch_sub(const double* __restrict__ sub, const 
 // subcell averages of one cell's nodal data held in shared memory:
 // sequential per-axis contraction with P_sub (limiter.py:27-33)
 // WARP = true: the calling warp alone does the cell (tid = lane, nt = 32)
-template <int D, int P, bool WARP = false>
+// Ps: the projection matrix P_sub [S][P] staged in shared memory (the
+// lanes of a pass index different rows: constant-bank reads would replay
+// once per distinct row); null -> the constant tables
+template <int D, int P, bool WARP = false, bool SPS = false>
 __device__ void project_cell(const double* __restrict__ nodal, double* __restrict__ tmp,
-                             double* __restrict__ out, int tid, int nt) {
+                             double* __restrict__ out, int tid, int nt,
+                             const double* __restrict__ Ps = nullptr) {
   using C = LimCfg<D, P>;
   constexpr int S = C::S, M = C::M;
   const DegreeTables& T = tab<P>();
+  auto pm = [&](int idx) { return SPS ? Ps[idx] : T.sub_project[idx]; };
   if (D == 1) {
     for (int x = tid; x < S * M; x += nt) {
       const int s = x / M, v = x - s * M;
       double acc = 0.0;
 #pragma unroll
-      for (int i = 0; i < P; ++i) acc = fma(T.sub_project[s * P + i], nodal[i * M + v], acc);
+      for (int i = 0; i < P; ++i) acc = fma(pm(s * P + i), nodal[i * M + v], acc);
       out[x] = acc;
     }
     return;
@@ -174,7 +179,7 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
       double acc = 0.0;
 #pragma unroll
       for (int i0 = 0; i0 < P; ++i0)
-        acc = fma(T.sub_project[s0 * P + i0], nodal[(i0 * P + i1) * M + v], acc);
+        acc = fma(pm(s0 * P + i0), nodal[(i0 * P + i1) * M + v], acc);
       tmp[x] = acc;
     }
     if (WARP) __syncwarp(); else __syncthreads();
@@ -183,7 +188,7 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
       double acc = 0.0;
 #pragma unroll
       for (int i1 = 0; i1 < P; ++i1)
-        acc = fma(T.sub_project[s1 * P + i1], tmp[(s0 * P + i1) * M + v], acc);
+        acc = fma(pm(s1 * P + i1), tmp[(s0 * P + i1) * M + v], acc);
       out[x] = acc;
     }
     return;
@@ -193,7 +198,7 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
     const int s0 = x / (P * P * M), r = x - s0 * P * P * M;
     double acc = 0.0;
 #pragma unroll
-    for (int i0 = 0; i0 < P; ++i0) acc = fma(T.sub_project[s0 * P + i0], nodal[i0 * P * P * M + r], acc);
+    for (int i0 = 0; i0 < P; ++i0) acc = fma(pm(s0 * P + i0), nodal[i0 * P * P * M + r], acc);
     out[x] = acc;
   }
   if (WARP) __syncwarp(); else __syncthreads();
@@ -203,7 +208,7 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
     double acc = 0.0;
 #pragma unroll
     for (int i1 = 0; i1 < P; ++i1)
-      acc = fma(T.sub_project[s1 * P + i1], out[(s0 * P + i1) * P * M + r2], acc);
+      acc = fma(pm(s1 * P + i1), out[(s0 * P + i1) * P * M + r2], acc);
     tmp[x] = acc;
   }
   if (WARP) __syncwarp(); else __syncthreads();
@@ -212,7 +217,7 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
     double acc = 0.0;
 #pragma unroll
     for (int i2 = 0; i2 < P; ++i2)
-      acc = fma(T.sub_project[s2 * P + i2], tmp[(s01 * P + i2) * M + v], acc);
+      acc = fma(pm(s2 * P + i2), tmp[(s01 * P + i2) * M + v], acc);
     out[x] = acc;
   }
 }
@@ -236,18 +241,30 @@ struct WarpCfg {
   static constexpr int PER_WARP = C::PD * C::M + OUT + SCR + 2 * C::M;   // doubles
   static constexpr int W0 = (200 * 1024) / (PER_WARP * 8);
   static constexpr int WPB = W0 >= 8 ? 8 : (W0 >= 1 ? W0 : 1);   // warps (cells) per CTA
-  static constexpr size_t SMEM = (size_t)WPB * PER_WARP * 8;
+  static constexpr int PS = ((C::S * P + 1) / 2) * 2;   // staged P_sub (16-byte multiple)
+  static constexpr size_t SMEM = ((size_t)WPB * PER_WARP + PS) * 8;
 };
+
+// P_sub of this degree into the CTA's shared copy (before any warp uses it)
+template <int D, int P>
+__device__ __forceinline__ const double* stage_psub(double* dst) {
+  using C = LimCfg<D, P>;
+  const DegreeTables& T = tab<P>();
+  for (int x = threadIdx.x; x < C::S * P; x += blockDim.x) dst[x] = T.sub_project[x];
+  __syncthreads();
+  return dst;
+}
 
 // per-cell subcell averages + extrema of nodal data staged in a warp's
 // shared slice; writes sub / cmin / cmax of cell e when they are non-null
 template <int D, int P>
 __device__ __forceinline__ void warp_project_store(double* nodal, double* out, double* tmp,
                                                    int lane, int64_t e, double* sub,
-                                                   double* cmin, double* cmax) {
+                                                   double* cmin, double* cmax,
+                                                   const double* Ps) {
   using C = LimCfg<D, P>;
   constexpr int M = C::M, SD = C::SD;
-  project_cell<D, P, true>(nodal, tmp, out, lane, 32);
+  project_cell<D, P, true, true>(nodal, tmp, out, lane, 32, Ps);
   __syncwarp();
   if (sub)
     for (int x = lane; x < SD * M; x += 32) sub[(size_t)e * SD * M + x] = out[x];
@@ -282,13 +299,14 @@ subcell_prep_kernel(const double* __restrict__ u, int64_t E, double* __restrict_
   constexpr int M = C::M, PD = C::PD;
   extern __shared__ __align__(16) double lsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* Ps = stage_psub<D, P>(lsm + W::WPB * W::PER_WARP);
   double* nodal = lsm + warp * W::PER_WARP;
   double* out = nodal + PD * M;
   double* tmp = out + W::OUT;
   for (int64_t e = (int64_t)blockIdx.x * W::WPB + warp; e < E; e += (int64_t)gridDim.x * W::WPB) {
     for (int x = lane; x < PD * M; x += 32) nodal[x] = u[(size_t)e * PD * M + x];
     __syncwarp();
-    warp_project_store<D, P>(nodal, out, tmp, lane, e, sub, cmin, cmax);
+    warp_project_store<D, P>(nodal, out, tmp, lane, e, sub, cmin, cmax, Ps);
     __syncwarp();
   }
 }
@@ -391,6 +409,7 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
   constexpr int M = C::M, SD = C::SD, PD = C::PD;
   extern __shared__ __align__(16) double lsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* Ps = stage_psub<D, P>(lsm + W::WPB * W::PER_WARP);
   double* nodal = lsm + warp * W::PER_WARP;
   double* out = nodal + PD * M;
   double* tmp = out + W::OUT;
@@ -439,7 +458,7 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
       }
     }
     __syncwarp();
-    warp_project_store<D, P>(nodal, out, tmp, lane, e, sub_out, cmin_out, cmax_out);
+    warp_project_store<D, P>(nodal, out, tmp, lane, e, sub_out, cmin_out, cmax_out, Ps);
     int bad = lane == 0 ? (force_all || pred_bad[e]) : 0;
     for (int x = lane; x < SD; x += 32) {
       const double* q = out + x * M;
