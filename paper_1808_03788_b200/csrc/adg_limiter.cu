@@ -243,6 +243,11 @@ struct WarpCfg {
   static constexpr int WPB = W0 >= 8 ? 8 : (W0 >= 1 ? W0 : 1);   // warps (cells) per CTA
   static constexpr int PS = ((C::S * P + 1) / 2) * 2;   // staged P_sub (16-byte multiple)
   static constexpr size_t SMEM = ((size_t)WPB * PER_WARP + PS) * 8;
+  // tiles beyond shared memory (3-D, N >= 3): per-block slices of an
+  // L2-resident global scratch, 4 warps (cells) per block
+  static constexpr bool GS = SMEM > 227 * 1024;
+  static constexpr int WPBX = GS ? 4 : WPB;
+  static constexpr size_t BLOCK_DBL = (size_t)WPBX * PER_WARP + PS;
 };
 
 // P_sub of this degree into the CTA's shared copy (before any warp uses it)
@@ -254,6 +259,24 @@ __device__ __forceinline__ const double* stage_psub(double* dst) {
   __syncthreads();
   return dst;
 }
+
+// per-block scratch of the block-per-cell kernels (doubles); above 227 KB
+// they run on an L2-resident global scratch instead of shared memory
+template <int D, int P>
+struct LimDbl {
+  using C = LimCfg<D, P>;
+  static constexpr size_t TMP = D == 3 ? (size_t)P * C::S * C::S * C::M + (size_t)P * P * C::S * C::M
+                                       : (size_t)P * C::S * C::M;
+  static constexpr size_t RESCUE = (size_t)C::WD * C::M + (size_t)C::RD * C::M * (1 + D) +
+                                   (size_t)C::SD * C::M + TMP + (size_t)C::SD * C::M +
+                                   (size_t)C::PD * C::M + 64;
+  static constexpr size_t RECOVER = (size_t)C::SD * C::M + (size_t)C::PD * C::M + TMP;
+  static constexpr size_t POUT = D == 3 ? (size_t)C::S * P * P * C::M : (size_t)C::SD * C::M;
+  static constexpr size_t PTMP = D == 3 ? (size_t)C::S * C::S * P * C::M : (size_t)C::S * P * C::M;
+  static constexpr size_t PROJ = (size_t)C::PD * C::M +
+                                 (POUT > (size_t)C::SD * C::M ? POUT : (size_t)C::SD * C::M) + PTMP;
+  static constexpr size_t LIM = 227 * 1024 / 8;
+};
 
 // per-cell subcell averages + extrema of nodal data staged in a warp's
 // shared slice; writes sub / cmin / cmax of cell e when they are non-null
@@ -291,19 +314,20 @@ __device__ __forceinline__ void warp_project_store(double* nodal, double* out, d
 
 // prev_sub + per-cell extrema of u^n
 template <int D, int P>
-__global__ void __launch_bounds__(WarpCfg<D, P>::WPB * 32)
+__global__ void __launch_bounds__(WarpCfg<D, P>::WPBX * 32)
 subcell_prep_kernel(const double* __restrict__ u, int64_t E, double* __restrict__ sub,
-                    double* __restrict__ cmin, double* __restrict__ cmax) {
+                    double* __restrict__ cmin, double* __restrict__ cmax, double* gscr) {
   using C = LimCfg<D, P>;
   using W = WarpCfg<D, P>;
   constexpr int M = C::M, PD = C::PD;
-  extern __shared__ __align__(16) double lsm[];
+  extern __shared__ __align__(16) double lsm_s[];
+  double* lsm = W::GS ? gscr + (size_t)blockIdx.x * W::BLOCK_DBL : lsm_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* Ps = stage_psub<D, P>(lsm + W::WPB * W::PER_WARP);
+  const double* Ps = stage_psub<D, P>(lsm + W::WPBX * W::PER_WARP);
   double* nodal = lsm + warp * W::PER_WARP;
   double* out = nodal + PD * M;
   double* tmp = out + W::OUT;
-  for (int64_t e = (int64_t)blockIdx.x * W::WPB + warp; e < E; e += (int64_t)gridDim.x * W::WPB) {
+  for (int64_t e = (int64_t)blockIdx.x * W::WPBX + warp; e < E; e += (int64_t)gridDim.x * W::WPBX) {
     for (int x = lane; x < PD * M; x += 32) nodal[x] = u[(size_t)e * PD * M + x];
     __syncwarp();
     warp_project_store<D, P>(nodal, out, tmp, lane, e, sub, cmin, cmax, Ps);
@@ -397,25 +421,26 @@ __device__ void ghost_extrema(const double* __restrict__ sub, const double* __re
 // leaves alone they are exactly the next step's prev_sub, so the driver
 // skips the separate projection of u^(n+1).
 template <int D, int P>
-__global__ void __launch_bounds__(WarpCfg<D, P>::WPB * 32)
+__global__ void __launch_bounds__(WarpCfg<D, P>::WPBX * 32)
 detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cmin,
               const double* __restrict__ cmax, const double* __restrict__ cand,
               const uint8_t* __restrict__ pred_bad, LimGrid G, int64_t E, double delta0,
               double eps, int force_all, uint8_t* __restrict__ troubled, int32_t* idx,
               int32_t* count, double* __restrict__ sub_out, double* __restrict__ cmin_out,
-              double* __restrict__ cmax_out) {
+              double* __restrict__ cmax_out, double* gscr) {
   using C = LimCfg<D, P>;
   using W = WarpCfg<D, P>;
   constexpr int M = C::M, SD = C::SD, PD = C::PD;
-  extern __shared__ __align__(16) double lsm[];
+  extern __shared__ __align__(16) double lsm_s[];
+  double* lsm = W::GS ? gscr + (size_t)blockIdx.x * W::BLOCK_DBL : lsm_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* Ps = stage_psub<D, P>(lsm + W::WPB * W::PER_WARP);
+  const double* Ps = stage_psub<D, P>(lsm + W::WPBX * W::PER_WARP);
   double* nodal = lsm + warp * W::PER_WARP;
   double* out = nodal + PD * M;
   double* tmp = out + W::OUT;
   double* s_lo = tmp + W::SCR;
   double* s_hi = s_lo + M;
-  for (int64_t e = (int64_t)blockIdx.x * W::WPB + warp; e < E; e += (int64_t)gridDim.x * W::WPB) {
+  for (int64_t e = (int64_t)blockIdx.x * W::WPBX + warp; e < E; e += (int64_t)gridDim.x * W::WPBX) {
     for (int x = lane; x < PD * M; x += 32) nodal[x] = cand[(size_t)e * PD * M + x];
     // DMP bounds: lane v < M owns quantity v; own cell, then the face
     // neighbours in axis order, low then high (min / max are order-free)
@@ -564,12 +589,14 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
               double* __restrict__ u_out, int32_t* failed, const double* __restrict__ windows,
               double* __restrict__ avg_out, uint8_t* __restrict__ fail_each,
               double* __restrict__ sub_next, double* __restrict__ cmin_next,
-              double* __restrict__ cmax_next) {
+              double* __restrict__ cmax_next, double* gscr) {
   using C = LimCfg<D, P>;
   constexpr int M = C::M, S = C::S, SD = C::SD, PD = C::PD, W = C::W, WD = C::WD, R = C::R,
                 RD = C::RD, NT = C::NT;
   const DegreeTables& T = tab<P>();
-  extern __shared__ __align__(16) double lsm[];
+  constexpr bool GS = LimDbl<D, P>::RESCUE > LimDbl<D, P>::LIM;
+  extern __shared__ __align__(16) double lsm_s[];
+  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P>::RESCUE : lsm_s;
   double* win = lsm;                    // [WD][M]
   double* vh = win + WD * M;            // [RD][M]  half-step states
   double* sl = vh + RD * M;             // [RD][D][M] limited slopes
@@ -838,10 +865,13 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
 // nodal [E][P^d][m]
 template <int D, int P>
 __global__ void __launch_bounds__(LimCfg<D, P>::NT)
-recover_kernel(const double* __restrict__ ubar, int64_t E, double* __restrict__ out) {
+recover_kernel(const double* __restrict__ ubar, int64_t E, double* __restrict__ out,
+               double* gscr) {
   using C = LimCfg<D, P>;
   constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
-  extern __shared__ __align__(16) double lsm[];
+  constexpr bool GS = LimDbl<D, P>::RECOVER > LimDbl<D, P>::LIM;
+  extern __shared__ __align__(16) double lsm_s[];
+  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P>::RECOVER : lsm_s;
   double* nw = lsm;
   double* nod = nw + SD * M;
   double* tmp = nod + PD * M;
@@ -862,10 +892,12 @@ recover_kernel(const double* __restrict__ ubar, int64_t E, double* __restrict__ 
 template <int D, int P>
 __global__ void __launch_bounds__(LimCfg<D, P>::NT)
 flatten_cells_kernel(double* __restrict__ nodal, const double* __restrict__ averages, int64_t E,
-                     double gm1, int32_t* nflat) {
+                     double gm1, int32_t* nflat, double* gscr) {
   using C = LimCfg<D, P>;
   constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
-  extern __shared__ __align__(16) double lsm[];
+  constexpr bool GS = LimDbl<D, P>::PROJ > LimDbl<D, P>::LIM;
+  extern __shared__ __align__(16) double lsm_s[];
+  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P>::PROJ : lsm_s;
   double* nod = lsm;
   double* pj = nod + PD * M;
   double* tmp = pj + SD * M;
@@ -901,11 +933,14 @@ flatten_cells_kernel(double* __restrict__ nodal, const double* __restrict__ aver
 // IC flattening (driver.py:137-152): one block per cell
 template <int D, int P>
 __global__ void __launch_bounds__(LimCfg<D, P>::NT)
-flatten_ic_kernel(double* __restrict__ u, int64_t E, double gm1, int32_t* nflat) {
+flatten_ic_kernel(double* __restrict__ u, int64_t E, double gm1, int32_t* nflat,
+                  double* gscr) {
   using C = LimCfg<D, P>;
   constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
   const DegreeTables& T = tab<P>();
-  extern __shared__ __align__(16) double lsm[];
+  constexpr bool GS = LimDbl<D, P>::PROJ > LimDbl<D, P>::LIM;
+  extern __shared__ __align__(16) double lsm_s[];
+  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P>::PROJ : lsm_s;
   double* nodal = lsm;
   double* out = nodal + PD * M;
   double* tmp = out + SD * M;
@@ -943,6 +978,27 @@ flatten_ic_kernel(double* __restrict__ u, int64_t E, double gm1, int32_t* nflat)
     __syncthreads();
   }
 }
+
+// global scratch for the kernels above (one buffer per device, grown on demand)
+static double* lim_scratch(size_t bytes, std::string* err) {
+  static double* ptr[64] = {};
+  static size_t cap[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cap[dev] < bytes) {
+    if (ptr[dev]) cudaFree(ptr[dev]);
+    ptr[dev] = nullptr;
+    cap[dev] = 0;
+    if (cudaMalloc(&ptr[dev], bytes) != cudaSuccess) {
+      *err = "limiter scratch allocation failed";
+      return nullptr;
+    }
+    cap[dev] = bytes;
+  }
+  return ptr[dev];
+}
+constexpr int kScratchBlocks = 148 * 2;   // blocks of the global-scratch kernels
 
 // ------------------------------------------------------------- launchers
 static LimGrid lim_grid(const adg_grid* g, const adg_subcell_ghosts* gh = nullptr) {
@@ -1027,8 +1083,15 @@ static bool lim_supported(const adg_grid* g, const adg_subcell_ghosts* gh, std::
       case 49: rc = FN<3, 1>(__VA_ARGS__); break;                               \
       case 50: rc = FN<3, 2>(__VA_ARGS__); break;                               \
       case 51: rc = FN<3, 3>(__VA_ARGS__); break;                               \
+      case 52: rc = FN<3, 4>(__VA_ARGS__); break;                               \
+      case 53: rc = FN<3, 5>(__VA_ARGS__); break;                               \
+      case 54: rc = FN<3, 6>(__VA_ARGS__); break;                               \
+      case 55: rc = FN<3, 7>(__VA_ARGS__); break;                               \
+      case 56: rc = FN<3, 8>(__VA_ARGS__); break;                               \
+      case 57: rc = FN<3, 9>(__VA_ARGS__); break;                               \
+      case 58: rc = FN<3, 10>(__VA_ARGS__); break;                              \
       default:                                                                  \
-        *err = "subcell limiter on the device: dim 1-2 (any N) or 3 (N <= 2)";  \
+        *err = "subcell limiter on the device: unsupported dim / degree";      \
         return ADG_ERR_UNSUPPORTED;                                             \
     }                                                                           \
   } while (0)
@@ -1046,14 +1109,18 @@ template <int D, int P>
 static int launch_prep(const adg_grid* g, const double* u, double* sub, double* cmin,
                        double* cmax, cudaStream_t st, std::string* err) {
   using W = WarpCfg<D, P>;
-  if (!set_smem(subcell_prep_kernel<D, P>, W::SMEM)) {
+  if (!W::GS && !set_smem(subcell_prep_kernel<D, P>, W::SMEM)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   const int64_t E = n_elements(g);
-  const int64_t nb = (E + W::WPB - 1) / W::WPB;
-  const unsigned grid = (unsigned)(nb < 148 * 64 ? nb : 148 * 64);
-  subcell_prep_kernel<D, P><<<grid, W::WPB * 32, W::SMEM, st>>>(u, E, sub, cmin, cmax);
+  const int64_t nb = (E + W::WPBX - 1) / W::WPBX;
+  const int64_t cap = W::GS ? kScratchBlocks : 148 * 64;
+  const unsigned grid = (unsigned)(nb < cap ? nb : cap);
+  double* gs = nullptr;
+  if (W::GS && !(gs = lim_scratch((size_t)grid * W::BLOCK_DBL * 8, err))) return ADG_ERR_CUDA;
+  subcell_prep_kernel<D, P><<<grid, W::WPBX * 32, W::GS ? 0 : W::SMEM, st>>>(u, E, sub, cmin,
+                                                                           cmax, gs);
   return lerr(err);
 }
 
@@ -1064,17 +1131,20 @@ static int launch_detect(const adg_grid* g, const double* prev_sub, const double
                          uint8_t* troubled, int32_t* idx, int32_t* count, double* sub_out,
                          double* cmin_out, double* cmax_out, cudaStream_t st, std::string* err) {
   using W = WarpCfg<D, P>;
-  if (!set_smem(detect_kernel<D, P>, W::SMEM)) {
+  if (!W::GS && !set_smem(detect_kernel<D, P>, W::SMEM)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   const int64_t E = n_elements(g);
-  const int64_t nb = (E + W::WPB - 1) / W::WPB;
-  const unsigned grid = (unsigned)(nb < 148 * 64 ? nb : 148 * 64);
+  const int64_t nb = (E + W::WPBX - 1) / W::WPBX;
+  const int64_t cap = W::GS ? kScratchBlocks : 148 * 64;
+  const unsigned grid = (unsigned)(nb < cap ? nb : cap);
+  double* gs = nullptr;
+  if (W::GS && !(gs = lim_scratch((size_t)grid * W::BLOCK_DBL * 8, err))) return ADG_ERR_CUDA;
   cudaMemsetAsync(count, 0, sizeof(int32_t), st);
-  detect_kernel<D, P><<<grid, W::WPB * 32, W::SMEM, st>>>(
+  detect_kernel<D, P><<<grid, W::WPBX * 32, W::GS ? 0 : W::SMEM, st>>>(
       prev_sub, cmin, cmax, cand, pred_bad, lim_grid(g, gh), E, d0, eps, force, troubled, idx,
-      count, sub_out, cmin_out, cmax_out);
+      count, sub_out, cmin_out, cmax_out, gs);
   return lerr(err);
 }
 
@@ -1084,15 +1154,19 @@ static int launch_rescue(const adg_grid* g, const double* prev_sub, const int32_
                          const adg_subcell_ghosts* gh, double* u_out, int32_t* failed,
                          double* sub_next, double* cmin_next, double* cmax_next,
                          cudaStream_t st, std::string* err) {
-  const size_t sm = rescue_smem<D, P>();
-  if (!set_smem(rescue_kernel<D, P, 0>, sm)) {
+  constexpr bool GS = LimDbl<D, P>::RESCUE > LimDbl<D, P>::LIM;
+  const size_t sm = GS ? 0 : rescue_smem<D, P>();
+  if (!GS && !set_smem(rescue_kernel<D, P, 0>, sm)) {
     *err = "limiter window exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   if (cmax <= 0) return ADG_OK;
-  rescue_kernel<D, P, 0><<<(unsigned)cmax, LimCfg<D, P>::NT, sm, st>>>(
+  const unsigned grid = (unsigned)(GS && cmax > kScratchBlocks ? kScratchBlocks : cmax);
+  double* gs = nullptr;
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::RESCUE * 8, err))) return ADG_ERR_CUDA;
+  rescue_kernel<D, P, 0><<<grid, LimCfg<D, P>::NT, sm, st>>>(
       prev_sub, idx, count, lim_grid(g, gh), dt, u_out, failed, nullptr, nullptr, nullptr,
-      sub_next, cmin_next, cmax_next);
+      sub_next, cmin_next, cmax_next, gs);
   return lerr(err);
 }
 
@@ -1100,18 +1174,22 @@ template <int D, int P>
 static int launch_muscl_windows(const adg_grid* g, const double* windows, int64_t nwin,
                                 const int32_t* count_dev, const double* dt, double* avg_out,
                                 uint8_t* fail_each, cudaStream_t st, std::string* err) {
-  const size_t sm = rescue_smem<D, P>();
-  if (!set_smem(rescue_kernel<D, P, 1>, sm)) {
+  constexpr bool GS = LimDbl<D, P>::RESCUE > LimDbl<D, P>::LIM;
+  const size_t sm = GS ? 0 : rescue_smem<D, P>();
+  if (!GS && !set_smem(rescue_kernel<D, P, 1>, sm)) {
     *err = "limiter window exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   if (nwin <= 0) return ADG_OK;
-  const unsigned grid = (unsigned)(nwin < 65535 * 8 ? nwin : 65535 * 8);
+  const int64_t cap = GS ? kScratchBlocks : 65535 * 8;
+  const unsigned grid = (unsigned)(nwin < cap ? nwin : cap);
+  double* gs = nullptr;
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::RESCUE * 8, err))) return ADG_ERR_CUDA;
   LimGrid G = lim_grid(g);
   for (int j = 0; j < 3; ++j) G.h[j] = j < g->dim ? g->dx[j] : 1.0;   // dx = subcell widths here
   rescue_kernel<D, P, 1><<<grid, LimCfg<D, P>::NT, sm, st>>>(
       nullptr, nullptr, count_dev, G, dt, nullptr, nullptr, windows, avg_out, fail_each, nullptr,
-      nullptr, nullptr);
+      nullptr, nullptr, gs);
   return lerr(err);
 }
 
@@ -1119,47 +1197,57 @@ template <int D, int P>
 static int launch_recover(const adg_grid* g, const double* ubar, double* out, cudaStream_t st,
                           std::string* err) {
   using C = LimCfg<D, P>;
-  const size_t tmp = D == 3 ? (size_t)P * C::S * C::S * C::M + (size_t)P * P * C::S * C::M
-                            : (size_t)P * C::S * C::M;
-  const size_t sm = ((size_t)C::SD * C::M + (size_t)C::PD * C::M + tmp) * 8;
-  if (!set_smem(recover_kernel<D, P>, sm)) {
+  constexpr bool GS = LimDbl<D, P>::RECOVER > LimDbl<D, P>::LIM;
+  const size_t sm = GS ? 0 : LimDbl<D, P>::RECOVER * 8;
+  if (!GS && !set_smem(recover_kernel<D, P>, sm)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   const int64_t E = n_elements(g);
-  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
-  recover_kernel<D, P><<<grid, C::NT, sm, st>>>(ubar, E, out);
+  const int64_t cap = GS ? kScratchBlocks : 65535 * 8;
+  const unsigned grid = (unsigned)(E < cap ? E : cap);
+  double* gs = nullptr;
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::RECOVER * 8, err))) return ADG_ERR_CUDA;
+  recover_kernel<D, P><<<grid, C::NT, sm, st>>>(ubar, E, out, gs);
   return lerr(err);
 }
 
 template <int D, int P>
 static int launch_flatten_cells(const adg_grid* g, double* nodal, const double* averages,
                                 int32_t* nflat, cudaStream_t st, std::string* err) {
-  const size_t sm = proj_smem<D, P>();
-  if (!set_smem(flatten_cells_kernel<D, P>, sm)) {
+  constexpr bool GS = LimDbl<D, P>::PROJ > LimDbl<D, P>::LIM;
+  const size_t sm = GS ? 0 : proj_smem<D, P>();
+  if (!GS && !set_smem(flatten_cells_kernel<D, P>, sm)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   const int64_t E = n_elements(g);
-  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
+  const int64_t cap = GS ? kScratchBlocks : 65535 * 8;
+  const unsigned grid = (unsigned)(E < cap ? E : cap);
+  double* gs = nullptr;
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::PROJ * 8, err))) return ADG_ERR_CUDA;
   cudaMemsetAsync(nflat, 0, sizeof(int32_t), st);
   flatten_cells_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(nodal, averages, E,
-                                                                 g->gamma - 1.0, nflat);
+                                                                 g->gamma - 1.0, nflat, gs);
   return lerr(err);
 }
 
 template <int D, int P>
 static int launch_flatten(const adg_grid* g, double* u, int32_t* nflat, cudaStream_t st,
                           std::string* err) {
-  const size_t sm = proj_smem<D, P>();
-  if (!set_smem(flatten_ic_kernel<D, P>, sm)) {
+  constexpr bool GS = LimDbl<D, P>::PROJ > LimDbl<D, P>::LIM;
+  const size_t sm = GS ? 0 : proj_smem<D, P>();
+  if (!GS && !set_smem(flatten_ic_kernel<D, P>, sm)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   const int64_t E = n_elements(g);
-  const unsigned grid = (unsigned)(E < 65535 * 8 ? E : 65535 * 8);
+  const int64_t cap = GS ? kScratchBlocks : 65535 * 8;
+  const unsigned grid = (unsigned)(E < cap ? E : cap);
+  double* gs = nullptr;
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::PROJ * 8, err))) return ADG_ERR_CUDA;
   cudaMemsetAsync(nflat, 0, sizeof(int32_t), st);
-  flatten_ic_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(u, E, g->gamma - 1.0, nflat);
+  flatten_ic_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(u, E, g->gamma - 1.0, nflat, gs);
   return lerr(err);
 }
 
