@@ -48,12 +48,12 @@ struct PredCfg {
   static constexpr int TILE = PT * M;        // doubles in one space-time tile
   // space-time tile and x-line-major partial rows share padded strides: a
   // node's (or a row's) P x m block is contiguous (LS doubles); 3-D P = 4
-  // pads the middle axis by one double (power-of-two strides would put
+  // and P = 6 pad the middle axis by one double (even strides would put
   // every owner role's lanes on a few banks; tools/bankcheck.py)
   static constexpr int LS = P * M;
   // 2-D: node stride LS + 1 and an element stride chosen mod 16 doubles
   // (element tiles of a CTA would otherwise start on the same bank)
-  static constexpr int QPAD = (D == 3 && P == 4) ? 1 : 0;
+  static constexpr int QPAD = (D == 3 && (P == 4 || P == 6)) ? 1 : 0;
   static constexpr int QK = LS + ((D == 2 && P >= 3) ? 1 : 0);
   static constexpr int QJ = P * QK + QPAD;
   static constexpr int QI = P * QJ;
