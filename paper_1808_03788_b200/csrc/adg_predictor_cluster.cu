@@ -130,6 +130,8 @@ predict_cluster_kernel(const __grid_constant__ ClArgs a) {
   // x-owner row: x-line (j, k) = (a0, b0); node role: node (c, a0, b0)
   const int xrow = a0 * TJ + b0 * TK;
   const bool node_role = tid < PP;
+  constexpr int TPR = (P + 2) / 3;                // times per owner in the time operator
+  const int tlo = role * TPR, thi = tlo + TPR < P ? tlo + TPR : P;
   const int nnode = c * PP + rr;                 // valid when node_role (unpadded index)
   const int qnode = c * SI + a0 * SJ + b0 * M;   // its padded offset in Q
 
@@ -219,8 +221,8 @@ predict_cluster_kernel(const __grid_constant__ ClArgs a) {
     cluster_barrier();   // every CTA of the cluster is done with the previous element
     // ---------------- startup guess (each CTA for its own slice) ----------
     const double* ue = a.u + (size_t)e * PD * M;
-    double uu[M];     // node role: u^n at its node
-    if (node_role) {
+    double uu[M];     // u^n at node (c, a0, b0) (every owner shares the time operator)
+    if (owner) {
 #pragma unroll
       for (int v = 0; v < M; ++v) uu[v] = ue[nnode * M + v];
     }
@@ -301,8 +303,9 @@ predict_cluster_kernel(const __grid_constant__ ClArgs a) {
           }
       }
       // time operator for the nodes of x-plane c at every time
+      // node (c, a0, b0): the three owners of (a0, b0) split its P times
       double sd = 0.0, sq = 0.0;
-      if (node_role) {
+      if (owner) {
         wait(barG, phG);
         double r[P][M];
 #pragma unroll
@@ -311,6 +314,7 @@ predict_cluster_kernel(const __grid_constant__ ClArgs a) {
           for (int v = 0; v < M; ++v) r[s][v] = G[xrow + s * M + v];
 #pragma unroll
         for (int t = 0; t < P; ++t) {
+          if (t < tlo || t >= thi) continue;
           double* qo = B3 + xrow + t * M;   // previous iterate of (node, t), local
           const double g0 = T.g0[t];
 #pragma unroll
