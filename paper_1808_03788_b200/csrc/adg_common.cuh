@@ -211,6 +211,25 @@ __device__ __forceinline__ bool admissible(const double* q, double gm1) {
   return fin && (q[0] > 0.0) && (p > 0.0);
 }
 
+// systems.py:225-229 with the sign of p read from a Newton-refined
+// reciprocal of rho: within 1e-12 of cancellation the reference's IEEE
+// division decides, so the verdict equals admissible<D>'s exactly
+template <int D>
+__device__ __forceinline__ bool admissible_fast(const double* q, double gm1) {
+  bool fin = true;
+#pragma unroll
+  for (int v = 0; v < D + 2; ++v) fin = fin && isfinite(q[v]);
+  if (!fin || !(q[0] > 0.0)) return false;
+  const double r = rcp_nr(q[0]);
+  double kin = q[1] * q[1];
+#pragma unroll
+  for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
+  const double x = 0.5 * kin * r;
+  const double dd = q[D + 1] - x;
+  if (fabs(dd) > 1e-12 * (fabs(q[D + 1]) + fabs(x))) return dd > 0.0;
+  return pressure<D>(q, gm1) > 0.0;
+}
+
 // flux_all and admissible of one state sharing the reciprocal of rho: the
 // sign of p = gm1 (E - 0.5 kin / rho) is read from the reciprocal-based
 // E - 0.5 kin r, which is within a few ulp of the reference's quotient; only

@@ -172,6 +172,39 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
     }
     return;
   }
+  if (D == 2 && WARP) {
+    // one warp per cell: lanes own (i1, v) columns, then (s0, v) rows, and
+    // every P_sub coefficient is a compile-time constant-bank operand (same
+    // fma order per output as the generic passes below)
+    for (int x = tid; x < P * M; x += 32) {
+      const int i1 = x / M, v = x - (x / M) * M;
+      double col[P];
+#pragma unroll
+      for (int i0 = 0; i0 < P; ++i0) col[i0] = nodal[(i0 * P + i1) * M + v];
+#pragma unroll
+      for (int s0 = 0; s0 < S; ++s0) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i0 = 0; i0 < P; ++i0) acc = fma(T.sub_project[s0 * P + i0], col[i0], acc);
+        tmp[(s0 * P + i1) * M + v] = acc;
+      }
+    }
+    __syncwarp();
+    for (int x = tid; x < S * M; x += 32) {
+      const int s0 = x / M, v = x - (x / M) * M;
+      double row[P];
+#pragma unroll
+      for (int i1 = 0; i1 < P; ++i1) row[i1] = tmp[(s0 * P + i1) * M + v];
+#pragma unroll
+      for (int s1 = 0; s1 < S; ++s1) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i1 = 0; i1 < P; ++i1) acc = fma(T.sub_project[s1 * P + i1], row[i1], acc);
+        out[(s0 * S + s1) * M + v] = acc;
+      }
+    }
+    return;
+  }
   if (D == 2) {
     // axis 0: tmp[s0][i1][v]
     for (int x = tid; x < S * P * M; x += nt) {
@@ -455,17 +488,31 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
     }
     const int vq = lane < M ? lane : 0;
     double lo = cmin[e * M + vq], hi = cmax[e * M + vq];
+    // interior face neighbours: every load issued before any is folded
+    double nlo[2 * D], nhi[2 * D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const bool inside = side ? (c[j] + 1 < G.n[j]) : (c[j] > 0);
+        int64_t en = e;
+        if (inside) {
+          en = 0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) en = en * G.n[a] + c[a] + (a == j ? (side ? 1 : -1) : 0);
+        }
+        nlo[2 * j + side] = cmin[en * M + vq];
+        nhi[2 * j + side] = cmax[en * M + vq];
+      }
+    }
 #pragma unroll
     for (int j = 0; j < D; ++j) {
 #pragma unroll
       for (int side = 0; side < 2; ++side) {
         const bool inside = side ? (c[j] + 1 < G.n[j]) : (c[j] > 0);
         if (inside) {
-          int64_t en = 0;
-#pragma unroll
-          for (int a = 0; a < D; ++a) en = en * G.n[a] + c[a] + (a == j ? (side ? 1 : -1) : 0);
-          lo = fmin(lo, cmin[en * M + vq]);
-          hi = fmax(hi, cmax[en * M + vq]);
+          lo = fmin(lo, nlo[2 * j + side]);
+          hi = fmax(hi, nhi[2 * j + side]);
         } else {   // warp-uniform: a boundary face of this cell
           if (lane == 0) ghost_extrema<D, P>(prev_sub, cmin, cmax, G, c, j, side, s_lo, s_hi);
           __syncwarp();
@@ -489,9 +536,9 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
       const double* q = out + x * M;
 #pragma unroll
       for (int v = 0; v < M; ++v) bad |= (q[v] < s_lo[v]) | (q[v] > s_hi[v]);
-      bad |= !admissible<D>(q, G.gm1);
+      bad |= !admissible_fast<D>(q, G.gm1);
     }
-    for (int nd = lane; nd < PD; nd += 32) bad |= !admissible<D>(nodal + nd * M, G.gm1);
+    for (int nd = lane; nd < PD; nd += 32) bad |= !admissible_fast<D>(nodal + nd * M, G.gm1);
     bad = __any_sync(0xffffffffu, bad);
     if (lane == 0) {
       troubled[e] = (uint8_t)bad;
