@@ -122,8 +122,17 @@ struct PredCfg {
   static constexpr int FLAGS = 5 * EPB + 1;
   static constexpr size_t SMALL_BYTES = SMALL_DBL * 8 + ((FLAGS * 4 + 15) / 16) * 16;
   static constexpr size_t TILE_BYTES = (size_t)EPB * ELEM * 8;
-  static constexpr bool SMEM_TILES = (SMALL_BYTES + TILE_BYTES) <= 220 * 1024;
-  static constexpr size_t SMEM_BYTES = SMALL_BYTES + (SMEM_TILES ? TILE_BYTES : 0);
+  // 1-D / 2-D groups prefetch the next group's u^n into a dedicated buffer
+  // behind the tiles (when it still fits the CTAs per SM the tiles allow)
+  static constexpr size_t PFB_BYTES = (size_t)EPB * PD * M * 8;
+  static constexpr bool SMEM_TILES0 = (SMALL_BYTES + TILE_BYTES) <= 220 * 1024;
+  static constexpr int CTAS0 = (int)((228 * 1024) / (SMALL_BYTES + TILE_BYTES + 1024));
+  static constexpr bool PF_DED = ADG_PREFETCH_U && D <= 2 && SMEM_TILES0 &&
+      (SMALL_BYTES + TILE_BYTES + PFB_BYTES) <= 220 * 1024 &&
+      (int)((228 * 1024) / (SMALL_BYTES + TILE_BYTES + PFB_BYTES + 1024)) >= CTAS0;
+  static constexpr bool SMEM_TILES = SMEM_TILES0;
+  static constexpr size_t SMEM_BYTES =
+      SMALL_BYTES + (SMEM_TILES ? TILE_BYTES : 0) + (PF_DED ? PFB_BYTES : 0);
   // resident CTAs per SM the shared footprint allows (228 KB, 1 KB reserved
   // per CTA); passed to __launch_bounds__ so registers do not become the limit
   static constexpr int MINB0 = (int)((228 * 1024) / (SMEM_BYTES + 1024));
@@ -390,8 +399,18 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     for (int x = tid; x < PD * M; x += NT) cp_async8(dst + x, src + x);
     cp_async_commit();
   };
+  // PF_DED: the whole next group (contiguous elements) into pfb
+  double* pfb = C::PF_DED ? tiles + (size_t)EPB * C::ELEM : nullptr;
+  auto prefetch_group = [&](int64_t gg) {
+    const int64_t e0 = gg * EPB;
+    const int64_t ne = (a.n_elem - e0) < EPB ? (a.n_elem - e0) : EPB;
+    const double* src = a.u + (size_t)e0 * PD * M;
+    for (int x = tid; x < ne * PD * M; x += NT) cp_async8(pfb + x, src + x);
+    cp_async_commit();
+  };
   if (C::PREFETCH && (int64_t)blockIdx.x < ngroups)
     prefetch_u(blockIdx.x, tiles + 2 * C::RSZ + C::PF_OFF);
+  if (C::PF_DED && (int64_t)blockIdx.x < ngroups) prefetch_group(blockIdx.x);
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     const int64_t e = g * EPB + el;
     const bool valid = e < a.n_elem;
@@ -412,7 +431,8 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     // ---------------- startup guess --------------------------------------
     // k = L(w) = ((-D_x F_x) - D_y F_y) - D_z F_z at the spatial nodes,
     // w = u (k1) then u + dt k1 (k2); states staged node-major in Q[:PD*M]
-    double* W0 = C::PREFETCH ? B2 + C::PF_OFF : Q;   // staged states [node][v]
+    double* W0 = C::PREFETCH ? B2 + C::PF_OFF
+                             : (C::PF_DED ? pfb + el * PD * M : Q);   // staged states [node][v]
     double* PA = B1;                // per-direction pieces [dir][node][v]
     double uu[M];   // u^n (conservative), or its primitive state (PRIM)
     double k1[M];
@@ -420,7 +440,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     // u^n of the group's elements: coalesced cooperative copy into each
     // element's W0 (consecutive threads, consecutive doubles), then every
     // node thread takes its own state from shared memory
-    if constexpr (C::PREFETCH) {
+    if constexpr (C::PREFETCH || C::PF_DED) {
       cp_async_wait_all();   // this thread's part of u^n has landed in W0
     } else {
       for (int x = tid; x < EPB * PD * M; x += NT) {
@@ -481,7 +501,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         }
       }
     }
-    if (!C::PREFETCH) __syncthreads();   // W0 (inside Q) is about to be overwritten
+    if (!C::PREFETCH && !C::PF_DED) __syncthreads();   // W0 (inside Q) is about to be overwritten
     if (valid) {
 #pragma unroll
       for (int t = 0; t < P; ++t) {
@@ -836,6 +856,9 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 
     // B2 is dead until the next element's sweeps: start fetching its u^n
     if (C::PREFETCH && g + gridDim.x < ngroups) prefetch_u(g + gridDim.x, B2 + C::PF_OFF);
+    // every lane of the group has passed its startup (pfb is dead) since the
+    // sweep loop's barriers
+    if (C::PF_DED && g + gridDim.x < ngroups) prefetch_group(g + gridDim.x);
     if (PRIM) {
       // q_cons = prim_to_cons(q) (predictor.py:188), each node thread its own
       if (valid) {

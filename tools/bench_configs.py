@@ -72,6 +72,7 @@ def main():
     ap.add_argument("--only", default="C1,C2,C3,C4")
     ap.add_argument("--c4-steps", type=int, default=100)
     ap.add_argument("--c3-cells", type=int, default=32)
+    ap.add_argument("--c4-cells", type=int, default=512)
     args = ap.parse_args()
     which = set(args.only.split(","))
     if "C1" in which:
@@ -84,7 +85,8 @@ def main():
             run_case(f"C3_N{n}", [(0.0, 1.0)] * 3, (n3,) * 3, n, 0.9 / (3 * (2 * n + 1)),
                      "density_wave", 10)
     if "C4" in which:
-        run_case("C4", [(-1.0, 1.0), (-1.0, 1.0)], (512, 512), 5, 0.9 / 22.0, "explosion",
+        n4 = args.c4_cells
+        run_case("C4", [(-1.0, 1.0), (-1.0, 1.0)], (n4, n4), 5, 0.9 / 22.0, "explosion",
                  args.c4_steps, boundary="outflow", limiter=True, t_end=0.25)
 
 
