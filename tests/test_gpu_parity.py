@@ -287,3 +287,42 @@ def test_large_tile_predictor_matches_oracle(pkg, n):
             assert rel_linf(res.traces[(j, s)], tr[(j, s)]) <= 1e-12
     vol = dg.volume_integral(ref.q, EulerOracle(3), sp, dt, tabs)
     assert rel_linf(res.volume, vol) <= 1e-11
+
+
+@pytest.mark.parametrize("n", list(range(2, 10)))
+def test_c3_full_size_conservation_and_determinism(pkg, n):
+    """C3 at its full 32^3 size for every degree (the single-CTA, lone-element
+    and cluster predictors): periodic totals conserved to 1e-11 relative and
+    two runs bitwise identical (fixed-order reductions everywhere)."""
+    mesh = pkg.CartesianMesh([(0, 1)] * 3, (32, 32, 32))
+    system = pkg.make_system("euler", 3)
+    outs = []
+    for _ in range(2):
+        sim = pkg.Simulation(mesh, system, n, 0.9 / (3 * (2 * n + 1)))
+        sim.project_initial_condition(pkg.build_problem("density_wave", system)[0])
+        t0 = sim.conserved_totals()
+        sim.run(np.inf, max_steps=2)
+        t1 = sim.history[-1]["totals"]
+        assert np.max(np.abs(t1 - t0) / np.maximum(np.abs(t0), 1e-300)) <= 1e-11
+        outs.append(sim.u.clone())
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_c4_full_size_determinism(pkg):
+    """C4 at its full 512^2 size, 3 limited steps run twice: identical
+    troubled flags and bitwise identical states."""
+    res = []
+    for _ in range(2):
+        mesh = pkg.CartesianMesh([(-1.0, 1.0), (-1.0, 1.0)], (512, 512))
+        system = pkg.make_system("euler", 2)
+        sim = pkg.Simulation(mesh, system, 5, 0.9 / 22.0, boundary="outflow", use_limiter=True)
+        sim.project_initial_condition(pkg.build_problem("explosion", system)[0])
+        flags = []
+        for s in range(3):
+            sim.run(np.inf, max_steps=s + 1)
+            flags.append(sim.last_troubled.clone())
+        assert 0.0 < sim.last_limited_fraction < 0.05
+        res.append((sim.u.clone(), flags))
+    assert torch.equal(res[0][0], res[1][0])
+    for a, b in zip(res[0][1], res[1][1]):
+        assert torch.equal(a, b)
