@@ -51,12 +51,18 @@ typedef struct adg_handle adg_handle;
 
 /* Grid descriptor (POD).  cells are the LOCAL element counts of this rank;
  * dx are the element widths (mesh.py:32).  dim in 1..3, degree in 0..9,
- * nvars = dim + 2 (Euler).  mode = predictor_mode (driver.py:45-48):
+ * nvars = dim + 2 (Euler) or 1 (advection).  mode = predictor_mode (driver.py:45-48):
  * ADG_MODE_CONSERVATIVE evolves the predictor and the MUSCL-Hancock half
  * step in conservative variables, ADG_MODE_PRIMITIVE in primitive ones
  * (predictor.py:94-96, :165-189; limiter.py:127-177). */
 #define ADG_MODE_CONSERVATIVE 0
 #define ADG_MODE_PRIMITIVE 1
+
+/* PDE plugin (reference systems.py:355-361 make_system): ADG_SYS_EULER
+ * (CompressibleEuler, nvars = dim + 2, gamma) or ADG_SYS_ADVECTION
+ * (LinearAdvection, systems.py:77-109: nvars = 1, constant velocity) */
+#define ADG_SYS_EULER 0
+#define ADG_SYS_ADVECTION 1
 
 typedef struct adg_grid {
   int32_t dim;
@@ -67,6 +73,9 @@ typedef struct adg_grid {
   double dx[3];
   double gamma;
   int32_t bc[3][2];
+  int32_t system;       /* ADG_SYS_* */
+  int32_t reserved0;
+  double velocity[3];   /* ADG_SYS_ADVECTION: a_j (unused entries 0) */
 } adg_grid;
 
 /* Reduction record filled on device by adg_wavespeed / adg_update and read

@@ -20,6 +20,16 @@ ADG_ERR_UNSUPPORTED = 4
 
 BC_CODES = {"periodic": 0, "outflow": 1, "wall": 2, "exact": 3, "ghost": 3}
 MODE_CODES = {"conservative": 0, "primitive": 1}   # adg_grid.mode (ADG_MODE_*)
+SYSTEM_CODES = {"euler": 0, "advection": 1}        # adg_grid.system (ADG_SYS_*)
+
+
+def fill_system(g, system):
+    """adg_grid plugin fields from a systems.* descriptor."""
+    g.system = SYSTEM_CODES[system.name]
+    g.gamma = float(getattr(system, "gamma", 1.4))
+    vel = getattr(system, "velocity", None)
+    for j in range(3):
+        g.velocity[j] = float(vel[j]) if vel is not None and j < len(vel) else 0.0
 
 STATUS_NO_ADMISSIBLE = 1
 STATUS_NONFINITE = 2
@@ -39,7 +49,9 @@ class Grid(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int32), ("degree", ctypes.c_int32),
                 ("nvars", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("cells", ctypes.c_int64 * 3), ("dx", ctypes.c_double * 3),
-                ("gamma", ctypes.c_double), ("bc", (ctypes.c_int32 * 2) * 3)]
+                ("gamma", ctypes.c_double), ("bc", (ctypes.c_int32 * 2) * 3),
+                ("system", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("velocity", ctypes.c_double * 3)]
 
 
 class Reduce(ctypes.Structure):

@@ -66,7 +66,15 @@ static int check_grid(adg_handle* h, const adg_grid* g) {
   if (!g) return fail(h, ADG_ERR_INVALID, "null grid");
   if (g->dim < 1 || g->dim > 3) return fail(h, ADG_ERR_INVALID, "dim must be 1..3");
   if (g->degree < 0 || g->degree > 9) return fail(h, ADG_ERR_INVALID, "degree must be 0..9");
-  if (g->nvars != g->dim + 2) return fail(h, ADG_ERR_UNSUPPORTED, "only Euler (m = d+2)");
+  if (g->system == ADG_SYS_ADVECTION) {
+    if (g->nvars != 1) return fail(h, ADG_ERR_INVALID, "advection has m = 1");
+    if (g->mode != ADG_MODE_CONSERVATIVE)
+      return fail(h, ADG_ERR_UNSUPPORTED, "advection on the device: conservative predictor only");
+  } else if (g->system != ADG_SYS_EULER) {
+    return fail(h, ADG_ERR_UNSUPPORTED, "unknown system");
+  } else if (g->nvars != g->dim + 2) {
+    return fail(h, ADG_ERR_INVALID, "Euler has m = d + 2");
+  }
   for (int j = 0; j < g->dim; ++j) {
     if (g->cells[j] < 1) return fail(h, ADG_ERR_INVALID, "cell counts must be positive");
     if (!(g->dx[j] > 0.0)) return fail(h, ADG_ERR_INVALID, "spacings must be positive");
@@ -75,6 +83,18 @@ static int check_grid(adg_handle* h, const adg_grid* g) {
   }
   if (!h->tables_loaded[g->degree])
     return fail(h, ADG_ERR_INVALID, "tables for this degree not uploaded (adg_set_tables)");
+  return ADG_OK;
+}
+
+static bool is_adv(const adg_grid* g) { return g && g->system == ADG_SYS_ADVECTION; }
+
+// entry points with Euler kernels only (limiter, module-level pieces)
+static int check_euler(adg_handle* h, const adg_grid* g) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (is_adv(g))
+    return fail(h, ADG_ERR_UNSUPPORTED,
+                "advection on the device: the limiter and the module-level pieces are Euler only");
   return ADG_OK;
 }
 
@@ -122,6 +142,8 @@ int adg_wavespeed(adg_handle* h, const adg_grid* g, const double* u, adg_reduce*
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
+  if (is_adv(g))
+    return wrap(h, adg::adv_state_reduce(g, u, red, nullptr, (cudaStream_t)stream, &e), e);
   return wrap(h, adg::state_reduce(g, u, red, nullptr, (cudaStream_t)stream, &e), e);
 }
 
@@ -159,6 +181,10 @@ int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double*
     h->ws_bytes = need;
   }
   std::string e;
+  if (is_adv(g))
+    return wrap(h, adg::adv_predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out,
+                                    traces, pred_bad, sweeps, (cudaStream_t)stream,
+                                    h->num_sms, &e), e);
   return wrap(h, adg::predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out, traces,
                               pred_bad, sweeps, (cudaStream_t)stream, h->num_sms, h->ws,
                               h->ws_bytes, &e), e);
@@ -170,6 +196,9 @@ int adg_face_flux(adg_handle* h, const adg_grid* g, int axis, const double* trac
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
+  if (is_adv(g))
+    return wrap(h, adg::adv_face_flux(g, axis, traces, ghost_lo, ghost_hi, dbar_out,
+                                      (cudaStream_t)stream, &e), e);
   return wrap(h, adg::face_flux(g, axis, traces, ghost_lo, ghost_hi, dbar_out,
                                 (cudaStream_t)stream, &e), e);
 }
@@ -179,7 +208,7 @@ int64_t adg_update_blocks(const adg_grid* g) { return adg::update_blocks(g); }
 int64_t adg_trace_block(const adg_grid* g) {
   int64_t pd = 1;
   for (int j = 0; j < g->dim; ++j) pd *= g->degree + 1;
-  const int64_t b = pd * (g->dim + 2);
+  const int64_t b = pd * (g->system == ADG_SYS_ADVECTION ? 1 : g->dim + 2);
   return b + (b & 1);
 }
 
@@ -189,6 +218,9 @@ int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* 
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
+  if (is_adv(g))
+    return wrap(h, adg::adv_update(g, u, vol, fd, dt_dev, u_out, red_next, totals_partial,
+                                   (cudaStream_t)stream, &e), e);
   return wrap(h, adg::update(g, u, vol, fd, dt_dev, u_out, red_next, totals_partial,
                              (cudaStream_t)stream, &e), e);
 }
@@ -207,7 +239,8 @@ int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partia
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
-  rc = adg::state_reduce(g, u, nullptr, partial, (cudaStream_t)stream, &e);
+  rc = is_adv(g) ? adg::adv_state_reduce(g, u, nullptr, partial, (cudaStream_t)stream, &e)
+                 : adg::state_reduce(g, u, nullptr, partial, (cudaStream_t)stream, &e);
   if (rc) return wrap(h, rc, e);
   return wrap(h, adg::totals_finalize(g, partial, adg::reduce_blocks(g), totals_out,
                                       (cudaStream_t)stream, &e), e);
@@ -215,7 +248,7 @@ int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partia
 
 int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, double* sub_out,
                          double* cmin_out, double* cmax_out, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::project_subcells(g, u, sub_out, cmin_out, cmax_out, (cudaStream_t)stream,
@@ -227,7 +260,7 @@ int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub, const d
                double eps, int force_all, const adg_subcell_ghosts* ghosts, uint8_t* troubled,
                int32_t* idx, int32_t* count, double* cand_sub_out, double* cand_cmin_out,
                double* cand_cmax_out, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::detect(g, prev_sub, cmin, cmax, cand, pred_bad, delta0, eps, force_all,
@@ -239,7 +272,7 @@ int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const i
                const int32_t* count_dev, int32_t count_host_max, const double* dt_dev,
                const adg_subcell_ghosts* ghosts, double* u_out, int32_t* failed_dev,
                double* sub_next, double* cmin_next, double* cmax_next, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::rescue(g, prev_sub, idx, count_dev, count_host_max, dt_dev, ghosts, u_out,
@@ -249,7 +282,7 @@ int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const i
 
 int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const double* q_minus,
                     const double* q_plus, double* d_low, double* d_high, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   if (axis < 0 || axis >= g->dim) return fail(h, ADG_ERR_INVALID, "axis out of range");
   std::string e;
@@ -259,7 +292,7 @@ int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const
 
 int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const double* dt_dev,
                         double* vol_out, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::volume_integral(g, q, dt_dev, vol_out, (cudaStream_t)stream, &e), e);
@@ -267,7 +300,7 @@ int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const
 
 int adg_face_integral(adg_handle* h, const adg_grid* g, int axis, int side,
                       const double* d_values, const double* dt_dev, double* out, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   if (axis < 0 || axis >= g->dim || side < 0 || side > 1)
     return fail(h, ADG_ERR_INVALID, "axis / side out of range");
@@ -278,7 +311,7 @@ int adg_face_integral(adg_handle* h, const adg_grid* g, int axis, int side,
 
 int adg_element_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
                        const double* const* accs, int n_acc, double* u_out, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   if (n_acc < 0 || n_acc > 6 || (n_acc > 0 && !accs))
     return fail(h, ADG_ERR_INVALID, "0..6 face accumulators");
@@ -289,7 +322,7 @@ int adg_element_update(adg_handle* h, const adg_grid* g, const double* u, const 
 int adg_muscl_windows(adg_handle* h, const adg_grid* g, const double* windows, int64_t n_windows,
                       const int32_t* count_dev, const double* dt_dev, double* avg_out,
                       uint8_t* failed, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::muscl_windows(g, windows, n_windows, count_dev, dt_dev, avg_out, failed,
@@ -298,7 +331,7 @@ int adg_muscl_windows(adg_handle* h, const adg_grid* g, const double* windows, i
 
 int adg_recover_subcells(adg_handle* h, const adg_grid* g, const double* ubar, double* u_out,
                          void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::recover_subcells(g, ubar, u_out, (cudaStream_t)stream, &e), e);
@@ -306,14 +339,14 @@ int adg_recover_subcells(adg_handle* h, const adg_grid* g, const double* ubar, d
 
 int adg_flatten_cells(adg_handle* h, const adg_grid* g, double* nodal, const double* averages,
                       int32_t* nflat, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::flatten_cells(g, nodal, averages, nflat, (cudaStream_t)stream, &e), e);
 }
 
 int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat, void* stream) {
-  int rc = check_grid(h, g);
+  int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::flatten_ic(g, u, nflat, (cudaStream_t)stream, &e), e);

@@ -724,6 +724,10 @@ int totals_finalize(const adg_grid* g, const double* partial, int64_t nb, double
                     cudaStream_t st, std::string* err) {
   double cv = 1.0;
   for (int j = 0; j < g->dim; ++j) cv *= g->dx[j];
+  if (g->nvars == 1) {
+    totals_finalize_kernel<1><<<1, 1024, 0, st>>>(partial, nb, cv, out);
+    return check_launch(err);
+  }
   switch (g->dim) {
     case 1: totals_finalize_kernel<3><<<1, 1024, 0, st>>>(partial, nb, cv, out); break;
     case 2: totals_finalize_kernel<4><<<1, 1024, 0, st>>>(partial, nb, cv, out); break;

@@ -120,11 +120,23 @@ class Simulation:
             raise ValueError(
                 f"cfl must lie in (0, {max_cfl_number(degree)}) "
                 f"for degree {degree}, got {cfl}")
-        if getattr(system, "name", None) != "euler":
+        name = getattr(system, "name", None)
+        if name not in ("euler", "advection"):
             raise NotImplementedError(
-                f"system '{getattr(system, 'name', system)}' has no B200 kernels (Euler only)")
+                f"system '{getattr(system, 'name', system)}' has no B200 kernels "
+                "(euler, advection)")
         if predictor_mode not in ("conservative", "primitive"):
             raise ValueError(f"unknown predictor mode {predictor_mode!r}")
+        if name == "advection":
+            # the advection kernels cover the unlimited conservative step with
+            # periodic / outflow / wall faces
+            if use_limiter:
+                raise NotImplementedError("advection on the device: no subcell limiter")
+            if predictor_mode != "conservative":
+                raise NotImplementedError("advection on the device: conservative predictor")
+            kinds = normalize_boundary(boundary, mesh.dim).values()
+            if "exact" in kinds:
+                raise NotImplementedError("advection on the device: no exact faces")
         self.mesh = mesh
         self.system = system
         self.tables = basis_tables(degree)
@@ -186,7 +198,7 @@ class Simulation:
         for j in range(3):
             g.cells[j] = int(cells[j]) if j < d else 1
             g.dx[j] = float(spacings[j]) if j < d else 1.0
-        g.gamma = float(self.system.gamma)
+        _lib.fill_system(g, self.system)
         for j in range(d):
             for s in (0, 1):
                 kind = self.boundary[(j, s)]

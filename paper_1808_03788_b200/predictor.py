@@ -32,7 +32,7 @@ def _grid(system, cells, spacings, degree, boundary_codes=None, mode="conservati
     for j in range(3):
         g.cells[j] = int(cells[j]) if j < d else 1
         g.dx[j] = float(spacings[j]) if j < d else 1.0
-    g.gamma = float(system.gamma)
+    _lib.fill_system(g, system)
     for j in range(d):
         for s in (0, 1):
             g.bc[j][s] = 0 if boundary_codes is None else boundary_codes[j][s]

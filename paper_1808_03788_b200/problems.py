@@ -112,9 +112,53 @@ def blast_2d(system, r0=0.1, e0=1.0, p_ambient=1e-14):
     return ic, None
 
 
+def advected_sine(system):
+    """problems.py:54-66: sin(2 pi sum_j x_j) carried by the advection velocity."""
+    if system.name != "advection":
+        raise ValueError("the sine case needs the advection system")
+    vel = system.velocity
+
+    def exact(points, t):
+        phase = np.zeros(points.shape[:-1])
+        for j in range(system.dim):
+            phase += points[..., j] - vel[j] * t
+        return np.sin(2.0 * np.pi * phase)[..., None]
+
+    return (lambda points: exact(points, 0.0)), exact
+
+
+def gaussian_pulse(system, center=0.25, width=0.08, amplitude=1.0):
+    """problems.py:69-82: a Gaussian translated by the advection velocity."""
+    if system.name != "advection":
+        raise ValueError("the pulse case needs the advection system")
+    vel = system.velocity
+
+    def exact(points, t):
+        r2 = np.zeros(points.shape[:-1])
+        for j in range(system.dim):
+            d = points[..., j] - center - vel[j] * t
+            r2 += d * d
+        return (amplitude * np.exp(-r2 / (2.0 * width * width)))[..., None]
+
+    return (lambda points: exact(points, 0.0)), exact
+
+
+def step_function(system, position=0.5, left=1.0, right=0.0):
+    """problems.py:85-93: a discontinuous transport profile in x."""
+    if system.name != "advection":
+        raise ValueError("the step case needs the advection system")
+
+    def ic(points):
+        return np.where(points[..., 0] < position, left, right)[..., None]
+
+    return ic, None
+
+
 def constant_state(system, values=None):
-    """problems.py:176-192 (Euler)."""
-    q0 = np.asarray([1.0] + [0.1] * system.dim + [2.5] if values is None else values, float)
+    """problems.py:176-192."""
+    if values is None:
+        values = [0.75] if system.name == "advection" else [1.0] + [0.1] * system.dim + [2.5]
+    q0 = np.asarray(values, float)
     if q0.shape != (system.n_vars,):
         raise ValueError(f"constant state needs {system.n_vars} entries")
 
@@ -125,9 +169,9 @@ def constant_state(system, values=None):
 
 
 class ProblemSpec:
-    def __init__(self, builder, dim, extents, boundary, suggested_tend):
+    def __init__(self, builder, dim, extents, boundary, suggested_tend, system="euler"):
         self.builder = builder
-        self.system = "euler"
+        self.system = system
         self.dim = dim
         self.extents = extents
         self.boundary = boundary
@@ -138,7 +182,11 @@ PROBLEMS = {
     "vortex": ProblemSpec(isentropic_vortex, 2, ((0.0, 10.0), (0.0, 10.0)), "periodic", 10.0),
     "sod": ProblemSpec(sod_shock_tube, 1, ((0.0, 1.0),), "outflow", 0.2),
     "blast": ProblemSpec(blast_2d, 2, ((-1.0, 1.0), (-1.0, 1.0)), "wall", 0.05),
-    "constant": ProblemSpec(constant_state, None, None, "periodic", 1.0),
+    "constant": ProblemSpec(constant_state, None, None, "periodic", 1.0, system=None),
+    "sine": ProblemSpec(advected_sine, None, None, "periodic", 1.0, system="advection"),
+    "pulse": ProblemSpec(gaussian_pulse, None, None, {0: ("exact", "outflow")}, 0.5,
+                         system="advection"),
+    "step": ProblemSpec(step_function, None, None, "periodic", 0.5, system="advection"),
     "density_wave": ProblemSpec(density_wave, None, None, "periodic", 1.0),
     "explosion": ProblemSpec(circular_explosion, 2, ((-1.0, 1.0), (-1.0, 1.0)), "outflow",
                              0.25),
@@ -150,7 +198,7 @@ def build_problem(name, system, **params):
         spec = PROBLEMS[name]
     except KeyError:
         raise ValueError(f"unknown problem '{name}' (choose from {sorted(PROBLEMS)})")
-    if system.name != spec.system:
+    if spec.system is not None and system.name != spec.system:
         raise ValueError(f"problem '{name}' needs the {spec.system} system, got {system.name}")
     if spec.dim is not None and system.dim != spec.dim:
         raise ValueError(f"problem '{name}' is {spec.dim}-D")

@@ -95,14 +95,58 @@ class CompressibleEuler(HyperbolicSystem):
         return out
 
 
-_SYSTEMS = {"euler": CompressibleEuler}
+class LinearAdvection(HyperbolicSystem):
+    """Scalar transport q_t + a . grad q = 0 with constant velocity a
+    (systems.py:77-109); device kernels in csrc/adg_advection.cu."""
+
+    name = "advection"
+    has_flux = True
+
+    def __init__(self, dim, velocity=None):
+        if not 1 <= dim <= 3:
+            raise ValueError("dim must be 1, 2 or 3")
+        super().__init__(dim, 1, ("q",))
+        if velocity is None:
+            velocity = [1.0] * dim
+        self.velocity = np.asarray(velocity, dtype=float)
+        if self.velocity.shape != (dim,):
+            raise ValueError("advection velocity must have one entry per dimension")
+
+    def flux(self, q):
+        out = np.empty(q.shape[:-1] + (self.dim, 1))
+        for j in range(self.dim):
+            out[..., j, 0] = self.velocity[j] * q[..., 0]
+        return out
+
+    def max_abs_eigenvalue(self, q, normal):
+        a_n = abs(float(np.dot(self.velocity, normal)))
+        return np.broadcast_to(a_n, q.shape[:-1]).copy()
+
+    def admissible(self, q):
+        xp = _xp(q)
+        if xp is np:
+            return np.all(np.isfinite(q), axis=-1)
+        return xp.isfinite(q).all(dim=-1)
+
+    def cons_to_prim(self, q):
+        return q
+
+    def prim_to_cons(self, v):
+        return v
+
+    def reflect(self, q, axis):
+        return q.copy() if _xp(q) is np else q.clone()
+
+
+_SYSTEMS = {"euler": CompressibleEuler, "advection": LinearAdvection}
 
 
 def make_system(name, dim, **params):
-    """Registered systems (systems.py:355-361).  Only Euler has a B200 path;
-    'advection' / 'elasticity-di' raise NotImplementedError."""
-    if name in ("advection", "elasticity-di"):
-        raise NotImplementedError(f"system '{name}' has no B200 kernels (Euler only)")
+    """Registered systems (systems.py:355-361).  Euler and advection have a
+    B200 path; 'elasticity-di' (the NCP machinery) raises NotImplementedError
+    (SURVEY §8(f) rank 4)."""
+    if name == "elasticity-di":
+        raise NotImplementedError(f"system '{name}' has no B200 kernels (euler, advection)")
     try:
         cls = _SYSTEMS[name]
     except KeyError:

@@ -292,9 +292,33 @@ def gen_exact():
          cells=np.array(sim.mesh.cells), extents=np.array(sim.mesh.extents))
 
 
+def gen_advection():
+    """LinearAdvection plugin (systems.py:77-109) with the registry's sine /
+    pulse / step initial conditions (problems.py:54-93), periodic, outflow
+    and wall faces, degrees 2..9, d = 1..3."""
+    from aderdg.systems import LinearAdvection
+
+    def case(name, ext, cells, vel, degree, prob, steps, boundary="periodic"):
+        sysd = LinearAdvection(len(cells), velocity=vel)
+        ic, _ = aderdg.build_problem(prob, sysd)
+        cfl = 0.9 / (len(cells) * (2 * degree + 1))
+        run_case(name, aderdg.CartesianMesh(ext, cells), sysd, degree, cfl, ic, steps,
+                 boundary=boundary)
+
+    case("adv_sine_2d", [(0, 1), (0, 1)], (8, 6), [1.0, 0.5], 3, "sine", 6)
+    case("adv_sine_3d", [(0, 1)] * 3, (3, 3, 2), [1.0, -0.5, 0.3], 2, "sine", 4)
+    case("adv_sine_3d_N5", [(0, 1)] * 3, (2, 2, 2), [0.6, 0.8, -0.4], 5, "sine", 2)
+    case("adv_sine_2d_N9", [(0, 1), (0, 1)], (3, 2), [1.0, -0.7], 9, "sine", 3)
+    case("adv_pulse_1d", [(0, 1)], (20,), [1.0], 5, "pulse", 8, boundary="outflow")
+    case("adv_step_wall_2d", [(0, 1), (0, 1)], (6, 6), [0.7, -0.4], 4, "step", 4,
+         boundary="wall")
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tables", "pointwise", "predictor", "cases", "primitive", "output",
-                             "exact"]
+                             "exact", "advection"]
+    if "advection" in which:
+        gen_advection()
     if "tables" in which:
         gen_tables()
     if "pointwise" in which:

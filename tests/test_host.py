@@ -152,7 +152,14 @@ def test_simulation_argument_errors_precede_device_use():
     with pytest.raises(ValueError):
         Simulation(mesh, e2, 3, 0.05, predictor_mode="characteristic")
     with pytest.raises(NotImplementedError):
-        make_system("advection", 2)
+        make_system("elasticity-di", 2)
+    adv = make_system("advection", 2, velocity=[1.0, 0.5])
+    with pytest.raises(NotImplementedError):
+        Simulation(mesh, adv, 3, 0.05, use_limiter=True)
+    with pytest.raises(NotImplementedError):
+        Simulation(mesh, adv, 3, 0.05, predictor_mode="primitive")
+    with pytest.raises(ValueError):
+        make_system("advection", 2, velocity=[1.0])
     import torch
 
     if not torch.cuda.is_available():
