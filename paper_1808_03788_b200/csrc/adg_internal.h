@@ -24,6 +24,12 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
             int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
             std::string* err);
 
+bool predict_stream_supported(const adg_grid* g);
+size_t predict_stream_workspace_bytes(int P, int num_sms);
+int predict_stream(const adg_grid* g, const double* u, const double* dt_dev, double tol,
+                   int max_iter, int min_iter, double* q_out, double* vol, double* traces,
+                   uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms, double* ws,
+                   size_t ws_bytes, std::string* err);
 bool predict_cluster_supported(const adg_grid* g);
 int predict_cluster(const adg_grid* g, const double* u, const double* dt_dev, double tol,
                     int max_iter, int min_iter, double* q_out, double* vol, double* traces,

@@ -30,6 +30,8 @@
 // the reference's global rule by <= 1e-14.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "adg_common.cuh"
 #include "adg_internal.h"
 
@@ -1103,7 +1105,19 @@ static size_t ws_need(int num_sms) {
 size_t predict_workspace_bytes(int dim, int P, int num_sms) {
   if (dim == 1) { ADG_DISPATCH_P(1, ws_need, num_sms) }
   if (dim == 2) { ADG_DISPATCH_P(2, ws_need, num_sms) }
-  if (dim == 3) { ADG_DISPATCH_P(3, ws_need, num_sms) }
+  if (dim == 3) {
+    // 3-D P >= 8: the slice-streaming kernel's scratch or the large-tile
+    // variant's (primitive mode), whichever is larger
+    const size_t s = predict_stream_workspace_bytes(P, num_sms);
+    size_t t = 0;
+    switch (P) {
+      case 8: t = ws_need<3, 8>(num_sms); break;
+      case 9: t = ws_need<3, 9>(num_sms); break;
+      case 10: t = ws_need<3, 10>(num_sms); break;
+      default: { ADG_DISPATCH_P(3, ws_need, num_sms) }
+    }
+    return s > t ? s : t;
+  }
   return 0;
 }
 
@@ -1111,9 +1125,14 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
             int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
             int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
             std::string* err) {
+  // 3-D tiles beyond one SM's shared memory: one CTA per element streaming
+  // time slices through shared memory (adg_predictor_stream.cu)
+  if (!getenv("ADG_CLUSTER_PREDICTOR") && predict_stream_supported(g))
+    return predict_stream(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
+                          sweeps, st, num_sms, ws, ws_bytes, err);
 #ifndef ADG_NO_CLUSTER
-  // 3-D tiles beyond one SM's shared memory: thread-block cluster, one time
-  // slice per CTA (adg_predictor_cluster.cu)
+  // the earlier design: thread-block cluster, one time slice per CTA
+  // (adg_predictor_cluster.cu), kept for A/B runs (ADG_CLUSTER_PREDICTOR=1)
   if (predict_cluster_supported(g))
     return predict_cluster(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
                            sweeps, st, num_sms, err);

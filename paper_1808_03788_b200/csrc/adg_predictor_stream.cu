@@ -1,0 +1,469 @@
+// adg_predictor_stream.cu -- the fused ADER-DG predictor for the large 3-D
+// space-time tiles (P = N+1 = 8..10: 160-391 KB per element, more than one
+// SM's shared memory) as a slice-streaming kernel: one CTA per element, the
+// element's space-time iterate and rates in a per-CTA global scratch that
+// stays in L2, one time slice at a time in shared memory.
+//
+// Same algorithm and outputs as predict_kernel (adg_predictor.cu): startup
+// guess (predictor.py:99-126), Picard sweeps with per-element freezing
+// (predictor.py:135-191), admissibility (:188-189), face traces (:218-230)
+// and the volume integral (corrector.py:141-177).
+//
+// The Picard rate L(q_t) = -sum_dir D_dir F_dir(q_t) only couples the nodes of
+// one time slice, and the time operator q_new = dt gw (x)_t rate + g0 (x) u
+// only couples the time levels of one spatial node.  So a sweep is
+//   (1) for t = 0..P-1: slice t of q -> shared memory (cp.async; the next
+//       slice is fetched while the current slice's rates are stored), the
+//       3 P^2 line owners contract flux lines as in the cluster kernel, and
+//       the x-owner stores the slice's rates to the scratch;
+//   (2) node phase: every thread takes nodes n, reads rate[0..P-1][n] (P x m
+//       values in registers), forms q_new at every time, the residual
+//       partials and stores q_new over q.
+// All CTAs of the GPU stay busy on their own element (no cluster scheduling
+// constraints), and the spatial phase keeps the cluster kernel's
+// conflict-light padded slice layouts.  The startup guess needs only two
+// spatial passes on u (k1 = L(u), k2 = L(u + dt k1)); the q at every time is a
+// pointwise formula of (u, k1, k2).
+#include <algorithm>
+#include <type_traits>
+
+#include "adg_common.cuh"
+#include "adg_internal.h"
+
+namespace adg {
+
+template <int P>
+struct StCfg {
+  static constexpr int M = 5;
+  static constexpr int PP = P * P;
+  static constexpr int PD = P * P * P;
+  // padded slice layouts (tools/cluster_bankcheck.py): Q node-major
+  // [i][j][k][v] strides (SI, SJ, M); B x-line-major [j][k][i][v] strides
+  // (TJ, TK, M)
+  static constexpr int SJ = P * M + (P == 8 ? 1 : (P == 10 ? 3 : 0));
+  static constexpr int SI = P * SJ;
+  static constexpr int TK = P * M + (P == 8 ? 2 : (P == 10 ? 1 : 0));
+  static constexpr int TJ = P * TK + (P == 8 ? 1 : 0);
+  static constexpr int QSZ = P * SI;
+  static constexpr int BSZ = P * TJ;
+  static constexpr int QSZP = QSZ + (QSZ & 1);
+  static constexpr int BSZP = BSZ + (BSZ & 1);
+  // warp-aligned line roles (every warp contracts along one compile-time
+  // direction: D/dx coefficients as constant-bank operands, no divergence)
+  static constexpr int RP = ((PP + 31) / 32) * 32;
+  static constexpr int NT = 3 * RP;
+  static constexpr int NW = NT / 32;
+  static constexpr size_t SMEM = ((size_t)QSZP + 2 * (size_t)BSZP + 2 * NW + 2 * P + 2) * 8;
+  // CTAs per SM: at most what shared memory allows, and few enough that the
+  // P x m line accumulators stay in registers (>= 168 per thread)
+  static constexpr int MINB0 = (int)((228 * 1024) / (SMEM + 1024));
+  static constexpr int MINB_R = 65536 / (168 * NT) > 0 ? 65536 / (168 * NT) : 1;
+  static constexpr int MINB1 = MINB0 < MINB_R ? MINB0 : MINB_R;
+  static constexpr int MINB = MINB1 < 1 ? 1 : MINB1;
+  static constexpr int TB = PD * M + ((PD * M) & 1);   // trace block (face kernel layout)
+  static constexpr size_t SLICE = (size_t)PD * M;      // doubles per time slice
+  static constexpr size_t SCR = 2 * (size_t)P * SLICE; // q + rates per CTA (doubles)
+};
+
+struct StArgs {
+  const double* u;
+  const double* dt;
+  double* q_out;
+  double* vol;
+  double* traces;
+  uint8_t* pred_bad;
+  int32_t* sweeps;
+  double* scr;          // per-CTA [q: P slices][rates: P slices], slice = [node][v]
+  int64_t n_elem;
+  double dx[3];
+  double gamma;
+  double tol;
+  int max_iter;
+  int min_iter;
+  double dd[3 * kMaxP * kMaxP];   // D / dx_dir, [dir][P][P] (kernel-parameter constant bank)
+};
+
+template <int P>
+__global__ void __launch_bounds__(StCfg<P>::NT, StCfg<P>::MINB)
+predict_stream_kernel(const __grid_constant__ StArgs a) {
+  using C = StCfg<P>;
+  constexpr int M = C::M, PP = C::PP, PD = C::PD, NT = C::NT, NW = C::NW;
+  constexpr int SI = C::SI, SJ = C::SJ, TJ = C::TJ, TK = C::TK;
+  const DegreeTables& T = tab<P>();
+  extern __shared__ __align__(16) double smem[];
+  double* Q = smem;                 // slice tile, node-major (padded)
+  double* B1 = Q + C::QSZP;         // y partials (x-line-major, padded)
+  double* B2 = B1 + C::BSZP;        // z partials (x-line-major)
+  double* red = B2 + C::BSZP;       // [NW][2] warp partials
+  double* cst = red + 2 * NW;       // startup coefficients [P] s_t = tau_t dt, [P] s_t^2 / (2 dt)
+  double* Qg = a.scr + (size_t)blockIdx.x * C::SCR;   // q[t][node][v]
+  double* Rg = Qg + P * C::SLICE;                      // rate[t][node][v]; k1 at startup
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const double gm1 = a.gamma - 1.0;
+  const double dt = *a.dt;
+
+  // line ownership: role 0/1/2 = x/y/z line (a0, b0) of the slice, one
+  // warp-aligned group of RP threads per role; lanes rr >= P^2 are idle
+  const int role0 = tid / C::RP;
+  const int rr0 = tid - role0 * C::RP;
+  const bool owner = rr0 < PP;
+  const int role = owner ? role0 : 3;
+  const int rr = owner ? rr0 : 0;
+  const int a0 = rr / P, b0 = rr - (rr / P) * P;
+  const int qbase = role == 0 ? a0 * SJ + b0 * M : (role == 1 ? a0 * SI + b0 * M : a0 * SI + b0 * SJ);
+  const int qstride = role == 0 ? SI : (role == 1 ? SJ : M);
+  const int nbase = role == 0 ? a0 * P + b0 : (role == 1 ? a0 * PP + b0 : a0 * PP + b0 * P);
+  const int nstride = role == 0 ? PP : (role == 1 ? P : 1);
+  const int pbase = role == 1 ? b0 * TK + a0 * M : b0 * TJ + a0 * M;
+  const int pstride = role == 1 ? TJ : TK;
+  double* pdst = role == 1 ? B1 : B2;
+  const int xrow = a0 * TJ + b0 * TK;     // x-owner's row in B1/B2
+
+  const double cv = a.dx[0] * a.dx[1] * a.dx[2];
+  const double sc0 = dt * cv / a.dx[0], sc1 = dt * cv / a.dx[1], sc2 = dt * cv / a.dx[2];
+
+  if (tid < P) {
+    const double s = T.nodes[tid] * dt;
+    cst[tid] = s;
+    cst[P + tid] = 0.5 * s * s / dt;
+  }
+  // (visible after the element loop's first barrier)
+
+  // one line's P states -> flux along DIR -> P x P contraction, l-outer
+  // (MODE 0: D/dx_DIR; MODE 1: the stiffness, plus the admissibility screen)
+  auto line_dir = [&](auto dirc, auto modec, double (&acc)[P][M], bool& ok) {
+    constexpr int DIR = decltype(dirc)::value;
+    constexpr int MODE = decltype(modec)::value;
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int v = 0; v < M; ++v) acc[i][v] = 0.0;
+    // l not unrolled: one source node's flux live at a time next to the
+    // P x m accumulators (the unrolled loop spills at P >= 9)
+#pragma unroll 1
+    for (int l = 0; l < P; ++l) {
+      double q[M], f[M];
+      const double* src = Q + qbase + l * qstride;
+#pragma unroll
+      for (int v = 0; v < M; ++v) q[v] = src[v];
+      flux_axis<3>(q, gm1, DIR, f);
+      if (MODE == 1) ok = ok && admissible<3>(q, gm1);
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const double d = MODE == 0 ? a.dd[DIR * PP + i * P + l] : T.stiff[i * P + l];
+#pragma unroll
+        for (int v = 0; v < M; ++v) acc[i][v] = fma(d, f[v], acc[i][v]);
+      }
+    }
+  };
+  auto line_contract = [&](auto modec, double (&acc)[P][M], bool& ok) {
+    if (role == 0) line_dir(std::integral_constant<int, 0>{}, modec, acc, ok);
+    else if (role == 1) line_dir(std::integral_constant<int, 1>{}, modec, acc, ok);
+    else line_dir(std::integral_constant<int, 2>{}, modec, acc, ok);
+  };
+  auto publish = [&](const double (&acc)[P][M]) {
+#pragma unroll
+    for (int o = 0; o < P; ++o)
+#pragma unroll
+      for (int v = 0; v < M; ++v) pdst[pbase + o * pstride + v] = acc[o][v];
+  };
+  // a [node][v] slice (global) into the padded Q (asynchronous 8-byte copies)
+  auto fetch = [&](const double* src) {
+    for (int x = tid; x < PD * M; x += NT) {
+      const int n = x / M, v = x - (x / M) * M;
+      const int i = n / PP, j = (n / P) % P, k = n % P;
+      cp_async8(Q + i * SI + j * SJ + k * M + v, src + x);
+    }
+    cp_async_commit();
+  };
+  // fixed-order block sum of two partials (warp trees, warps in order)
+  auto block_sum2 = [&](double& s1, double& s2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      red[2 * warp] = s1;
+      red[2 * warp + 1] = s2;
+    }
+    __syncthreads();
+    double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      t1 += red[2 * w];
+      t2 += red[2 * w + 1];
+    }
+    s1 = t1;
+    s2 = t2;
+  };
+
+  for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
+    const double* ue = a.u + (size_t)e * PD * M;
+    __syncthreads();   // previous element's readers of Q / B / red are done
+    // ---------------- startup guess: k1 = L(u), k2 = L(u + dt k1) ---------
+    fetch(ue);
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      cp_async_wait_all();
+      __syncthreads();
+      double acc[P][M];
+      bool dummy = true;
+      if (owner) line_contract(std::integral_constant<int, 0>{}, acc, dummy);
+      if (role == 1 || role == 2) publish(acc);
+      __syncthreads();
+      if (role == 0) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const int n = nbase + i * nstride;
+          double* qn = Q + qbase + i * qstride;
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            const double k = (-acc[i][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
+            if (pass == 0) {
+              Rg[n * M + v] = k;            // k1 (own nodes: no barrier needed)
+              qn[v] = qn[v] + dt * k;       // w = u + dt k1
+            } else {
+              const double k1 = Rg[n * M + v];
+              const double un = ue[n * M + v];
+#pragma unroll
+              for (int t = 0; t < P; ++t) {
+                Qg[t * C::SLICE + n * M + v] = un + cst[t] * k1 + cst[P + t] * (k - k1);
+              }
+            }
+          }
+        }
+      }
+    }
+
+    // ---------------- Picard sweeps -----------------------------------
+    int it = 0, conv = 0, nsw = 0;
+    bool fz = false;
+    for (; it < a.max_iter && !fz; ++it) {
+      __syncthreads();   // startup / previous node phase stores visible
+      fetch(Qg);
+#pragma unroll 1
+      for (int t = 0; t < P; ++t) {
+        cp_async_wait_all();
+        __syncthreads();
+        double acc[P][M];
+        bool dummy = true;
+        if (owner) line_contract(std::integral_constant<int, 0>{}, acc, dummy);
+        if (role == 1 || role == 2) publish(acc);
+        __syncthreads();
+        if (t + 1 < P) fetch(Qg + (t + 1) * C::SLICE);   // Q is dead: next slice
+        if (role == 0) {
+          double* rt = Rg + t * C::SLICE;
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            const int n = nbase + i * nstride;
+#pragma unroll
+            for (int v = 0; v < M; ++v)
+              rt[n * M + v] = (-acc[i][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
+          }
+        }
+      }
+      __syncthreads();   // every slice's rates stored
+      // node phase: time operator, residual partials, q <- q_new
+      double sd = 0.0, sq = 0.0;
+      for (int n = tid; n < PD; n += NT) {
+        double r[P][M];
+#pragma unroll
+        for (int s = 0; s < P; ++s)
+#pragma unroll
+          for (int v = 0; v < M; ++v) r[s][v] = Rg[s * C::SLICE + n * M + v];
+        double uu[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) uu[v] = ue[n * M + v];
+#pragma unroll
+        for (int t = 0; t < P; ++t) {
+          const double g0 = T.g0[t];
+          double* qo = Qg + t * C::SLICE + n * M;
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            double cc = 0.0;
+#pragma unroll
+            for (int s = 0; s < P; ++s) cc = fma(T.gw[t * P + s], r[s][v], cc);
+            const double qn = cc * dt + g0 * uu[v];
+            const double dq = qo[v] - qn;
+            sd = fma(dq, dq, sd);
+            sq = fma(qn, qn, sq);
+            qo[v] = qn;
+          }
+        }
+      }
+      block_sum2(sd, sq);
+      const double res = T.k1_opnorm * sqrt(sd);
+      const double scale = 1.0 + sqrt(sq);
+      conv = res <= a.tol * scale;
+      nsw = it + 1;
+      if (conv && it + 1 >= a.min_iter) fz = true;
+    }
+
+    // ---------------- traces, admissibility, volume ---------------------
+    bool ok = true;
+    __syncthreads();   // node-phase stores of the final iterate visible
+    fetch(Qg);
+    double* vole = a.vol + (size_t)e * PD * M;
+#pragma unroll 1
+    for (int t = 0; t < P; ++t) {
+      cp_async_wait_all();
+      __syncthreads();
+      double acc[P][M];
+      if (owner) {
+        // face traces of the line at time t (face-kernel block layouts:
+        // x [j][k][t][v], y [k][t][i][v], z [t][i][j][v])
+        double lo[M], hi[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) lo[v] = hi[v] = 0.0;
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+          const double* src = Q + qbase + l * qstride;
+          const double pl = T.left[l], pr = T.right[l];
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            lo[v] = fma(pl, src[v], lo[v]);
+            hi[v] = fma(pr, src[v], hi[v]);
+          }
+        }
+        const int dir = role;
+        const int pos = role == 0 ? (a0 * P + b0) * P + t
+                                  : (role == 1 ? (b0 * P + t) * P + a0 : (t * P + a0) * P + b0);
+        const size_t fs = (size_t)a.n_elem * C::TB;
+        double* tlo = a.traces + (size_t)(2 * dir) * fs + (size_t)e * C::TB + (size_t)pos * M;
+        double* thi = tlo + fs;
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          tlo[v] = lo[v];
+          thi[v] = hi[v];
+        }
+        line_contract(std::integral_constant<int, 1>{}, acc, ok);
+      }
+      if (role == 1 || role == 2) publish(acc);
+      if (a.q_out) {
+        for (int x = tid; x < PD; x += NT) {
+          const int i = x / PP, j = (x / P) % P, k = x % P;
+#pragma unroll
+          for (int v = 0; v < M; ++v)
+            a.q_out[(((size_t)e * PD + x) * P + t) * M + v] = Q[i * SI + j * SJ + k * M + v];
+        }
+      }
+      __syncthreads();
+      if (t + 1 < P) fetch(Qg + (t + 1) * C::SLICE);
+      if (role == 0) {
+        // slice t's volume part at the x-line's nodes (i, a0, b0), summed
+        // over slices in slice order: w_t sum_dir scale_dir(node) stiff x_dir F_dir(q_t)
+        const double wtc = T.weights[t];
+        const double wa = T.weights[a0], wb = T.weights[b0];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const double wi = T.weights[i];
+          const double s0 = sc0 * (wa * wb), s1 = sc1 * (wi * wb), s2 = sc2 * (wi * wa);
+          double* out = vole + (nbase + i * nstride) * M;
+#pragma unroll
+          for (int v = 0; v < M; ++v) {
+            double vv = s0 * acc[i][v];
+            vv += s1 * B1[xrow + i * M + v];
+            vv += s2 * B2[xrow + i * M + v];
+            const double part = wtc * vv;
+            out[v] = t == 0 ? 0.0 + part : out[v] + part;
+          }
+        }
+      }
+    }
+    const int all_ok = __syncthreads_and(ok ? 1 : 0);
+    if (tid == 0) {
+      a.pred_bad[e] = !(conv && all_ok);
+      a.sweeps[e] = nsw ? nsw : it;
+    }
+  }
+}
+
+template <int P>
+static size_t stream_ws_need(int num_sms) {
+  using C = StCfg<P>;
+  return (size_t)num_sms * C::MINB * C::SCR * 8;
+}
+
+template <int P>
+static int launch_stream(const StArgs& a0, cudaStream_t st, int num_sms, double* ws,
+                         size_t ws_bytes, std::string* err) {
+  using C = StCfg<P>;
+  auto kern = predict_stream_kernel<P>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)C::SMEM);
+    if (ce != cudaSuccess) {
+      *err = cudaGetErrorString(ce);
+      return ADG_ERR_CUDA;
+    }
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, C::SMEM);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = (int64_t)(ws_bytes / (C::SCR * 8));
+  const int64_t grid = std::min<int64_t>(a0.n_elem, std::min<int64_t>(cap, (int64_t)num_sms * per_sm));
+  if (a0.n_elem < 1) return ADG_OK;
+  if (grid < 1 || !ws) {
+    *err = "predictor workspace too small";
+    return ADG_ERR_RUNTIME;
+  }
+  StArgs a = a0;
+  a.scr = ws;
+  kern<<<(unsigned)grid, C::NT, C::SMEM, st>>>(a);
+  cudaError_t ce = cudaGetLastError();
+  if (ce != cudaSuccess) {
+    *err = cudaGetErrorString(ce);
+    return ADG_ERR_CUDA;
+  }
+  return ADG_OK;
+}
+
+bool predict_stream_supported(const adg_grid* g) {
+  return g->dim == 3 && g->degree >= 7 && g->degree <= 9 && g->mode != ADG_MODE_PRIMITIVE;
+}
+
+size_t predict_stream_workspace_bytes(int P, int num_sms) {
+  switch (P) {
+    case 8: return stream_ws_need<8>(num_sms);
+    case 9: return stream_ws_need<9>(num_sms);
+    case 10: return stream_ws_need<10>(num_sms);
+  }
+  return 0;
+}
+
+int predict_stream(const adg_grid* g, const double* u, const double* dt_dev, double tol,
+                   int max_iter, int min_iter, double* q_out, double* vol, double* traces,
+                   uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms, double* ws,
+                   size_t ws_bytes, std::string* err) {
+  StArgs a{};
+  a.u = u;
+  a.dt = dt_dev;
+  a.q_out = q_out;
+  a.vol = vol;
+  a.traces = traces;
+  a.pred_bad = pred_bad;
+  a.sweeps = sweeps;
+  a.n_elem = g->cells[0] * g->cells[1] * g->cells[2];
+  for (int j = 0; j < 3; ++j) a.dx[j] = g->dx[j];
+  a.gamma = g->gamma;
+  a.tol = tol;
+  a.max_iter = max_iter > 0 ? max_iter : 2 * g->degree + 2;
+  a.min_iter = min_iter;
+  const int P = g->degree + 1;
+  for (int dir = 0; dir < 3; ++dir)
+    for (int x = 0; x < P * P; ++x) a.dd[dir * P * P + x] = h_tab[g->degree].diff[x] / g->dx[dir];
+  switch (P) {
+    case 8: return launch_stream<8>(a, st, num_sms, ws, ws_bytes, err);
+    case 9: return launch_stream<9>(a, st, num_sms, ws, ws_bytes, err);
+    case 10: return launch_stream<10>(a, st, num_sms, ws, ws_bytes, err);
+  }
+  *err = "stream predictor: unsupported degree";
+  return ADG_ERR_UNSUPPORTED;
+}
+
+}  // namespace adg

@@ -73,6 +73,7 @@ def main():
     ap.add_argument("--c4-steps", type=int, default=100)
     ap.add_argument("--c3-cells", type=int, default=32)
     ap.add_argument("--c4-cells", type=int, default=512)
+    ap.add_argument("--c3-degrees", default="2,3,4,5,6,7,8,9")
     args = ap.parse_args()
     which = set(args.only.split(","))
     if "C1" in which:
@@ -81,7 +82,7 @@ def main():
         run_case("C2", [(0.0, 1.0)] * 3, (64, 64, 64), 4, 0.9 / 27.0, "density_wave", 20)
     if "C3" in which:
         n3 = args.c3_cells
-        for n in range(2, 10):
+        for n in [int(x) for x in args.c3_degrees.split(",")]:
             run_case(f"C3_N{n}", [(0.0, 1.0)] * 3, (n3,) * 3, n, 0.9 / (3 * (2 * n + 1)),
                      "density_wave", 10)
     if "C4" in which:
