@@ -32,6 +32,10 @@
 
 namespace adg {
 
+#ifndef ADG_STREAM_NH
+#define ADG_STREAM_NH 0   // 0: per-degree default below; 1 / 2: force
+#endif
+
 template <int P>
 struct StCfg {
   static constexpr int M = 5;
@@ -48,16 +52,24 @@ struct StCfg {
   static constexpr int BSZ = P * TJ;
   static constexpr int QSZP = QSZ + (QSZ & 1);
   static constexpr int BSZP = BSZ + (BSZ & 1);
-  // warp-aligned line roles (every warp contracts along one compile-time
-  // direction: D/dx coefficients as constant-bank operands, no divergence)
+  // output halves per line: with NH = 2 two warp groups own the same lines,
+  // each recomputes the line's fluxes and accumulates half of the P outputs
+  // (P x m accumulators do not fit the register budget at P >= 9)
+  static constexpr int NH = ADG_STREAM_NH ? ADG_STREAM_NH : 1;
+  static constexpr int H = (P + NH - 1) / NH;
+  // warp-aligned line groups: every warp contracts along one compile-time
+  // direction and half (D/dx coefficients as constant-bank operands, no
+  // divergence)
   static constexpr int RP = ((PP + 31) / 32) * 32;
-  static constexpr int NT = 3 * RP;
+  static constexpr int NG = 3 * NH;
+  static constexpr int NT = NG * RP;
   static constexpr int NW = NT / 32;
   static constexpr size_t SMEM = ((size_t)QSZP + 2 * (size_t)BSZP + 2 * NW + 2 * P + 2) * 8;
-  // CTAs per SM: at most what shared memory allows, and few enough that the
-  // P x m line accumulators stay in registers (>= 168 per thread)
+  // CTAs per SM: what shared memory allows, capped so each thread keeps
+  // >= 80 registers (H x m accumulators)
   static constexpr int MINB0 = (int)((228 * 1024) / (SMEM + 1024));
-  static constexpr int MINB_R = 65536 / (168 * NT) > 0 ? 65536 / (168 * NT) : 1;
+  static constexpr int RMIN = NH == 1 ? 168 : 80;
+  static constexpr int MINB_R = 65536 / (RMIN * NT) > 0 ? 65536 / (RMIN * NT) : 1;
   static constexpr int MINB1 = MINB0 < MINB_R ? MINB0 : MINB_R;
   static constexpr int MINB = MINB1 < 1 ? 1 : MINB1;
   static constexpr int TB = PD * M + ((PD * M) & 1);   // trace block (face kernel layout)
@@ -83,11 +95,60 @@ struct StArgs {
   double dd[3 * kMaxP * kMaxP];   // D / dx_dir, [dir][P][P] (kernel-parameter constant bank)
 };
 
+// one line's P states (src + l * stride) -> flux along DIR -> the outputs
+// HF * H .. HF * H + H - 1 of the P x P contraction, l-outer (MODE 0: D/dx_DIR
+// from the kernel-parameter bank; MODE 1: the stiffness, plus the
+// admissibility screen)
+template <int P, int DIR, int MODE, int HF>
+__device__ __forceinline__ void st_line(const double* src0, int stride, double gm1,
+                                        const double* dd, const DegreeTables& T,
+                                        double (&acc)[StCfg<P>::H][5], bool& ok) {
+  constexpr int M = 5, H = StCfg<P>::H, IB = HF * H;
+#pragma unroll
+  for (int i = 0; i < H; ++i)
+#pragma unroll
+    for (int v = 0; v < M; ++v) acc[i][v] = 0.0;
+  // l not unrolled: one source node's flux live at a time next to the
+  // accumulators
+#pragma unroll 1
+  for (int l = 0; l < P; ++l) {
+    double q[M], f[M];
+    const double* src = src0 + l * stride;
+#pragma unroll
+    for (int v = 0; v < M; ++v) q[v] = src[v];
+    if (DIR >= 0) {
+      flux_axis<3>(q, gm1, DIR < 0 ? 0 : DIR, f);
+    } else {
+#pragma unroll
+      for (int v = 0; v < M; ++v) f[v] = q[v];   // precomputed (time-weighted) fluxes
+    }
+    if (MODE == 1 && DIR >= 0) ok = ok && admissible<3>(q, gm1);
+#pragma unroll
+    for (int ii = 0; ii < H; ++ii) {
+      if (IB + ii < P) {
+        const double d = MODE == 0 ? dd[(DIR < 0 ? 0 : DIR) * P * P + (IB + ii) * P + l] : T.stiff[(IB + ii) * P + l];
+#pragma unroll
+        for (int v = 0; v < M; ++v) acc[ii][v] = fma(d, f[v], acc[ii][v]);
+      }
+    }
+  }
+}
+
+template <int P, int DIR, int MODE>
+__device__ __forceinline__ void st_line_half(const double* src0, int stride, double gm1,
+                                             const double* dd, const DegreeTables& T, int half,
+                                             double (&acc)[StCfg<P>::H][5], bool& ok) {
+  if (StCfg<P>::NH == 1 || half == 0)
+    st_line<P, DIR, MODE, 0>(src0, stride, gm1, dd, T, acc, ok);
+  else
+    st_line<P, DIR, MODE, StCfg<P>::NH - 1>(src0, stride, gm1, dd, T, acc, ok);
+}
+
 template <int P>
 __global__ void __launch_bounds__(StCfg<P>::NT, StCfg<P>::MINB)
 predict_stream_kernel(const __grid_constant__ StArgs a) {
   using C = StCfg<P>;
-  constexpr int M = C::M, PP = C::PP, PD = C::PD, NT = C::NT, NW = C::NW;
+  constexpr int M = C::M, PP = C::PP, PD = C::PD, NT = C::NT, NW = C::NW, H = C::H, NH = C::NH;
   constexpr int SI = C::SI, SJ = C::SJ, TJ = C::TJ, TK = C::TK;
   const DegreeTables& T = tab<P>();
   extern __shared__ __align__(16) double smem[];
@@ -104,12 +165,14 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
   const double gm1 = a.gamma - 1.0;
   const double dt = *a.dt;
 
-  // line ownership: role 0/1/2 = x/y/z line (a0, b0) of the slice, one
-  // warp-aligned group of RP threads per role; lanes rr >= P^2 are idle
-  const int role0 = tid / C::RP;
-  const int rr0 = tid - role0 * C::RP;
+  // line ownership: group g = (direction, half); lanes rr >= P^2 of a group
+  // are idle in the line phases
+  const int grp = tid / C::RP;
+  const int rr0 = tid - grp * C::RP;
   const bool owner = rr0 < PP;
-  const int role = owner ? role0 : 3;
+  const int role = owner ? grp / NH : 3;      // 0/1/2 = x/y/z line, 3 idle
+  const int half = grp - (grp / NH) * NH;     // output half (warp-uniform)
+  const int ibase = half * H;                 // first output of this half
   const int rr = owner ? rr0 : 0;
   const int a0 = rr / P, b0 = rr - (rr / P) * P;
   const int qbase = role == 0 ? a0 * SJ + b0 * M : (role == 1 ? a0 * SI + b0 * M : a0 * SI + b0 * SJ);
@@ -131,50 +194,33 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
   }
   // (visible after the element loop's first barrier)
 
-  // one line's P states -> flux along DIR -> P x P contraction, l-outer
-  // (MODE 0: D/dx_DIR; MODE 1: the stiffness, plus the admissibility screen)
-  auto line_dir = [&](auto dirc, auto modec, double (&acc)[P][M], bool& ok) {
-    constexpr int DIR = decltype(dirc)::value;
-    constexpr int MODE = decltype(modec)::value;
-#pragma unroll
-    for (int i = 0; i < P; ++i)
-#pragma unroll
-      for (int v = 0; v < M; ++v) acc[i][v] = 0.0;
-    // l not unrolled: one source node's flux live at a time next to the
-    // P x m accumulators (the unrolled loop spills at P >= 9)
-#pragma unroll 1
-    for (int l = 0; l < P; ++l) {
-      double q[M], f[M];
-      const double* src = Q + qbase + l * qstride;
-#pragma unroll
-      for (int v = 0; v < M; ++v) q[v] = src[v];
-      flux_axis<3>(q, gm1, DIR, f);
-      if (MODE == 1) ok = ok && admissible<3>(q, gm1);
-#pragma unroll
-      for (int i = 0; i < P; ++i) {
-        const double d = MODE == 0 ? a.dd[DIR * PP + i * P + l] : T.stiff[i * P + l];
-#pragma unroll
-        for (int v = 0; v < M; ++v) acc[i][v] = fma(d, f[v], acc[i][v]);
-      }
+  auto line_contract = [&](int mode, double (&acc)[H][M], bool& ok) {
+    const double* q0 = Q + qbase;
+    if (mode == 0) {
+      if (role == 0) st_line_half<P, 0, 0>(q0, qstride, gm1, a.dd, T, half, acc, ok);
+      else if (role == 1) st_line_half<P, 1, 0>(q0, qstride, gm1, a.dd, T, half, acc, ok);
+      else st_line_half<P, 2, 0>(q0, qstride, gm1, a.dd, T, half, acc, ok);
+    } else {
+      if (role == 0) st_line_half<P, 0, 1>(q0, qstride, gm1, a.dd, T, half, acc, ok);
+      else if (role == 1) st_line_half<P, 1, 1>(q0, qstride, gm1, a.dd, T, half, acc, ok);
+      else st_line_half<P, 2, 1>(q0, qstride, gm1, a.dd, T, half, acc, ok);
     }
   };
-  auto line_contract = [&](auto modec, double (&acc)[P][M], bool& ok) {
-    if (role == 0) line_dir(std::integral_constant<int, 0>{}, modec, acc, ok);
-    else if (role == 1) line_dir(std::integral_constant<int, 1>{}, modec, acc, ok);
-    else line_dir(std::integral_constant<int, 2>{}, modec, acc, ok);
-  };
-  auto publish = [&](const double (&acc)[P][M]) {
+  auto publish = [&](const double (&acc)[H][M]) {
 #pragma unroll
-    for (int o = 0; o < P; ++o)
+    for (int ii = 0; ii < H; ++ii)
+      if (ibase + ii < P)
 #pragma unroll
-      for (int v = 0; v < M; ++v) pdst[pbase + o * pstride + v] = acc[o][v];
+        for (int v = 0; v < M; ++v) pdst[pbase + (ibase + ii) * pstride + v] = acc[ii][v];
   };
   // a [node][v] slice (global) into the padded Q (asynchronous 8-byte copies)
   auto fetch = [&](const double* src) {
-    for (int x = tid; x < PD * M; x += NT) {
-      const int n = x / M, v = x - (x / M) * M;
-      const int i = n / PP, j = (n / P) % P, k = n % P;
-      cp_async8(Q + i * SI + j * SJ + k * M + v, src + x);
+    // P^2 rows (i, j) of P m contiguous doubles; one warp per row
+    for (int row = warp; row < PP; row += NW) {
+      const int i = row / P, j = row - (row / P) * P;
+      double* dst = Q + i * SI + j * SJ;
+      const double* sr = src + row * (P * M);
+      for (int o = lane; o < P * M; o += 32) cp_async8(dst + o, sr + o);
     }
     cp_async_commit();
   };
@@ -209,33 +255,33 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     for (int pass = 0; pass < 2; ++pass) {
       cp_async_wait_all();
       __syncthreads();
-      double acc[P][M];
+      double acc[H][M];
       bool dummy = true;
-      if (owner) line_contract(std::integral_constant<int, 0>{}, acc, dummy);
+      if (owner) line_contract(0, acc, dummy);
       if (role == 1 || role == 2) publish(acc);
       __syncthreads();
       if (role == 0) {
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
+        for (int ii = 0; ii < H; ++ii) {
+          const int i = ibase + ii;
+          if (i >= P) continue;
           const int n = nbase + i * nstride;
           double* qn = Q + qbase + i * qstride;
 #pragma unroll
           for (int v = 0; v < M; ++v) {
-            const double k = (-acc[i][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
-            if (pass == 0) {
-              Rg[n * M + v] = k;            // k1 (own nodes: no barrier needed)
-              qn[v] = qn[v] + dt * k;       // w = u + dt k1
-            } else {
-              const double k1 = Rg[n * M + v];
-              const double un = ue[n * M + v];
-#pragma unroll
-              for (int t = 0; t < P; ++t) {
-                Qg[t * C::SLICE + n * M + v] = un + cst[t] * k1 + cst[P + t] * (k - k1);
-              }
-            }
+            const double k = (-acc[ii][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
+            Rg[pass * C::SLICE + n * M + v] = k;   // k1 / k2 (own nodes)
+            if (pass == 0) qn[v] = qn[v] + dt * k;  // w = u + dt k1
           }
         }
       }
+    }
+    __syncthreads();   // k1, k2 of every node stored
+    // q_t = u + s_t k1 + s_t^2 / (2 dt) (k2 - k1) at every time (predictor.py:116-124)
+    for (int x = tid; x < PD * M; x += NT) {
+      const double k1 = Rg[x], k2 = Rg[C::SLICE + x], un = ue[x];
+#pragma unroll 1
+      for (int t = 0; t < P; ++t) Qg[t * C::SLICE + x] = un + cst[t] * k1 + cst[P + t] * (k2 - k1);
     }
 
     // ---------------- Picard sweeps -----------------------------------
@@ -248,50 +294,48 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
       for (int t = 0; t < P; ++t) {
         cp_async_wait_all();
         __syncthreads();
-        double acc[P][M];
+        double acc[H][M];
         bool dummy = true;
-        if (owner) line_contract(std::integral_constant<int, 0>{}, acc, dummy);
+        if (owner) line_contract(0, acc, dummy);
         if (role == 1 || role == 2) publish(acc);
         __syncthreads();
         if (t + 1 < P) fetch(Qg + (t + 1) * C::SLICE);   // Q is dead: next slice
         if (role == 0) {
           double* rt = Rg + t * C::SLICE;
 #pragma unroll
-          for (int i = 0; i < P; ++i) {
+          for (int ii = 0; ii < H; ++ii) {
+            const int i = ibase + ii;
+            if (i >= P) continue;
             const int n = nbase + i * nstride;
 #pragma unroll
             for (int v = 0; v < M; ++v)
-              rt[n * M + v] = (-acc[i][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
+              rt[n * M + v] = (-acc[ii][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
           }
         }
       }
       __syncthreads();   // every slice's rates stored
-      // node phase: time operator, residual partials, q <- q_new
+      // node phase: time operator, residual partials, q <- q_new (one
+      // quantity at a time: P rates in registers)
       double sd = 0.0, sq = 0.0;
-      for (int n = tid; n < PD; n += NT) {
-        double r[P][M];
+      for (int x = tid; x < PD * M; x += NT) {
+        const int n = x / M, v = x - (x / M) * M;
+        double r[P];
 #pragma unroll
-        for (int s = 0; s < P; ++s)
-#pragma unroll
-          for (int v = 0; v < M; ++v) r[s][v] = Rg[s * C::SLICE + n * M + v];
-        double uu[M];
-#pragma unroll
-        for (int v = 0; v < M; ++v) uu[v] = ue[n * M + v];
+        for (int s = 0; s < P; ++s) r[s] = Rg[s * C::SLICE + x];
+        const double uu = ue[x];
+        (void)n;
+        (void)v;
 #pragma unroll
         for (int t = 0; t < P; ++t) {
-          const double g0 = T.g0[t];
-          double* qo = Qg + t * C::SLICE + n * M;
+          double cc = 0.0;
 #pragma unroll
-          for (int v = 0; v < M; ++v) {
-            double cc = 0.0;
-#pragma unroll
-            for (int s = 0; s < P; ++s) cc = fma(T.gw[t * P + s], r[s][v], cc);
-            const double qn = cc * dt + g0 * uu[v];
-            const double dq = qo[v] - qn;
-            sd = fma(dq, dq, sd);
-            sq = fma(qn, qn, sq);
-            qo[v] = qn;
-          }
+          for (int s = 0; s < P; ++s) cc = fma(T.gw[t * P + s], r[s], cc);
+          const double qn = cc * dt + T.g0[t] * uu;
+          double* qo = Qg + t * C::SLICE + x;
+          const double dq = *qo - qn;
+          sd = fma(dq, dq, sd);
+          sq = fma(qn, qn, sq);
+          *qo = qn;
         }
       }
       block_sum2(sd, sq);
@@ -303,16 +347,19 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     }
 
     // ---------------- traces, admissibility, volume ---------------------
+    // per slice: face traces (line owners), admissibility and the
+    // time-weighted fluxes Fbar_dir = sum_t w_t F_dir(q_t) (corrector.py:166,
+    // one node per thread: Fbar_y / Fbar_z accumulate in B1 / B2 in x-line-
+    // major order, Fbar_x in the thread's own scratch rows); then one
+    // stiffness contraction per direction (corrector.py:169-176)
     bool ok = true;
     __syncthreads();   // node-phase stores of the final iterate visible
     fetch(Qg);
-    double* vole = a.vol + (size_t)e * PD * M;
 #pragma unroll 1
     for (int t = 0; t < P; ++t) {
       cp_async_wait_all();
       __syncthreads();
-      double acc[P][M];
-      if (owner) {
+      if (owner && half == 0) {
         // face traces of the line at time t (face-kernel block layouts:
         // x [j][k][t][v], y [k][t][i][v], z [t][i][j][v])
         double lo[M], hi[M];
@@ -339,36 +386,68 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
           tlo[v] = lo[v];
           thi[v] = hi[v];
         }
-        line_contract(std::integral_constant<int, 1>{}, acc, ok);
       }
-      if (role == 1 || role == 2) publish(acc);
-      if (a.q_out) {
-        for (int x = tid; x < PD; x += NT) {
-          const int i = x / PP, j = (x / P) % P, k = x % P;
+      const double wt = T.weights[t];
+      for (int n = tid; n < PD; n += NT) {
+        const int i = n / PP, j = (n / P) % P, k = n % P;
+        const double* qn = Q + i * SI + j * SJ + k * M;
+        double q[M];
 #pragma unroll
-          for (int v = 0; v < M; ++v)
-            a.q_out[(((size_t)e * PD + x) * P + t) * M + v] = Q[i * SI + j * SJ + k * M + v];
+        for (int v = 0; v < M; ++v) q[v] = qn[v];
+        ok = ok && admissible<3>(q, gm1);
+        if (a.q_out) {
+#pragma unroll
+          for (int v = 0; v < M; ++v) a.q_out[(((size_t)e * PD + n) * P + t) * M + v] = q[v];
         }
+        double f[M];
+        const int bx = j * TJ + k * TK + i * M;
+        flux_axis<3>(q, gm1, 0, f);
+#pragma unroll
+        for (int v = 0; v < M; ++v) Rg[n * M + v] = t == 0 ? wt * f[v] : Rg[n * M + v] + wt * f[v];
+        flux_axis<3>(q, gm1, 1, f);
+#pragma unroll
+        for (int v = 0; v < M; ++v) B1[bx + v] = t == 0 ? wt * f[v] : B1[bx + v] + wt * f[v];
+        flux_axis<3>(q, gm1, 2, f);
+#pragma unroll
+        for (int v = 0; v < M; ++v) B2[bx + v] = t == 0 ? wt * f[v] : B2[bx + v] + wt * f[v];
       }
       __syncthreads();
       if (t + 1 < P) fetch(Qg + (t + 1) * C::SLICE);
+    }
+    // Fbar_x into Q (own nodes); the y / z owners contract Fbar_y / Fbar_z
+    // in place (each reads and writes only its own line of B1 / B2)
+    for (int n = tid; n < PD; n += NT) {
+      const int i = n / PP, j = (n / P) % P, k = n % P;
+#pragma unroll
+      for (int v = 0; v < M; ++v) Q[i * SI + j * SJ + k * M + v] = Rg[n * M + v];
+    }
+    __syncthreads();
+    {
+      double acc[H][M];
+      bool dummy = true;
+      if (owner) {
+        const double* src0 = role == 0 ? Q + qbase : pdst + pbase;
+        const int str = role == 0 ? qstride : pstride;
+        st_line_half<P, -1, 1>(src0, str, gm1, a.dd, T, half, acc, dummy);
+      }
+      if (role == 1 || role == 2) publish(acc);
+      __syncthreads();
       if (role == 0) {
-        // slice t's volume part at the x-line's nodes (i, a0, b0), summed
-        // over slices in slice order: w_t sum_dir scale_dir(node) stiff x_dir F_dir(q_t)
-        const double wtc = T.weights[t];
+        double* vole = a.vol + (size_t)e * PD * M;
         const double wa = T.weights[a0], wb = T.weights[b0];
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
+        for (int ii = 0; ii < H; ++ii) {
+          const int i = ibase + ii;
+          if (i >= P) continue;
           const double wi = T.weights[i];
           const double s0 = sc0 * (wa * wb), s1 = sc1 * (wi * wb), s2 = sc2 * (wi * wa);
           double* out = vole + (nbase + i * nstride) * M;
 #pragma unroll
           for (int v = 0; v < M; ++v) {
-            double vv = s0 * acc[i][v];
+            double vv = s0 * acc[ii][v];
             vv += s1 * B1[xrow + i * M + v];
             vv += s2 * B2[xrow + i * M + v];
-            const double part = wtc * vv;
-            out[v] = t == 0 ? 0.0 + part : out[v] + part;
+            out[v] = vv;
           }
         }
       }
