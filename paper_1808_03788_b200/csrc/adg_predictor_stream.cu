@@ -246,6 +246,30 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     s2 = t2;
   };
 
+  // rates of the slice in Q at the line owners' nodes -> rt ([node][v]);
+  // once every owner has read Q, the next slice (if any) is fetched into it
+  auto slice_rates = [&](const double* next, double* rt) {
+    cp_async_wait_all();
+    __syncthreads();
+    double acc[H][M];
+    bool dummy = true;
+    if (owner) line_contract(0, acc, dummy);
+    if (role == 1 || role == 2) publish(acc);
+    __syncthreads();
+    if (next) fetch(next);   // Q is dead
+    if (role == 0) {
+#pragma unroll
+      for (int ii = 0; ii < H; ++ii) {
+        const int i = ibase + ii;
+        if (i >= P) continue;
+        const int n = nbase + i * nstride;
+#pragma unroll
+        for (int v = 0; v < M; ++v)
+          rt[n * M + v] = (-acc[ii][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
+      }
+    }
+  };
+
   for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
     const double* ue = a.u + (size_t)e * PD * M;
     __syncthreads();   // previous element's readers of Q / B / red are done
@@ -253,30 +277,18 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     fetch(ue);
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
-      cp_async_wait_all();
-      __syncthreads();
-      double acc[H][M];
-      bool dummy = true;
-      if (owner) line_contract(0, acc, dummy);
-      if (role == 1 || role == 2) publish(acc);
-      __syncthreads();
-      if (role == 0) {
-#pragma unroll
-        for (int ii = 0; ii < H; ++ii) {
-          const int i = ibase + ii;
-          if (i >= P) continue;
-          const int n = nbase + i * nstride;
-          double* qn = Q + qbase + i * qstride;
-#pragma unroll
-          for (int v = 0; v < M; ++v) {
-            const double k = (-acc[ii][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
-            Rg[pass * C::SLICE + n * M + v] = k;   // k1 / k2 (own nodes)
-            if (pass == 0) qn[v] = qn[v] + dt * k;  // w = u + dt k1
-          }
+      if (pass == 1) {
+        // w = u + dt k1 in the tile (row-parallel, like fetch)
+        for (int row = warp; row < PP; row += NW) {
+          const int i = row / P, j = row - (row / P) * P;
+          double* dst = Q + i * SI + j * SJ;
+          const double* k1 = Rg + row * (P * M);
+          for (int o = lane; o < P * M; o += 32) dst[o] = dst[o] + dt * k1[o];
         }
       }
+      slice_rates(nullptr, Rg + pass * C::SLICE);   // k1 / k2
+      __syncthreads();   // stores of every x-owner visible
     }
-    __syncthreads();   // k1, k2 of every node stored
     // q_t = u + s_t k1 + s_t^2 / (2 dt) (k2 - k1) at every time (predictor.py:116-124)
     for (int x = tid; x < PD * M; x += NT) {
       const double k1 = Rg[x], k2 = Rg[C::SLICE + x], un = ue[x];
@@ -291,51 +303,30 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
       __syncthreads();   // startup / previous node phase stores visible
       fetch(Qg);
 #pragma unroll 1
-      for (int t = 0; t < P; ++t) {
-        cp_async_wait_all();
-        __syncthreads();
-        double acc[H][M];
-        bool dummy = true;
-        if (owner) line_contract(0, acc, dummy);
-        if (role == 1 || role == 2) publish(acc);
-        __syncthreads();
-        if (t + 1 < P) fetch(Qg + (t + 1) * C::SLICE);   // Q is dead: next slice
-        if (role == 0) {
-          double* rt = Rg + t * C::SLICE;
-#pragma unroll
-          for (int ii = 0; ii < H; ++ii) {
-            const int i = ibase + ii;
-            if (i >= P) continue;
-            const int n = nbase + i * nstride;
-#pragma unroll
-            for (int v = 0; v < M; ++v)
-              rt[n * M + v] = (-acc[ii][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
-          }
-        }
-      }
+      for (int t = 0; t < P; ++t)
+        slice_rates(t + 1 < P ? Qg + (t + 1) * C::SLICE : nullptr, Rg + t * C::SLICE);
       __syncthreads();   // every slice's rates stored
       // node phase: time operator, residual partials, q <- q_new (one
-      // quantity at a time: P rates in registers)
+      // quantity of one node per item: its P rates and P iterates loaded
+      // up front)
       double sd = 0.0, sq = 0.0;
       for (int x = tid; x < PD * M; x += NT) {
-        const int n = x / M, v = x - (x / M) * M;
-        double r[P];
+        double r[P], qo[P];
 #pragma unroll
         for (int s = 0; s < P; ++s) r[s] = Rg[s * C::SLICE + x];
+#pragma unroll
+        for (int t = 0; t < P; ++t) qo[t] = Qg[t * C::SLICE + x];
         const double uu = ue[x];
-        (void)n;
-        (void)v;
 #pragma unroll
         for (int t = 0; t < P; ++t) {
           double cc = 0.0;
 #pragma unroll
           for (int s = 0; s < P; ++s) cc = fma(T.gw[t * P + s], r[s], cc);
           const double qn = cc * dt + T.g0[t] * uu;
-          double* qo = Qg + t * C::SLICE + x;
-          const double dq = *qo - qn;
+          const double dq = qo[t] - qn;
           sd = fma(dq, dq, sd);
           sq = fma(qn, qn, sq);
-          *qo = qn;
+          Qg[t * C::SLICE + x] = qn;
         }
       }
       block_sum2(sd, sq);
