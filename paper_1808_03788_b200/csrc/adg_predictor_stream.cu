@@ -75,6 +75,9 @@ struct StCfg {
   static constexpr int TB = PD * M + ((PD * M) & 1);   // trace block (face kernel layout)
   static constexpr size_t SLICE = (size_t)PD * M;      // doubles per time slice
   static constexpr size_t SCR = 2 * (size_t)P * SLICE; // q + rates per CTA (doubles)
+  // startup and sweeps through one slice-rate call site (fewer spills; measured
+  // faster at P = 8, 9, slower at P = 10)
+  static constexpr bool UNIFIED = P != 10;
 };
 
 struct StArgs {
@@ -273,6 +276,87 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
   for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
     const double* ue = a.u + (size_t)e * PD * M;
     __syncthreads();   // previous element's readers of Q / B / red are done
+    int it = 0, conv = 0, nsw = 0;
+    if constexpr (StCfg<P>::UNIFIED) {
+    // ---------------- startup guess and Picard sweeps --------------------
+    // one slice-rate call site for both (a second inlined copy spills):
+    // stage 0 / 1 are the startup passes k1 = L(u), k2 = L(u + dt k1)
+    // (predictor.py:99-126) on the tile in Q, stage 2 the sweeps' slices
+    fetch(ue);
+    bool fz = a.max_iter <= 0;
+    int stage = 0, t = 0;
+#pragma unroll 1
+    while (true) {
+      double* rt = Rg + (stage < 2 ? stage : t) * C::SLICE;
+      const double* next = (stage == 2 && t + 1 < P) ? Qg + (t + 1) * C::SLICE : nullptr;
+      slice_rates(next, rt);
+      if (stage == 0) {
+        __syncthreads();   // k1 stored
+        // w = u + dt k1 in the tile (row-parallel, like fetch)
+        for (int row = warp; row < PP; row += NW) {
+          const int i = row / P, j = row - (row / P) * P;
+          double* dst = Q + i * SI + j * SJ;
+          const double* k1 = Rg + row * (P * M);
+          for (int o = lane; o < P * M; o += 32) dst[o] = dst[o] + dt * k1[o];
+        }
+        stage = 1;
+        continue;
+      }
+      if (stage == 1) {
+        __syncthreads();   // k2 stored
+        // q_t = u + s_t k1 + s_t^2 / (2 dt) (k2 - k1) at every time (predictor.py:116-124)
+        for (int x = tid; x < PD * M; x += NT) {
+          const double k1 = Rg[x], k2 = Rg[C::SLICE + x], un = ue[x];
+#pragma unroll 1
+          for (int tt = 0; tt < P; ++tt)
+            Qg[tt * C::SLICE + x] = un + cst[tt] * k1 + cst[P + tt] * (k2 - k1);
+        }
+        if (fz) break;
+        stage = 2;
+        t = 0;
+        __syncthreads();   // startup iterate stored
+        fetch(Qg);
+        continue;
+      }
+      if (++t < P) continue;
+      __syncthreads();   // every slice's rates stored
+      // node phase: time operator, residual partials, q <- q_new (one
+      // quantity of one node per item: its P rates and P iterates loaded
+      // up front)
+      double sd = 0.0, sq = 0.0;
+      for (int x = tid; x < PD * M; x += NT) {
+        double r[P], qo[P];
+#pragma unroll
+        for (int s = 0; s < P; ++s) r[s] = Rg[s * C::SLICE + x];
+#pragma unroll
+        for (int t = 0; t < P; ++t) qo[t] = Qg[t * C::SLICE + x];
+        const double uu = ue[x];
+#pragma unroll
+        for (int t = 0; t < P; ++t) {
+          double cc = 0.0;
+#pragma unroll
+          for (int s = 0; s < P; ++s) cc = fma(T.gw[t * P + s], r[s], cc);
+          const double qn = cc * dt + T.g0[t] * uu;
+          const double dq = qo[t] - qn;
+          sd = fma(dq, dq, sd);
+          sq = fma(qn, qn, sq);
+          Qg[t * C::SLICE + x] = qn;
+        }
+      }
+      block_sum2(sd, sq);
+      const double res = T.k1_opnorm * sqrt(sd);
+      const double scale = 1.0 + sqrt(sq);
+      conv = res <= a.tol * scale;
+      nsw = it + 1;
+      ++it;
+      if (conv && it >= a.min_iter) fz = true;
+      if (fz || it >= a.max_iter) break;
+      t = 0;
+      __syncthreads();   // node-phase stores visible
+      fetch(Qg);
+    }
+
+    } else {
     // ---------------- startup guess: k1 = L(u), k2 = L(u + dt k1) ---------
     fetch(ue);
 #pragma unroll 1
@@ -297,7 +381,6 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     }
 
     // ---------------- Picard sweeps -----------------------------------
-    int it = 0, conv = 0, nsw = 0;
     bool fz = false;
     for (; it < a.max_iter && !fz; ++it) {
       __syncthreads();   // startup / previous node phase stores visible
@@ -337,6 +420,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
       if (conv && it + 1 >= a.min_iter) fz = true;
     }
 
+    }
     // ---------------- traces, admissibility, volume ---------------------
     // per slice: face traces (line owners), admissibility and the
     // time-weighted fluxes Fbar_dir = sum_t w_t F_dir(q_t) (corrector.py:166,
