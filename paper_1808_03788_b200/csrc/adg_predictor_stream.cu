@@ -273,6 +273,42 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     }
   };
 
+  // time operator of the sweep (predictor.py:175-185) over the element's
+  // P^3 m values: q_new(t) = dt sum_s gw[t][s] rate(s) + g0[t] u, residual
+  // partials, q <- q_new.  Two items per thread in flight: their 2P rates and
+  // 2P iterates are loaded before any arithmetic (L2 latency overlapped)
+  auto node_phase = [&](const double* ue, double& sd, double& sq) {
+    constexpr int NB = 2;
+    for (int x0 = tid; x0 < PD * M; x0 += NB * NT) {
+      double r[NB][P], qo[NB][P], uu[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int x = x0 + b * NT < PD * M ? x0 + b * NT : x0;
+#pragma unroll
+        for (int s2 = 0; s2 < P; ++s2) r[b][s2] = Rg[s2 * C::SLICE + x];
+#pragma unroll
+        for (int t2 = 0; t2 < P; ++t2) qo[b][t2] = Qg[t2 * C::SLICE + x];
+        uu[b] = ue[x];
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int x = x0 + b * NT;
+        if (x >= PD * M) break;
+#pragma unroll
+        for (int t2 = 0; t2 < P; ++t2) {
+          double cc = 0.0;
+#pragma unroll
+          for (int s2 = 0; s2 < P; ++s2) cc = fma(T.gw[t2 * P + s2], r[b][s2], cc);
+          const double qn = cc * dt + T.g0[t2] * uu[b];
+          const double dq = qo[b][t2] - qn;
+          sd = fma(dq, dq, sd);
+          sq = fma(qn, qn, sq);
+          Qg[t2 * C::SLICE + x] = qn;
+        }
+      }
+    }
+  };
+
   for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
     const double* ue = a.u + (size_t)e * PD * M;
     __syncthreads();   // previous element's readers of Q / B / red are done
@@ -324,25 +360,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
       // quantity of one node per item: its P rates and P iterates loaded
       // up front)
       double sd = 0.0, sq = 0.0;
-      for (int x = tid; x < PD * M; x += NT) {
-        double r[P], qo[P];
-#pragma unroll
-        for (int s = 0; s < P; ++s) r[s] = Rg[s * C::SLICE + x];
-#pragma unroll
-        for (int t = 0; t < P; ++t) qo[t] = Qg[t * C::SLICE + x];
-        const double uu = ue[x];
-#pragma unroll
-        for (int t = 0; t < P; ++t) {
-          double cc = 0.0;
-#pragma unroll
-          for (int s = 0; s < P; ++s) cc = fma(T.gw[t * P + s], r[s], cc);
-          const double qn = cc * dt + T.g0[t] * uu;
-          const double dq = qo[t] - qn;
-          sd = fma(dq, dq, sd);
-          sq = fma(qn, qn, sq);
-          Qg[t * C::SLICE + x] = qn;
-        }
-      }
+      node_phase(ue, sd, sq);
       block_sum2(sd, sq);
       const double res = T.k1_opnorm * sqrt(sd);
       const double scale = 1.0 + sqrt(sq);
@@ -393,25 +411,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
       // quantity of one node per item: its P rates and P iterates loaded
       // up front)
       double sd = 0.0, sq = 0.0;
-      for (int x = tid; x < PD * M; x += NT) {
-        double r[P], qo[P];
-#pragma unroll
-        for (int s = 0; s < P; ++s) r[s] = Rg[s * C::SLICE + x];
-#pragma unroll
-        for (int t = 0; t < P; ++t) qo[t] = Qg[t * C::SLICE + x];
-        const double uu = ue[x];
-#pragma unroll
-        for (int t = 0; t < P; ++t) {
-          double cc = 0.0;
-#pragma unroll
-          for (int s = 0; s < P; ++s) cc = fma(T.gw[t * P + s], r[s], cc);
-          const double qn = cc * dt + T.g0[t] * uu;
-          const double dq = qo[t] - qn;
-          sd = fma(dq, dq, sd);
-          sq = fma(qn, qn, sq);
-          Qg[t * C::SLICE + x] = qn;
-        }
-      }
+      node_phase(ue, sd, sq);
       block_sum2(sd, sq);
       const double res = T.k1_opnorm * sqrt(sd);
       const double scale = 1.0 + sqrt(sq);
@@ -428,6 +428,8 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     // major order, Fbar_x in the thread's own scratch rows); then one
     // stiffness contraction per direction (corrector.py:169-176)
     bool ok = true;
+    constexpr int NPT = (PD + NT - 1) / NT;   // nodes per thread
+    double fbx[NPT][M];                        // Fbar_x of the thread's nodes
     __syncthreads();   // node-phase stores of the final iterate visible
     fetch(Qg);
 #pragma unroll 1
@@ -463,7 +465,10 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
         }
       }
       const double wt = T.weights[t];
-      for (int n = tid; n < PD; n += NT) {
+#pragma unroll
+      for (int kk = 0; kk < NPT; ++kk) {
+        const int n = tid + kk * NT;
+        if (n >= PD) break;
         const int i = n / PP, j = (n / P) % P, k = n % P;
         const double* qn = Q + i * SI + j * SJ + k * M;
         double q[M];
@@ -478,7 +483,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
         const int bx = j * TJ + k * TK + i * M;
         flux_axis<3>(q, gm1, 0, f);
 #pragma unroll
-        for (int v = 0; v < M; ++v) Rg[n * M + v] = t == 0 ? wt * f[v] : Rg[n * M + v] + wt * f[v];
+        for (int v = 0; v < M; ++v) fbx[kk][v] = t == 0 ? wt * f[v] : fbx[kk][v] + wt * f[v];
         flux_axis<3>(q, gm1, 1, f);
 #pragma unroll
         for (int v = 0; v < M; ++v) B1[bx + v] = t == 0 ? wt * f[v] : B1[bx + v] + wt * f[v];
@@ -491,10 +496,13 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     }
     // Fbar_x into Q (own nodes); the y / z owners contract Fbar_y / Fbar_z
     // in place (each reads and writes only its own line of B1 / B2)
-    for (int n = tid; n < PD; n += NT) {
+#pragma unroll
+    for (int kk = 0; kk < NPT; ++kk) {
+      const int n = tid + kk * NT;
+      if (n >= PD) break;
       const int i = n / PP, j = (n / P) % P, k = n % P;
 #pragma unroll
-      for (int v = 0; v < M; ++v) Q[i * SI + j * SJ + k * M + v] = Rg[n * M + v];
+      for (int v = 0; v < M; ++v) Q[i * SI + j * SJ + k * M + v] = fbx[kk][v];
     }
     __syncthreads();
     {
