@@ -32,6 +32,9 @@
 
 namespace adg {
 
+#ifndef ADG_STREAM_LUNROLL
+#define ADG_STREAM_LUNROLL 1
+#endif
 #ifndef ADG_STREAM_NH
 #define ADG_STREAM_NH 0   // 0: per-degree default below; 1 / 2: force
 #endif
@@ -75,9 +78,12 @@ struct StCfg {
   static constexpr int TB = PD * M + ((PD * M) & 1);   // trace block (face kernel layout)
   static constexpr size_t SLICE = (size_t)PD * M;      // doubles per time slice
   static constexpr size_t SCR = 2 * (size_t)P * SLICE; // q + rates per CTA (doubles)
-  // startup and sweeps through one slice-rate call site (fewer spills; measured
-  // faster at P = 8, 9, slower at P = 10)
-  static constexpr bool UNIFIED = P != 10;
+  // startup and sweeps through one slice-rate call site (fewer spills; C3
+  // N=9: 109 -> 81 ms/step); 0 keeps the two-site variant for A/B runs
+#ifndef ADG_STREAM_UNIFIED_ALL
+#define ADG_STREAM_UNIFIED_ALL 1
+#endif
+  static constexpr bool UNIFIED = ADG_STREAM_UNIFIED_ALL || P != 10;
 };
 
 struct StArgs {
@@ -111,9 +117,10 @@ __device__ __forceinline__ void st_line(const double* src0, int stride, double g
   for (int i = 0; i < H; ++i)
 #pragma unroll
     for (int v = 0; v < M; ++v) acc[i][v] = 0.0;
-  // l not unrolled: one source node's flux live at a time next to the
-  // accumulators
-#pragma unroll 1
+  // l unrolled by ADG_STREAM_LUNROLL (1: one source node's flux live at a
+  // time next to the accumulators)
+  constexpr int LU = ADG_STREAM_LUNROLL;
+#pragma unroll LU
   for (int l = 0; l < P; ++l) {
     double q[M], f[M];
     const double* src = src0 + l * stride;

@@ -249,12 +249,20 @@ def test_fused_subcell_reuse_is_bitwise(pkg):
     assert torch.equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("cluster", [False, True], ids=["stream", "cluster"])
 @pytest.mark.parametrize("n", [6, 7, 8, 9])
-def test_large_tile_predictor_matches_oracle(pkg, n):
-    """3-D N>=7 tiles run as a thread-block cluster (one time slice per CTA,
-    time operator over DSMEM): q, traces, volume and sweep counts against the
-    oracle's per-element Picard on seeded, anisotropic data (N=6 is the
-    single-CTA shared-memory kernel, for comparison)."""
+def test_large_tile_predictor_matches_oracle(pkg, n, cluster, monkeypatch):
+    """3-D N>=7 tiles run on the slice-streaming kernel (one CTA per element,
+    one time slice at a time in shared memory, q and rates in an L2-resident
+    scratch) or, with ADG_CLUSTER_PREDICTOR=1, on the thread-block cluster
+    kernel (one time slice per CTA, time operator over DSMEM): q, traces,
+    volume and sweep counts against the oracle's per-element Picard on
+    seeded, anisotropic data (N=6 is the single-CTA shared-memory kernel, for
+    comparison)."""
+    if cluster:
+        if n < 7:
+            pytest.skip("the cluster kernel covers N = 7..9")
+        monkeypatch.setenv("ADG_CLUSTER_PREDICTOR", "1")
     from oracle import dg
     from oracle.basis import oracle_tables
     from oracle.euler import EulerOracle
@@ -292,7 +300,7 @@ def test_large_tile_predictor_matches_oracle(pkg, n):
 @pytest.mark.parametrize("n", list(range(2, 10)))
 def test_c3_full_size_conservation_and_determinism(pkg, n):
     """C3 at its full 32^3 size for every degree (the single-CTA, lone-element
-    and cluster predictors): periodic totals conserved to 1e-11 relative and
+    and slice-streaming predictors): periodic totals conserved to 1e-11 relative and
     two runs bitwise identical (fixed-order reductions everywhere)."""
     mesh = pkg.CartesianMesh([(0, 1)] * 3, (32, 32, 32))
     system = pkg.make_system("euler", 3)
