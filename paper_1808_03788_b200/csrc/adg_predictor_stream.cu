@@ -67,7 +67,9 @@ struct StCfg {
   static constexpr int NG = 3 * NH;
   static constexpr int NT = NG * RP;
   static constexpr int NW = NT / 32;
-  static constexpr size_t SMEM = ((size_t)QSZP + 2 * (size_t)BSZP + 2 * NW + 2 * P + 2) * 8;
+  static constexpr int CSTP = (2 * P + 1) / 2 * 2;  // startup coefficients, padded to 16 B
+  // two slice buffers (the next slice lands while the current one is contracted)
+  static constexpr size_t SMEM = (2 * (size_t)QSZP + 2 * (size_t)BSZP + 2 * NW + CSTP) * 8;
   // CTAs per SM: what shared memory allows, capped so each thread keeps
   // >= 80 registers (H x m accumulators)
   static constexpr int MINB0 = (int)((228 * 1024) / (SMEM + 1024));
@@ -78,12 +80,6 @@ struct StCfg {
   static constexpr int TB = PD * M + ((PD * M) & 1);   // trace block (face kernel layout)
   static constexpr size_t SLICE = (size_t)PD * M;      // doubles per time slice
   static constexpr size_t SCR = 2 * (size_t)P * SLICE; // q + rates per CTA (doubles)
-  // startup and sweeps through one slice-rate call site (fewer spills; C3
-  // N=9: 109 -> 81 ms/step); 0 keeps the two-site variant for A/B runs
-#ifndef ADG_STREAM_UNIFIED_ALL
-#define ADG_STREAM_UNIFIED_ALL 1
-#endif
-  static constexpr bool UNIFIED = ADG_STREAM_UNIFIED_ALL || P != 10;
 };
 
 struct StArgs {
@@ -162,11 +158,13 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
   constexpr int SI = C::SI, SJ = C::SJ, TJ = C::TJ, TK = C::TK;
   const DegreeTables& T = tab<P>();
   extern __shared__ __align__(16) double smem[];
-  double* Q = smem;                 // slice tile, node-major (padded)
+  double* Q = smem;                 // current slice tile, node-major (padded)
   double* B1 = Q + C::QSZP;         // y partials (x-line-major, padded)
   double* B2 = B1 + C::BSZP;        // z partials (x-line-major)
   double* red = B2 + C::BSZP;       // [NW][2] warp partials
   double* cst = red + 2 * NW;       // startup coefficients [P] s_t = tau_t dt, [P] s_t^2 / (2 dt)
+  double* const Qa = Q;             // the two slice buffers; Q is the current one
+  double* const Qb = cst + C::CSTP;
   double* Qg = a.scr + (size_t)blockIdx.x * C::SCR;   // q[t][node][v]
   double* Rg = Qg + P * C::SLICE;                      // rate[t][node][v]; k1 at startup
 
@@ -224,16 +222,17 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
         for (int v = 0; v < M; ++v) pdst[pbase + (ibase + ii) * pstride + v] = acc[ii][v];
   };
   // a [node][v] slice (global) into the padded Q (asynchronous 8-byte copies)
-  auto fetch = [&](const double* src) {
+  auto fetch_to = [&](double* buf, const double* src) {
     // P^2 rows (i, j) of P m contiguous doubles; one warp per row
     for (int row = warp; row < PP; row += NW) {
       const int i = row / P, j = row - (row / P) * P;
-      double* dst = Q + i * SI + j * SJ;
+      double* dst = buf + i * SI + j * SJ;
       const double* sr = src + row * (P * M);
       for (int o = lane; o < P * M; o += 32) cp_async8(dst + o, sr + o);
     }
     cp_async_commit();
   };
+  auto fetch = [&](const double* src) { fetch_to(Q, src); };
   // fixed-order block sum of two partials (warp trees, warps in order)
   auto block_sum2 = [&](double& s1, double& s2) {
 #pragma unroll
@@ -257,16 +256,19 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
   };
 
   // rates of the slice in Q at the line owners' nodes -> rt ([node][v]);
-  // once every owner has read Q, the next slice (if any) is fetched into it
+  // the next slice (if any) is fetched into the other buffer meanwhile
   auto slice_rates = [&](const double* next, double* rt) {
     cp_async_wait_all();
     __syncthreads();
+    // the other buffer held the previous slice (its readers passed the
+    // barrier above): the next slice lands there during this contraction
+    double* const Qn = Q == Qa ? Qb : Qa;
+    if (next) fetch_to(Qn, next);
     double acc[H][M];
     bool dummy = true;
     if (owner) line_contract(0, acc, dummy);
     if (role == 1 || role == 2) publish(acc);
     __syncthreads();
-    if (next) fetch(next);   // Q is dead
     if (role == 0) {
 #pragma unroll
       for (int ii = 0; ii < H; ++ii) {
@@ -278,6 +280,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
           rt[n * M + v] = (-acc[ii][v] - B1[xrow + i * M + v]) - B2[xrow + i * M + v];
       }
     }
+    if (next) Q = Qn;
   };
 
   // time operator of the sweep (predictor.py:175-185) over the element's
@@ -320,7 +323,6 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     const double* ue = a.u + (size_t)e * PD * M;
     __syncthreads();   // previous element's readers of Q / B / red are done
     int it = 0, conv = 0, nsw = 0;
-    if constexpr (StCfg<P>::UNIFIED) {
     // ---------------- startup guess and Picard sweeps --------------------
     // one slice-rate call site for both (a second inlined copy spills):
     // stage 0 / 1 are the startup passes k1 = L(u), k2 = L(u + dt k1)
@@ -381,53 +383,6 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
       fetch(Qg);
     }
 
-    } else {
-    // ---------------- startup guess: k1 = L(u), k2 = L(u + dt k1) ---------
-    fetch(ue);
-#pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 1) {
-        // w = u + dt k1 in the tile (row-parallel, like fetch)
-        for (int row = warp; row < PP; row += NW) {
-          const int i = row / P, j = row - (row / P) * P;
-          double* dst = Q + i * SI + j * SJ;
-          const double* k1 = Rg + row * (P * M);
-          for (int o = lane; o < P * M; o += 32) dst[o] = dst[o] + dt * k1[o];
-        }
-      }
-      slice_rates(nullptr, Rg + pass * C::SLICE);   // k1 / k2
-      __syncthreads();   // stores of every x-owner visible
-    }
-    // q_t = u + s_t k1 + s_t^2 / (2 dt) (k2 - k1) at every time (predictor.py:116-124)
-    for (int x = tid; x < PD * M; x += NT) {
-      const double k1 = Rg[x], k2 = Rg[C::SLICE + x], un = ue[x];
-#pragma unroll 1
-      for (int t = 0; t < P; ++t) Qg[t * C::SLICE + x] = un + cst[t] * k1 + cst[P + t] * (k2 - k1);
-    }
-
-    // ---------------- Picard sweeps -----------------------------------
-    bool fz = false;
-    for (; it < a.max_iter && !fz; ++it) {
-      __syncthreads();   // startup / previous node phase stores visible
-      fetch(Qg);
-#pragma unroll 1
-      for (int t = 0; t < P; ++t)
-        slice_rates(t + 1 < P ? Qg + (t + 1) * C::SLICE : nullptr, Rg + t * C::SLICE);
-      __syncthreads();   // every slice's rates stored
-      // node phase: time operator, residual partials, q <- q_new (one
-      // quantity of one node per item: its P rates and P iterates loaded
-      // up front)
-      double sd = 0.0, sq = 0.0;
-      node_phase(ue, sd, sq);
-      block_sum2(sd, sq);
-      const double res = T.k1_opnorm * sqrt(sd);
-      const double scale = 1.0 + sqrt(sq);
-      conv = res <= a.tol * scale;
-      nsw = it + 1;
-      if (conv && it + 1 >= a.min_iter) fz = true;
-    }
-
-    }
     // ---------------- traces, admissibility, volume ---------------------
     // per slice: face traces (line owners), admissibility and the
     // time-weighted fluxes Fbar_dir = sum_t w_t F_dir(q_t) (corrector.py:166,
