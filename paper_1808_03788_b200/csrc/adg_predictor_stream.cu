@@ -69,11 +69,18 @@ struct StCfg {
   static constexpr int NW = NT / 32;
   static constexpr int CSTP = (2 * P + 1) / 2 * 2;  // startup coefficients, padded to 16 B
   // two slice buffers (the next slice lands while the current one is contracted)
-  static constexpr size_t SMEM = (2 * (size_t)QSZP + 2 * (size_t)BSZP + 2 * NW + CSTP) * 8;
+#ifndef ADG_STREAM_DBUF
+#define ADG_STREAM_DBUF 0   // 1: second slice buffer (measured neutral: C3 N=7..9 within 1 %)
+#endif
+  static constexpr int NQB = ADG_STREAM_DBUF ? 2 : 1;
+  static constexpr size_t SMEM = (NQB * (size_t)QSZP + 2 * (size_t)BSZP + 2 * NW + CSTP) * 8;
   // CTAs per SM: what shared memory allows, capped so each thread keeps
   // >= 80 registers (H x m accumulators)
   static constexpr int MINB0 = (int)((228 * 1024) / (SMEM + 1024));
-  static constexpr int RMIN = NH == 1 ? 168 : 80;
+#ifndef ADG_STREAM_RMIN
+#define ADG_STREAM_RMIN 168
+#endif
+  static constexpr int RMIN = NH == 1 ? ADG_STREAM_RMIN : 80;
   static constexpr int MINB_R = 65536 / (RMIN * NT) > 0 ? 65536 / (RMIN * NT) : 1;
   static constexpr int MINB1 = MINB0 < MINB_R ? MINB0 : MINB_R;
   static constexpr int MINB = MINB1 < 1 ? 1 : MINB1;
@@ -164,7 +171,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
   double* red = B2 + C::BSZP;       // [NW][2] warp partials
   double* cst = red + 2 * NW;       // startup coefficients [P] s_t = tau_t dt, [P] s_t^2 / (2 dt)
   double* const Qa = Q;             // the two slice buffers; Q is the current one
-  double* const Qb = cst + C::CSTP;
+  double* const Qb = C::NQB == 2 ? cst + C::CSTP : Qa;
   double* Qg = a.scr + (size_t)blockIdx.x * C::SCR;   // q[t][node][v]
   double* Rg = Qg + P * C::SLICE;                      // rate[t][node][v]; k1 at startup
 
@@ -263,12 +270,13 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     // the other buffer held the previous slice (its readers passed the
     // barrier above): the next slice lands there during this contraction
     double* const Qn = Q == Qa ? Qb : Qa;
-    if (next) fetch_to(Qn, next);
+    if (C::NQB == 2 && next) fetch_to(Qn, next);
     double acc[H][M];
     bool dummy = true;
     if (owner) line_contract(0, acc, dummy);
     if (role == 1 || role == 2) publish(acc);
     __syncthreads();
+    if (C::NQB == 1 && next) fetch_to(Q, next);   // single buffer: Q is dead now
     if (role == 0) {
 #pragma unroll
       for (int ii = 0; ii < H; ++ii) {
