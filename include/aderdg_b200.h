@@ -63,6 +63,9 @@ typedef struct adg_handle adg_handle;
  * (LinearAdvection, systems.py:77-109: nvars = 1, constant velocity) */
 #define ADG_SYS_EULER 0
 #define ADG_SYS_ADVECTION 1
+/* DiffuseInterfaceElasticity (systems.py:237-345): dim = 2, nvars = 9, a pure
+ * nonconservative product with path-conservative faces (corrector.py:65-129) */
+#define ADG_SYS_ELASTICITY 2
 
 typedef struct adg_grid {
   int32_t dim;

@@ -20,7 +20,7 @@ ADG_ERR_UNSUPPORTED = 4
 
 BC_CODES = {"periodic": 0, "outflow": 1, "wall": 2, "exact": 3, "ghost": 3}
 MODE_CODES = {"conservative": 0, "primitive": 1}   # adg_grid.mode (ADG_MODE_*)
-SYSTEM_CODES = {"euler": 0, "advection": 1}        # adg_grid.system (ADG_SYS_*)
+SYSTEM_CODES = {"euler": 0, "advection": 1, "elasticity-di": 2}        # adg_grid.system (ADG_SYS_*)
 
 
 def fill_system(g, system):

@@ -70,6 +70,12 @@ static int check_grid(adg_handle* h, const adg_grid* g) {
     if (g->nvars != 1) return fail(h, ADG_ERR_INVALID, "advection has m = 1");
     if (g->mode != ADG_MODE_CONSERVATIVE)
       return fail(h, ADG_ERR_UNSUPPORTED, "advection on the device: conservative predictor only");
+  } else if (g->system == ADG_SYS_ELASTICITY) {
+    if (g->dim != 2) return fail(h, ADG_ERR_INVALID, "elasticity-di is 2-D");
+    if (g->nvars != 9) return fail(h, ADG_ERR_INVALID, "elasticity-di has m = 9");
+    if (g->mode != ADG_MODE_CONSERVATIVE)
+      return fail(h, ADG_ERR_UNSUPPORTED,
+                  "elasticity-di on the device: conservative predictor only");
   } else if (g->system != ADG_SYS_EULER) {
     return fail(h, ADG_ERR_UNSUPPORTED, "unknown system");
   } else if (g->nvars != g->dim + 2) {
@@ -87,14 +93,16 @@ static int check_grid(adg_handle* h, const adg_grid* g) {
 }
 
 static bool is_adv(const adg_grid* g) { return g && g->system == ADG_SYS_ADVECTION; }
+static bool is_el(const adg_grid* g) { return g && g->system == ADG_SYS_ELASTICITY; }
 
 // entry points with Euler kernels only (limiter, module-level pieces)
 static int check_euler(adg_handle* h, const adg_grid* g) {
   int rc = check_grid(h, g);
   if (rc) return rc;
-  if (is_adv(g))
+  if (is_adv(g) || is_el(g))
     return fail(h, ADG_ERR_UNSUPPORTED,
-                "advection on the device: the limiter and the module-level pieces are Euler only");
+                "advection / elasticity-di on the device: the limiter and the module-level "
+                "pieces are Euler only");
   return ADG_OK;
 }
 
@@ -144,6 +152,8 @@ int adg_wavespeed(adg_handle* h, const adg_grid* g, const double* u, adg_reduce*
   std::string e;
   if (is_adv(g))
     return wrap(h, adg::adv_state_reduce(g, u, red, nullptr, (cudaStream_t)stream, &e), e);
+  if (is_el(g))
+    return wrap(h, adg::el_state_reduce(g, u, red, nullptr, (cudaStream_t)stream, &e), e);
   return wrap(h, adg::state_reduce(g, u, red, nullptr, (cudaStream_t)stream, &e), e);
 }
 
@@ -185,6 +195,10 @@ int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double*
     return wrap(h, adg::adv_predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out,
                                     traces, pred_bad, sweeps, (cudaStream_t)stream,
                                     h->num_sms, &e), e);
+  if (is_el(g))
+    return wrap(h, adg::el_predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out,
+                                   traces, pred_bad, sweeps, (cudaStream_t)stream,
+                                   h->num_sms, &e), e);
   return wrap(h, adg::predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out, traces,
                               pred_bad, sweeps, (cudaStream_t)stream, h->num_sms, h->ws,
                               h->ws_bytes, &e), e);
@@ -199,6 +213,9 @@ int adg_face_flux(adg_handle* h, const adg_grid* g, int axis, const double* trac
   if (is_adv(g))
     return wrap(h, adg::adv_face_flux(g, axis, traces, ghost_lo, ghost_hi, dbar_out,
                                       (cudaStream_t)stream, &e), e);
+  if (is_el(g))
+    return wrap(h, adg::el_face_flux(g, axis, traces, ghost_lo, ghost_hi, dbar_out,
+                                     (cudaStream_t)stream, &e), e);
   return wrap(h, adg::face_flux(g, axis, traces, ghost_lo, ghost_hi, dbar_out,
                                 (cudaStream_t)stream, &e), e);
 }
@@ -208,7 +225,8 @@ int64_t adg_update_blocks(const adg_grid* g) { return adg::update_blocks(g); }
 int64_t adg_trace_block(const adg_grid* g) {
   int64_t pd = 1;
   for (int j = 0; j < g->dim; ++j) pd *= g->degree + 1;
-  const int64_t b = pd * (g->system == ADG_SYS_ADVECTION ? 1 : g->dim + 2);
+  const int64_t b = pd * (g->system == ADG_SYS_ADVECTION ? 1
+                          : (g->system == ADG_SYS_ELASTICITY ? 9 : g->dim + 2));
   return b + (b & 1);
 }
 
@@ -221,6 +239,9 @@ int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* 
   if (is_adv(g))
     return wrap(h, adg::adv_update(g, u, vol, fd, dt_dev, u_out, red_next, totals_partial,
                                    (cudaStream_t)stream, &e), e);
+  if (is_el(g))
+    return wrap(h, adg::el_update(g, u, vol, fd, dt_dev, u_out, red_next, totals_partial,
+                                  (cudaStream_t)stream, &e), e);
   return wrap(h, adg::update(g, u, vol, fd, dt_dev, u_out, red_next, totals_partial,
                              (cudaStream_t)stream, &e), e);
 }
@@ -239,8 +260,9 @@ int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partia
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
-  rc = is_adv(g) ? adg::adv_state_reduce(g, u, nullptr, partial, (cudaStream_t)stream, &e)
-                 : adg::state_reduce(g, u, nullptr, partial, (cudaStream_t)stream, &e);
+  rc = is_adv(g)  ? adg::adv_state_reduce(g, u, nullptr, partial, (cudaStream_t)stream, &e)
+       : is_el(g) ? adg::el_state_reduce(g, u, nullptr, partial, (cudaStream_t)stream, &e)
+                  : adg::state_reduce(g, u, nullptr, partial, (cudaStream_t)stream, &e);
   if (rc) return wrap(h, rc, e);
   return wrap(h, adg::totals_finalize(g, partial, adg::reduce_blocks(g), totals_out,
                                       (cudaStream_t)stream, &e), e);

@@ -728,6 +728,10 @@ int totals_finalize(const adg_grid* g, const double* partial, int64_t nb, double
     totals_finalize_kernel<1><<<1, 1024, 0, st>>>(partial, nb, cv, out);
     return check_launch(err);
   }
+  if (g->nvars == 9) {   // elasticity-di
+    totals_finalize_kernel<9><<<1, 1024, 0, st>>>(partial, nb, cv, out);
+    return check_launch(err);
+  }
   switch (g->dim) {
     case 1: totals_finalize_kernel<3><<<1, 1024, 0, st>>>(partial, nb, cv, out); break;
     case 2: totals_finalize_kernel<4><<<1, 1024, 0, st>>>(partial, nb, cv, out); break;

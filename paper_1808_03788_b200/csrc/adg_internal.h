@@ -49,6 +49,19 @@ int adv_update(const adg_grid* g, const double* u, const double* vol, const doub
 int adv_state_reduce(const adg_grid* g, const double* u, adg_reduce* red, double* partial,
                      cudaStream_t st, std::string* err);
 
+// diffuse-interface elasticity, 2-D (adg_elasticity.cu)
+int el_predict(const adg_grid* g, const double* u, const double* dt_dev, double tol,
+               int max_iter, int min_iter, double* q_out, double* vol, double* traces,
+               uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms,
+               std::string* err);
+int el_face_flux(const adg_grid* g, int axis, const double* traces, const double* ghost_lo,
+                 const double* ghost_hi, double* fd, cudaStream_t st, std::string* err);
+int el_update(const adg_grid* g, const double* u, const double* vol, const double* fd,
+              const double* dt_dev, double* u_out, adg_reduce* red_next, double* partial,
+              cudaStream_t st, std::string* err);
+int el_state_reduce(const adg_grid* g, const double* u, adg_reduce* red, double* partial,
+                    cudaStream_t st, std::string* err);
+
 int state_reduce(const adg_grid* g, const double* u, adg_reduce* red, double* partial,
                  cudaStream_t st, std::string* err);
 int timestep(const adg_grid* g, const adg_reduce* red, double cfl, const double* t_dev,

@@ -121,22 +121,25 @@ class Simulation:
                 f"cfl must lie in (0, {max_cfl_number(degree)}) "
                 f"for degree {degree}, got {cfl}")
         name = getattr(system, "name", None)
-        if name not in ("euler", "advection"):
+        if name not in ("euler", "advection", "elasticity-di"):
             raise NotImplementedError(
                 f"system '{getattr(system, 'name', system)}' has no B200 kernels "
-                "(euler, advection)")
+                "(euler, advection, elasticity-di)")
         if predictor_mode not in ("conservative", "primitive"):
             raise ValueError(f"unknown predictor mode {predictor_mode!r}")
-        if name == "advection":
-            # the advection kernels cover the unlimited conservative step with
-            # periodic / outflow / wall faces
+        if name in ("advection", "elasticity-di"):
+            # the advection / elasticity kernels cover the unlimited
+            # conservative step with periodic / outflow / wall faces (SURVEY.md
+            # §8(f) rank 4)
             if use_limiter:
-                raise NotImplementedError("advection on the device: no subcell limiter")
+                raise NotImplementedError(f"{name} on the device: no subcell limiter")
             if predictor_mode != "conservative":
-                raise NotImplementedError("advection on the device: conservative predictor")
+                raise NotImplementedError(f"{name} on the device: conservative predictor")
             kinds = normalize_boundary(boundary, mesh.dim).values()
             if "exact" in kinds:
-                raise NotImplementedError("advection on the device: no exact faces")
+                raise NotImplementedError(f"{name} on the device: no exact faces")
+            if name == "elasticity-di" and degree > 5:
+                raise NotImplementedError("elasticity-di on the device: degree <= 5")
         self.mesh = mesh
         self.system = system
         self.tables = basis_tables(degree)

@@ -157,7 +157,9 @@ def step_function(system, position=0.5, left=1.0, right=0.0):
 def constant_state(system, values=None):
     """problems.py:176-192."""
     if values is None:
-        values = [0.75] if system.name == "advection" else [1.0] + [0.1] * system.dim + [2.5]
+        values = {"advection": [0.75],
+                  "elasticity-di": [0.3, 0.2, 0.1, 0.05, -0.04, 0.7, 2.0, 1.0, 1.0]}.get(
+                      system.name, [1.0] + [0.1] * system.dim + [2.5])
     q0 = np.asarray(values, float)
     if q0.shape != (system.n_vars,):
         raise ValueError(f"constant state needs {system.n_vars} entries")
@@ -166,6 +168,37 @@ def constant_state(system, values=None):
         return np.broadcast_to(q0, points.shape[:-1] + q0.shape).copy()
 
     return (lambda points: exact(points, 0.0)), exact
+
+
+def elastic_pwave(system, alpha_min=1e-3, interface=0.7, pulse_center=0.3,
+                  pulse_width=0.05, amplitude=1e-3, lam=2.0, mu=1.0, rho=1.0,
+                  interface_width=0.05):
+    """problems.py:135-173: a right-moving plane P-wave pulse in solid
+    (alpha = 1) running toward a tanh ramp to alpha_min (the free surface)."""
+    if system.name != "elasticity-di":
+        raise ValueError("the P-wave case needs the diffuse-interface system")
+    if interface_width <= 0.0:
+        raise ValueError("interface_width must be positive")
+    cp = np.sqrt((lam + 2.0 * mu) / rho)
+
+    def exact(points, t):
+        x = points[..., 0]
+        vx = amplitude * np.exp(-((x - pulse_center - cp * t) / pulse_width) ** 2)
+        sxx = -rho * cp * vx
+        syy = lam / (lam + 2.0 * mu) * sxx
+        ramp = 0.5 * (1.0 - np.tanh((x - interface) / interface_width))
+        alpha = alpha_min + (1.0 - alpha_min) * ramp
+        out = np.zeros(points.shape[:-1] + (9,))
+        out[..., 0] = sxx
+        out[..., 1] = syy
+        out[..., 3] = alpha * vx
+        out[..., 5] = alpha
+        out[..., 6] = lam
+        out[..., 7] = mu
+        out[..., 8] = rho
+        return out
+
+    return (lambda points: exact(points, 0.0)), None
 
 
 class ProblemSpec:
@@ -187,6 +220,8 @@ PROBLEMS = {
     "pulse": ProblemSpec(gaussian_pulse, None, None, {0: ("exact", "outflow")}, 0.5,
                          system="advection"),
     "step": ProblemSpec(step_function, None, None, "periodic", 0.5, system="advection"),
+    "pwave": ProblemSpec(elastic_pwave, 2, ((0.0, 1.0), (0.0, 0.25)), "outflow", 0.15,
+                         system="elasticity-di"),
     "density_wave": ProblemSpec(density_wave, None, None, "periodic", 1.0),
     "explosion": ProblemSpec(circular_explosion, 2, ((-1.0, 1.0), (-1.0, 1.0)), "outflow",
                              0.25),

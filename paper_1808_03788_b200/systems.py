@@ -138,15 +138,72 @@ class LinearAdvection(HyperbolicSystem):
         return q.copy() if _xp(q) is np else q.clone()
 
 
-_SYSTEMS = {"euler": CompressibleEuler, "advection": LinearAdvection}
+ALPHA_FLOOR = 1e-3   # systems.py:13
+
+
+class DiffuseInterfaceElasticity(HyperbolicSystem):
+    """2-D linear elasticity with a diffuse solid boundary (systems.py:237-345):
+    state (sxx, syy, sxy, avx, avy, alpha, lam, mu, rho), a pure
+    nonconservative product B(q).grad q, wave speeds c_p / c_s from the
+    material constants.  Device kernels in csrc/adg_elasticity.cu (predictor
+    with rate -ncp(q, grad q), path-conservative faces, update)."""
+
+    name = "elasticity-di"
+    has_flux = False
+    has_ncp = True
+    SXX, SYY, SXY, AVX, AVY, ALPHA, LAM, MU, RHO = range(9)
+    # alpha and the material constants obey d/dt = 0: no jump dissipation
+    diss_mask = np.array([1.0, 1.0, 1.0, 1.0, 1.0, 0.0, 0.0, 0.0, 0.0])
+
+    def __init__(self, dim=2):
+        if dim != 2:
+            raise ValueError("the diffuse-interface elasticity system is 2-D")
+        super().__init__(2, 9, ("sxx", "syy", "sxy", "avx", "avy", "alpha", "lam", "mu", "rho"))
+
+    def max_abs_eigenvalue(self, q, normal):
+        xp = _xp(q)
+        return xp.sqrt((q[..., self.LAM] + 2.0 * q[..., self.MU]) / q[..., self.RHO])
+
+    def eigenvalues(self, q, normal):
+        c_p = np.sqrt((q[..., self.LAM] + 2.0 * q[..., self.MU]) / q[..., self.RHO])
+        c_s = np.sqrt(q[..., self.MU] / q[..., self.RHO])
+        out = np.zeros(q.shape[:-1] + (9,))
+        out[..., 0] = -c_p
+        out[..., 1] = -c_s
+        out[..., 7] = c_s
+        out[..., 8] = c_p
+        return out
+
+    def admissible(self, q):
+        xp = _xp(q)
+        if xp is np:
+            return np.all(np.isfinite(q), axis=-1)
+        return xp.isfinite(q).all(dim=-1)
+
+    def cons_to_prim(self, q):
+        return q
+
+    def prim_to_cons(self, v):
+        return v
+
+    def reflect(self, q, axis):
+        out = q.copy() if _xp(q) is np else q.clone()
+        if axis == 0:
+            out[..., self.SXX] = -q[..., self.SXX]
+            out[..., self.SXY] = -q[..., self.SXY]
+        else:
+            out[..., self.SYY] = -q[..., self.SYY]
+            out[..., self.SXY] = -q[..., self.SXY]
+        return out
+
+
+_SYSTEMS = {"euler": CompressibleEuler, "advection": LinearAdvection,
+            "elasticity-di": DiffuseInterfaceElasticity}
 
 
 def make_system(name, dim, **params):
-    """Registered systems (systems.py:355-361).  Euler and advection have a
-    B200 path; 'elasticity-di' (the NCP machinery) raises NotImplementedError
-    (SURVEY §8(f) rank 4)."""
-    if name == "elasticity-di":
-        raise NotImplementedError(f"system '{name}' has no B200 kernels (euler, advection)")
+    """Registered systems (systems.py:355-361): Euler, advection and the 2-D
+    diffuse-interface elasticity all have a B200 path."""
     try:
         cls = _SYSTEMS[name]
     except KeyError:

@@ -314,9 +314,33 @@ def gen_advection():
          boundary="wall")
 
 
+def gen_elasticity():
+    """DiffuseInterfaceElasticity plugin (systems.py:237-345): the registry's
+    P-wave toward the diffuse free surface (problems.py:135-173) with
+    outflow and wall faces, and a periodic constant state (problems.py:
+    176-192), degrees 2..5 (the NCP /
+    path-conservative machinery of corrector.py:65-129)."""
+    from aderdg.systems import DiffuseInterfaceElasticity
+
+    sysd = DiffuseInterfaceElasticity(2)
+
+    def case(name, cells, degree, prob, steps, boundary, ext=((0.0, 1.0), (0.0, 0.25))):
+        ic, _ = aderdg.build_problem(prob, sysd)
+        cfl = 0.9 / (2 * (2 * degree + 1))
+        run_case(name, aderdg.CartesianMesh([tuple(e) for e in ext], cells), sysd, degree, cfl,
+                 ic, steps, boundary=boundary)
+
+    case("el_pwave", (16, 4), 3, "pwave", 8, "outflow")
+    case("el_pwave_N5", (8, 2), 5, "pwave", 4, "outflow")
+    case("el_pwave_wall", (12, 3), 2, "pwave", 6, "wall")
+    case("el_constant", (4, 4), 3, "constant", 3, "periodic", ext=((0.0, 1.0), (0.0, 1.0)))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tables", "pointwise", "predictor", "cases", "primitive", "output",
-                             "exact", "advection"]
+                             "exact", "advection", "elasticity"]
+    if "elasticity" in which:
+        gen_elasticity()
     if "advection" in which:
         gen_advection()
     if "tables" in which:

@@ -151,8 +151,14 @@ def test_simulation_argument_errors_precede_device_use():
         Simulation(mesh, e2, 3, 0.05, boundary="exact")
     with pytest.raises(ValueError):
         Simulation(mesh, e2, 3, 0.05, predictor_mode="characteristic")
+    with pytest.raises(ValueError):
+        make_system("elasticity-di", 3)               # the system is 2-D
+    el = make_system("elasticity-di", 2)
+    assert (el.n_vars, el.has_ncp, el.has_flux) == (9, True, False)
     with pytest.raises(NotImplementedError):
-        make_system("elasticity-di", 2)
+        Simulation(mesh, el, 3, 0.05, use_limiter=True)
+    with pytest.raises(NotImplementedError):
+        Simulation(mesh, el, 6, 0.05)                 # device kernels to N = 5
     adv = make_system("advection", 2, velocity=[1.0, 0.5])
     with pytest.raises(NotImplementedError):
         Simulation(mesh, adv, 3, 0.05, use_limiter=True)
