@@ -121,6 +121,14 @@ int adg_timestep(adg_handle* h, const adg_grid* g, const adg_reduce* red, double
 int adg_advance_time(adg_handle* h, double* t_dev, const double* dt_dev, double* t_out,
                      void* stream);
 
+/* History bookkeeping of a device-resident batch (driver.py:344-350 rows):
+ * rows[*cnt] = row[0:ncols], status[*cnt] = *status_in, sweeps[*cnt] =
+ * max(elem_sweeps[0:n_elem]), then *cnt += 1.  One launch instead of a
+ * reduction and three indexed copies per step in the replayed CUDA graph. */
+int adg_log_step(adg_handle* h, const double* row, int64_t ncols, const int32_t* status_in,
+                 const int32_t* elem_sweeps, int64_t n_elem, double* rows, int32_t* status,
+                 int32_t* sweeps, int64_t* cnt, void* stream);
+
 /* -- predictor: startup_guess + picard_solve + extract_traces + the
  *    corrector's volume_integral, fused per element
  *    (predictor.py:99-191, :218-230; corrector.py:141-177) -------------- */

@@ -41,7 +41,7 @@ EXPORTS = (
     "adg_update_blocks", "adg_trace_block", "adg_totals_finalize", "adg_totals", "adg_project_subcells",
     "adg_detect", "adg_rescue", "adg_flatten_ic", "adg_face_fluxes", "adg_volume_integral",
     "adg_face_integral", "adg_element_update", "adg_muscl_windows", "adg_recover_subcells",
-    "adg_flatten_cells",
+    "adg_flatten_cells", "adg_log_step",
 )
 
 
@@ -81,6 +81,7 @@ _SIGS = {
     "adg_wavespeed": (_I, [_P, _P, _P, _P, _P]),
     "adg_timestep": (_I, [_P, _P, _P, _D, _P, _D, _P, _P, _P]),
     "adg_advance_time": (_I, [_P, _P, _P, _P, _P]),
+    "adg_log_step": (_I, [_P, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "adg_predict": (_I, [_P, _P, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P]),
     "adg_face_flux": (_I, [_P, _P, _I, _P, _P, _P, _P, _P]),
     "adg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -176,6 +176,17 @@ int adg_advance_time(adg_handle* h, double* t_dev, const double* dt_dev, double*
   return wrap(h, adg::advance_time(t_dev, dt_dev, t_out, (cudaStream_t)stream, &e), e);
 }
 
+int adg_log_step(adg_handle* h, const double* row, int64_t ncols, const int32_t* status_in,
+                 const int32_t* elem_sweeps, int64_t n_elem, double* rows, int32_t* status,
+                 int32_t* sweeps, int64_t* cnt, void* stream) {
+  if (!h || !row || !status_in || !elem_sweeps || !rows || !status || !sweeps || !cnt ||
+      ncols < 0 || n_elem < 1)
+    return fail(h, ADG_ERR_INVALID, "adg_log_step: bad arguments");
+  std::string e;
+  return wrap(h, adg::log_step(row, ncols, status_in, elem_sweeps, n_elem, rows, status, sweeps,
+                               cnt, (cudaStream_t)stream, &e), e);
+}
+
 int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double* dt_dev,
                 double tol, int max_iter, int min_iter, double* q_out, double* vol_out,
                 double* traces, uint8_t* pred_bad, int32_t* sweeps, void* stream) {

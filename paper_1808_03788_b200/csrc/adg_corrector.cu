@@ -187,6 +187,31 @@ __global__ void timestep_kernel(const adg_reduce* red, int dim, double dx0, doub
   if (status) *status |= st;
 }
 
+// batch history row (adg_log_step): max element sweep count (warp trees,
+// warps in order), then the slot *cnt of the row / status / sweep logs
+__global__ void __launch_bounds__(256)
+log_step_kernel(const double* __restrict__ row, int64_t ncols, const int32_t* status_in,
+                const int32_t* __restrict__ elem_sweeps, int64_t n_elem, double* rows,
+                int32_t* status, int32_t* sweeps, int64_t* cnt) {
+  __shared__ int s_max[8];
+  int m = 0;
+  for (int64_t e = threadIdx.x; e < n_elem; e += 256) m = max(m, elem_sweeps[e]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = m;
+  __syncthreads();
+  const int64_t c = *cnt;
+  for (int64_t j = threadIdx.x; j < ncols; j += 256) rows[c * ncols + j] = row[j];
+  if (threadIdx.x == 0) {
+    int mm = s_max[0];
+    for (int w = 1; w < 8; ++w) mm = max(mm, s_max[w]);
+    sweeps[c] = mm;
+    status[c] = *status_in;
+  }
+  __syncthreads();   // every thread has read *cnt
+  if (threadIdx.x == 0) *cnt = c + 1;
+}
+
 __global__ void advance_time_kernel(double* t, const double* dt, double* t_out) {
   const double tn = *t + *dt;
   *t = tn;
@@ -652,6 +677,14 @@ int timestep(const adg_grid* g, const adg_reduce* red, double cfl, const double*
 int advance_time(double* t_dev, const double* dt_dev, double* t_out, cudaStream_t st,
                  std::string* err) {
   advance_time_kernel<<<1, 1, 0, st>>>(t_dev, dt_dev, t_out);
+  return check_launch(err);
+}
+
+int log_step(const double* row, int64_t ncols, const int32_t* status_in,
+             const int32_t* elem_sweeps, int64_t n_elem, double* rows, int32_t* status,
+             int32_t* sweeps, int64_t* cnt, cudaStream_t st, std::string* err) {
+  log_step_kernel<<<1, 256, 0, st>>>(row, ncols, status_in, elem_sweeps, n_elem, rows, status,
+                                     sweeps, cnt);
   return check_launch(err);
 }
 

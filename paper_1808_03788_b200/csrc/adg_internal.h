@@ -66,6 +66,9 @@ int state_reduce(const adg_grid* g, const double* u, adg_reduce* red, double* pa
                  cudaStream_t st, std::string* err);
 int timestep(const adg_grid* g, const adg_reduce* red, double cfl, const double* t_dev,
              double t_end, double* dt_dev, int32_t* status, cudaStream_t st, std::string* err);
+int log_step(const double* row, int64_t ncols, const int32_t* status_in,
+             const int32_t* elem_sweeps, int64_t n_elem, double* rows, int32_t* status,
+             int32_t* sweeps, int64_t* cnt, cudaStream_t st, std::string* err);
 int advance_time(double* t_dev, const double* dt_dev, double* t_out, cudaStream_t st,
                  std::string* err);
 int face_flux(const adg_grid* g, int axis, const double* traces, const double* ghost_lo,

@@ -573,13 +573,17 @@ class Simulation:
             return g
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
+        ncols = bb["rows"].shape[1]
         with torch.cuda.graph(g):
             for j in range(2):
-                self._step_into(bb["srow"], bb["sst"], bb["ssw"], j)
-                bb["rows"].index_copy_(0, bb["cnt"], bb["srow"][j:j + 1])
-                bb["status"].index_copy_(0, bb["cnt"], bb["sst"][j:j + 1])
-                bb["sweeps"].index_copy_(0, bb["cnt"], bb["ssw"][j:j + 1])
-                bb["cnt"].add_(1)
+                srow, sst = bb["srow"][j], bb["sst"][j:j + 1]
+                self._timestep_into(srow[0:1], sst, math.inf)
+                self._enqueue_unlimited(srow[0:1], srow[2:], srow[1:2])
+                # history row, status and max sweep count into slot cnt
+                self._h.call("adg_log_step", _ptr(srow), ncols, _ptr(sst),
+                             _ptr(self._buf.sweeps), self.mesh.n_elements, _ptr(bb["rows"]),
+                             _ptr(bb["status"]), _ptr(bb["sweeps"]), _ptr(bb["cnt"]),
+                             _stream_ptr())
         # capture only recorded the launches: state is back where it started
         bb["graphs"][key] = g
         return g
