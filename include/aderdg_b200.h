@@ -147,6 +147,22 @@ int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double*
                 double tol, int max_iter, int min_iter, double* q_out, double* vol_out,
                 double* traces, uint8_t* pred_bad, int32_t* sweeps, void* stream);
 
+/* -- the same predictor on the element range [e_begin, e_begin + e_count)
+ *    of the grid (element order = the reference's C order of `u`).  u,
+ *    vol_out, traces, pred_bad, sweeps (and q_out) are the WHOLE grid's
+ *    arrays; only the range's entries are written.  Results are bitwise
+ *    those of adg_predict (per-element arithmetic).  Used by the slab
+ *    decomposition to predict the two boundary layers first and overlap
+ *    their halo exchange with the interior (no reference counterpart: the
+ *    reference is single-process).  ADG_ERR_UNSUPPORTED unless
+ *    adg_predict_range_supported(g) (3-D N >= 7 conservative grids run the
+ *    slice-streaming kernel, which takes the whole grid). */
+int adg_predict_range(adg_handle* h, const adg_grid* g, int64_t e_begin, int64_t e_count,
+                      const double* u, const double* dt_dev, double tol, int max_iter,
+                      int min_iter, double* q_out, double* vol_out, double* traces,
+                      uint8_t* pred_bad, int32_t* sweeps, void* stream);
+int adg_predict_range_supported(const adg_grid* g);
+
 /* -- face coupling along one axis: driver._face_states (driver.py:234-261)
  *    + corrector.face_fluxes (corrector.py:100-129) + the time weighting of
  *    face_integral (corrector.py:186) ------------------------------------ */

@@ -41,7 +41,7 @@ EXPORTS = (
     "adg_update_blocks", "adg_trace_block", "adg_totals_finalize", "adg_totals", "adg_project_subcells",
     "adg_detect", "adg_rescue", "adg_flatten_ic", "adg_face_fluxes", "adg_volume_integral",
     "adg_face_integral", "adg_element_update", "adg_muscl_windows", "adg_recover_subcells",
-    "adg_flatten_cells", "adg_log_step",
+    "adg_flatten_cells", "adg_log_step", "adg_predict_range", "adg_predict_range_supported",
 )
 
 
@@ -83,6 +83,8 @@ _SIGS = {
     "adg_advance_time": (_I, [_P, _P, _P, _P, _P]),
     "adg_log_step": (_I, [_P, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "adg_predict": (_I, [_P, _P, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "adg_predict_range": (_I, [_P, _P, _I64, _I64, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "adg_predict_range_supported": (_I, [_P]),
     "adg_face_flux": (_I, [_P, _P, _I, _P, _P, _P, _P, _P]),
     "adg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "adg_update_blocks": (_I64, [_P]),

@@ -215,6 +215,33 @@ int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double*
                               h->ws_bytes, &e), e);
 }
 
+int adg_predict_range_supported(const adg_grid* g) {
+  return g && !is_adv(g) && !is_el(g) && adg::predict_range_supported(g) ? 1 : 0;
+}
+
+int adg_predict_range(adg_handle* h, const adg_grid* g, int64_t e_begin, int64_t e_count,
+                      const double* u, const double* dt_dev, double tol, int max_iter,
+                      int min_iter, double* q_out, double* vol_out, double* traces,
+                      uint8_t* pred_bad, int32_t* sweeps, void* stream) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (!adg_predict_range_supported(g))
+    return fail(h, ADG_ERR_UNSUPPORTED, "adg_predict_range: grid runs a whole-grid predictor");
+  const size_t need = adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms);
+  if (need > h->ws_bytes) {
+    if (h->ws) cudaFree(h->ws);
+    h->ws = nullptr;
+    h->ws_bytes = 0;
+    if (cudaMalloc(&h->ws, need) != cudaSuccess)
+      return fail(h, ADG_ERR_CUDA, "cannot allocate predictor workspace");
+    h->ws_bytes = need;
+  }
+  std::string e;
+  return wrap(h, adg::predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out, traces,
+                              pred_bad, sweeps, (cudaStream_t)stream, h->num_sms, h->ws,
+                              h->ws_bytes, &e, e_begin, e_count), e);
+}
+
 int adg_face_flux(adg_handle* h, const adg_grid* g, int axis, const double* traces,
                   const double* ghost_lo, const double* ghost_hi, double* dbar_out,
                   void* stream) {

@@ -22,7 +22,9 @@ size_t predict_workspace_bytes(int dim, int P, int num_sms);
 int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol, int max_iter,
             int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
             int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
-            std::string* err);
+            std::string* err, int64_t e_begin = 0, int64_t e_count = -1);
+// element ranges run on the shared-tile predictor only
+bool predict_range_supported(const adg_grid* g);
 
 bool predict_stream_supported(const adg_grid* g);
 size_t predict_stream_workspace_bytes(int P, int num_sms);

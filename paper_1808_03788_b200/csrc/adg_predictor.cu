@@ -161,7 +161,8 @@ struct PredArgs {
   uint8_t* pred_bad;
   int32_t* sweeps;
   double* ws;          // global tile workspace (large-tile variant)
-  int64_t n_elem;
+  int64_t n_elem;      // elements this launch processes (u, vol, traces offset to the first)
+  int64_t tr_elems;    // elements per face plane of the trace arrays (the whole grid)
   double dx[3];
   double gamma;
   double tol;
@@ -902,7 +903,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       // offset item*m (x: [j][k][t], y: [k][t][i], z: [t][i][j])
       // element trace blocks padded to a 16-byte multiple (TMA in the face kernel)
       constexpr int TB = C::TB;
-      const size_t face_stride = (size_t)a.n_elem * TB;
+      const size_t face_stride = (size_t)a.tr_elems * TB;
       const size_t eoff = (size_t)e * TB + (size_t)item * M;
       double* stage = B1 + C::ST_OFF;
 #pragma unroll
@@ -954,7 +955,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     }
     __syncthreads();
     if (C::TR_STAGE && tid < EPB && valid_e[tid]) {
-      const size_t face_stride = (size_t)a.n_elem * C::TB;
+      const size_t face_stride = (size_t)a.tr_elems * C::TB;
       const double* st = tiles + tid * C::ELEM + TP + C::ST_OFF;
       double* dst = a.traces + (size_t)(g * EPB + tid) * C::TB;
 #pragma unroll
@@ -1121,10 +1122,27 @@ size_t predict_workspace_bytes(int dim, int P, int num_sms) {
   return 0;
 }
 
+bool predict_range_supported(const adg_grid* g) {
+  return !(predict_stream_supported(g) || getenv("ADG_CLUSTER_PREDICTOR") ||
+           predict_cluster_supported(g));
+}
+
 int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol, int max_iter,
             int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
             int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
-            std::string* err) {
+            std::string* err, int64_t e_begin, int64_t e_count) {
+  const int64_t n_all =
+      g->cells[0] * (g->dim >= 2 ? g->cells[1] : 1) * (g->dim == 3 ? g->cells[2] : 1);
+  if (e_count < 0) e_count = n_all - e_begin;
+  if (e_begin < 0 || e_begin + e_count > n_all) {
+    *err = "element range outside the grid";
+    return ADG_ERR_INVALID;
+  }
+  const bool whole = e_begin == 0 && e_count == n_all;
+  if (!whole && !predict_range_supported(g)) {
+    *err = "element ranges need the shared-tile predictor (not the 3-D N>=7 stream/cluster kernels)";
+    return ADG_ERR_UNSUPPORTED;
+  }
   // 3-D tiles beyond one SM's shared memory: one CTA per element streaming
   // time slices through shared memory (adg_predictor_stream.cu)
   if (!getenv("ADG_CLUSTER_PREDICTOR") && predict_stream_supported(g))
@@ -1137,16 +1155,27 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
     return predict_cluster(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
                            sweeps, st, num_sms, err);
 #endif
+  // an element range [e_begin, e_begin + e_count) is the same launch on
+  // pointers advanced to its first element; only the trace planes keep the
+  // whole grid's stride (the slab decomposition predicts its boundary layers
+  // first and overlaps their halo exchange with the interior, decomp.py)
+  const int Pn = g->degree + 1;
+  int64_t pd = 1;
+  for (int j = 0; j < g->dim; ++j) pd *= Pn;
+  const int64_t blk = pd * (g->dim + 2);
+  const int64_t tb = blk + (blk & 1);
   PredArgs a{};
-  a.u = u;
+  a.u = u + e_begin * blk;
   a.dt = dt_dev;
-  a.q_out = q_out;
-  a.vol = vol;
-  a.traces = traces;
-  a.pred_bad = pred_bad;
-  a.sweeps = sweeps;
+  a.q_out = q_out ? q_out + e_begin * blk * Pn : nullptr;
+  a.vol = vol + e_begin * blk;
+  a.traces = traces + e_begin * tb;
+  a.pred_bad = pred_bad + e_begin;
+  a.sweeps = sweeps + e_begin;
   a.ws = nullptr;
-  a.n_elem = g->cells[0] * (g->dim >= 2 ? g->cells[1] : 1) * (g->dim == 3 ? g->cells[2] : 1);
+  a.n_elem = e_count;
+  a.tr_elems = n_all;
+  if (e_count == 0) return ADG_OK;
   for (int j = 0; j < 3; ++j) a.dx[j] = j < g->dim ? g->dx[j] : 1.0;
   a.gamma = g->gamma;
   a.tol = tol;

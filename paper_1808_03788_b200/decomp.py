@@ -24,6 +24,7 @@ gloo at world_size 2.
 import torch
 import torch.distributed as dist
 
+from . import _lib
 from .driver import Simulation
 from .mesh import CartesianMesh
 
@@ -47,12 +48,15 @@ def local_mesh(global_mesh, world, rank):
     return mesh
 
 
-def exchange_planes(send_lo, send_hi, recv_lo, recv_hi, group=None):
-    """Periodic ring halo swap along x.
+def exchange_planes_start(send_lo, send_hi, recv_lo, recv_hi, group=None):
+    """Post the periodic ring halo swap along x; returns the pending works.
 
     send_lo -> rank-1 (it becomes that rank's high ghost), send_hi -> rank+1
     (its low ghost); recv_lo <- rank-1's send_hi, recv_hi <- rank+1's send_lo.
-    All four are contiguous tensors on this rank's device.
+    All four are contiguous tensors on this rank's device.  On NCCL the
+    transfers are ordered after the work already on the current stream and
+    run on NCCL's stream, so kernels launched before the works are waited
+    on overlap them.
     """
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
@@ -61,14 +65,24 @@ def exchange_planes(send_lo, send_hi, recv_lo, recv_hi, group=None):
     if world == 1:
         recv_lo.copy_(send_hi)
         recv_hi.copy_(send_lo)
-        return
+        return []
     g = lambda r: dist.get_global_rank(group, r) if group is not None else r  # noqa: E731
     ops = [dist.P2POp(dist.isend, send_lo, g(left), group),
            dist.P2POp(dist.irecv, recv_hi, g(right), group),
            dist.P2POp(dist.isend, send_hi, g(right), group),
            dist.P2POp(dist.irecv, recv_lo, g(left), group)]
-    for req in dist.batch_isend_irecv(ops):
+    return dist.batch_isend_irecv(ops)
+
+
+def exchange_planes_wait(works):
+    """Complete exchange_planes_start (NCCL: the current stream waits)."""
+    for req in works:
         req.wait()
+
+
+def exchange_planes(send_lo, send_hi, recv_lo, recv_hi, group=None):
+    """Periodic ring halo swap along x (exchange_planes_start + wait)."""
+    exchange_planes_wait(exchange_planes_start(send_lo, send_hi, recv_lo, recv_hi, group))
 
 
 def combine_reduce(red, group=None):
@@ -109,15 +123,43 @@ class SlabSimulation(Simulation):
         super().__init__(mesh, system, degree, cfl, boundary=boundary, _ghost=ghost, **kw)
         if self.world > 1:
             self._exchange = SlabSimulation._swap_halos
+        # boundary-layer predictor + halo swap overlapped with the interior
+        self.overlap_halos = True
+        self._range_ok = (self.world > 1 and
+                          bool(_lib.load().adg_predict_range_supported(self._gp())))
 
-    def _swap_halos(self):
+    def _swap_halos(self, wait=True):
         buf = self._buf
         n = self._ghost[(0, 0)].numel()
         face = self.mesh.n_elements * buf.tb
         lo_plane = buf.traces[0:n]                       # axis 0, side 0, first layer
         hi_plane = buf.traces[2 * face - n:2 * face]     # axis 0, side 1, last layer
-        exchange_planes(lo_plane, hi_plane, self._ghost[(0, 0)], self._ghost[(0, 1)],
-                        self.group)
+        works = exchange_planes_start(lo_plane, hi_plane, self._ghost[(0, 0)],
+                                      self._ghost[(0, 1)], self.group)
+        if wait:
+            exchange_planes_wait(works)
+            return []
+        return works
+
+    def _predict_exchange(self, dt_dev):
+        """Boundary layers first, their halo exchange overlapped with the
+        interior predictor: predict the first and last x-layers
+        of the slab, post the trace-plane swap, predict the interior, then
+        make the stream wait for the swap before the face kernels."""
+        if self.world == 1:
+            return super()._predict_exchange(dt_dev)
+        nx = self.mesh.cells[0]
+        E = self.mesh.n_elements
+        layer = E // nx
+        if not (self.overlap_halos and nx >= 3 and self._range_ok):
+            self._predict(dt_dev)
+            self._swap_halos()
+            return
+        self._predict_part(dt_dev, 0, layer)
+        self._predict_part(dt_dev, E - layer, layer)
+        works = self._swap_halos(wait=False)
+        self._predict_part(dt_dev, layer, E - 2 * layer)
+        exchange_planes_wait(works)
 
     def _timestep_into(self, dt_dst, status_dst, t_end):
         if self._red_cur is None:

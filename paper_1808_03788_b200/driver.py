@@ -378,14 +378,28 @@ class Simulation:
     def _enqueue_unlimited(self, dt_dev, totals_dst, t_dst):
         """One unlimited step on the stream; commits u <- u_next."""
         buf = self._buf
-        self._predict(dt_dev)
-        if self._exchange is not None:
-            self._exchange(self)   # neighbour-rank face traces -> ghost buffers
+        self._predict_exchange(dt_dev)
         self._faces()
         nxt = self._update(dt_dev, totals_dst)
         self._h.call("adg_advance_time", _ptr(buf.t), _ptr(dt_dev), _ptr(t_dst), _stream_ptr())
         self._u, self._u_next = self._u_next, self._u
         self._red_cur = nxt
+
+    def _predict_exchange(self, dt_dev):
+        """Predictor, then (slab decomposition) the neighbour-rank face-trace
+        halos into the ghost buffers; decomp.SlabSimulation overlaps the two."""
+        self._predict(dt_dev)
+        if self._exchange is not None:
+            self._exchange(self)
+
+    def _predict_part(self, dt_dev, e_begin, e_count):
+        """The predictor on elements [e_begin, e_begin + e_count) of the
+        whole-grid buffers (adg_predict_range)."""
+        buf = self._buf
+        self._h.call("adg_predict_range", self._gp(), int(e_begin), int(e_count),
+                     _ptr(self._u), _ptr(dt_dev), self.picard_tol, 0, self.min_picard_iter,
+                     None, _ptr(buf.vol), _ptr(buf.traces), _ptr(buf.pred_bad),
+                     _ptr(buf.sweeps), _stream_ptr())
 
     _exchange = None   # hook for slab decomposition (decomp.SlabSimulation)
 

@@ -24,7 +24,8 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1808_03788_b200.decomp import combine_reduce, exchange_planes
+        from paper_1808_03788_b200.decomp import (combine_reduce, exchange_planes,
+                                                  exchange_planes_start, exchange_planes_wait)
 
         n = 7
         send_lo = torch.full((n,), 100.0 * rank + 1.0, dtype=torch.float64)
@@ -35,6 +36,13 @@ def _worker(rank, world, port, q):
         left, right = (rank - 1) % world, (rank + 1) % world
         ok_x = bool(torch.all(recv_lo == 100.0 * left + 2.0)) and \
             bool(torch.all(recv_hi == 100.0 * right + 1.0))
+        # split form (SlabSimulation._predict_exchange): post, work, wait
+        works = exchange_planes_start(send_lo * 3, send_hi * 3, recv_lo, recv_hi)
+        busy = torch.arange(1000, dtype=torch.float64).sum()   # "interior" work
+        exchange_planes_wait(works)
+        ok_x = ok_x and float(busy) == 499500.0 and \
+            bool(torch.all(recv_lo == 3 * (100.0 * left + 2.0))) and \
+            bool(torch.all(recv_hi == 3 * (100.0 * right + 1.0)))
         # adg_reduce record: lam bits MAX, counts SUM
         lam = np.array([0.5 + rank, 3.0 - rank, 1.25], dtype=np.float64)
         red = torch.zeros(8, dtype=torch.int64)

@@ -14,7 +14,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def _run_inprocess(pkg, gmesh, system, degree, cfl, u0, steps, nslabs):
+def _run_inprocess(pkg, gmesh, system, degree, cfl, u0, steps, nslabs, ranges=False):
     from paper_1808_03788_b200.decomp import local_mesh
     from paper_1808_03788_b200.driver import Simulation
 
@@ -46,7 +46,16 @@ def _run_inprocess(pkg, gmesh, system, degree, cfl, u0, steps, nslabs):
             row = torch.zeros(2 + m, dtype=torch.float64, device="cuda")
             st = torch.zeros(1, dtype=torch.int32, device="cuda")
             sim._timestep_into(row[0:1], st, math.inf)
-            sim._predict(row[0:1])
+            if ranges:
+                # SlabSimulation._predict_exchange's overlap schedule: first and
+                # last x-layer, then the interior (adg_predict_range)
+                E = sim.mesh.n_elements
+                layer = E // sim.mesh.cells[0]
+                sim._predict_part(row[0:1], 0, layer)
+                sim._predict_part(row[0:1], E - layer, layer)
+                sim._predict_part(row[0:1], layer, E - 2 * layer)
+            else:
+                sim._predict(row[0:1])
             rows.append(row)
         for r, sim in enumerate(sims):
             n = sim._ghost[(0, 0)].numel()
@@ -64,9 +73,10 @@ def _run_inprocess(pkg, gmesh, system, degree, cfl, u0, steps, nslabs):
     return torch.cat([s.u for s in sims], dim=0), dts
 
 
-@pytest.mark.parametrize("nslabs,cells,degree", [(2, (4, 3, 2), 3), (4, (8, 2, 2), 4),
+@pytest.mark.parametrize("ranges", [False, True], ids=["whole", "ranges"])
+@pytest.mark.parametrize("nslabs,cells,degree", [(2, (6, 3, 2), 3), (4, (12, 2, 2), 4),
                                                  (2, (6, 4), 5)])
-def test_slabs_equal_single_domain(nslabs, cells, degree):
+def test_slabs_equal_single_domain(nslabs, cells, degree, ranges):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1808_03788_b200 as pkg
@@ -80,6 +90,71 @@ def test_slabs_equal_single_domain(nslabs, cells, degree):
     ref.project_initial_condition(ic)
     u0 = ref.u.clone()
     ref.run(np.inf, max_steps=3)
-    u, dts = _run_inprocess(pkg, gmesh, system, degree, cfl, u0, 3, nslabs)
+    u, dts = _run_inprocess(pkg, gmesh, system, degree, cfl, u0, 3, nslabs, ranges)
     np.testing.assert_array_equal(dts, [h["dt"] for h in ref.history])
     assert torch.equal(u, ref.u)
+
+
+@pytest.mark.parametrize("cells,degree,mode", [((5, 4, 3), 4, "conservative"),
+                                               ((4, 3, 3), 2, "primitive"),
+                                               ((7, 5), 3, "conservative"),
+                                               ((9,), 5, "conservative")])
+def test_predict_range_bitwise(cells, degree, mode):
+    """adg_predict_range over a split of the elements == one adg_predict."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1808_03788_b200 as pkg
+
+    d = len(cells)
+    mesh = pkg.CartesianMesh([(0.0, 1.0)] * d, cells)
+    system = pkg.make_system("euler", d)
+    sim = pkg.Simulation(mesh, system, degree, 0.9 / (d * (2 * degree + 1)),
+                         predictor_mode=mode)
+    sim.project_initial_condition(pkg.build_problem("density_wave", system)[0])
+    dt = torch.tensor([sim.max_timestep()], dtype=torch.float64, device=sim.device)
+    sim._ensure_buffers()
+    buf = sim._buf
+
+    def poison():
+        # a sentinel both runs start from (entries a range misses show up)
+        for x in (buf.vol, buf.traces):
+            x.fill_(12345.0)
+        buf.pred_bad.fill_(7)
+        buf.sweeps.fill_(-1)
+
+    poison()
+    sim._predict(dt)
+    want = [x.clone() for x in (buf.vol, buf.traces, buf.pred_bad, buf.sweeps)]
+    poison()
+    E = mesh.n_elements
+    cuts = [0, 1, E // 3, E // 3, E - 2, E]   # includes an empty range
+    for b, c in zip(cuts[:-1], cuts[1:]):
+        sim._predict_part(dt, b, c - b)
+    got = [buf.vol, buf.traces, buf.pred_bad, buf.sweeps]
+    # the trace blocks' padding double carries whatever the staged bulk copy
+    # held: compare the P^d m values of every block
+    blk = (degree + 1) ** d * (d + 2)
+    want[1] = want[1].view(-1, buf.tb)[:, :blk]
+    got[1] = got[1].view(-1, buf.tb)[:, :blk]
+    for w, g in zip(want, got):
+        assert torch.equal(w, g)
+
+
+def test_predict_range_errors():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1808_03788_b200 as pkg
+
+    mesh = pkg.CartesianMesh([(0.0, 1.0)] * 3, (2, 2, 2))
+    system = pkg.make_system("euler", 3)
+    sim = pkg.Simulation(mesh, system, 4, 0.9 / 27)
+    sim.project_initial_condition(pkg.build_problem("density_wave", system)[0])
+    dt = torch.tensor([1e-3], dtype=torch.float64, device=sim.device)
+    sim._ensure_buffers()
+    with pytest.raises(ValueError):
+        sim._predict_part(dt, 4, 5)
+    big = pkg.Simulation(mesh, system, 7, 0.9 / 45)   # 3-D N=7: slice-streaming kernel
+    big.project_initial_condition(pkg.build_problem("density_wave", system)[0])
+    big._ensure_buffers()
+    with pytest.raises(NotImplementedError):
+        big._predict_part(dt, 0, 8)
