@@ -342,14 +342,20 @@ def ours(args, rank, world, local_rank):
                 "cells_per_gpu": [n, n, n], "degree": N, "cfl": cfl,
                 "l2": "inputs larger than L2 (u = %.2f GB per GPU)" % (
                     dofs_per_step_rank * (d + 2) * 8 / 1e9),
-                "parallelism": "single GPU" if world == 1 else f"slab-x dp{world} (NCCL halos)",
+                "parallelism": "single GPU" if world == 1 else (
+                    f"slab-x dp{world} ({dist.get_backend()} halos"
+                    + (", all ranks on cuda:0: NOT a bench value)"
+                       if os.environ.get("ADG_BENCH_ONE_DEVICE") == "1" else ")")),
                 "picard_sweeps_max": S_exec, "picard_sweeps_mean": avg_sweeps},
             "roofline": {"kernel": "adg_predict (predict_kernel<3,5>)" if world == 1 else
                          "adg_predict_range x3 (predict_kernel<3,5>: boundary layers, "
                          "interior; halo swap overlapped)", "bound": "fp64",
                          "achieved": achieved, "peak": peaks["fp64_dfma_tflops"],
                          "unit": "TFLOP/s", "frac": achieved / peaks["fp64_dfma_tflops"],
-                         "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                         # the ncu capture is of the C2 grid on one GPU
+                         "traffic": (traffic.get("bytes_per_launch")
+                                     if traffic and world == 1 and n == 64 and N == 4
+                                     else None),
                          "peak_source": peaks["fp64_source"],
                          "algorithmic_flops_per_launch": flops,
                          "avg_launch_ms": avg_pred_ms,
@@ -373,12 +379,21 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank)
         return
+    # development check of the N > 1 code path on a one-GPU box:
+    # ADG_BENCH_ONE_DEVICE=1 puts every rank on cuda:0 over gloo (host-staged
+    # halos; ranks never wait on each other's kernels).  Its numbers are not
+    # bench values; the driver's runs use NCCL with one GPU per rank.
+    if os.environ.get("ADG_BENCH_ONE_DEVICE") == "1":
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("ADG_BENCH_ONE_DEVICE") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         ours(args, rank, world, local_rank)
     finally:

@@ -67,11 +67,32 @@ def exchange_planes_start(send_lo, send_hi, recv_lo, recv_hi, group=None):
         recv_hi.copy_(send_lo)
         return []
     g = lambda r: dist.get_global_rank(group, r) if group is not None else r  # noqa: E731
+    staged = send_lo.is_cuda and dist.get_backend(group) != "nccl"
+    if staged:
+        # host-transport backends (gloo) move host memory only: stage the
+        # device planes through host copies (the multi-process CPU/GPU tests)
+        send_lo, send_hi = send_lo.cpu(), send_hi.cpu()
+        dev_lo, dev_hi = recv_lo, recv_hi
+        recv_lo, recv_hi = torch.empty_like(send_lo), torch.empty_like(send_hi)
     ops = [dist.P2POp(dist.isend, send_lo, g(left), group),
            dist.P2POp(dist.irecv, recv_hi, g(right), group),
            dist.P2POp(dist.isend, send_hi, g(right), group),
            dist.P2POp(dist.irecv, recv_lo, g(left), group)]
-    return dist.batch_isend_irecv(ops)
+    works = dist.batch_isend_irecv(ops)
+    if staged:
+        works.append(_HostToDevice(((recv_lo, dev_lo), (recv_hi, dev_hi))))
+    return works
+
+
+class _HostToDevice:
+    """Pending copy of host-staged receive planes into their device buffers."""
+
+    def __init__(self, pairs):
+        self.pairs = pairs
+
+    def wait(self):
+        for host, dev in self.pairs:
+            dev.copy_(host)
 
 
 def exchange_planes_wait(works):
