@@ -557,11 +557,13 @@ class Simulation:
         self._enqueue_unlimited(rows[s, 0:1], rows[s, 2:], rows[s, 1:2])
         torch.amax(self._buf.sweeps, dim=0, keepdim=True, out=sweeps[s:s + 1])
 
-    # CUDA graph of two consecutive steps (the u / u_next and wave-speed
-    # double buffers return to their starting roles after two steps), replayed
-    # with a device-side slot counter; removes the per-launch host cost that
-    # bounds small grids (C1: ~8 launches per step)
+    # CUDA graph of an even number of consecutive steps (the u / u_next and
+    # wave-speed double buffers return to their starting roles after two
+    # steps), replayed with a device-side slot counter; removes the per-launch
+    # host cost that bounds small grids (C1: ~8 launches per step).  Batches
+    # shorter than graph_steps (or their tail) replay a two-step graph.
     graphs_enabled = True
+    graph_steps = 8
 
     def _batch_buffers(self, k):
         bb = getattr(self, "_bb", None)
@@ -580,8 +582,8 @@ class Simulation:
             self._bb = bb
         return bb
 
-    def _pair_graph(self, bb):
-        key = (self._u.data_ptr(), self._red_cur)
+    def _pair_graph(self, bb, nsteps=2):
+        key = (self._u.data_ptr(), self._red_cur, nsteps)
         g = bb["graphs"].get(key)
         if g is not None:
             return g
@@ -589,8 +591,8 @@ class Simulation:
         g = torch.cuda.CUDAGraph()
         ncols = bb["rows"].shape[1]
         with torch.cuda.graph(g):
-            for j in range(2):
-                srow, sst = bb["srow"][j], bb["sst"][j:j + 1]
+            for j in range(nsteps):
+                srow, sst = bb["srow"][j % 2], bb["sst"][j % 2:j % 2 + 1]
                 self._timestep_into(srow[0:1], sst, math.inf)
                 self._enqueue_unlimited(srow[0:1], srow[2:], srow[1:2])
                 # history row, status and max sweep count into slot cnt
@@ -620,11 +622,15 @@ class Simulation:
         s = 0
         while s < k:
             if use_graph and self._red_cur is not None and k - s >= 2:
-                g = self._pair_graph(bb)
                 bb["cnt"].fill_(s)
-                while k - s >= 2:
-                    g.replay()
-                    s += 2
+                for n in sorted({max(2, self.graph_steps - self.graph_steps % 2), 2},
+                                reverse=True):
+                    if k - s < n:
+                        continue
+                    g = self._pair_graph(bb, n)
+                    while k - s >= n:
+                        g.replay()
+                        s += n
                 continue
             self._step_into(bb["rows"], bb["status"], bb["sweeps"], s)
             s += 1
