@@ -562,8 +562,10 @@ class Simulation:
     # steps), replayed with a device-side slot counter; removes the per-launch
     # host cost that bounds small grids (C1: ~8 launches per step).  Batches
     # shorter than graph_steps (or their tail) replay a two-step graph.
+    # Default 2: a longer graph saves ~1 us per C1 step but its first capture
+    # costs ~4 ms (profiles/r01k_graph_unroll.jsonl, r01l_configs.jsonl).
     graphs_enabled = True
-    graph_steps = 8
+    graph_steps = 2
 
     def _batch_buffers(self, k):
         bb = getattr(self, "_bb", None)
