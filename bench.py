@@ -4,10 +4,18 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N=1 runs BASELINE config C2 (64^3 elements, N=4, smooth density wave,
-periodic unit cube, cfl = 0.9/(3(2N+1)) = 1/30).  Under torchrun with N>1
-every rank owns a 64^3 slab of an x-extended domain [0, N] x [0, 1]^2 (the
-C5 weak-scaling construction; --cells 128 gives C5's 128^3 per GPU), x-slab
-decomposed with NCCL halo exchange and wave-speed all-reduce.
+periodic unit cube, cfl = 0.9/(3(2N+1)) = 1/30).  With N>1 (launched under
+torchrun, or `--gpus N` alone: bench.py then starts the N ranks itself
+through torch.distributed.run on 127.0.0.1) it runs BASELINE config C5:
+
+* weak scaling (default): every rank owns 128^3 elements of the x-extended
+  domain [0, N] x [0, 1]^2 (dx = 1/128 at every N);
+* `--scaling strong`: the fixed 256^3 unit cube, x-slabs of 256/N layers
+  (one slab Simulation needs ~107 GB at 128 x 256^2 elements, so N = 8 is
+  the smallest feasible strong-scaling point; smaller N stop with a clear
+  message instead of running out of memory);
+
+x-slab decomposed with NCCL halo exchange and wave-speed all-reduce.
 
 A "step" is one ADER-DG time step (dt reduction, predictor, face fluxes,
 update) over the whole grid.  value = DOF-updates/s = E P^d K / t over all
@@ -42,7 +50,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cells", type=int, default=64, help="elements per axis per GPU")
+    ap.add_argument("--cells", type=int, default=None,
+                    help="elements per axis per GPU (weak; default 64 at N=1 (C2), 128 at N>1 "
+                         "(C5)) or of the global cube (strong; default 256)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher / domain check on CPU (gloo), no GPU work")
     ap.add_argument("--degree", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -204,13 +217,20 @@ def ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    n = args.cells
     N = args.degree
     d = 3
     P = N + 1
     cfl = 0.9 / (d * (2 * N + 1))
-    gmesh = pkg.CartesianMesh([(0.0, float(world)), (0.0, 1.0), (0.0, 1.0)],
-                              (n * world, n, n))
+    strong = args.scaling == "strong"
+    ext, gcells, slab_cells, workload = plan(args, world)
+    gmesh = pkg.CartesianMesh(ext, gcells)
+    # one slab Simulation: u, u_next, vol, 2d trace planes, face terms
+    e_slab = slab_cells[0] * slab_cells[1] * slab_cells[2]
+    need = e_slab * P ** d * (d + 2) * 8 * (3 + 2 * d) + e_slab * 2 * d * P ** (d - 1) * (d + 2) * 8
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    if need > 0.97 * free_b:
+        raise SystemExit(f"{slab_cells} elements per GPU need {need / 1e9:.0f} GB "
+                         f"({free_b / 1e9:.0f} GB free): use more GPUs")
     system = pkg.make_system("euler", d)
     ic, _ = pkg.build_problem("density_wave", system)
 
@@ -284,13 +304,16 @@ def ours(args, rank, world, local_rank):
                                        peaks["hbm_gbs"] * 1e9) * world
 
     e2e = None
+    local = sim.mesh
+    tables = sim.tables
+    del sim, counter, pred_events, sweeps_total, orig_predict
+    torch.cuda.empty_cache()
     if not args.no_e2e:
         # end to end through the public API: pinned host IC -> device -> K steps ->
-        # final state back to pinned host memory
-        host_u0 = sim.u.new_empty(sim.u.shape, device="cpu").pin_memory()
-        src = make()
-        host_u0.copy_(src.u)
-        del src
+        # final state back to pinned host memory (the timed Simulation is freed
+        # first and the IC is collocated on the host: one slab Simulation per GPU)
+        host_u0 = torch.from_numpy(np.ascontiguousarray(
+            ic(local.node_coords(tables)), dtype=np.float64)).pin_memory()
         host_out = torch.empty_like(host_u0).pin_memory()
         sim2 = SlabSimulation(gmesh, system, N, cfl, device=local_rank)
         sim2.set_state(host_u0)   # allocate workspaces outside the timed region
@@ -332,14 +355,12 @@ def ours(args, rank, world, local_rank):
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (closed-form density-wave IC, BASELINE C2/C5)",
             "config": {
-                "workload": ("C2: 3-D Euler smooth density wave, 64^3 elements, N=4, "
-                             "periodic unit cube, cfl=1/30" if world == 1 and n == 64 else
-                             f"C5 weak: {n}^3 elements per GPU on [0,{world}]x[0,1]^2, N=4, "
-                             f"x-slab decomposition over {world} GPUs"),
-                "cells_per_gpu": [n, n, n], "degree": N, "cfl": cfl,
+                "workload": workload,
+                "cells_per_gpu": list(slab_cells), "degree": N, "cfl": cfl,
                 "l2": "inputs larger than L2 (u = %.2f GB per GPU)" % (
                     dofs_per_step_rank * (d + 2) * 8 / 1e9),
                 "parallelism": "single GPU" if world == 1 else (
@@ -354,8 +375,8 @@ def ours(args, rank, world, local_rank):
                          "unit": "TFLOP/s", "frac": achieved / peaks["fp64_dfma_tflops"],
                          # the ncu capture is of the C2 grid on one GPU
                          "traffic": (traffic.get("bytes_per_launch")
-                                     if traffic and world == 1 and n == 64 and N == 4
-                                     else None),
+                                     if traffic and world == 1 and slab_cells == (64, 64, 64)
+                                     and N == 4 else None),
                          "peak_source": peaks["fp64_source"],
                          "algorithmic_flops_per_launch": flops,
                          "avg_launch_ms": avg_pred_ms,
@@ -371,11 +392,72 @@ def ours(args, rank, world, local_rank):
         print(json.dumps(out), flush=True)
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 and relay rank 0's JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def plan(args, world):
+    """Domain of this run: (global extents, global cells, cells per rank,
+    workload text).  Weak: 128^3 per rank on [0, N] x [0, 1]^2 (C2's 64^3 at
+    N = 1); strong: the fixed cube split into x-slabs."""
+    if args.scaling == "strong":
+        n = args.cells or 256
+        if n % world:
+            raise SystemExit(f"--scaling strong: {n} x-layers do not split over {world} ranks")
+        return ([(0.0, 1.0)] * 3, (n, n, n), (n // world, n, n),
+                f"C5 strong: {n}^3 unit cube, N={args.degree}, x-slabs of {n // world} layers "
+                f"over {world} GPUs")
+    n = args.cells or (64 if world == 1 else 128)
+    work = ("C2: 3-D Euler smooth density wave, 64^3 elements, N=4, periodic unit cube, "
+            "cfl=1/30" if world == 1 and n == 64 and args.degree == 4 else
+            f"C5 weak: {n}^3 elements per GPU on [0,{world}]x[0,1]^2, N={args.degree}, "
+            f"x-slab decomposition over {world} GPUs")
+    return ([(0.0, float(world)), (0.0, 1.0), (0.0, 1.0)], (n * world, n, n), (n, n, n), work)
+
+
+def dry_run(args, rank, world):
+    """Launcher check without a GPU (CPU tests): every rank joins a gloo group,
+    agrees on the plan, and rank 0 prints it as one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    ext, cells, slab, work = plan(args, world)
+    t = torch.tensor([float(slab[0])])
+    if world > 1:
+        dist.all_reduce(t)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "scaling": args.scaling,
+                          "layers_total": float(t.item()),
+                          "config": {"workload": work, "global_cells": list(cells),
+                                     "cells_per_gpu": list(slab), "extents": ext}}),
+              flush=True)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run:
+        dry_run(args, rank, world)
+        return
     if args.impl == "reference":
         reference_arm(args, rank)
         return

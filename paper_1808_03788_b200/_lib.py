@@ -1,7 +1,7 @@
 """ctypes binding of libaderdg_b200.so (the C-ABI in include/aderdg_b200.h).
 
-The shared library is built in-tree by `python setup_ext.py` /
-`__graft_entry__.build()` (nvcc, -gencode arch=compute_100a,code=sm_100a).
+The shared library is built in-tree by `__graft_entry__.build()`
+(`make -C paper_1808_03788_b200/csrc`) (nvcc, -gencode arch=compute_100a,code=sm_100a).
 There is no fallback: if the library or a CUDA device is missing, every
 entry point raises.
 """
@@ -145,7 +145,12 @@ def check(handle, rc, what):
 
 
 class Handle:
-    """One adg_handle per CUDA device; tables are uploaded on demand."""
+    """An adg_handle bound to one CUDA device; tables are uploaded on demand.
+
+    `Handle.get(dev)` is the shared per-device handle of the module-level
+    functions; every `Simulation` owns a private one (its predictor
+    workspace is then never shared or reallocated under another
+    Simulation's captured CUDA graphs)."""
 
     _per_device = {}
 
@@ -179,3 +184,17 @@ class Handle:
     def call(self, name, *args):
         rc = getattr(self.lib, name)(self.ptr, *args)
         check(self.ptr, rc, name)
+
+    def stream(self):
+        """cudaStream_t of torch's current stream on this handle's device."""
+        import torch
+
+        return torch.cuda.current_stream(self.device_index).cuda_stream
+
+    def __del__(self):
+        ptr, self.ptr = getattr(self, "ptr", None), None
+        if ptr and getattr(self, "lib", None) is not None:
+            try:
+                self.lib.adg_destroy(ptr)
+            except Exception:
+                pass

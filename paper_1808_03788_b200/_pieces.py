@@ -46,10 +46,6 @@ def handle_for(t, tables=None):
     return h
 
 
-def stream():
-    return torch.cuda.current_stream().cuda_stream
-
-
 def scalar(x, device):
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=torch.float64).reshape(1).contiguous()

@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._pieces import as_device, flat_grid, handle_for, require_euler, scalar, stream
+from ._pieces import as_device, flat_grid, handle_for, require_euler, scalar
 from .basis import basis_tables
 from .basis import weight_tensor as _weights
 
@@ -50,9 +50,9 @@ def compute_timestep(u, system, spacings, cfl, degree):
     dt = torch.empty(1, dtype=torch.float64, device=u.device)
     st = torch.zeros(1, dtype=torch.int32, device=u.device)
     gp = _lib.ctypes.byref(g)
-    h.call("adg_wavespeed", gp, u.data_ptr(), red.data_ptr(), stream())
+    h.call("adg_wavespeed", gp, u.data_ptr(), red.data_ptr(), h.stream())
     h.call("adg_timestep", gp, red.data_ptr(), float(cfl), None, math.inf, dt.data_ptr(),
-           st.data_ptr(), stream())
+           st.data_ptr(), h.stream())
     if int(st.item()) & _lib.STATUS_NO_ADMISSIBLE:
         raise RuntimeError("no admissible state found while sizing the time step")
     return float(dt.item())
@@ -77,7 +77,7 @@ def face_fluxes(q_minus, q_plus, axis, system):
     h = handle_for(qm, basis_tables(0))
     g = flat_grid(system, 0, 1)
     h.call("adg_face_fluxes", _lib.ctypes.byref(g), int(axis), int(n), qm.data_ptr(),
-           qp.data_ptr(), dlow.data_ptr(), dhigh.data_ptr(), stream())
+           qp.data_ptr(), dlow.data_ptr(), dhigh.data_ptr(), h.stream())
     return dlow, dhigh
 
 
@@ -98,7 +98,7 @@ def volume_integral(q, system, spacings, dt, tables, width=None):
     g = flat_grid(system, tables.degree, E, spacings)
     dt_dev = scalar(dt, q.device)
     h.call("adg_volume_integral", _lib.ctypes.byref(g), q.data_ptr(), dt_dev.data_ptr(),
-           vol.data_ptr(), stream())
+           vol.data_ptr(), h.stream())
     return vol
 
 
@@ -116,7 +116,7 @@ def face_integral(d_values, axis, side, spacings, dt, tables, dim):
     g = flat_grid(system, tables.degree, E, spacings)
     dt_dev = scalar(dt, dv.device)
     h.call("adg_face_integral", _lib.ctypes.byref(g), int(axis), int(side), dv.data_ptr(),
-           dt_dev.data_ptr(), out.data_ptr(), stream())
+           dt_dev.data_ptr(), out.data_ptr(), h.stream())
     return out
 
 
@@ -135,7 +135,7 @@ def element_update(u, volume_acc, face_accs, spacings, tables, dim):
     h = handle_for(u, tables)
     g = flat_grid(_EulerShape(dim, m), tables.degree, E, spacings)
     h.call("adg_element_update", _lib.ctypes.byref(g), u.data_ptr(), vol.data_ptr(),
-           _lib.ctypes.cast(ptrs, _lib.ctypes.c_void_p), len(accs), out.data_ptr(), stream())
+           _lib.ctypes.cast(ptrs, _lib.ctypes.c_void_p), len(accs), out.data_ptr(), h.stream())
     return out
 
 

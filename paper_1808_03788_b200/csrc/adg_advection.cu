@@ -540,12 +540,11 @@ static int adv_check(std::string* err) {
 template <int D, int P>
 static void adv_launch_predict(const AdvArgs& a, int num_sms, cudaStream_t st) {
   using C = AdvCfg<D, P>;
-  static bool attr = false;
-  if (!attr && C::SMEM > 48 * 1024) {
+  static PerDevice attr;
+  if (attr.first() && C::SMEM > 48 * 1024) {
     cudaFuncSetAttribute(adv_predict_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM);
   }
-  attr = true;
   const int64_t ngroups = (a.n_elem + C::EPB - 1) / C::EPB;
   const int64_t grid = std::min<int64_t>(ngroups, (int64_t)num_sms * 16);
   if (grid > 0) adv_predict_kernel<D, P><<<(unsigned)grid, C::NT, C::SMEM, st>>>(a);

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "adg_common.cuh"
 #include "adg_internal.h"
@@ -53,9 +54,42 @@ struct adg_handle {
   int num_sms = 148;
   std::string err;
   bool tables_loaded[10] = {false};
-  double* ws = nullptr;   // predictor global-tile workspace (large 3-D tiles)
+  // predictor global-tile workspace (large 3-D tiles).  It only grows, and a
+  // buffer it outgrows is retired (freed at adg_destroy), never freed while a
+  // captured CUDA graph may still hold its address.
+  double* ws = nullptr;
   size_t ws_bytes = 0;
+  std::vector<double*> retired;
 };
+
+// Every entry point runs on the handle's device and restores the caller's
+// current device on return (a handle is bound to one device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const adg_handle* h) {
+    if (!h) return;
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != h->device &&
+        cudaSetDevice(h->device) == cudaSuccess)
+      prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+static int grow_workspace(adg_handle* h, size_t need) {
+  if (need <= h->ws_bytes) return ADG_OK;
+  double* p = nullptr;
+  if (cudaMalloc(&p, need) != cudaSuccess) {
+    h->err = "cannot allocate predictor workspace";
+    return ADG_ERR_CUDA;
+  }
+  if (h->ws) h->retired.push_back(h->ws);
+  h->ws = p;
+  h->ws_bytes = need;
+  return ADG_OK;
+}
 
 static int fail(adg_handle* h, int rc, const std::string& msg) {
   if (h) h->err = msg;
@@ -118,8 +152,9 @@ int adg_version(void) { return 1; }
 int adg_create(int device, adg_handle** out) {
   if (!out) return ADG_ERR_INVALID;
   *out = nullptr;
-  cudaError_t ce = cudaSetDevice(device);
-  if (ce != cudaSuccess) return ADG_ERR_CUDA;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return ADG_ERR_CUDA;
   adg_handle* h = new adg_handle();
   h->device = device;
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
@@ -129,7 +164,9 @@ int adg_create(int device, adg_handle** out) {
 
 int adg_destroy(adg_handle* h) {
   if (!h) return ADG_OK;
+  DeviceGuard dg(h);
   if (h->ws) cudaFree(h->ws);
+  for (double* p : h->retired) cudaFree(p);
   delete h;
   return ADG_OK;
 }
@@ -137,6 +174,7 @@ int adg_destroy(adg_handle* h) {
 const char* adg_last_error(const adg_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
 int adg_set_tables(adg_handle* h, int degree, const double* host_blob, int64_t n) {
+  DeviceGuard dg(h);
   if (!h || !host_blob) return ADG_ERR_INVALID;
   std::string e;
   int rc = ADG_OK;
@@ -147,6 +185,7 @@ int adg_set_tables(adg_handle* h, int degree, const double* host_blob, int64_t n
 
 int adg_wavespeed(adg_handle* h, const adg_grid* g, const double* u, adg_reduce* red,
                   void* stream) {
+  DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
@@ -160,6 +199,7 @@ int adg_wavespeed(adg_handle* h, const adg_grid* g, const double* u, adg_reduce*
 int adg_timestep(adg_handle* h, const adg_grid* g, const adg_reduce* red, double cfl,
                  const double* t_dev, double t_end, double* dt_dev, int32_t* status_dev,
                  void* stream) {
+  DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
   if (!(cfl < 1.0 / (2 * g->degree + 1)))
@@ -171,6 +211,7 @@ int adg_timestep(adg_handle* h, const adg_grid* g, const adg_reduce* red, double
 
 int adg_advance_time(adg_handle* h, double* t_dev, const double* dt_dev, double* t_out,
                      void* stream) {
+  DeviceGuard dg(h);
   if (!h || !t_dev || !dt_dev) return ADG_ERR_INVALID;
   std::string e;
   return wrap(h, adg::advance_time(t_dev, dt_dev, t_out, (cudaStream_t)stream, &e), e);
@@ -179,6 +220,7 @@ int adg_advance_time(adg_handle* h, double* t_dev, const double* dt_dev, double*
 int adg_log_step(adg_handle* h, const double* row, int64_t ncols, const int32_t* status_in,
                  const int32_t* elem_sweeps, int64_t n_elem, double* rows, int32_t* status,
                  int32_t* sweeps, int64_t* cnt, void* stream) {
+  DeviceGuard dg(h);
   if (!h || !row || !status_in || !elem_sweeps || !rows || !status || !sweeps || !cnt ||
       ncols < 0 || n_elem < 1)
     return fail(h, ADG_ERR_INVALID, "adg_log_step: bad arguments");
@@ -190,17 +232,11 @@ int adg_log_step(adg_handle* h, const double* row, int64_t ncols, const int32_t*
 int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double* dt_dev,
                 double tol, int max_iter, int min_iter, double* q_out, double* vol_out,
                 double* traces, uint8_t* pred_bad, int32_t* sweeps, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
-  const size_t need = adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms);
-  if (need > h->ws_bytes) {
-    if (h->ws) cudaFree(h->ws);
-    h->ws = nullptr;
-    h->ws_bytes = 0;
-    if (cudaMalloc(&h->ws, need) != cudaSuccess)
-      return fail(h, ADG_ERR_CUDA, "cannot allocate predictor workspace");
-    h->ws_bytes = need;
-  }
+  rc = grow_workspace(h, adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms));
+  if (rc) return rc;
   std::string e;
   if (is_adv(g))
     return wrap(h, adg::adv_predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out,
@@ -223,19 +259,13 @@ int adg_predict_range(adg_handle* h, const adg_grid* g, int64_t e_begin, int64_t
                       const double* u, const double* dt_dev, double tol, int max_iter,
                       int min_iter, double* q_out, double* vol_out, double* traces,
                       uint8_t* pred_bad, int32_t* sweeps, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
   if (!adg_predict_range_supported(g))
     return fail(h, ADG_ERR_UNSUPPORTED, "adg_predict_range: grid runs a whole-grid predictor");
-  const size_t need = adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms);
-  if (need > h->ws_bytes) {
-    if (h->ws) cudaFree(h->ws);
-    h->ws = nullptr;
-    h->ws_bytes = 0;
-    if (cudaMalloc(&h->ws, need) != cudaSuccess)
-      return fail(h, ADG_ERR_CUDA, "cannot allocate predictor workspace");
-    h->ws_bytes = need;
-  }
+  rc = grow_workspace(h, adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms));
+  if (rc) return rc;
   std::string e;
   return wrap(h, adg::predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out, traces,
                               pred_bad, sweeps, (cudaStream_t)stream, h->num_sms, h->ws,
@@ -245,6 +275,7 @@ int adg_predict_range(adg_handle* h, const adg_grid* g, int64_t e_begin, int64_t
 int adg_face_flux(adg_handle* h, const adg_grid* g, int axis, const double* traces,
                   const double* ghost_lo, const double* ghost_hi, double* dbar_out,
                   void* stream) {
+  DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
@@ -271,6 +302,7 @@ int64_t adg_trace_block(const adg_grid* g) {
 int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
                const double* fd, const double* dt_dev, double* u_out, adg_reduce* red_next,
                double* totals_partial, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
@@ -286,6 +318,7 @@ int adg_update(adg_handle* h, const adg_grid* g, const double* u, const double* 
 
 int adg_totals_finalize(adg_handle* h, const adg_grid* g, const double* totals_partial,
                         int64_t nblocks, double* totals_out, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
@@ -295,6 +328,7 @@ int adg_totals_finalize(adg_handle* h, const adg_grid* g, const double* totals_p
 
 int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partial,
                double* totals_out, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
   std::string e;
@@ -308,6 +342,7 @@ int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partia
 
 int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, double* sub_out,
                          double* cmin_out, double* cmax_out, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
@@ -320,6 +355,7 @@ int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub, const d
                double eps, int force_all, const adg_subcell_ghosts* ghosts, uint8_t* troubled,
                int32_t* idx, int32_t* count, double* cand_sub_out, double* cand_cmin_out,
                double* cand_cmax_out, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
@@ -332,6 +368,7 @@ int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const i
                const int32_t* count_dev, int32_t count_host_max, const double* dt_dev,
                const adg_subcell_ghosts* ghosts, double* u_out, int32_t* failed_dev,
                double* sub_next, double* cmin_next, double* cmax_next, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
@@ -342,6 +379,7 @@ int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const i
 
 int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const double* q_minus,
                     const double* q_plus, double* d_low, double* d_high, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   if (axis < 0 || axis >= g->dim) return fail(h, ADG_ERR_INVALID, "axis out of range");
@@ -352,6 +390,7 @@ int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const
 
 int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const double* dt_dev,
                         double* vol_out, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
@@ -360,6 +399,7 @@ int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const
 
 int adg_face_integral(adg_handle* h, const adg_grid* g, int axis, int side,
                       const double* d_values, const double* dt_dev, double* out, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   if (axis < 0 || axis >= g->dim || side < 0 || side > 1)
@@ -371,6 +411,7 @@ int adg_face_integral(adg_handle* h, const adg_grid* g, int axis, int side,
 
 int adg_element_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
                        const double* const* accs, int n_acc, double* u_out, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   if (n_acc < 0 || n_acc > 6 || (n_acc > 0 && !accs))
@@ -382,6 +423,7 @@ int adg_element_update(adg_handle* h, const adg_grid* g, const double* u, const 
 int adg_muscl_windows(adg_handle* h, const adg_grid* g, const double* windows, int64_t n_windows,
                       const int32_t* count_dev, const double* dt_dev, double* avg_out,
                       uint8_t* failed, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
@@ -391,6 +433,7 @@ int adg_muscl_windows(adg_handle* h, const adg_grid* g, const double* windows, i
 
 int adg_recover_subcells(adg_handle* h, const adg_grid* g, const double* ubar, double* u_out,
                          void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
@@ -399,6 +442,7 @@ int adg_recover_subcells(adg_handle* h, const adg_grid* g, const double* ubar, d
 
 int adg_flatten_cells(adg_handle* h, const adg_grid* g, double* nodal, const double* averages,
                       int32_t* nflat, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;
@@ -406,6 +450,7 @@ int adg_flatten_cells(adg_handle* h, const adg_grid* g, double* nodal, const dou
 }
 
 int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat, void* stream) {
+  DeviceGuard dg(h);
   int rc = check_euler(h, g);
   if (rc) return rc;
   std::string e;

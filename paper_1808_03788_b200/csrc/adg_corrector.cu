@@ -700,11 +700,9 @@ static void launch_face(const adg_grid* g, int axis, const double* traces, const
   auto kern = axis == 0 ? face_kernel<D, P, 0>
                         : (axis == 1 ? face_kernel<D, P, (D > 1 ? 1 : 0)>
                                      : face_kernel<D, P, (D > 2 ? 2 : 0)>);
-  static bool attr[3] = {false, false, false};
-  if (!attr[axis]) {
+  static PerDevice attr[3];
+  if (attr[axis].first())
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    attr[axis] = true;
-  }
   const int64_t blocks = std::min<int64_t>(chunks, 148 * 8);
   kern<<<(unsigned)blocks, C::NT, C::SMEM, st>>>(
       traces, glo, ghi, fd, g->cells[0], D >= 2 ? g->cells[1] : 1, D == 3 ? g->cells[2] : 1,
@@ -730,12 +728,10 @@ template <int D, int P>
 static void launch_update(const adg_grid* g, const double* u, const double* vol, const double* fd,
                           const double* dt_dev, double* u_out, adg_reduce* red, double* partial,
                           cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first())
     cudaFuncSetAttribute(update_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)UpdCfg<D, P>::SMEM);
-    attr = true;
-  }
   update_kernel<D, P><<<(unsigned)update_blocks(g), kReduceThreads, UpdCfg<D, P>::SMEM, st>>>(
       u, vol, fd, dt_dev, u_out, n_elements(g), g->dx[0], D >= 2 ? g->dx[1] : 1.0,
       D == 3 ? g->dx[2] : 1.0, g->gamma, red, partial);

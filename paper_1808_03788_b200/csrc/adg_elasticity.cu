@@ -617,11 +617,10 @@ static int el_check(std::string* err) {
 template <int P>
 static void el_launch_predict(const ElArgs& a, int num_sms, cudaStream_t st) {
   using C = ElCfg<P>;
-  static bool attr = false;
-  if (!attr && C::SMEM > 48 * 1024)
+  static PerDevice attr;
+  if (attr.first() && C::SMEM > 48 * 1024)
     cudaFuncSetAttribute(el_predict_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM);
-  attr = true;
   const int64_t ngroups = (a.n_elem + C::EPB - 1) / C::EPB;
   const int64_t grid = std::min<int64_t>(ngroups, (int64_t)num_sms * 16);
   if (grid > 0) el_predict_kernel<P><<<(unsigned)grid, C::NT, C::SMEM, st>>>(a);

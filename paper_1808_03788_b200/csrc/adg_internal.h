@@ -10,6 +10,21 @@
 
 namespace adg {
 
+// Per-device "done once" flag: kernel attributes (max dynamic shared memory,
+// cluster sizes) are per device, so a process driving several devices sets
+// them once on each (bit = device ordinal of the calling thread).
+struct PerDevice {
+  unsigned mask = 0;
+  bool first() {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned bit = 1u << (d & 31);
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+  }
+};
+
 constexpr int kReduceThreads = 256;
 constexpr int64_t kReduceBlocksCap = 4096;  // fixed -> bitwise-reproducible totals
 constexpr int64_t kUpdateBlocksCap = 148 * 8;

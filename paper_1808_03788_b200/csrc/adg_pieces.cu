@@ -186,15 +186,14 @@ int launch_volume(const adg_grid* g, const double* q, const double* dt, double* 
                   cudaStream_t st, std::string* err) {
   const int64_t E = n_elements(g);
   const size_t sm = (size_t)D * ipow(P, D) * (D + 2) * 8;
-  static bool attr = false;
-  if (!attr && sm > 48 * 1024) {
+  static PerDevice attr;
+  if (attr.first() && sm > 48 * 1024) {
     if (cudaFuncSetAttribute(volume_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sm) != cudaSuccess) {
       *err = "volume tile exceeds shared memory";
       return ADG_ERR_UNSUPPORTED;
     }
   }
-  attr = true;
   volume_kernel<D, P><<<grid_for(E * kPieceThreads), kPieceThreads, sm, st>>>(
       q, E, g->dx[0], g->dx[1], g->dx[2], g->gamma, dt, vol);
   return lerr(err);

@@ -1043,8 +1043,8 @@ static int launch_predict(const PredArgs& a0, cudaStream_t st, int num_sms, doub
                           size_t ws_bytes, std::string* err) {
   using C = PredCfg<D, P>;
   auto kern = a0.prim ? predict_kernel<D, P, 1> : predict_kernel<D, P, 0>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[a0.prim ? 1 : 0]) {
+  static PerDevice attr_set[2];
+  if (attr_set[a0.prim ? 1 : 0].first()) {
     if (C::SMEM_BYTES > 48 * 1024) {
       cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)C::SMEM_BYTES);
@@ -1053,7 +1053,6 @@ static int launch_predict(const PredArgs& a0, cudaStream_t st, int num_sms, doub
         return ADG_ERR_CUDA;
       }
     }
-    attr_set[a0.prim ? 1 : 0] = true;
   }
   PredArgs a = a0;
   const int64_t ngroups = (a.n_elem + C::EPB - 1) / C::EPB;

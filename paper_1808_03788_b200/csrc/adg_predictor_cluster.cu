@@ -468,8 +468,8 @@ template <int P>
 static int launch_cluster(const ClArgs& a, cudaStream_t st, int num_sms, std::string* err) {
   using C = ClCfg<P>;
   auto kern = predict_cluster_kernel<P>;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)C::SMEM);
     if (ce == cudaSuccess && C::C > 8)
@@ -478,7 +478,6 @@ static int launch_cluster(const ClArgs& a, cudaStream_t st, int num_sms, std::st
       *err = cudaGetErrorString(ce);
       return ADG_ERR_CUDA;
     }
-    attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];

@@ -524,15 +524,14 @@ static int launch_stream(const StArgs& a0, cudaStream_t st, int num_sms, double*
                          size_t ws_bytes, std::string* err) {
   using C = StCfg<P>;
   auto kern = predict_stream_kernel<P>;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)C::SMEM);
     if (ce != cudaSuccess) {
       *err = cudaGetErrorString(ce);
       return ADG_ERR_CUDA;
     }
-    attr = true;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, C::SMEM);

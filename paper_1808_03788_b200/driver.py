@@ -73,10 +73,6 @@ def normalize_boundary(spec, dim):
     return table
 
 
-def _stream_ptr():
-    return torch.cuda.current_stream().cuda_stream
-
-
 def _ptr(t):
     return None if t is None else t.data_ptr()
 
@@ -162,7 +158,8 @@ class Simulation:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", torch.device(device).index
                                    if isinstance(device, torch.device) else int(device))
-        self._h = _lib.Handle.get(self.device.index)
+        # a private handle: the predictor workspace belongs to this Simulation
+        self._h = _lib.Handle(self.device.index)
         self._h.ensure_tables(self.tables)
         self._ghost = _ghost or {}
         # "exact" faces: exterior traces / subcell slabs evaluated from
@@ -235,7 +232,7 @@ class Simulation:
         if self.use_limiter:
             nflat = torch.zeros(1, dtype=torch.int32, device=self.device)
             self._h.call("adg_flatten_ic", self._gp(), _ptr(self._u), _ptr(nflat),
-                         _stream_ptr())
+                         self._h.stream())
             self.ic_flattened = int(nflat.item())
             self._red_cur = None
         return self._u
@@ -265,7 +262,7 @@ class Simulation:
     def _wavespeed(self):
         buf = self._ensure_buffers()
         red = buf.red[0]
-        self._h.call("adg_wavespeed", self._gp(), _ptr(self._u), _ptr(red), _stream_ptr())
+        self._h.call("adg_wavespeed", self._gp(), _ptr(self._u), _ptr(red), self._h.stream())
         self._red_cur = 0
 
     def _timestep_into(self, dt_dst, status_dst, t_end):
@@ -274,13 +271,13 @@ class Simulation:
             self._wavespeed()
         red = buf.red[self._red_cur]
         self._h.call("adg_timestep", self._gp(), _ptr(red), self.cfl, _ptr(buf.t),
-                     float(t_end), _ptr(dt_dst), _ptr(status_dst), _stream_ptr())
+                     float(t_end), _ptr(dt_dst), _ptr(status_dst), self._h.stream())
 
     def _predict(self, dt_dev, q_out=None):
         buf = self._buf
         self._h.call("adg_predict", self._gp(), _ptr(self._u), _ptr(dt_dev), self.picard_tol,
                      0, self.min_picard_iter, _ptr(q_out), _ptr(buf.vol), _ptr(buf.traces),
-                     _ptr(buf.pred_bad), _ptr(buf.sweeps), _stream_ptr())
+                     _ptr(buf.pred_bad), _ptr(buf.sweeps), self._h.stream())
 
     # -- exact faces ----------------------------------------------------
     def _trace_strides(self, axis):
@@ -362,17 +359,17 @@ class Simulation:
             glo = self._ghost.get((a, 0), self._exact_trace.get((a, 0)))
             ghi = self._ghost.get((a, 1), self._exact_trace.get((a, 1)))
             self._h.call("adg_face_flux", self._gp(), a, _ptr(buf.traces), _ptr(glo),
-                         _ptr(ghi), _ptr(buf.fd), _stream_ptr())
+                         _ptr(ghi), _ptr(buf.fd), self._h.stream())
 
     def _update(self, dt_dev, totals_dst):
         buf = self._buf
         nxt = 1 - (self._red_cur or 0)
         self._h.call("adg_update", self._gp(), _ptr(self._u), _ptr(buf.vol), _ptr(buf.fd),
                      _ptr(dt_dev), _ptr(self._u_next), _ptr(buf.red[nxt]), _ptr(buf.partial),
-                     _stream_ptr())
+                     self._h.stream())
         if totals_dst is not None:
             self._h.call("adg_totals_finalize", self._gp(), _ptr(buf.partial), buf.nblocks,
-                         _ptr(totals_dst), _stream_ptr())
+                         _ptr(totals_dst), self._h.stream())
         return nxt
 
     def _enqueue_unlimited(self, dt_dev, totals_dst, t_dst):
@@ -381,7 +378,7 @@ class Simulation:
         self._predict_exchange(dt_dev)
         self._faces()
         nxt = self._update(dt_dev, totals_dst)
-        self._h.call("adg_advance_time", _ptr(buf.t), _ptr(dt_dev), _ptr(t_dst), _stream_ptr())
+        self._h.call("adg_advance_time", _ptr(buf.t), _ptr(dt_dev), _ptr(t_dst), self._h.stream())
         self._u, self._u_next = self._u_next, self._u
         self._red_cur = nxt
 
@@ -399,7 +396,7 @@ class Simulation:
         self._h.call("adg_predict_range", self._gp(), int(e_begin), int(e_count),
                      _ptr(self._u), _ptr(dt_dev), self.picard_tol, 0, self.min_picard_iter,
                      None, _ptr(buf.vol), _ptr(buf.traces), _ptr(buf.pred_bad),
-                     _ptr(buf.sweeps), _stream_ptr())
+                     _ptr(buf.sweeps), self._h.stream())
 
     _exchange = None   # hook for slab decomposition (decomp.SlabSimulation)
 
@@ -478,7 +475,7 @@ class Simulation:
         Returns (accepted, limited_fraction, troubled flags)."""
         buf = self._buf
         lb = self._limiter_buffers()
-        sp = _stream_ptr()
+        sp = self._h.stream()
         dt_dev = row[0:1]
         if lb["sub_of"] is not self._u or self._red_cur is None:
             # t^n subcell averages and their per-cell extrema (once per step)
@@ -585,7 +582,10 @@ class Simulation:
         return bb
 
     def _pair_graph(self, bb, nsteps=2):
-        key = (self._u.data_ptr(), self._red_cur, nsteps)
+        # everything a replay bakes in: buffer roles, step count and the
+        # scalar arguments of the captured launches
+        key = (self._u.data_ptr(), self._red_cur, nsteps, self.cfl, self.picard_tol,
+               self.min_picard_iter)
         g = bb["graphs"].get(key)
         if g is not None:
             return g
@@ -601,7 +601,7 @@ class Simulation:
                 self._h.call("adg_log_step", _ptr(srow), ncols, _ptr(sst),
                              _ptr(self._buf.sweeps), self.mesh.n_elements, _ptr(bb["rows"]),
                              _ptr(bb["status"]), _ptr(bb["sweeps"]), _ptr(bb["cnt"]),
-                             _stream_ptr())
+                             self._h.stream())
         # capture only recorded the launches: state is back where it started
         bb["graphs"][key] = g
         return g
@@ -616,6 +616,7 @@ class Simulation:
         rows, status, sweeps = bb["rows"][:k], bb["status"][:k], bb["sweeps"][:k]
         rows.zero_()
         status.zero_()
+        bb["sst"].zero_()   # timestep_kernel ORs status bits into the step slots
         buf.t.fill_(self.t)
         # only launch-bound grids gain from the graph (capture + instantiate
         # costs tens of ms once; a C2-size step is ~16 ms of GPU work)
@@ -661,7 +662,7 @@ class Simulation:
         buf = self._ensure_buffers()
         out = torch.empty(self._m, dtype=torch.float64, device=self.device)
         self._h.call("adg_totals", self._gp(), _ptr(self._u), _ptr(buf.partial), _ptr(out),
-                     _stream_ptr())
+                     self._h.stream())
         return out.cpu().numpy()
 
     def error_norms(self, reference=None, t=None):

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._pieces import as_device, flat_grid, handle_for, require_euler, scalar, stream
+from ._pieces import as_device, flat_grid, handle_for, require_euler, scalar
 from .basis import basis_tables
 
 DMP_DELTA0 = 1e-3
@@ -51,7 +51,7 @@ def project_to_subcells(u, tables, dim):
     h = handle_for(u, tables)
     g = flat_grid(sysd, tables.degree, E)
     h.call("adg_project_subcells", _lib.ctypes.byref(g), u.data_ptr(), out.data_ptr(),
-           cmin.data_ptr(), cmax.data_ptr(), stream())
+           cmin.data_ptr(), cmax.data_ptr(), h.stream())
     return out
 
 
@@ -66,7 +66,7 @@ def recover_from_subcells(ubar, tables, dim):
     h = handle_for(ubar, tables)
     g = flat_grid(sysd, tables.degree, E)
     h.call("adg_recover_subcells", _lib.ctypes.byref(g), ubar.data_ptr(), out.data_ptr(),
-           stream())
+           h.stream())
     return out
 
 
@@ -152,7 +152,7 @@ def muscl_subcell_step(windows, system, sub_spacings, dt, mode="conservative"):
     hnd = handle_for(win, tables)
     dt_dev = scalar(dt, win.device)
     hnd.call("adg_muscl_windows", _lib.ctypes.byref(g), win.data_ptr(), int(T),
-             count.data_ptr(), dt_dev.data_ptr(), out.data_ptr(), failed.data_ptr(), stream())
+             count.data_ptr(), dt_dev.data_ptr(), out.data_ptr(), failed.data_ptr(), hnd.stream())
     return out, failed.bool()
 
 
@@ -167,7 +167,7 @@ def flatten_inadmissible(nodal, averages, system, tables, dim):
     h = handle_for(nod, tables)
     g = flat_grid(system, tables.degree, E)
     h.call("adg_flatten_cells", _lib.ctypes.byref(g), nod.data_ptr(), avg.data_ptr(),
-           nflat.data_ptr(), stream())
+           nflat.data_ptr(), h.stream())
     return nod, int(nflat.item())
 
 

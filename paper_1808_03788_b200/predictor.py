@@ -69,7 +69,7 @@ def run_predictor(u, system, spacings, dt, tables, tol=1e-12, max_iter=None, min
     h.call("adg_predict", _lib.ctypes.byref(g), u.data_ptr(), dt_dev.data_ptr(), float(tol),
            mi, int(min_iter), q.data_ptr() if q is not None else None, vol.data_ptr(),
            traces.data_ptr(), bad.data_ptr(), sweeps.data_ptr(),
-           torch.cuda.current_stream().cuda_stream)
+           h.stream())
     # the kernel writes each face's trace block in its owner role's order
     # (x: [j][k][t], y: [k][t][i], z: [t][i][j]; 2-D y: [t][i]); present them
     # in the reference layout (tangential axes ascending, then t, then m)

@@ -1,0 +1,140 @@
+"""GPU parity at the BASELINE configs' STATED sizes and step counts, against
+fixtures produced by running the reference package
+(`tests/golden/make_golden_stated.py`):
+
+* C2 (3-D density wave, N=4) for the stated 20 steps (12^3, full state) and
+  at the stated 64^3 for 2 steps (seeded 1024-element subsample, per-x-layer
+  checksums, dt, totals);
+* C3 N=2..9 for the stated 10 steps (4^3, full state);
+* C4 (circular explosion, N=5, limiter) at 64^2 run to the stated t = 0.25
+  with the troubled flags of every step, and at the stated 512^2 for the
+  first 2 steps (flags of both steps, subsample of troubled cells, their
+  neighbours and seeded random cells, per-row checksums).
+
+Bar (BASELINE.json north_star): relative L-inf <= 1e-10 against the
+reference, troubled flags identical.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1808_03788_b200 as p
+    from paper_1808_03788_b200 import _lib
+
+    _lib.load()
+    return p
+
+
+def make_sim(pkg, g, problem, **kw):
+    mesh = pkg.CartesianMesh([tuple(e) for e in g["extents"]], [int(c) for c in g["cells"]])
+    system = pkg.make_system("euler", mesh.dim)
+    sim = pkg.Simulation(mesh, system, int(g["degree"]), float(g["cfl"]), **kw)
+    sim.project_initial_condition(pkg.build_problem(problem, system)[0])
+    return sim
+
+
+def rel_linf(a, b, scale=None):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    s = np.max(np.abs(b)) if scale is None else scale
+    return float(np.max(np.abs(a - b)) / s)
+
+
+def unpack_flags(g):
+    n = int(g["n_cells"])
+    return np.unpackbits(g["troubled_bits"], axis=1)[:, :n].astype(bool)
+
+
+def test_c2_stated_20_steps(pkg, golden):
+    g = golden("c2_wave_12x20")
+    sim = make_sim(pkg, g, "density_wave")
+    assert rel_linf(sim.u, g["u0"]) <= 1e-14
+    sim.run(np.inf, max_steps=20)
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-12)
+    assert sim.sweep_log == [int(x) for x in g["iters"]]
+    assert rel_linf(sim.u, g["u"]) <= TOL
+    np.testing.assert_allclose(np.array([h["totals"] for h in sim.history]), g["totals"],
+                               rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("n", range(2, 10))
+def test_c3_stated_10_steps(pkg, golden, n):
+    g = golden(f"c3_wave_N{n}_4x10")
+    sim = make_sim(pkg, g, "density_wave")
+    sim.run(np.inf, max_steps=10)
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-12)
+    # the reference's global Picard count is the max of the per-element ones
+    assert sim.sweep_log == [int(x) for x in g["iters"]]
+    assert rel_linf(sim.u, g["u"]) <= TOL
+
+
+def test_c2_stated_size_64cubed(pkg, golden):
+    g = golden("c2_wave_64_2")
+    sim = make_sim(pkg, g, "density_wave")
+    E = int(np.prod(g["cells"]))
+    idx = torch.as_tensor(g["sample_idx"], device=sim.device)
+    flat = sim.u.reshape(E, -1)
+    assert rel_linf(flat[idx], g["u0_sample"]) <= 1e-14
+    for k in (1, 2):
+        sim.run(np.inf, max_steps=k)
+        flat = sim.u.reshape(E, -1)
+        scale = float(np.max(g[f"u{k}_absmax"]))
+        assert rel_linf(flat[idx], g[f"u{k}_sample"], scale) <= TOL
+        got = sim.u.sum(dim=(1, 2, 3, 4, 5)).cpu().numpy()
+        np.testing.assert_allclose(got, g[f"u{k}_layersum"], rtol=1e-12)
+        np.testing.assert_allclose(sim.u.abs().reshape(-1, 5).amax(0).cpu().numpy(),
+                                   g[f"u{k}_absmax"], rtol=1e-10)
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-12)
+    assert sim.sweep_log == [int(x) for x in g["iters"]]
+    np.testing.assert_allclose(np.array([h["totals"] for h in sim.history]), g["totals"],
+                               rtol=1e-11)
+
+
+def test_c4_stated_t_end(pkg, golden):
+    """C4 at 64^2 to t = 0.25: every step's troubled flags identical."""
+    g = golden("c4_explosion_64_full")
+    ref_flags = unpack_flags(g)
+    sim = make_sim(pkg, g, "explosion", boundary="outflow", use_limiter=True)
+    assert rel_linf(sim.u, g["u0"]) <= 1e-14
+    flags = []
+    sim.run(0.25, on_step=lambda s: flags.append(s.last_troubled.cpu().numpy().ravel()))
+    assert sim.step_count == int(g["step_count"])
+    got = np.stack(flags)
+    mism = np.flatnonzero((got != ref_flags).any(axis=1))
+    assert mism.size == 0, f"flags differ at steps {mism[:10] + 1}"
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-10)
+    np.testing.assert_allclose([h["limited_fraction"] for h in sim.history], g["fracs"])
+    assert abs(sim.t - float(g["t"])) <= 1e-14
+    assert rel_linf(sim.u, g["u"]) <= TOL
+    np.testing.assert_allclose(np.array([h["totals"] for h in sim.history]), g["totals"],
+                               rtol=1e-10, atol=1e-13)
+
+
+def test_c4_stated_size_512(pkg, golden):
+    g = golden("c4_explosion_512_2")
+    ref_flags = unpack_flags(g)
+    sim = make_sim(pkg, g, "explosion", boundary="outflow", use_limiter=True)
+    idx = torch.as_tensor(g["sample_idx"], device=sim.device)
+    E = int(g["n_cells"])
+    for k in (1, 2):
+        sim.run(np.inf, max_steps=k)
+        f = sim.last_troubled.cpu().numpy().ravel()
+        np.testing.assert_array_equal(f, ref_flags[k - 1])
+        flat = sim.u.reshape(E, -1)
+        scale = float(np.max(g[f"u{k}_absmax"]))
+        assert rel_linf(flat[idx], g[f"u{k}_sample"].reshape(len(idx), -1), scale) <= TOL
+        rows = sim.u.reshape(512, 512, -1, 4).sum(dim=(1, 2)).cpu().numpy()
+        np.testing.assert_allclose(rows, g[f"u{k}_rowsum"], rtol=1e-11, atol=1e-9)
+    np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-12)
+    np.testing.assert_allclose(np.array([h["totals"] for h in sim.history]), g["totals"],
+                               rtol=1e-11)
