@@ -336,9 +336,57 @@ def gen_elasticity():
     case("el_constant", (4, 4), 3, "constant", 3, "periodic", ext=((0.0, 1.0), (0.0, 1.0)))
 
 
+def gen_plugins():
+    """Plugin-contract methods (systems.py:16-74, :158-223, :269-318) on seeded
+    states: Euler eigenvalues / cons_to_prim / prim_to_cons / primitive_rhs,
+    advection eigenvalues / primitive_rhs, elasticity ncp / ncp_matrix."""
+    from aderdg.systems import DiffuseInterfaceElasticity, HyperbolicSystem, LinearAdvection
+
+    out = {}
+    rng = np.random.default_rng(77)
+    for d in (1, 2, 3):
+        sysd = CompressibleEuler(d, gamma=GAMMA)
+        q = euler_states(d, 64, seed=30 + d)
+        grad = rng.uniform(-1, 1, (64, d, d + 2))
+        normal = rng.uniform(-1, 1, d)
+        out[f"e{d}_q"] = q
+        out[f"e{d}_grad"] = grad
+        out[f"e{d}_normal"] = normal
+        out[f"e{d}_eig"] = sysd.eigenvalues(q, normal)
+        out[f"e{d}_prim"] = sysd.cons_to_prim(q)
+        out[f"e{d}_cons"] = sysd.prim_to_cons(sysd.cons_to_prim(q))
+        out[f"e{d}_prim_rhs"] = sysd.primitive_rhs(sysd.cons_to_prim(q), grad)
+        adv = LinearAdvection(d, velocity=rng.uniform(-1, 1, d))
+        qa = rng.uniform(-1, 1, (16, 1))
+        ga = rng.uniform(-1, 1, (16, d, 1))
+        out[f"a{d}_vel"] = adv.velocity
+        out[f"a{d}_q"] = qa
+        out[f"a{d}_grad"] = ga
+        out[f"a{d}_eig"] = adv.eigenvalues(qa, normal)
+        out[f"a{d}_prim_rhs"] = adv.primitive_rhs(qa, ga)
+    el = DiffuseInterfaceElasticity(2)
+    qe = rng.uniform(0.2, 2.0, (64, 9))
+    qe[:8, el.ALPHA] = rng.uniform(0.0, 2e-3, 8)   # below / around the floor
+    ge = rng.uniform(-1, 1, (64, 2, 9))
+    ne = np.array([0.6, -0.8])
+    out["el_q"] = qe
+    out["el_grad"] = ge
+    out["el_normal"] = ne
+    out["el_ncp"] = el.ncp(qe, ge)
+    out["el_ncp_matrix"] = el.ncp_matrix(qe, ne)
+    out["el_prim_rhs"] = el.primitive_rhs(qe, ge)
+    out["el_eig"] = el.eigenvalues(qe, ne)
+    base = HyperbolicSystem(2, 3, ("a", "b", "c"))
+    out["base_flux"] = base.flux(qe[:4, :3])
+    out["base_ncp_matrix"] = base.ncp_matrix(qe[:4, :3], ne)
+    save("plugins", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tables", "pointwise", "predictor", "cases", "primitive", "output",
-                             "exact", "advection", "elasticity"]
+                             "exact", "advection", "elasticity", "plugins"]
+    if "plugins" in which:
+        gen_plugins()
     if "elasticity" in which:
         gen_elasticity()
     if "advection" in which:
