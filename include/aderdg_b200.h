@@ -141,11 +141,47 @@ int adg_log_step(adg_handle* h, const double* row, int64_t ncols, const int32_t*
  * traces  : [d][2][E][adg_trace_block(g)] face traces (side 0 = low
  *           face); the block holds P^(d-1) x P_t x m values ordered per
  *           axis x: [j][k][t][v], y: [k][t][i][v], z: [t][i][j][v]
- * pred_bad: [E] uint8, !(converged && admissible)   (driver.py:212)
+ * pred_bad: [E] uint8, ADG_PRED_* bits; 0 = converged && admissible
+ *           (driver.py:212)
  * sweeps  : [E] int32 Picard sweeps taken                                 */
 int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double* dt_dev,
                 double tol, int max_iter, int min_iter, double* q_out, double* vol_out,
                 double* traces, uint8_t* pred_bad, int32_t* sweeps, void* stream);
+
+/* pred_bad bits (predictor.py:57-62 PredictorResult flags; any bit set means
+ * the element goes to the limiter, driver.py:212) */
+#define ADG_PRED_NOT_CONVERGED 1   /* residual above tol at the last sweep */
+#define ADG_PRED_INADMISSIBLE 2    /* a converged space-time node is inadmissible */
+
+/* -- picard_solve with the reference's optional arguments
+ *    (predictor.py:135-191, :99-126; Euler and advection):
+ * q_init  : optional starting iterate [E, P^d, P_t, m] in the iterate
+ *           variables (conservative, or primitive in ADG_MODE_PRIMITIVE),
+ *           replacing the startup guess (picard_solve initial=); NULL = the
+ *           startup guess
+ * flags   : ADG_PRED_STARTUP_ONLY -> no sweeps; q_out receives the startup
+ *           guess itself in the iterate variables (predictor.startup_guess)
+ * other arguments as adg_predict.  Euler runs the shared-tile kernel (its
+ * large-tile variant for 3-D N >= 7). */
+#define ADG_PRED_STARTUP_ONLY 1
+int adg_predict_ex(adg_handle* h, const adg_grid* g, const double* u, const double* q_init,
+                   const double* dt_dev, double tol, int max_iter, int min_iter, int flags,
+                   double* q_out, double* vol_out, double* traces, uint8_t* pred_bad,
+                   int32_t* sweeps, void* stream);
+
+/* -- predictor.extract_traces (predictor.py:218-230) of a given space-time
+ *    q [E, P^d, P_t, m]: out [d][2 sides][E][P^(d-1) tangential][P_t][m]
+ *    (tangential axes ascending, side 0 = phi(0)); any system (linear) */
+int adg_extract_traces(adg_handle* h, const adg_grid* g, const double* q, double* out,
+                       void* stream);
+
+/* -- the space-time rate L(q) at every node of q [E, P^d, P_t, m] (Euler,
+ *    advection): conservative -sum_j (D/dx_j) F_j(q) in _rhs_conservative's order
+ *    (predictor.py:74-91), or primitive_rhs(v, grad v) for
+ *    ADG_MODE_PRIMITIVE (q holds primitive states, predictor.py:94-96).
+ *    The building block of weak_form_defect (predictor.py:194-215). */
+int adg_spacetime_rate(adg_handle* h, const adg_grid* g, const double* q, double* rate,
+                       void* stream);
 
 /* -- the same predictor on the element range [e_begin, e_begin + e_count)
  *    of the grid (element order = the reference's C order of `u`).  u,
@@ -217,7 +253,8 @@ typedef struct adg_subcell_ghosts {
 /* Subcell averages of u^n (limiter.project_to_subcells, limiter.py:27-33)
  * sub_out [E, S^d, m] (S = 2N+1) and their per-cell extrema cmin/cmax
  * [E, m] (the per-cell part of limiter.relaxed_bounds, limiter.py:62-63).
- * Device limiter: dim 1-2 any degree, dim 3 degree <= 2. */
+ * Device limiter: every dimension and degree (3-D windows beyond shared
+ * memory run on L2-resident global scratch). */
 int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, double* sub_out,
                          double* cmin_out, double* cmax_out, void* stream);
 /* Troubled-cell detection (limiter.py:51-86 + driver.py:272-285): DMP
@@ -260,6 +297,16 @@ int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat,
  * d_low, d_high [n][m] across a face with normal +e_axis */
 int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const double* q_minus,
                     const double* q_plus, double* d_low, double* d_high, void* stream);
+/* Pointwise face terms for n state pairs [n][m] and a general unit normal
+ * (host double[3]) -- corrector.riemann_dminus (corrector.py:81-97, mode 0:
+ * out_a = D(q-, q+).n for the element with outward normal n), face_fluxes
+ * (mode 1: out_a = d_low, out_b = d_high for n = e_axis, corrector.py:100-129)
+ * -- and, for the nonconservative system, path_integral_B (corrector.py:65-78):
+ * bpath [n][m][m] (may be NULL; mode -1 computes only it).  Euler, advection
+ * and elasticity-di. */
+int adg_riemann_points(adg_handle* h, const adg_grid* g, int64_t n, const double* normal,
+                       int mode, const double* q_minus, const double* q_plus, double* out_a,
+                       double* out_b, double* bpath, void* stream);
 /* corrector.volume_integral (corrector.py:141-177): q [E][P^d][P_t][m] ->
  * vol [E][P^d][m] */
 int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const double* dt_dev,

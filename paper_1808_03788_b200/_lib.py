@@ -42,7 +42,12 @@ EXPORTS = (
     "adg_detect", "adg_rescue", "adg_flatten_ic", "adg_face_fluxes", "adg_volume_integral",
     "adg_face_integral", "adg_element_update", "adg_muscl_windows", "adg_recover_subcells",
     "adg_flatten_cells", "adg_log_step", "adg_predict_range", "adg_predict_range_supported",
+    "adg_predict_ex", "adg_extract_traces", "adg_spacetime_rate", "adg_riemann_points",
 )
+
+PRED_NOT_CONVERGED = 1   # pred_bad bits (ADG_PRED_*)
+PRED_INADMISSIBLE = 2
+PRED_STARTUP_ONLY = 1    # adg_predict_ex flags
 
 
 class Grid(ctypes.Structure):
@@ -85,6 +90,10 @@ _SIGS = {
     "adg_predict": (_I, [_P, _P, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P]),
     "adg_predict_range": (_I, [_P, _P, _I64, _I64, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P]),
     "adg_predict_range_supported": (_I, [_P]),
+    "adg_predict_ex": (_I, [_P, _P, _P, _P, _P, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "adg_extract_traces": (_I, [_P, _P, _P, _P, _P]),
+    "adg_riemann_points": (_I, [_P, _P, _I64, _P, _I, _P, _P, _P, _P, _P, _P]),
+    "adg_spacetime_rate": (_I, [_P, _P, _P, _P, _P]),
     "adg_face_flux": (_I, [_P, _P, _I, _P, _P, _P, _P, _P]),
     "adg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "adg_update_blocks": (_I64, [_P]),

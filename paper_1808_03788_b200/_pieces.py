@@ -35,7 +35,7 @@ def flat_grid(system, degree, n_elem, spacings=None, mode="conservative"):
     for j in range(3):
         g.cells[j] = int(max(n_elem, 1)) if j == 0 else 1
         g.dx[j] = float(spacings[j]) if (spacings is not None and j < d) else 1.0
-    g.gamma = float(system.gamma)
+    _lib.fill_system(g, system)
     return g
 
 

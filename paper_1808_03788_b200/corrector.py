@@ -3,7 +3,10 @@
 Same names, arguments and error conventions as the reference module, for
 callers that drive the pieces themselves; Simulation uses the fused
 kernels instead.  Inputs may be numpy arrays or CUDA tensors; results are
-CUDA fp64 tensors in the reference layouts.  Euler only.
+CUDA fp64 tensors in the reference layouts.  The pointwise face terms cover
+the three device plugins (Euler, advection, elasticity-di); face_integral /
+element_update are linear and take any number of quantities;
+volume_integral is the Euler kernel.
 """
 
 import math
@@ -33,6 +36,13 @@ def _grid_cells(u, system, degree):
     return int(np.prod(lead)) if lead else 1
 
 
+def _device_system(system):
+    if getattr(system, "name", None) not in _lib.SYSTEM_CODES:
+        raise NotImplementedError(
+            f"system '{getattr(system, 'name', system)}' has no B200 kernels "
+            "(euler, advection, elasticity-di)")
+
+
 def compute_timestep(u, system, spacings, cfl, degree):
     """Largest stable dt over the admissible nodes (corrector.py:30-55);
     adg_wavespeed + adg_timestep."""
@@ -40,7 +50,7 @@ def compute_timestep(u, system, spacings, cfl, degree):
         raise ValueError(
             f"cfl {cfl} violates the stability bound 1/(2N+1) = "
             f"{max_cfl_number(degree):.6g} for degree {degree}")
-    require_euler(system)
+    _device_system(system)
     u = as_device(u)
     tables = basis_tables(degree)
     h = handle_for(u, tables)
@@ -65,9 +75,59 @@ def rusanov_theta(q_minus, q_plus, normal, system):
     return torch.maximum(system.max_abs_eigenvalue(qm, n), system.max_abs_eigenvalue(qp, n))
 
 
+def _points(q_minus, q_plus, system, normal, mode, want_b=False):
+    """adg_riemann_points on state pairs (..., m): (out_a, out_b, bpath)."""
+    _device_system(system)
+    qm, qp = as_device(q_minus), as_device(q_plus, q_minus.device
+                                            if isinstance(q_minus, torch.Tensor) else None)
+    m = system.n_vars
+    if qm.shape != qp.shape or qm.shape[-1] != m:
+        raise ValueError("q_minus / q_plus must share a (..., n_vars) shape")
+    n = qm.numel() // m
+    nv = np.zeros(3)
+    nv[:system.dim] = np.asarray(normal, dtype=float)[:system.dim]
+    nvec = (_lib.ctypes.c_double * 3)(*nv)
+    out_a = torch.empty_like(qm) if mode >= 0 else None
+    out_b = torch.empty_like(qm) if mode == 1 else None
+    bpath = (torch.empty(tuple(qm.shape) + (m,), dtype=torch.float64, device=qm.device)
+             if want_b else None)
+    h = handle_for(qm, basis_tables(0))
+    g = flat_grid(system, 0, 1)
+    h.call("adg_riemann_points", _lib.ctypes.byref(g), int(n), nvec, int(mode), qm.data_ptr(),
+           qp.data_ptr(), None if out_a is None else out_a.data_ptr(),
+           None if out_b is None else out_b.data_ptr(),
+           None if bpath is None else bpath.data_ptr(), h.stream())
+    return out_a, out_b, bpath
+
+
+def path_integral_B(q_minus, q_plus, normal, system, n_points=3):
+    """int_0^1 B(psi(s)).n ds along q- -> q+ by the 3-point Gauss rule
+    (corrector.py:65-78); zeros for flux-only systems."""
+    if n_points != 3:
+        raise NotImplementedError("the device path rule is the reference's 3-point Gauss rule")
+    if not getattr(system, "has_ncp", False):
+        qm = as_device(q_minus)
+        m = system.n_vars
+        return torch.zeros(tuple(qm.shape[:-1]) + (m, m), dtype=torch.float64, device=qm.device)
+    return _points(q_minus, q_plus, system, normal, -1, want_b=True)[2]
+
+
+def riemann_dminus(q_minus, q_plus, normal, system):
+    """One-sided face term for the element with outward normal `normal`
+    (corrector.py:81-97)."""
+    return _points(q_minus, q_plus, system, normal, 0)[0]
+
+
 def face_fluxes(q_minus, q_plus, axis, system):
-    """Both one-sided Rusanov face terms (corrector.py:100-129): adg_face_fluxes."""
-    require_euler(system)
+    """Both one-sided face terms of an interface with normal +e_axis
+    (corrector.py:100-129); d_low + d_high == 0 bit for bit for flux systems.
+    Euler goes through adg_face_fluxes (the subcell rescue's pair), the
+    other plugins through adg_riemann_points."""
+    if getattr(system, "name", None) != "euler":
+        nv = np.zeros(system.dim)
+        nv[axis] = 1.0
+        d_low, d_high, _ = _points(q_minus, q_plus, system, nv, 1)
+        return d_low, d_high
     qm, qp = as_device(q_minus), as_device(q_plus)
     if qm.shape != qp.shape or qm.shape[-1] != system.n_vars:
         raise ValueError("q_minus / q_plus must share a (..., n_vars) shape")
@@ -111,7 +171,7 @@ def face_integral(d_values, axis, side, spacings, dt, tables, dim):
     lead = dv.shape[:dv.ndim - 1 - dim]
     E = int(np.prod(lead)) if lead else 1
     out = torch.empty(tuple(lead) + (P,) * dim + (m,), dtype=torch.float64, device=dv.device)
-    system = _EulerShape(dim, m)
+    system = _Shape(dim, m)
     h = handle_for(dv, tables)
     g = flat_grid(system, tables.degree, E, spacings)
     dt_dev = scalar(dt, dv.device)
@@ -133,24 +193,23 @@ def element_update(u, volume_acc, face_accs, spacings, tables, dim):
     out = torch.empty_like(u)
     ptrs = (_lib.ctypes.c_void_p * max(len(accs), 1))(*[a.data_ptr() for a in accs])
     h = handle_for(u, tables)
-    g = flat_grid(_EulerShape(dim, m), tables.degree, E, spacings)
+    g = flat_grid(_Shape(dim, m), tables.degree, E, spacings)
     h.call("adg_element_update", _lib.ctypes.byref(g), u.data_ptr(), vol.data_ptr(),
            _lib.ctypes.cast(ptrs, _lib.ctypes.c_void_p), len(accs), out.data_ptr(), h.stream())
     return out
 
 
-class _EulerShape:
-    """Minimal system descriptor for the shape-only calls."""
+class _Shape:
+    """Minimal descriptor for the linear, system-independent calls."""
 
     name = "euler"
+    gamma = 1.4
 
     def __init__(self, dim, m):
-        if m != dim + 2:
-            raise NotImplementedError("Euler states only (m = d + 2)")
         self.dim = dim
         self.n_vars = m
-        self.gamma = 1.4
 
 
 __all__ = ["max_cfl_number", "weight_tensor", "compute_timestep", "rusanov_theta",
-           "face_fluxes", "volume_integral", "face_integral", "element_update"]
+           "path_integral_B", "riemann_dminus", "face_fluxes", "volume_integral",
+           "face_integral", "element_update"]

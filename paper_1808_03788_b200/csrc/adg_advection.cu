@@ -33,6 +33,7 @@ struct AdvCfg {
 
 struct AdvArgs {
   const double* u;
+  const double* q_init;   // optional starting iterate [E][P^d][P_t] (picard_solve initial=)
   const double* dt;
   double* q_out;
   double* vol;
@@ -141,6 +142,7 @@ adv_predict_kernel(const __grid_constant__ AdvArgs a) {
         const double c2 = 0.5 * s * s / dt;
         q[t] = uu + s * k1 + c2 * (k2 - k1);
       }
+      if (a.q_init && valid) q[t] = a.q_init[((size_t)e * PD + item) * P + t];
     }
     // Picard sweeps (predictor.py:135-191), per-element freezing
     int it = 0;
@@ -266,7 +268,7 @@ adv_predict_kernel(const __grid_constant__ AdvArgs a) {
     __syncthreads();
     if (tid < EPB && g * EPB + tid < a.n_elem) {
       const int64_t ee = g * EPB + tid;
-      a.pred_bad[ee] = !(fl[4 * tid + 1] && fl[4 * tid + 3]);
+      a.pred_bad[ee] = (fl[4 * tid + 1] ? 0 : ADG_PRED_NOT_CONVERGED) | (fl[4 * tid + 3] ? 0 : ADG_PRED_INADMISSIBLE);
       a.sweeps[ee] = fl[4 * tid + 2] ? fl[4 * tid + 2] : it;
     }
   }
@@ -537,6 +539,46 @@ static int adv_check(std::string* err) {
   return ADG_OK;
 }
 
+// L(q) = ((0 - D_x (a_x q)) - D_y (a_y q)) - .. at every node of a
+// space-time q [E][P^d][P_t] (predictor.py:74-91 for m = 1); the
+// weak_form_defect building block
+template <int D, int P>
+__global__ void __launch_bounds__(256)
+adv_rate_kernel(const double* __restrict__ q, int64_t E, AdvArgs a, double* __restrict__ rate) {
+  constexpr int PD = ipow(P, D);
+  const int64_t total = E * PD * P;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = x / (PD * P);
+    const int nd = (int)((x / P) % PD);
+    const int t = (int)(x % P);
+    const int ni = D == 3 ? nd / (P * P) : (D == 2 ? nd / P : nd);
+    const int nj = D == 3 ? (nd / P) % P : (D == 2 ? nd % P : 0);
+    const int nk = D == 3 ? nd % P : 0;
+    double r = 0.0;
+#pragma unroll
+    for (int dir = 0; dir < D; ++dir) {
+      const int row = dir == 0 ? ni : (dir == 1 ? nj : nk);
+      double y = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const int n2 = dir == 0 ? adv_node<D, P>(l, nj, nk)
+                                : (dir == 1 ? adv_node<D, P>(ni, l, nk) : adv_node<D, P>(ni, nj, l));
+        y = fma(a.dd[dir * P * P + row * P + l], a.a[dir] * q[((size_t)e * PD + n2) * P + t], y);
+      }
+      r -= y;
+    }
+    rate[x] = r;
+  }
+}
+
+template <int D, int P>
+static void adv_launch_rate(const AdvArgs& a, const double* q, double* rate, cudaStream_t st) {
+  const int64_t work = a.n_elem * ipow(P, D) * P;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 32));
+  adv_rate_kernel<D, P><<<(unsigned)blocks, 256, 0, st>>>(q, a.n_elem, a, rate);
+}
+
 template <int D, int P>
 static void adv_launch_predict(const AdvArgs& a, int num_sms, cudaStream_t st) {
   using C = AdvCfg<D, P>;
@@ -553,9 +595,10 @@ static void adv_launch_predict(const AdvArgs& a, int num_sms, cudaStream_t st) {
 int adv_predict(const adg_grid* g, const double* u, const double* dt_dev, double tol,
                 int max_iter, int min_iter, double* q_out, double* vol, double* traces,
                 uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms,
-                std::string* err) {
+                std::string* err, const double* q_init, int startup_only) {
   AdvArgs a{};
   a.u = u;
+  a.q_init = q_init;
   a.dt = dt_dev;
   a.q_out = q_out;
   a.vol = vol;
@@ -568,13 +611,27 @@ int adv_predict(const adg_grid* g, const double* u, const double* dt_dev, double
     a.a[j] = j < g->dim ? g->velocity[j] : 0.0;
   }
   a.tol = tol;
-  a.max_iter = max_iter > 0 ? max_iter : 2 * g->degree + 2;
+  a.max_iter = startup_only ? 0 : (max_iter > 0 ? max_iter : 2 * g->degree + 2);
   a.min_iter = min_iter;
   const int Pl = g->degree + 1;
   for (int dir = 0; dir < 3; ++dir)
     for (int x = 0; x < Pl * Pl; ++x)
       a.dd[dir * Pl * Pl + x] = dir < g->dim ? h_tab[g->degree].diff[x] / g->dx[dir] : 0.0;
   ADG_ADV_SWITCH(adv_launch_predict, a, num_sms, st);
+  return adv_check(err);
+}
+
+int adv_spacetime_rate(const adg_grid* g, const double* q, double* rate, cudaStream_t st,
+                       std::string* err) {
+  AdvArgs a{};
+  a.n_elem = n_elements(g);
+  for (int j = 0; j < 3; ++j) a.a[j] = j < g->dim ? g->velocity[j] : 0.0;
+  const int Pl = g->degree + 1;
+  for (int dir = 0; dir < 3; ++dir)
+    for (int x = 0; x < Pl * Pl; ++x)
+      a.dd[dir * Pl * Pl + x] = dir < g->dim ? h_tab[g->degree].diff[x] / g->dx[dir] : 0.0;
+  if (a.n_elem == 0) return ADG_OK;
+  ADG_ADV_SWITCH(adv_launch_rate, a, q, rate, st);
   return adv_check(err);
 }
 

@@ -251,6 +251,56 @@ int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double*
                               h->ws_bytes, &e), e);
 }
 
+int adg_predict_ex(adg_handle* h, const adg_grid* g, const double* u, const double* q_init,
+                   const double* dt_dev, double tol, int max_iter, int min_iter, int flags,
+                   double* q_out, double* vol_out, double* traces, uint8_t* pred_bad,
+                   int32_t* sweeps, void* stream) {
+  DeviceGuard dg(h);
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (flags & ~ADG_PRED_STARTUP_ONLY) return fail(h, ADG_ERR_INVALID, "unknown predictor flags");
+  std::string e;
+  if (is_adv(g))
+    return wrap(h, adg::adv_predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out,
+                                    traces, pred_bad, sweeps, (cudaStream_t)stream, h->num_sms,
+                                    &e, q_init, (flags & ADG_PRED_STARTUP_ONLY) ? 1 : 0), e);
+  if (is_el(g))
+    return fail(h, ADG_ERR_UNSUPPORTED,
+                "elasticity-di on the device: no starting iterate / startup-only predictor");
+  rc = grow_workspace(h, adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms));
+  if (rc) return rc;
+  return wrap(h, adg::predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out, traces,
+                              pred_bad, sweeps, (cudaStream_t)stream, h->num_sms, h->ws,
+                              h->ws_bytes, &e, 0, -1, q_init,
+                              (flags & ADG_PRED_STARTUP_ONLY) ? 1 : 0), e);
+}
+
+int adg_extract_traces(adg_handle* h, const adg_grid* g, const double* q, double* out,
+                       void* stream) {
+  DeviceGuard dg(h);
+  // linear in q: any number of quantities, no plugin
+  if (!g || g->dim < 1 || g->dim > 3 || g->degree < 0 || g->degree > 9 || g->nvars < 1 ||
+      g->cells[0] < 0)
+    return fail(h, ADG_ERR_INVALID, "adg_extract_traces: bad grid");
+  if (!h->tables_loaded[g->degree])
+    return fail(h, ADG_ERR_INVALID, "tables for this degree not uploaded (adg_set_tables)");
+  if (!q || !out) return fail(h, ADG_ERR_INVALID, "adg_extract_traces: null array");
+  std::string e;
+  return wrap(h, adg::extract_traces(g, q, out, (cudaStream_t)stream, &e), e);
+}
+
+int adg_spacetime_rate(adg_handle* h, const adg_grid* g, const double* q, double* rate,
+                       void* stream) {
+  DeviceGuard dg(h);
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (!q || !rate) return fail(h, ADG_ERR_INVALID, "adg_spacetime_rate: null array");
+  std::string e;
+  if (is_adv(g)) return wrap(h, adg::adv_spacetime_rate(g, q, rate, (cudaStream_t)stream, &e), e);
+  if (is_el(g)) return fail(h, ADG_ERR_UNSUPPORTED, "adg_spacetime_rate: Euler and advection");
+  return wrap(h, adg::spacetime_rate(g, q, rate, (cudaStream_t)stream, &e), e);
+}
+
 int adg_predict_range_supported(const adg_grid* g) {
   return g && !is_adv(g) && !is_el(g) && adg::predict_range_supported(g) ? 1 : 0;
 }
@@ -388,6 +438,24 @@ int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const
                                   (cudaStream_t)stream, &e), e);
 }
 
+int adg_riemann_points(adg_handle* h, const adg_grid* g, int64_t n, const double* normal,
+                       int mode, const double* q_minus, const double* q_plus, double* out_a,
+                       double* out_b, double* bpath, void* stream) {
+  DeviceGuard dg(h);
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (!normal || n < 0 || mode < -1 || mode > 1 || (n > 0 && (!q_minus || !q_plus)) ||
+      (mode >= 0 && !out_a) || (mode == 1 && !out_b))
+    return fail(h, ADG_ERR_INVALID, "adg_riemann_points: bad arguments");
+  std::string e;
+  if (is_el(g))
+    return wrap(h, adg::el_points(n, normal, mode, q_minus, q_plus, out_a, out_b, bpath,
+                                  (cudaStream_t)stream, &e), e);
+  if (mode < 0) return fail(h, ADG_ERR_INVALID, "path integral: nonconservative systems only");
+  return wrap(h, adg::riemann_points(g, n, normal, mode, q_minus, q_plus, out_a, out_b,
+                                     (cudaStream_t)stream, &e), e);
+}
+
 int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const double* dt_dev,
                         double* vol_out, void* stream) {
   DeviceGuard dg(h);
@@ -397,10 +465,21 @@ int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const
   return wrap(h, adg::volume_integral(g, q, dt_dev, vol_out, (cudaStream_t)stream, &e), e);
 }
 
+// linear, system-independent pieces: any number of quantities
+static int check_linear(adg_handle* h, const adg_grid* g) {
+  if (!g || g->dim < 1 || g->dim > 3 || g->degree < 0 || g->degree > 9 || g->nvars < 1)
+    return fail(h, ADG_ERR_INVALID, "bad grid");
+  for (int j = 0; j < g->dim; ++j)
+    if (g->cells[j] < 0 || !(g->dx[j] > 0.0)) return fail(h, ADG_ERR_INVALID, "bad grid");
+  if (!h->tables_loaded[g->degree])
+    return fail(h, ADG_ERR_INVALID, "tables for this degree not uploaded (adg_set_tables)");
+  return ADG_OK;
+}
+
 int adg_face_integral(adg_handle* h, const adg_grid* g, int axis, int side,
                       const double* d_values, const double* dt_dev, double* out, void* stream) {
   DeviceGuard dg(h);
-  int rc = check_euler(h, g);
+  int rc = check_linear(h, g);
   if (rc) return rc;
   if (axis < 0 || axis >= g->dim || side < 0 || side > 1)
     return fail(h, ADG_ERR_INVALID, "axis / side out of range");
@@ -412,7 +491,7 @@ int adg_face_integral(adg_handle* h, const adg_grid* g, int axis, int side,
 int adg_element_update(adg_handle* h, const adg_grid* g, const double* u, const double* vol,
                        const double* const* accs, int n_acc, double* u_out, void* stream) {
   DeviceGuard dg(h);
-  int rc = check_euler(h, g);
+  int rc = check_linear(h, g);
   if (rc) return rc;
   if (n_acc < 0 || n_acc > 6 || (n_acc > 0 && !accs))
     return fail(h, ADG_ERR_INVALID, "0..6 face accumulators");

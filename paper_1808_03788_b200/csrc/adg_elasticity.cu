@@ -88,7 +88,98 @@ __device__ __forceinline__ void ncp_matrix_acc(const double* q, int axis, double
 }
 
 __device__ __forceinline__ double cp(const double* q) { return sqrt((q[LAM] + 2.0 * q[MU]) / q[RHO]); }
+
+// the full 9 x 9 B(q).n for a general normal (systems.py:296-322), as a
+// dense row-major matrix accumulated with weight w (path_integral_B)
+__device__ __forceinline__ void ncp_matrix_dense_acc(const double* q, double nx, double ny,
+                                                     double w, double* b) {
+  const double a = fmax(q[ALPHA], ALPHA_FLOOR);
+  const double lam = q[LAM], mu = q[MU], rho = q[RHO];
+  const double vx = q[AVX] / a;
+  const double vy = q[AVY] / a;
+  const double lp2m = lam + 2.0 * mu;
+  b[SXX * 9 + AVX] += w * (-lp2m * nx / a);
+  b[SXX * 9 + AVY] += w * (-lam * ny / a);
+  b[SXX * 9 + ALPHA] += w * ((lp2m * vx * nx + lam * vy * ny) / a);
+  b[SYY * 9 + AVX] += w * (-lam * nx / a);
+  b[SYY * 9 + AVY] += w * (-lp2m * ny / a);
+  b[SYY * 9 + ALPHA] += w * ((lam * vx * nx + lp2m * vy * ny) / a);
+  b[SXY * 9 + AVX] += w * (-mu * ny / a);
+  b[SXY * 9 + AVY] += w * (-mu * nx / a);
+  b[SXY * 9 + ALPHA] += w * (mu * (vx * ny + vy * nx) / a);
+  b[AVX * 9 + SXX] += w * (-a * nx / rho);
+  b[AVX * 9 + SXY] += w * (-a * ny / rho);
+  b[AVX * 9 + ALPHA] += w * (-(q[SXX] * nx + q[SXY] * ny) / rho);
+  b[AVY * 9 + SXY] += w * (-a * nx / rho);
+  b[AVY * 9 + SYY] += w * (-a * ny / rho);
+  b[AVY * 9 + ALPHA] += w * (-(q[SXY] * nx + q[SYY] * ny) / rho);
+}
 }  // namespace el
+
+// Pointwise face terms of the module API (corrector.py:58-129) for state
+// pairs [n][9] and a general normal: path_integral_B (3-point Gauss rule
+// along q- -> q+), riemann_dminus (mode 0) or the face_fluxes pair (mode 1).
+__global__ void el_points_kernel(const double* __restrict__ qm_all,
+                                 const double* __restrict__ qp_all, int64_t n, double nx,
+                                 double ny, int mode, double* __restrict__ out_a,
+                                 double* __restrict__ out_b, double* __restrict__ bpath) {
+  constexpr int M = el::M;
+  const double r15 = sqrt(0.6);
+  const double sn[3] = {0.5 - 0.5 * r15, 0.5, 0.5 + 0.5 * r15};
+  const double sw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double qm[M], qp[M], jump[M], b[M * M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) {
+      qm[v] = qm_all[i * M + v];
+      qp[v] = qp_all[i * M + v];
+      jump[v] = qp[v] - qm[v];
+    }
+#pragma unroll
+    for (int k = 0; k < M * M; ++k) b[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double psi[M];
+#pragma unroll
+      for (int v = 0; v < M; ++v) psi[v] = qm[v] + sn[k] * jump[v];
+      el::ncp_matrix_dense_acc(psi, nx, ny, sw[k], b);
+    }
+    if (bpath) {
+#pragma unroll
+      for (int k = 0; k < M * M; ++k) bpath[i * M * M + k] = b[k];
+    }
+    if (mode < 0) continue;
+    const double smax = fmax(el::cp(qm), el::cp(qp));
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      double bj = 0.0;
+#pragma unroll
+      for (int c = 0; c < M; ++c) bj = fma(b[r * M + c], jump[c], bj);
+      const double diss = ((0.5 * smax) * jump[r]) * el::mask(r);
+      if (mode == 0) {
+        out_a[i * M + r] = -diss + 0.5 * bj;
+      } else {
+        out_a[i * M + r] = (0.0 + 0.5 * bj) - diss;
+        out_b[i * M + r] = (-0.0 + 0.5 * bj) + diss;
+      }
+    }
+  }
+}
+
+int el_points(int64_t n, const double* normal, int mode, const double* qm, const double* qp,
+              double* out_a, double* out_b, double* bpath, cudaStream_t st, std::string* err) {
+  if (n <= 0) return ADG_OK;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, 148 * 16));
+  el_points_kernel<<<(unsigned)blocks, 128, 0, st>>>(qm, qp, n, normal[0], normal[1], mode,
+                                                      out_a, out_b, bpath);
+  cudaError_t ce = cudaGetLastError();
+  if (ce != cudaSuccess) {
+    *err = cudaGetErrorString(ce);
+    return ADG_ERR_CUDA;
+  }
+  return ADG_OK;
+}
 
 template <int P>
 struct ElCfg {
@@ -337,7 +428,7 @@ el_predict_kernel(const __grid_constant__ ElArgs a) {
     __syncthreads();
     if (tid < EPB && g * EPB + tid < a.n_elem) {
       const int64_t ee = g * EPB + tid;
-      a.pred_bad[ee] = !(fl[4 * tid + 1] && fl[4 * tid + 3]);
+      a.pred_bad[ee] = (fl[4 * tid + 1] ? 0 : ADG_PRED_NOT_CONVERGED) | (fl[4 * tid + 3] ? 0 : ADG_PRED_INADMISSIBLE);
       a.sweeps[ee] = fl[4 * tid + 2] ? fl[4 * tid + 2] : it;
     }
   }

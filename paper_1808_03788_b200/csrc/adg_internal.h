@@ -37,7 +37,8 @@ size_t predict_workspace_bytes(int dim, int P, int num_sms);
 int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol, int max_iter,
             int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
             int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
-            std::string* err, int64_t e_begin = 0, int64_t e_count = -1);
+            std::string* err, int64_t e_begin = 0, int64_t e_count = -1,
+            const double* q_init = nullptr, int startup_only = 0);
 // element ranges run on the shared-tile predictor only
 bool predict_range_supported(const adg_grid* g);
 
@@ -57,7 +58,9 @@ int predict_cluster(const adg_grid* g, const double* u, const double* dt_dev, do
 int adv_predict(const adg_grid* g, const double* u, const double* dt_dev, double tol,
                 int max_iter, int min_iter, double* q_out, double* vol, double* traces,
                 uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms,
-                std::string* err);
+                std::string* err, const double* q_init = nullptr, int startup_only = 0);
+int adv_spacetime_rate(const adg_grid* g, const double* q, double* rate, cudaStream_t st,
+                       std::string* err);
 int adv_face_flux(const adg_grid* g, int axis, const double* traces, const double* ghost_lo,
                   const double* ghost_hi, double* fd, cudaStream_t st, std::string* err);
 int adv_update(const adg_grid* g, const double* u, const double* vol, const double* fd,
@@ -126,6 +129,15 @@ int volume_integral(const adg_grid* g, const double* q, const double* dt_dev, do
                     cudaStream_t st, std::string* err);
 int face_integral(const adg_grid* g, int axis, int side, const double* d_values,
                   const double* dt_dev, double* out, cudaStream_t st, std::string* err);
+int riemann_points(const adg_grid* g, int64_t n, const double* normal, int mode,
+                   const double* qm, const double* qp, double* out_a, double* out_b,
+                   cudaStream_t st, std::string* err);
+int el_points(int64_t n, const double* normal, int mode, const double* qm, const double* qp,
+              double* out_a, double* out_b, double* bpath, cudaStream_t st, std::string* err);
+int extract_traces(const adg_grid* g, const double* q, double* out, cudaStream_t st,
+                   std::string* err);
+int spacetime_rate(const adg_grid* g, const double* q, double* rate, cudaStream_t st,
+                   std::string* err);
 int element_update(const adg_grid* g, const double* u, const double* vol,
                    const double* const* accs, int nacc, double* out, cudaStream_t st,
                    std::string* err);

@@ -5,6 +5,9 @@
 //   volume_integral (corrector.py:141-177)  from a given space-time q
 //   face_integral   (corrector.py:180-196)  one face's accumulator
 //   element_update  (corrector.py:199-205)  u + (vol - sum faces) / mass
+//   extract_traces  (predictor.py:218-230)  face states of a given q
+//   space-time rate (predictor.py:74-91, :94-96)  L(q) at every node (the
+//                   weak_form_defect check of predictor.py:194-215)
 // The fused time step (adg_predict / adg_face_flux / adg_update) does not
 // use these; they trade fusion for the reference's array interfaces.
 // Arrays are in the reference layouts with the element grid flattened to E.
@@ -36,6 +39,80 @@ face_points_kernel(const double* __restrict__ qm, const double* __restrict__ qp,
     for (int v = 0; v < M; ++v) {
       dlow[i * M + v] = lo[v];
       dhigh[i * M + v] = hi[v];
+    }
+  }
+}
+
+// One-sided Rusanov term for a general outward normal (riemann_dminus,
+// corrector.py:81-97): -1/2 s (q+ - q-) + sum_j 1/2 n_j (F_j(q-) + F_j(q+)),
+// s = max(|lambda(q-).n|, |lambda(q+).n|).  SYS 0: Euler (m = D + 2);
+// SYS 1: advection (m = 1, F_j = a_j q).  MODE 1 forms the face_fluxes pair
+// (corrector.py:100-129) for n = e_axis instead.
+template <int SYS, int D>
+__global__ void __launch_bounds__(kPieceThreads)
+riemann_points_kernel(const double* __restrict__ qm_all, const double* __restrict__ qp_all,
+                      int64_t n, double n0, double n1, double n2, double gamma, double a0,
+                      double a1, double a2, int mode, double* __restrict__ out_a,
+                      double* __restrict__ out_b) {
+  constexpr int M = SYS == 0 ? D + 2 : 1;
+  const double nv[3] = {n0, n1, n2};
+  const double av[3] = {a0, a1, a2};
+  const double gm1 = gamma - 1.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double qm[M], qp[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) {
+      qm[v] = qm_all[i * M + v];
+      qp[v] = qp_all[i * M + v];
+    }
+    double s;
+    if (SYS == 0) {
+      double um = 0.0, up = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        um = um + qm[1 + j] * nv[j];
+        up = up + qp[1 + j] * nv[j];
+      }
+      const double lm = fabs(um / qm[0]) + sqrt(gamma * pressure<D>(qm, gm1) / qm[0]);
+      const double lp = fabs(up / qp[0]) + sqrt(gamma * pressure<D>(qp, gm1) / qp[0]);
+      s = fmax(lm, lp);
+    } else {
+      double an = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) an = an + av[j] * nv[j];
+      s = fabs(an);
+    }
+    double out[M], fm[M], fp[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) out[v] = -0.5 * s * (qp[v] - qm[v]);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      if (nv[j] == 0.0) continue;
+      if (SYS == 0) {
+        flux_axis<D>(qm, gm1, j, fm);
+        flux_axis<D>(qp, gm1, j, fp);
+      } else {
+        fm[0] = av[j] * qm[0];
+        fp[0] = av[j] * qp[0];
+      }
+      if (mode == 1) {
+        // face pair along e_j (only one nonzero component)
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          const double central = 0.5 * (fm[v] + fp[v]);
+          const double diss = 0.5 * s * (qp[v] - qm[v]);
+          out_a[i * M + v] = (central + 0.0) - diss;
+          out_b[i * M + v] = (-central + 0.0) + diss;
+        }
+        break;
+      }
+#pragma unroll
+      for (int v = 0; v < M; ++v) out[v] += 0.5 * nv[j] * (fm[v] + fp[v]);
+    }
+    if (mode == 0) {
+#pragma unroll
+      for (int v = 0; v < M; ++v) out_a[i * M + v] = out[v];
     }
   }
 }
@@ -107,8 +184,8 @@ volume_kernel(const double* __restrict__ q, int64_t E, double dx0, double dx1, d
 template <int D, int P>
 __global__ void __launch_bounds__(kPieceThreads)
 face_integral_kernel(const double* __restrict__ d, int64_t E, int axis, int side, double area,
-                     const double* __restrict__ dt_dev, double* __restrict__ out) {
-  constexpr int M = D + 2, PD = ipow(P, D), PF = PD / P;
+                     const double* __restrict__ dt_dev, int M, double* __restrict__ out) {
+  constexpr int PD = ipow(P, D), PF = PD / P;
   const DegreeTables& T = tab<P>();
   const double dt = *dt_dev;
   const int64_t total = E * PD;
@@ -133,13 +210,124 @@ face_integral_kernel(const double* __restrict__ d, int64_t E, int axis, int side
       }
     const double vec = side ? T.right[k[axis]] : T.left[k[axis]];
     const double* src = d + ((size_t)e * PF + tg) * P * M;
-#pragma unroll
     for (int v = 0; v < M; ++v) {
       double db = 0.0;
       for (int t = 0; t < P; ++t) db = fma(T.weights[t], src[t * M + v], db);
       if (D > 1) db = db * wt;
       out[(size_t)x * M + v] = (dt * area) * (vec * db);
     }
+  }
+}
+
+// extract_traces: q [E][P^D][P_t][m] -> out [D][2][E][P^(D-1)][P_t][m],
+// phi(0) / phi(1) contracted along spatial axis j (tangential axes ascending)
+template <int D, int P>
+__global__ void __launch_bounds__(kPieceThreads)
+traces_kernel(const double* __restrict__ q, int64_t E, int m, double* __restrict__ out) {
+  constexpr int PD = ipow(P, D), PF = PD / P;
+  const DegreeTables& T = tab<P>();
+  const int64_t per_dir = E * PF * P;            // (element, tangential node, t)
+  const int64_t total = D * per_dir;
+  const size_t plane = (size_t)E * PF * P * m;   // one (j, side) output array
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(x / per_dir);
+    const int64_t r = x - j * per_dir;
+    const int64_t e = r / (PF * P);
+    const int tg = (int)((r / P) % PF);
+    const int t = (int)(r % P);
+    // spatial node of line position l: the tangential digits of tg with l
+    // inserted at axis j (row-major, last axis fastest)
+    int dig[3] = {0, 0, 0};
+    {
+      int rem = tg;
+      for (int i = D - 1; i >= 0; --i) {
+        if (i == j) continue;
+        dig[i] = rem % P;
+        rem /= P;
+      }
+    }
+    int stride = 1;
+    for (int i = D - 1; i > j; --i) stride *= P;
+    int base = 0;
+    for (int i = 0; i < D; ++i) base = base * P + (i == j ? 0 : dig[i]);
+    const double* src = q + ((size_t)e * PD + base) * P * m + (size_t)t * m;
+    double* lo = out + (size_t)(2 * j) * plane + ((size_t)r) * m;
+    double* hi = lo + plane;
+    for (int v = 0; v < m; ++v) {
+      double a = 0.0, b = 0.0;
+      for (int l = 0; l < P; ++l) {
+        const double qv = src[(size_t)l * stride * P * m + v];
+        a = fma(T.left[l], qv, a);
+        b = fma(T.right[l], qv, b);
+      }
+      lo[v] = a;
+      hi[v] = b;
+    }
+  }
+}
+
+// Space-time rate at every node of q [E][P^D][P_t][m] (Euler):
+// conservative L(q) = ((0 - (D/dx_0) F_0) - (D/dx_1) F_1) - .. in the order of
+// _rhs_conservative (predictor.py:74-91); primitive primitive_rhs(v, grad v)
+// with grad_j = (D/dx_j) v (predictor.py:94-96).  A test hook: every thread
+// re-evaluates the fluxes of its P line neighbours per direction.
+template <int D, int P>
+__global__ void __launch_bounds__(kPieceThreads)
+st_rate_kernel(const double* __restrict__ q, int64_t E, double dx0, double dx1, double dx2,
+               double gamma, int prim, double* __restrict__ rate) {
+  constexpr int M = D + 2, PD = ipow(P, D);
+  const DegreeTables& T = tab<P>();
+  const double dx[3] = {dx0, dx1, dx2};
+  const double gm1 = gamma - 1.0;
+  const int64_t total = E * PD * P;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = x / (PD * P);
+    const int nd = (int)((x / P) % PD);
+    const int t = (int)(x % P);
+    int k[3] = {0, 0, 0};
+    {
+      int rem = nd;
+      for (int i = D - 1; i >= 0; --i) {
+        k[i] = rem % P;
+        rem /= P;
+      }
+    }
+    const double* qe = q + (size_t)e * PD * P * M;
+    double out[M], grad[D][M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) out[v] = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      int stride = 1;
+      for (int i = D - 1; i > j; --i) stride *= P;
+      const int base = nd - k[j] * stride;
+      double acc[M];
+#pragma unroll
+      for (int v = 0; v < M; ++v) acc[v] = 0.0;
+      for (int l = 0; l < P; ++l) {
+        const double* ql = qe + ((size_t)(base + l * stride) * P + t) * M;
+        double f[M];
+        if (prim) {
+#pragma unroll
+          for (int v = 0; v < M; ++v) f[v] = ql[v];
+        } else {
+          flux_axis<D>(ql, gm1, j, f);
+        }
+        const double c = T.diff[k[j] * P + l] / dx[j];   // (diff / spacing)[k][l]
+#pragma unroll
+        for (int v = 0; v < M; ++v) acc[v] = fma(c, f[v], acc[v]);
+      }
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        grad[j][v] = acc[v];
+        out[v] -= acc[v];
+      }
+    }
+    if (prim) primitive_rhs<D>(qe + ((size_t)nd * P + t) * M, grad, gamma, out);
+#pragma unroll
+    for (int v = 0; v < M; ++v) rate[(size_t)x * M + v] = out[v];
   }
 }
 
@@ -151,8 +339,8 @@ struct AccList {
 template <int D, int P>
 __global__ void __launch_bounds__(kPieceThreads)
 element_update_kernel(const double* __restrict__ u, const double* __restrict__ vol, AccList acc,
-                      int nacc, int64_t E, double cv, double* __restrict__ out) {
-  constexpr int M = D + 2, PD = ipow(P, D);
+                      int nacc, int64_t E, double cv, int M, double* __restrict__ out) {
+  constexpr int PD = ipow(P, D);
   const DegreeTables& T = tab<P>();
   const int64_t total = E * PD * M;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
@@ -208,7 +396,7 @@ int launch_face_integral(const adg_grid* g, int axis, int side, const double* dv
   for (int j = 0; j < g->dim; ++j) vol *= g->dx[j];
   const double area = vol / g->dx[axis];
   face_integral_kernel<D, P><<<grid_for(E * ipow(P, D)), kPieceThreads, 0, st>>>(
-      dv, E, axis, side, area, dt, out);
+      dv, E, axis, side, area, dt, g->nvars, out);
   return lerr(err);
 }
 
@@ -221,8 +409,26 @@ int launch_element_update(const adg_grid* g, const double* u, const double* vol,
   for (int i = 0; i < nacc; ++i) a.p[i] = accs[i];
   double cv = 1.0;
   for (int j = 0; j < g->dim; ++j) cv *= g->dx[j];
-  element_update_kernel<D, P><<<grid_for(E * ipow(P, D) * (D + 2)), kPieceThreads, 0, st>>>(
-      u, vol, a, nacc, E, cv, out);
+  element_update_kernel<D, P><<<grid_for(E * ipow(P, D) * g->nvars), kPieceThreads, 0, st>>>(
+      u, vol, a, nacc, E, cv, g->nvars, out);
+  return lerr(err);
+}
+
+template <int D, int P>
+int launch_traces(const adg_grid* g, const double* q, double* out, cudaStream_t st,
+                  std::string* err) {
+  const int64_t E = n_elements(g);
+  traces_kernel<D, P><<<grid_for(E * D * ipow(P, D)), kPieceThreads, 0, st>>>(q, E, g->nvars,
+                                                                             out);
+  return lerr(err);
+}
+
+template <int D, int P>
+int launch_st_rate(const adg_grid* g, const double* q, double* rate, cudaStream_t st,
+                   std::string* err) {
+  const int64_t E = n_elements(g);
+  st_rate_kernel<D, P><<<grid_for(E * ipow(P, D + 1)), kPieceThreads, 0, st>>>(
+      q, E, g->dx[0], g->dx[1], g->dx[2], g->gamma, g->mode == ADG_MODE_PRIMITIVE ? 1 : 0, rate);
   return lerr(err);
 }
 
@@ -277,6 +483,27 @@ int face_points(const adg_grid* g, int axis, int64_t n, const double* qm, const 
   return lerr(err);
 }
 
+int riemann_points(const adg_grid* g, int64_t n, const double* normal, int mode,
+                   const double* qm, const double* qp, double* out_a, double* out_b,
+                   cudaStream_t st, std::string* err) {
+  if (n <= 0) return ADG_OK;
+  const unsigned grid = grid_for(n);
+  const double* a = g->velocity;
+#define ADG_RIEMANN(SYS, D)                                                                 \
+  riemann_points_kernel<SYS, D><<<grid, kPieceThreads, 0, st>>>(                            \
+      qm, qp, n, normal[0], normal[1], normal[2], g->gamma, a[0], a[1], a[2], mode, out_a, \
+      out_b)
+  const int sys = g->system == ADG_SYS_ADVECTION ? 1 : 0;
+  if (sys == 0 && g->dim == 1) ADG_RIEMANN(0, 1);
+  if (sys == 0 && g->dim == 2) ADG_RIEMANN(0, 2);
+  if (sys == 0 && g->dim == 3) ADG_RIEMANN(0, 3);
+  if (sys == 1 && g->dim == 1) ADG_RIEMANN(1, 1);
+  if (sys == 1 && g->dim == 2) ADG_RIEMANN(1, 2);
+  if (sys == 1 && g->dim == 3) ADG_RIEMANN(1, 3);
+#undef ADG_RIEMANN
+  return lerr(err);
+}
+
 int volume_integral(const adg_grid* g, const double* q, const double* dt_dev, double* vol,
                     cudaStream_t st, std::string* err) {
   ADG_PIECE_SWITCH(launch_volume, g, q, dt_dev, vol, st, err);
@@ -285,6 +512,16 @@ int volume_integral(const adg_grid* g, const double* q, const double* dt_dev, do
 int face_integral(const adg_grid* g, int axis, int side, const double* d_values,
                   const double* dt_dev, double* out, cudaStream_t st, std::string* err) {
   ADG_PIECE_SWITCH(launch_face_integral, g, axis, side, d_values, dt_dev, out, st, err);
+}
+
+int extract_traces(const adg_grid* g, const double* q, double* out, cudaStream_t st,
+                   std::string* err) {
+  ADG_PIECE_SWITCH(launch_traces, g, q, out, st, err);
+}
+
+int spacetime_rate(const adg_grid* g, const double* q, double* rate, cudaStream_t st,
+                   std::string* err) {
+  ADG_PIECE_SWITCH(launch_st_rate, g, q, rate, st, err);
 }
 
 int element_update(const adg_grid* g, const double* u, const double* vol,

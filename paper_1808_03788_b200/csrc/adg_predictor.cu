@@ -154,6 +154,7 @@ struct PredCfg {
 
 struct PredArgs {
   const double* u;
+  const double* q_init;   // optional starting iterate [E][P^d][P_t][m] (picard_solve initial=)
   const double* dt;
   double* q_out;
   double* vol;
@@ -169,6 +170,8 @@ struct PredArgs {
   int max_iter;
   int min_iter;
   int prim;            // predictor_mode: 0 conservative, 1 primitive
+  int startup_only;    // stop after the startup guess (startup_guess): no sweeps,
+                       // q_out keeps the iterate variables
   // D / dx_dir for the three directions, [dir][P][P] (rows packed with the
   // launch's P).  Kernel parameters live in the constant bank, so every
   // contraction coefficient is a DFMA constant operand: no shared-memory
@@ -471,8 +474,9 @@ predict_kernel(const __grid_constant__ PredArgs a) {
         for (int v = 0; v < M; ++v) W0[item * M + v] = uu[v];
       }
     }
+    const int npass = a.q_init ? 0 : (P >= 3 ? 2 : 1);
 #pragma unroll kPassUnroll
-    for (int pass = 0; pass < (P >= 3 ? 2 : 1); ++pass) {
+    for (int pass = 0; pass < npass; ++pass) {
       // pass 0 reads the u^n staged before the barrier above (PRIM
       // rewrites it with primitive states first)
       if (pass > 0 || PRIM) __syncthreads();
@@ -505,7 +509,12 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       }
     }
     if (!C::PREFETCH && !C::PF_DED) __syncthreads();   // W0 (inside Q) is about to be overwritten
-    if (valid) {
+    if (valid && a.q_init) {
+      // caller's starting iterate (picard_solve initial=, predictor.py:159-162)
+      const double* qi = a.q_init + (size_t)e * C::TILE + (size_t)item * LS;
+#pragma unroll
+      for (int x = 0; x < LS; ++x) Q[qn0 + x] = qi[x];
+    } else if (valid) {
 #pragma unroll
       for (int t = 0; t < P; ++t) {
         const double s = T.nodes[t] * dt;
@@ -862,7 +871,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     // every lane of the group has passed its startup (pfb is dead) since the
     // sweep loop's barriers
     if (C::PF_DED && g + gridDim.x < ngroups) prefetch_group(g + gridDim.x);
-    if (PRIM) {
+    if (PRIM && !a.startup_only) {
       // q_cons = prim_to_cons(q) (predictor.py:188), each node thread its own
       if (valid) {
 #pragma unroll
@@ -1031,7 +1040,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
     }
     if (tid < EPB && valid_e[tid]) {
       const int64_t ee = g * EPB + tid;
-      a.pred_bad[ee] = !(conv[tid] && okf[tid]);
+      a.pred_bad[ee] = (conv[tid] ? 0 : ADG_PRED_NOT_CONVERGED) | (okf[tid] ? 0 : ADG_PRED_INADMISSIBLE);
       a.sweeps[ee] = nsw[tid] ? nsw[tid] : it;
     }
   }
@@ -1129,7 +1138,8 @@ bool predict_range_supported(const adg_grid* g) {
 int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol, int max_iter,
             int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
             int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
-            std::string* err, int64_t e_begin, int64_t e_count) {
+            std::string* err, int64_t e_begin, int64_t e_count, const double* q_init,
+            int startup_only) {
   const int64_t n_all =
       g->cells[0] * (g->dim >= 2 ? g->cells[1] : 1) * (g->dim == 3 ? g->cells[2] : 1);
   if (e_count < 0) e_count = n_all - e_begin;
@@ -1142,15 +1152,18 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
     *err = "element ranges need the shared-tile predictor (not the 3-D N>=7 stream/cluster kernels)";
     return ADG_ERR_UNSUPPORTED;
   }
+  // a caller's starting iterate or a startup-only call runs the shared-tile
+  // kernel (its large-tile variant for 3-D N >= 7)
+  const bool plain = q_init == nullptr && !startup_only;
   // 3-D tiles beyond one SM's shared memory: one CTA per element streaming
   // time slices through shared memory (adg_predictor_stream.cu)
-  if (!getenv("ADG_CLUSTER_PREDICTOR") && predict_stream_supported(g))
+  if (plain && !getenv("ADG_CLUSTER_PREDICTOR") && predict_stream_supported(g))
     return predict_stream(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
                           sweeps, st, num_sms, ws, ws_bytes, err);
 #ifndef ADG_NO_CLUSTER
   // the earlier design: thread-block cluster, one time slice per CTA
   // (adg_predictor_cluster.cu), kept for A/B runs (ADG_CLUSTER_PREDICTOR=1)
-  if (predict_cluster_supported(g))
+  if (plain && predict_cluster_supported(g))
     return predict_cluster(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
                            sweeps, st, num_sms, err);
 #endif
@@ -1165,6 +1178,8 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   const int64_t tb = blk + (blk & 1);
   PredArgs a{};
   a.u = u + e_begin * blk;
+  a.q_init = q_init ? q_init + e_begin * blk * Pn : nullptr;
+  a.startup_only = startup_only ? 1 : 0;
   a.dt = dt_dev;
   a.q_out = q_out ? q_out + e_begin * blk * Pn : nullptr;
   a.vol = vol + e_begin * blk;
@@ -1178,7 +1193,7 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   for (int j = 0; j < 3; ++j) a.dx[j] = j < g->dim ? g->dx[j] : 1.0;
   a.gamma = g->gamma;
   a.tol = tol;
-  a.max_iter = max_iter > 0 ? max_iter : 2 * g->degree + 2;
+  a.max_iter = startup_only ? 0 : (max_iter > 0 ? max_iter : 2 * g->degree + 2);
   a.min_iter = min_iter;
   a.prim = g->mode == ADG_MODE_PRIMITIVE ? 1 : 0;
   {

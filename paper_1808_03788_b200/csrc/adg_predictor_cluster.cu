@@ -455,7 +455,7 @@ predict_cluster_kernel(const __grid_constant__ ClArgs a) {
       if (c == 0) {
         int okall = 1;
         for (int s = 0; s < C::C; ++s) okall &= okg[s] != 0.0;
-        a.pred_bad[e] = !(conv && okall);
+        a.pred_bad[e] = (conv ? 0 : ADG_PRED_NOT_CONVERGED) | (okall ? 0 : ADG_PRED_INADMISSIBLE);
         a.sweeps[e] = nsw ? nsw : it;
       }
     }

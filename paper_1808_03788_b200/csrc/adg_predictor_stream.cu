@@ -507,7 +507,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     }
     const int all_ok = __syncthreads_and(ok ? 1 : 0);
     if (tid == 0) {
-      a.pred_bad[e] = !(conv && all_ok);
+      a.pred_bad[e] = (conv ? 0 : ADG_PRED_NOT_CONVERGED) | (all_ok ? 0 : ADG_PRED_INADMISSIBLE);
       a.sweeps[e] = nsw ? nsw : it;
     }
   }
