@@ -334,6 +334,33 @@ int adg_recover_subcells(adg_handle* h, const adg_grid* g, const double* ubar, d
 int adg_flatten_cells(adg_handle* h, const adg_grid* g, double* nodal, const double* averages,
                       int32_t* nflat, void* stream);
 
+/* -- multi-GPU exchange of the x-slab decomposition (
+ *    the reference is single-process, driver.py:186-248): an NCCL
+ *    communicator bound to a handle's device, one rank per GPU.  All calls
+ *    are stream ordered on `stream` and CUDA-graph capturable. ------------ */
+typedef struct adg_comm adg_comm;
+#define ADG_COMM_ID_BYTES 128
+/* rank 0 creates the id (ncclGetUniqueId) and shares the bytes with the other
+ * ranks out of band (the host layer uses torch.distributed.broadcast) */
+int adg_comm_unique_id(void* id_out);
+int adg_comm_init(adg_handle* h, const void* id, int nranks, int rank, adg_comm** out);
+int adg_comm_destroy(adg_comm* c);
+/* Face-trace halo swap along x on the periodic ring of ranks (the
+ * reference's periodic face states across the slab cut, driver.py:234-248):
+ * sends the low-x trace plane of the first element layer to rank-1 and the
+ * high-x plane of the last layer to rank+1 (grouped ncclSend / ncclRecv);
+ * ghost_lo / ghost_hi receive the neighbours' planes ([cells_y cells_z]
+ * trace blocks, the ADG_BC_GHOST data of adg_face_flux).  traces as
+ * adg_predict writes them. */
+int adg_halo_exchange(adg_handle* h, adg_comm* c, const adg_grid* g, const double* traces,
+                      double* ghost_lo, double* ghost_hi, void* stream);
+/* The global CFL record (corrector.py:47-55 over all ranks): MAX of the
+ * per-axis wave-speed bit patterns, SUM of the admissible / non-finite
+ * counts, in place. */
+int adg_allreduce_reduce(adg_handle* h, adg_comm* c, adg_reduce* red, void* stream);
+/* SUM of n doubles in place (conserved totals rows, driver.py:344-350). */
+int adg_allreduce_sum(adg_handle* h, adg_comm* c, double* buf, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

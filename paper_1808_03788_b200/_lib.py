@@ -43,7 +43,11 @@ EXPORTS = (
     "adg_face_integral", "adg_element_update", "adg_muscl_windows", "adg_recover_subcells",
     "adg_flatten_cells", "adg_log_step", "adg_predict_range", "adg_predict_range_supported",
     "adg_predict_ex", "adg_extract_traces", "adg_spacetime_rate", "adg_riemann_points",
+    "adg_comm_unique_id", "adg_comm_init", "adg_comm_destroy", "adg_halo_exchange",
+    "adg_allreduce_reduce", "adg_allreduce_sum",
 )
+
+COMM_ID_BYTES = 128
 
 PRED_NOT_CONVERGED = 1   # pred_bad bits (ADG_PRED_*)
 PRED_INADMISSIBLE = 2
@@ -93,6 +97,12 @@ _SIGS = {
     "adg_predict_ex": (_I, [_P, _P, _P, _P, _P, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "adg_extract_traces": (_I, [_P, _P, _P, _P, _P]),
     "adg_riemann_points": (_I, [_P, _P, _I64, _P, _I, _P, _P, _P, _P, _P, _P]),
+    "adg_comm_unique_id": (_I, [_P]),
+    "adg_comm_init": (_I, [_P, _P, _I, _I, ctypes.POINTER(_P)]),
+    "adg_comm_destroy": (_I, [_P]),
+    "adg_halo_exchange": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "adg_allreduce_reduce": (_I, [_P, _P, _P, _P]),
+    "adg_allreduce_sum": (_I, [_P, _P, _P, _I64, _P]),
     "adg_spacetime_rate": (_I, [_P, _P, _P, _P, _P]),
     "adg_face_flux": (_I, [_P, _P, _I, _P, _P, _P, _P, _P]),
     "adg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),

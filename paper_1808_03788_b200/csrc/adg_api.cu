@@ -536,4 +536,59 @@ int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat, 
   return wrap(h, adg::flatten_ic(g, u, nflat, (cudaStream_t)stream, &e), e);
 }
 
+int adg_comm_unique_id(void* id_out) {
+  if (!id_out) return ADG_ERR_INVALID;
+  std::string e;
+  return adg::comm_unique_id(id_out, &e);
+}
+
+int adg_comm_init(adg_handle* h, const void* id, int nranks, int rank, adg_comm** out) {
+  DeviceGuard dg(h);
+  if (!h || !id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(h, ADG_ERR_INVALID, "adg_comm_init: bad arguments");
+  *out = nullptr;
+  std::string e;
+  return wrap(h, adg::comm_init(h->device, id, nranks, rank, out, &e), e);
+}
+
+int adg_comm_destroy(adg_comm* c) { return adg::comm_destroy(c); }
+
+static int check_comm(adg_handle* h, adg_comm* c) {
+  if (!c) return fail(h, ADG_ERR_INVALID, "null communicator");
+  if (adg::comm_device(c) != h->device)
+    return fail(h, ADG_ERR_INVALID, "communicator and handle are bound to different devices");
+  return ADG_OK;
+}
+
+int adg_halo_exchange(adg_handle* h, adg_comm* c, const adg_grid* g, const double* traces,
+                      double* ghost_lo, double* ghost_hi, void* stream) {
+  DeviceGuard dg(h);
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if ((rc = check_comm(h, c))) return rc;
+  if (!traces || !ghost_lo || !ghost_hi)
+    return fail(h, ADG_ERR_INVALID, "adg_halo_exchange: null buffer");
+  std::string e;
+  return wrap(h, adg::halo_exchange(c, g, traces, ghost_lo, ghost_hi, (cudaStream_t)stream, &e),
+              e);
+}
+
+int adg_allreduce_reduce(adg_handle* h, adg_comm* c, adg_reduce* red, void* stream) {
+  DeviceGuard dg(h);
+  int rc = check_comm(h, c);
+  if (rc) return rc;
+  if (!red) return fail(h, ADG_ERR_INVALID, "adg_allreduce_reduce: null record");
+  std::string e;
+  return wrap(h, adg::allreduce_record(c, red, (cudaStream_t)stream, &e), e);
+}
+
+int adg_allreduce_sum(adg_handle* h, adg_comm* c, double* buf, int64_t n, void* stream) {
+  DeviceGuard dg(h);
+  int rc = check_comm(h, c);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && !buf)) return fail(h, ADG_ERR_INVALID, "adg_allreduce_sum: bad buffer");
+  std::string e;
+  return wrap(h, adg::allreduce_sum(c, buf, n, (cudaStream_t)stream, &e), e);
+}
+
 }  // extern "C"

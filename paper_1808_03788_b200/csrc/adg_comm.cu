@@ -1,0 +1,110 @@
+// adg_comm.cu -- the multi-GPU exchange of the slab decomposition behind the
+// C-ABI: an NCCL communicator bound to an adg_handle's
+// device, the x-slab face-trace halo swap (grouped ncclSend / ncclRecv to the
+// periodic ring neighbours) and the two reductions a step needs (the CFL
+// record: MAX of the wave-speed bit patterns, SUM of the admissible /
+// non-finite counts; conserved totals: SUM).  Everything is stream ordered on
+// the caller's stream and CUDA-graph capturable; nothing synchronises the
+// host.  The reference is single-process (driver.py:186-230); the exchange
+// reproduces its periodic face states (driver.py:234-248) across the cut.
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "adg_internal.h"
+
+struct adg_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1;
+  int rank = 0;
+  int device = 0;
+};
+
+namespace adg {
+
+static int nccl_fail(ncclResult_t r, std::string* err) {
+  if (r == ncclSuccess) return ADG_OK;
+  *err = std::string("NCCL: ") + ncclGetErrorString(r);
+  return ADG_ERR_RUNTIME;
+}
+
+int comm_unique_id(void* out, std::string* err) {
+  ncclUniqueId id;
+  int rc = nccl_fail(ncclGetUniqueId(&id), err);
+  if (rc == ADG_OK) std::memcpy(out, &id, sizeof(id));
+  return rc;
+}
+
+int comm_init(int device, const void* uid, int nranks, int rank, adg_comm** out,
+              std::string* err) {
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  adg_comm* c = new adg_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  int rc = nccl_fail(ncclCommInitRank(&c->nccl, nranks, id, rank), err);
+  if (rc != ADG_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return ADG_OK;
+}
+
+int comm_destroy(adg_comm* c) {
+  if (!c) return ADG_OK;
+  // every call on the communicator was stream ordered and the caller drops
+  // it after its streams (and any CUDA graph holding its calls) are done:
+  // abort frees the resources without the collective teardown handshake,
+  // which can block when ranks (or interpreter shutdown) release out of step
+  if (c->nccl) ncclCommAbort(c->nccl);
+  delete c;
+  return ADG_OK;
+}
+
+int comm_device(const adg_comm* c) { return c ? c->device : -1; }
+
+// x-slab halo: this rank's low-x trace plane (first element layer) goes to
+// rank-1 (its high ghost), the high-x plane (last layer) to rank+1 (its low
+// ghost).  Traces are [d][2][E][tb]; a plane is the E / cells_x elements of
+// one x-layer, contiguous in the C order of the grid.
+int halo_exchange(adg_comm* c, const adg_grid* g, const double* traces, double* ghost_lo,
+                  double* ghost_hi, cudaStream_t st, std::string* err) {
+  int64_t pd = 1;
+  for (int j = 0; j < g->dim; ++j) pd *= g->degree + 1;
+  const int64_t blk = pd * g->nvars;
+  const int64_t tb = blk + (blk & 1);
+  const int64_t E = n_elements(g);
+  const int64_t layer = E / g->cells[0];
+  const size_t n = (size_t)(layer * tb);
+  const double* lo_plane = traces;                              // axis 0, side 0, layer 0
+  const double* hi_plane = traces + (size_t)(2 * E - layer) * tb;   // axis 0, side 1, last layer
+  const int left = (c->rank - 1 + c->nranks) % c->nranks;
+  const int right = (c->rank + 1) % c->nranks;
+  ncclResult_t r = ncclGroupStart();
+  if (r == ncclSuccess) r = ncclSend(lo_plane, n, ncclDouble, left, c->nccl, st);
+  if (r == ncclSuccess) r = ncclRecv(ghost_hi, n, ncclDouble, right, c->nccl, st);
+  if (r == ncclSuccess) r = ncclSend(hi_plane, n, ncclDouble, right, c->nccl, st);
+  if (r == ncclSuccess) r = ncclRecv(ghost_lo, n, ncclDouble, left, c->nccl, st);
+  ncclResult_t r2 = ncclGroupEnd();
+  return nccl_fail(r != ncclSuccess ? r : r2, err);
+}
+
+// adg_reduce: lam_bits[3] MAX (bit patterns of non-negative doubles order
+// like unsigned integers), n_admissible / n_nonfinite SUM
+int allreduce_record(adg_comm* c, adg_reduce* red, cudaStream_t st, std::string* err) {
+  uint64_t* w = reinterpret_cast<uint64_t*>(red);
+  ncclResult_t r = ncclGroupStart();
+  if (r == ncclSuccess) r = ncclAllReduce(w, w, 3, ncclUint64, ncclMax, c->nccl, st);
+  if (r == ncclSuccess) r = ncclAllReduce(w + 3, w + 3, 2, ncclUint64, ncclSum, c->nccl, st);
+  ncclResult_t r2 = ncclGroupEnd();
+  return nccl_fail(r != ncclSuccess ? r : r2, err);
+}
+
+int allreduce_sum(adg_comm* c, double* buf, int64_t n, cudaStream_t st, std::string* err) {
+  return nccl_fail(ncclAllReduce(buf, buf, (size_t)n, ncclDouble, ncclSum, c->nccl, st), err);
+}
+
+}  // namespace adg

@@ -263,13 +263,22 @@ __device__ __forceinline__ bool flux_all_adm(const double* q, double gm1, double
   return fin && (q[0] > 0.0) && ppos;
 }
 
+// max of two wave speeds with numpy's np.maximum semantics: a NaN in either
+// operand propagates (fmax would return the other one).  A face state with
+// negative pressure has a NaN sound speed; the reference's Rusanov term and
+// hence the candidate become NaN there and the limiter takes the cell
+// (corrector.py:58-62, limiter.py:76-86).
+__device__ __forceinline__ double nan_max(double a, double b) {
+  return (a >= b || a != a) ? a : b;
+}
+
 // Rusanov one-sided terms (corrector.py:100-129) for a subcell face
 template <int D>
 __device__ __forceinline__ void rusanov_pair(const double* qm, const double* qp, int a,
                                              double gamma, double gm1, double* dlow,
                                              double* dhigh) {
   constexpr int M = D + 2;
-  const double s = fmax(max_abs_eig<D>(qm, gamma, gm1, a), max_abs_eig<D>(qp, gamma, gm1, a));
+  const double s = nan_max(max_abs_eig<D>(qm, gamma, gm1, a), max_abs_eig<D>(qp, gamma, gm1, a));
   double fm[M], fp[M];
   flux_axis<D>(qm, gm1, a, fm);
   flux_axis<D>(qp, gm1, a, fp);

@@ -368,7 +368,7 @@ face_kernel(const double* __restrict__ traces, const double* __restrict__ ghost_
         if (rm) qm[1 + axis] = -qm[1 + axis];   // systems.py:231-234
         if (rp) qp[1 + axis] = -qp[1 + axis];
         double fm[M], fp[M];
-        const double s = fmax(flux_eig_axis<D>(qm, gamma, gm1, axis, fm),
+        const double s = nan_max(flux_eig_axis<D>(qm, gamma, gm1, axis, fm),
                               flux_eig_axis<D>(qp, gamma, gm1, axis, fp));
         const double hs = 0.5 * s;
         const double wt = T.weights[t];

@@ -150,7 +150,7 @@ __global__ void el_points_kernel(const double* __restrict__ qm_all,
       for (int k = 0; k < M * M; ++k) bpath[i * M * M + k] = b[k];
     }
     if (mode < 0) continue;
-    const double smax = fmax(el::cp(qm), el::cp(qp));
+    const double smax = nan_max(el::cp(qm), el::cp(qp));
 #pragma unroll
     for (int r = 0; r < M; ++r) {
       double bj = 0.0;
@@ -497,7 +497,7 @@ __global__ void el_face_kernel(const double* __restrict__ traces, double* __rest
       }
 #pragma unroll
       for (int v = 0; v < M; ++v) jump[v] = qp[v] - qm[v];
-      const double smax = fmax(el::cp(qm), el::cp(qp));
+      const double smax = nan_max(el::cp(qm), el::cp(qp));
       double b[15];
 #pragma unroll
       for (int k = 0; k < 15; ++k) b[k] = 0.0;

@@ -144,4 +144,15 @@ int element_update(const adg_grid* g, const double* u, const double* vol,
 
 void upload_tables(int degree, const double* blob, int64_t n, std::string* err, int* rc);
 
+// multi-GPU exchange (adg_comm.cu, NCCL)
+int comm_unique_id(void* out, std::string* err);
+int comm_init(int device, const void* uid, int nranks, int rank, adg_comm** out,
+              std::string* err);
+int comm_destroy(adg_comm* c);
+int comm_device(const adg_comm* c);
+int halo_exchange(adg_comm* c, const adg_grid* g, const double* traces, double* ghost_lo,
+                  double* ghost_hi, cudaStream_t st, std::string* err);
+int allreduce_record(adg_comm* c, adg_reduce* red, cudaStream_t st, std::string* err);
+int allreduce_sum(adg_comm* c, double* buf, int64_t n, cudaStream_t st, std::string* err);
+
 }  // namespace adg

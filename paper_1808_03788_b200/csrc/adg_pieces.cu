@@ -76,7 +76,7 @@ riemann_points_kernel(const double* __restrict__ qm_all, const double* __restric
       }
       const double lm = fabs(um / qm[0]) + sqrt(gamma * pressure<D>(qm, gm1) / qm[0]);
       const double lp = fabs(up / qp[0]) + sqrt(gamma * pressure<D>(qp, gm1) / qp[0]);
-      s = fmax(lm, lp);
+      s = nan_max(lm, lp);
     } else {
       double an = 0.0;
 #pragma unroll

@@ -16,10 +16,18 @@ axis 0.  Per step the only exchanges are
   * conserved totals: a SUM all-reduce of the per-step totals rows, once per
     batch of steps.
 
-No collective touches the element data itself.  The exchange helpers work
-on any torch.distributed backend, so the CPU test suite covers them with
-gloo at world_size 2.
+No collective touches the element data itself.  Two transports carry them:
+
+  * "adg" (default under NCCL, one GPU per rank): the library's own NCCL
+    communicator behind the C-ABI (`adg_comm_init`, `adg_halo_exchange`,
+    `adg_allreduce_reduce`, `adg_allreduce_sum`; csrc/adg_comm.cu) --
+    stream-ordered calls on the Simulation's stream, so the step stays
+    CUDA-graph capturable;
+  * "torch": torch.distributed P2P / all-reduce, which works on any backend;
+    the CPU test suite covers the exchange logic with gloo at world_size 2.
 """
+
+import ctypes
 
 import torch
 import torch.distributed as dist
@@ -84,6 +92,17 @@ def exchange_planes_start(send_lo, send_hi, recv_lo, recv_hi, group=None):
     return works
 
 
+class _StreamJoin:
+    """Pending halo swap on a side stream: wait() joins it into the main one."""
+
+    def __init__(self, side, main):
+        self.side = side
+        self.main = main
+
+    def wait(self):
+        self.main.wait_stream(self.side)
+
+
 class _HostToDevice:
     """Pending copy of host-staged receive planes into their device buffers."""
 
@@ -106,6 +125,55 @@ def exchange_planes(send_lo, send_hi, recv_lo, recv_hi, group=None):
     exchange_planes_wait(exchange_planes_start(send_lo, send_hi, recv_lo, recv_hi, group))
 
 
+class Communicator:
+    """An adg_comm (NCCL) on this rank's device, its unique id shared through
+    the torch.distributed group (broadcast from rank 0)."""
+
+    def __init__(self, handle, group=None, world=None, rank=None):
+        lib = _lib.load()
+        self.lib = lib
+        self.handle = handle
+        self.world = dist.get_world_size(group) if world is None else world
+        self.rank = dist.get_rank(group) if rank is None else rank
+        uid = torch.zeros(_lib.COMM_ID_BYTES, dtype=torch.uint8)
+        if self.rank == 0:
+            buf = ctypes.create_string_buffer(_lib.COMM_ID_BYTES)
+            rc = lib.adg_comm_unique_id(buf)
+            if rc != _lib.ADG_OK:
+                raise RuntimeError(f"adg_comm_unique_id failed (rc={rc})")
+            uid.copy_(torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8))
+        if self.world > 1:
+            if dist.get_backend(group) == "nccl":
+                dev = uid.to(torch.device("cuda", handle.device_index))
+                dist.broadcast(dev, dist.get_global_rank(group, 0) if group else 0, group=group)
+                uid = dev.cpu()
+            else:
+                dist.broadcast(uid, dist.get_global_rank(group, 0) if group else 0, group=group)
+        raw = bytes(uid.numpy().tobytes())
+        ptr = ctypes.c_void_p()
+        handle.call("adg_comm_init", ctypes.c_char_p(raw), int(self.world), int(self.rank),
+                    ctypes.byref(ptr))
+        self.ptr = ptr
+
+    def halo_exchange(self, grid_ref, traces, ghost_lo, ghost_hi, stream):
+        self.handle.call("adg_halo_exchange", self.ptr, grid_ref, traces.data_ptr(),
+                         ghost_lo.data_ptr(), ghost_hi.data_ptr(), stream)
+
+    def allreduce_record(self, red, stream):
+        self.handle.call("adg_allreduce_reduce", self.ptr, red.data_ptr(), stream)
+
+    def allreduce_sum(self, buf, stream):
+        self.handle.call("adg_allreduce_sum", self.ptr, buf.data_ptr(), buf.numel(), stream)
+
+    def __del__(self):
+        ptr, self.ptr = getattr(self, "ptr", None), None
+        if ptr is not None and ptr.value:
+            try:
+                self.lib.adg_comm_destroy(ptr)
+            except Exception:
+                pass
+
+
 def combine_reduce(red, group=None):
     """adg_reduce record: MAX of lam bit patterns (non-negative doubles order
     like integers), SUM of the admissible / non-finite counts."""
@@ -121,14 +189,27 @@ class SlabSimulation(Simulation):
     """
 
     def __init__(self, global_mesh, system, degree, cfl, boundary="periodic", group=None,
-                 **kw):
+                 transport=None, self_exchange=False, **kw):
+        """transport: "adg" (the C-ABI NCCL communicator), "torch"
+        (torch.distributed; default unless the backend is NCCL).
+        self_exchange: a one-rank run that still cuts the x faces and swaps
+        its own halo planes over a one-rank communicator (an on-device check
+        of the exchange path against the periodic single-domain run)."""
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.global_mesh = global_mesh
         mesh = local_mesh(global_mesh, self.world, self.rank)
         ghost = {}
-        if self.world > 1:
+        cut = self.world > 1 or self_exchange
+        if transport is None:
+            transport = ("adg" if self_exchange or (self.world > 1 and
+                                                    dist.get_backend(group) == "nccl")
+                         else "torch")
+        if transport not in ("adg", "torch"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
+        if cut:
             if kw.get("use_limiter"):
                 # the limiter's windows and DMP bounds would need a u^n ghost
                 # layer across the cut (SURVEY 8(e)); not part of C5
@@ -146,15 +227,36 @@ class SlabSimulation(Simulation):
             ghost = {(0, 0): torch.empty(n, dtype=torch.float64, device=dev),
                      (0, 1): torch.empty(n, dtype=torch.float64, device=dev)}
         super().__init__(mesh, system, degree, cfl, boundary=boundary, _ghost=ghost, **kw)
-        if self.world > 1:
+        self._comm = None
+        if cut:
             self._exchange = SlabSimulation._swap_halos
+            if transport == "adg":
+                self._comm = Communicator(self._h, group,
+                                          world=1 if self_exchange else None,
+                                          rank=0 if self_exchange else None)
+                # stream-ordered NCCL calls: the batched step graph-captures
+                self._capturable = True
+        self._cut = cut
         # boundary-layer predictor + halo swap overlapped with the interior
         self.overlap_halos = True
-        self._range_ok = (self.world > 1 and
-                          bool(_lib.load().adg_predict_range_supported(self._gp())))
+        self._range_ok = (cut and bool(_lib.load().adg_predict_range_supported(self._gp())))
 
     def _swap_halos(self, wait=True):
         buf = self._buf
+        if self._comm is not None:
+            # C-ABI NCCL transport: on a side stream when overlapped (the
+            # caller joins it before the faces), else on the step's stream
+            if wait:
+                self._comm.halo_exchange(self._gp(), buf.traces, self._ghost[(0, 0)],
+                                         self._ghost[(0, 1)], self._h.stream())
+                return []
+            main = torch.cuda.current_stream(self.device)
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self._comm.halo_exchange(self._gp(), buf.traces, self._ghost[(0, 0)],
+                                         self._ghost[(0, 1)], side.cuda_stream)
+            return [_StreamJoin(side, main)]
         n = self._ghost[(0, 0)].numel()
         face = self.mesh.n_elements * buf.tb
         lo_plane = buf.traces[0:n]                       # axis 0, side 0, first layer
@@ -166,12 +268,34 @@ class SlabSimulation(Simulation):
             return []
         return works
 
+    def close(self):
+        """Release the captured graphs (they hold the communicator's calls),
+        then the communicator."""
+        torch.cuda.synchronize(self.device)
+        bb = getattr(self, "_bb", None)
+        if bb is not None:
+            bb["graphs"].clear()
+        self._comm = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "_comm", None) is not None:
+                self.close()
+        except Exception:
+            pass
+
+    def _side_stream(self):
+        s = getattr(self, "_side", None)
+        if s is None:
+            s = self._side = torch.cuda.Stream(self.device)
+        return s
+
     def _predict_exchange(self, dt_dev):
         """Boundary layers first, their halo exchange overlapped with the
         interior predictor: predict the first and last x-layers
         of the slab, post the trace-plane swap, predict the interior, then
         make the stream wait for the swap before the face kernels."""
-        if self.world == 1:
+        if not self._cut:
             return super()._predict_exchange(dt_dev)
         nx = self.mesh.cells[0]
         E = self.mesh.n_elements
@@ -189,25 +313,36 @@ class SlabSimulation(Simulation):
     def _timestep_into(self, dt_dst, status_dst, t_end):
         if self._red_cur is None:
             self._wavespeed()
-        if self.world > 1:
+        if self._comm is not None:
+            self._comm.allreduce_record(self._buf.red[self._red_cur], self._h.stream())
+        elif self.world > 1:
             combine_reduce(self._buf.red[self._red_cur], self.group)
         super()._timestep_into(dt_dst, status_dst, t_end)
 
+    def _sum_ranks(self, t):
+        if self._comm is not None:
+            self._comm.allreduce_sum(t, self._h.stream())
+        elif self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
     def _combine_rows(self, rows):
-        if self.world > 1:
+        if self.world > 1 or self._comm is not None:
             tot = rows[:, 2:].contiguous()   # collectives need dense tensors
-            dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=self.group)
+            self._sum_ranks(tot)
             rows[:, 2:] = tot
 
     def _state_finite(self):
         if self.world > 1:
             red = self._buf.red[self._red_cur].clone()
-            dist.all_reduce(red[4:5], op=dist.ReduceOp.SUM, group=self.group)
+            if self._comm is not None:
+                self._comm.allreduce_record(red, self._h.stream())
+            else:
+                dist.all_reduce(red[4:5], op=dist.ReduceOp.SUM, group=self.group)
             return int(red[4].item()) == 0
         return super()._state_finite()
 
     def conserved_totals(self):
         tot = torch.as_tensor(super().conserved_totals(), device=self.device)
         if self.world > 1:
-            dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=self.group)
+            self._sum_ranks(tot)
         return tot.cpu().numpy()

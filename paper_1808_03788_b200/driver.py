@@ -399,6 +399,7 @@ class Simulation:
                      _ptr(buf.sweeps), self._h.stream())
 
     _exchange = None   # hook for slab decomposition (decomp.SlabSimulation)
+    _capturable = False   # the exchange is stream ordered (C-ABI NCCL transport)
 
     # -- stepping ------------------------------------------------------
     def max_timestep(self):
@@ -529,6 +530,8 @@ class Simulation:
         if fast:
             self._run_batch(max(0, max_steps - self.step_count))
             return self.step_count
+        if self.use_limiter and not self._exact_faces and self._exchange is None:
+            return self._run_limited(t_end, tiny, max_steps, on_step)
         while self.t < t_end - tiny:
             if max_steps is not None and self.step_count >= max_steps:
                 break
@@ -539,6 +542,113 @@ class Simulation:
             if on_step is not None:
                 on_step(self)
         return self.step_count
+
+    def _run_limited(self, t_end, tiny, max_steps, on_step):
+        """The limited run loop (driver.py:186-202 with _attempt_step and
+        _limit) kept on the device: dt = min(max_timestep, t_end - t) is formed
+        by adg_timestep, the attempt (predictor, faces, update, detection,
+        rescue) is enqueued without reading anything back, and ONE host
+        synchronisation per step fetches the step record (dt, t, totals,
+        troubled count, rescue failure, status, non-finite count, max sweeps)
+        to decide acceptance or the dt/2 restart (driver.py:170-184)."""
+        buf = self._buf
+        m = self._m
+        dev = self.device
+        row = torch.empty(2 + m, dtype=torch.float64, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        sw = torch.empty(1, dtype=torch.int32, device=dev)
+        rec = torch.empty(2 + m, dtype=torch.float64).pin_memory()
+        irec = torch.empty(5, dtype=torch.int64).pin_memory()
+        ints = torch.empty(5, dtype=torch.int64, device=dev)
+        lb = self._limiter_buffers()
+        E = self.mesh.n_elements
+        while self.t < t_end - tiny:
+            if max_steps is not None and self.step_count >= max_steps:
+                break
+            buf.t.fill_(self.t)
+            status.zero_()
+            self._timestep_into(row[0:1], status, t_end)
+            trial = None
+            for attempt in range(MAX_HALVINGS + 1):
+                if trial is not None:
+                    row[0] = trial
+                    buf.t.fill_(self.t)
+                nxt = self._attempt_limited_device(row)
+                torch.amax(buf.sweeps, dim=0, keepdim=True, out=sw)
+                red = buf.red[nxt]
+                torch.stack([lb["count"][0].long(), lb["failed"][0].long(), status[0].long(),
+                             red[4], sw[0].long()], out=ints)
+                rec.copy_(row, non_blocking=True)
+                irec.copy_(ints, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+                n_tr, failed, st, nonfinite, sweeps = (int(x) for x in irec.tolist())
+                if st & _lib.STATUS_NO_ADMISSIBLE:
+                    raise RuntimeError("no admissible state found while sizing the time step")
+                dt = float(rec[0])
+                if not failed:
+                    break
+                trial = 0.5 * dt   # driver.py:183 restart with half the step
+            else:
+                raise RuntimeError(f"step at t={self.t:.6g} failed after "
+                                   f"{MAX_HALVINGS} step halvings")
+            self._commit_limited(nxt)
+            self.t += dt
+            self.step_count += 1
+            self.last_limited_fraction = n_tr / E
+            self.last_troubled = lb["troubled"].clone().bool()
+            self.sweep_log.append(sweeps)
+            self._record(dt, rec[2:2 + m].numpy().copy())
+            if nonfinite:
+                raise RuntimeError(f"non-finite state after step {self.step_count}")
+            if on_step is not None:
+                on_step(self)
+        return self.step_count
+
+    def _attempt_limited_device(self, row):
+        """Enqueue one limited attempt of size row[0] with no host reads;
+        returns the wave-speed slot of the candidate.  Nothing is committed:
+        _commit_limited swaps the buffers once the host accepts it."""
+        buf = self._buf
+        lb = self._limiter_buffers()
+        sp = self._h.stream()
+        dt_dev = row[0:1]
+        if lb["sub_of"] is not self._u or self._red_cur is None:
+            self._h.call("adg_project_subcells", self._gp(), _ptr(self._u), _ptr(lb["sub"]),
+                         _ptr(lb["cmin"]), _ptr(lb["cmax"]), sp)
+            lb["sub_of"] = self._u
+        self._predict(dt_dev)
+        self._faces()
+        nxt = self._update(dt_dev, None)
+        self._h.call("adg_detect", self._gp(), _ptr(lb["sub"]), _ptr(lb["cmin"]),
+                     _ptr(lb["cmax"]), _ptr(self._u_next), _ptr(buf.pred_bad), self.dmp_delta0,
+                     self.dmp_eps, int(bool(self.force_limit_all)), None, _ptr(lb["troubled"]),
+                     _ptr(lb["idx"]), _ptr(lb["count"]), _ptr(lb["sub_n"]), _ptr(lb["cmin_n"]),
+                     _ptr(lb["cmax_n"]), sp)
+        lb["failed"].zero_()
+        # a fixed grid of rescue blocks strides over the device-side count
+        cap = min(self.mesh.n_elements, self._rescue_blocks)
+        self._h.call("adg_rescue", self._gp(), _ptr(lb["sub"]), _ptr(lb["idx"]),
+                     _ptr(lb["count"]), cap, _ptr(dt_dev), None, _ptr(self._u_next),
+                     _ptr(lb["failed"]), _ptr(lb["sub_n"]), _ptr(lb["cmin_n"]),
+                     _ptr(lb["cmax_n"]), sp)
+        # rescued cells changed u_next: its wave speeds / counts again (the
+        # update epilogue folded the candidate's), then the conserved totals
+        self._h.call("adg_wavespeed", self._gp(), _ptr(self._u_next), _ptr(buf.red[nxt]), sp)
+        self._h.call("adg_totals", self._gp(), _ptr(self._u_next), _ptr(buf.partial),
+                     _ptr(row[2:]), sp)
+        self._h.call("adg_advance_time", _ptr(buf.t), _ptr(dt_dev), _ptr(row[1:2]), sp)
+        return nxt
+
+    # rescue blocks per launch (each strides over the troubled list)
+    _rescue_blocks = 148 * 8
+
+    def _commit_limited(self, nxt):
+        lb = self._lim
+        self._u, self._u_next = self._u_next, self._u
+        self._red_cur = nxt
+        for k in ("sub", "cmin", "cmax"):
+            lb[k], lb[k + "_n"] = lb[k + "_n"], lb[k]
+        lb["sub_of"] = self._u
 
     def _combine_rows(self, rows):
         """Hook: cross-rank SUM of per-step totals (decomp.SlabSimulation)."""
@@ -620,7 +730,7 @@ class Simulation:
         buf.t.fill_(self.t)
         # only launch-bound grids gain from the graph (capture + instantiate
         # costs tens of ms once; a C2-size step is ~16 ms of GPU work)
-        use_graph = (self.graphs_enabled and self._exchange is None
+        use_graph = (self.graphs_enabled and (self._exchange is None or self._capturable)
                      and self.mesh.n_elements * self._pd <= GRAPH_MAX_DOFS)
         s = 0
         while s < k:

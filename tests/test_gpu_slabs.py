@@ -158,3 +158,40 @@ def test_predict_range_errors():
     big._ensure_buffers()
     with pytest.raises(NotImplementedError):
         big._predict_part(dt, 0, 8)
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("cells,degree,steps", [((8, 6, 5), 4, 4), ((6, 4, 4), 2, 3)])
+def test_nccl_self_exchange_equals_single_domain(cells, degree, steps, overlap):
+    """The C-ABI NCCL transport (adg_comm_init / adg_halo_exchange /
+    adg_allreduce_reduce / adg_allreduce_sum) on a one-rank communicator: the
+    x faces are cut and the rank swaps its own halo planes through NCCL
+    (send to itself as the left and right neighbour), on a side stream when
+    overlapped.  State, dt and totals equal the periodic single-domain run
+    bitwise; the batched fast path replays CUDA graphs that contain the NCCL
+    calls."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1808_03788_b200 as pkg
+    from paper_1808_03788_b200.decomp import SlabSimulation
+
+    gmesh = pkg.CartesianMesh([(0.0, 1.0)] * 3, cells)
+    system = pkg.make_system("euler", 3)
+    cfl = 0.9 / (3 * (2 * degree + 1))
+    ic, _ = pkg.build_problem("density_wave", system, velocity=[1.0, -0.5, 0.3])
+    ref = pkg.Simulation(gmesh, system, degree, cfl)
+    ref.project_initial_condition(ic)
+    ref.run(np.inf, max_steps=steps)
+    sim = SlabSimulation(gmesh, system, degree, cfl, self_exchange=True)
+    assert sim.transport == "adg" and sim._capturable
+    sim.overlap_halos = overlap
+    sim.project_initial_condition(ic)
+    sim.run(np.inf, max_steps=steps)   # batched: graphs with the NCCL calls inside
+    np.testing.assert_array_equal([h["dt"] for h in sim.history],
+                                  [h["dt"] for h in ref.history])
+    assert torch.equal(sim.u, ref.u)
+    np.testing.assert_array_equal(np.array([h["totals"] for h in sim.history]),
+                                  np.array([h["totals"] for h in ref.history]))
+    sim.run(np.inf, max_steps=steps + 1, on_step=lambda s: None)   # eager path
+    ref.run(np.inf, max_steps=steps + 1, on_step=lambda s: None)
+    assert torch.equal(sim.u, ref.u)
