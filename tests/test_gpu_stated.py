@@ -139,5 +139,9 @@ def test_c4_stated_size_512(pkg, golden):
         rows = sim.u.reshape(512, 512, -1, 4).sum(dim=(1, 2)).cpu().numpy()
         np.testing.assert_allclose(rows, g[f"u{k}_rowsum"], rtol=1e-11, atol=1e-9)
     np.testing.assert_allclose([h["dt"] for h in sim.history], g["dts"], rtol=1e-12)
+    # totals over 9.4e6 nodal terms: numpy accumulates the leading-axis
+    # reduction row by row (error bound ~ n eps ~ 1e-9 relative); the
+    # kernels' fixed-order block sums are the more accurate of the two.
+    # Momentum totals vanish by symmetry: absolute scale 1e-12.
     np.testing.assert_allclose(np.array([h["totals"] for h in sim.history]), g["totals"],
-                               rtol=1e-11)
+                               rtol=1e-9, atol=1e-12)
