@@ -11,8 +11,9 @@ Same contents as the reference's `BasisTables` (basis.py:166-202) and
   over the 2N+1 equal subcells; recovery as the mean-constrained least
   squares left inverse, solved through its KKT system.
 
-`tests/test_tables.py` pins all of them against the reference's tables to
-1e-13 (golden vectors from `tests/golden/make_golden.py`).
+`tests/test_host.py::test_product_tables_match_reference` pins all of them
+against the reference's tables to 1e-13 (golden vectors from
+`tests/golden/make_golden.py`).
 """
 
 import numpy as np
