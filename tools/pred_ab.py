@@ -36,7 +36,8 @@ tabs = pkg.basis_tables(deg)
 from paper_1808_03788_b200 import _lib
 from paper_1808_03788_b200.predictor import _grid
 h = _lib.Handle.get(u.device.index)
-g = _grid(system, (n, n, n), sim.mesh.spacings, deg)
+h.ensure_tables(tabs)
+g = _grid(system, n ** 3, sim.mesh.spacings, deg)
 E = n ** 3; pd = (deg + 1) ** 3; m = 5
 tb = pd * m + ((pd * m) & 1)
 f64 = dict(dtype=torch.float64, device=u.device)
