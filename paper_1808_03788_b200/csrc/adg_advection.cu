@@ -324,16 +324,22 @@ __global__ void adv_face_kernel(const double* __restrict__ traces, const double*
       return t;
     };
     // face states (driver.py:234-261): minus = hi trace of element fa-1,
-    // plus = lo trace of element fa; periodic wrap, or the interior trace
-    // for outflow and wall faces (a scalar's reflection is the identity,
-    // systems.py base reflect); ghost faces are refused by the launcher
+    // plus = lo trace of element fa; periodic wrap, the interior trace for
+    // outflow and wall faces (a scalar's reflection is the identity,
+    // systems.py base reflect), or the caller's exterior trace plane for
+    // ghost ("exact") faces
+    int64_t plane = 0;
+    for (int j = 0; j < D; ++j)
+      if (j != axis) plane = plane * n[j] + c[j];
     const double* pm;
     const double* pp;
     if (fa > 0) pm = tr_hi + (size_t)eidx(fa - 1) * TB;
     else if (bc_lo == ADG_BC_PERIODIC) pm = tr_hi + (size_t)eidx(n[axis] - 1) * TB;
+    else if (bc_lo == ADG_BC_GHOST) pm = ghost_lo + (size_t)plane * TB;
     else pm = tr_lo + (size_t)eidx(0) * TB;
     if (fa < n[axis]) pp = tr_lo + (size_t)eidx(fa) * TB;
     else if (bc_hi == ADG_BC_PERIODIC) pp = tr_lo + (size_t)eidx(0) * TB;
+    else if (bc_hi == ADG_BC_GHOST) pp = ghost_hi + (size_t)plane * TB;
     else pp = tr_hi + (size_t)eidx(n[axis] - 1) * TB;
     const double s = fabs(an);
     double dl = 0.0;
@@ -654,8 +660,9 @@ int adv_face_flux(const adg_grid* g, int axis, const double* traces, const doubl
     *err = "axis out of range";
     return ADG_ERR_INVALID;
   }
-  if (g->bc[axis][0] == ADG_BC_GHOST || g->bc[axis][1] == ADG_BC_GHOST) {
-    *err = "advection on the device: exact / ghost faces are not supported";
+  if ((g->bc[axis][0] == ADG_BC_GHOST && !ghost_lo) ||
+      (g->bc[axis][1] == ADG_BC_GHOST && !ghost_hi)) {
+    *err = "ghost boundary without ghost traces";
     return ADG_ERR_UNSUPPORTED;
   }
   ADG_ADV_SWITCH(adv_launch_face, g, axis, traces, ghost_lo, ghost_hi, fd, st);

@@ -140,6 +140,16 @@ static int check_euler(adg_handle* h, const adg_grid* g) {
   return ADG_OK;
 }
 
+// limiter entry points: the kernels carry Euler and advection policies
+static int check_limiter(adg_handle* h, const adg_grid* g) {
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (is_el(g))
+    return fail(h, ADG_ERR_UNSUPPORTED,
+                "elasticity-di on the device: no subcell limiter (Euler and advection)");
+  return ADG_OK;
+}
+
 static int wrap(adg_handle* h, int rc, const std::string& e) {
   if (rc != ADG_OK) h->err = e;
   return rc;
@@ -393,7 +403,7 @@ int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partia
 int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, double* sub_out,
                          double* cmin_out, double* cmax_out, void* stream) {
   DeviceGuard dg(h);
-  int rc = check_euler(h, g);
+  int rc = check_limiter(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::project_subcells(g, u, sub_out, cmin_out, cmax_out, (cudaStream_t)stream,
@@ -406,7 +416,7 @@ int adg_detect(adg_handle* h, const adg_grid* g, const double* prev_sub, const d
                int32_t* idx, int32_t* count, double* cand_sub_out, double* cand_cmin_out,
                double* cand_cmax_out, void* stream) {
   DeviceGuard dg(h);
-  int rc = check_euler(h, g);
+  int rc = check_limiter(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::detect(g, prev_sub, cmin, cmax, cand, pred_bad, delta0, eps, force_all,
@@ -419,7 +429,7 @@ int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const i
                const adg_subcell_ghosts* ghosts, double* u_out, int32_t* failed_dev,
                double* sub_next, double* cmin_next, double* cmax_next, void* stream) {
   DeviceGuard dg(h);
-  int rc = check_euler(h, g);
+  int rc = check_limiter(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::rescue(g, prev_sub, idx, count_dev, count_host_max, dt_dev, ghosts, u_out,
@@ -503,7 +513,7 @@ int adg_muscl_windows(adg_handle* h, const adg_grid* g, const double* windows, i
                       const int32_t* count_dev, const double* dt_dev, double* avg_out,
                       uint8_t* failed, void* stream) {
   DeviceGuard dg(h);
-  int rc = check_euler(h, g);
+  int rc = check_limiter(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::muscl_windows(g, windows, n_windows, count_dev, dt_dev, avg_out, failed,
@@ -513,7 +523,7 @@ int adg_muscl_windows(adg_handle* h, const adg_grid* g, const double* windows, i
 int adg_recover_subcells(adg_handle* h, const adg_grid* g, const double* ubar, double* u_out,
                          void* stream) {
   DeviceGuard dg(h);
-  int rc = check_euler(h, g);
+  int rc = check_limiter(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::recover_subcells(g, ubar, u_out, (cudaStream_t)stream, &e), e);
@@ -522,7 +532,7 @@ int adg_recover_subcells(adg_handle* h, const adg_grid* g, const double* ubar, d
 int adg_flatten_cells(adg_handle* h, const adg_grid* g, double* nodal, const double* averages,
                       int32_t* nflat, void* stream) {
   DeviceGuard dg(h);
-  int rc = check_euler(h, g);
+  int rc = check_limiter(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::flatten_cells(g, nodal, averages, nflat, (cudaStream_t)stream, &e), e);
@@ -530,7 +540,7 @@ int adg_flatten_cells(adg_handle* h, const adg_grid* g, double* nodal, const dou
 
 int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat, void* stream) {
   DeviceGuard dg(h);
-  int rc = check_euler(h, g);
+  int rc = check_limiter(h, g);
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::flatten_ic(g, u, nflat, (cudaStream_t)stream, &e), e);

@@ -7,12 +7,58 @@
 // the caller's stream and CUDA-graph capturable; nothing synchronises the
 // host.  The reference is single-process (driver.py:186-230); the exchange
 // reproduces its periodic face states (driver.py:234-248) across the cut.
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "adg_internal.h"
+
+// NCCL is bound at run time, not at link time: the process's NCCL is the one
+// torch.distributed already loaded (dlopen RTLD_NOLOAD finds it), else the
+// system libnccl.so.2.  Linking it would let a process that loads this
+// library before torch resolve torch's NCCL symbols against an older NCCL.
+namespace {
+struct NcclApi {
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommAbort) commAbort = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define ADG_NCCL_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+    ADG_NCCL_SYM(getUniqueId, "ncclGetUniqueId");
+    ADG_NCCL_SYM(commInitRank, "ncclCommInitRank");
+    ADG_NCCL_SYM(commAbort, "ncclCommAbort");
+    ADG_NCCL_SYM(groupStart, "ncclGroupStart");
+    ADG_NCCL_SYM(groupEnd, "ncclGroupEnd");
+    ADG_NCCL_SYM(send, "ncclSend");
+    ADG_NCCL_SYM(recv, "ncclRecv");
+    ADG_NCCL_SYM(allReduce, "ncclAllReduce");
+    ADG_NCCL_SYM(errorString, "ncclGetErrorString");
+#undef ADG_NCCL_SYM
+    api.ok = api.getUniqueId && api.commInitRank && api.commAbort && api.groupStart &&
+             api.groupEnd && api.send && api.recv && api.allReduce && api.errorString;
+  });
+  return api;
+}
+}  // namespace
 
 struct adg_comm {
   ncclComm_t nccl = nullptr;
@@ -25,26 +71,34 @@ namespace adg {
 
 static int nccl_fail(ncclResult_t r, std::string* err) {
   if (r == ncclSuccess) return ADG_OK;
-  *err = std::string("NCCL: ") + ncclGetErrorString(r);
+  *err = std::string("NCCL: ") + nccl().errorString(r);
   return ADG_ERR_RUNTIME;
 }
 
+static bool nccl_missing(std::string* err) {
+  if (nccl().ok) return false;
+  *err = "NCCL (libnccl.so.2) is not available in this process";
+  return true;
+}
+
 int comm_unique_id(void* out, std::string* err) {
+  if (nccl_missing(err)) return ADG_ERR_RUNTIME;
   ncclUniqueId id;
-  int rc = nccl_fail(ncclGetUniqueId(&id), err);
+  int rc = nccl_fail(nccl().getUniqueId(&id), err);
   if (rc == ADG_OK) std::memcpy(out, &id, sizeof(id));
   return rc;
 }
 
 int comm_init(int device, const void* uid, int nranks, int rank, adg_comm** out,
               std::string* err) {
+  if (nccl_missing(err)) return ADG_ERR_RUNTIME;
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof(id));
   adg_comm* c = new adg_comm();
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;
-  int rc = nccl_fail(ncclCommInitRank(&c->nccl, nranks, id, rank), err);
+  int rc = nccl_fail(nccl().commInitRank(&c->nccl, nranks, id, rank), err);
   if (rc != ADG_OK) {
     delete c;
     return rc;
@@ -59,7 +113,7 @@ int comm_destroy(adg_comm* c) {
   // it after its streams (and any CUDA graph holding its calls) are done:
   // abort frees the resources without the collective teardown handshake,
   // which can block when ranks (or interpreter shutdown) release out of step
-  if (c->nccl) ncclCommAbort(c->nccl);
+  if (c->nccl) nccl().commAbort(c->nccl);
   delete c;
   return ADG_OK;
 }
@@ -83,12 +137,12 @@ int halo_exchange(adg_comm* c, const adg_grid* g, const double* traces, double* 
   const double* hi_plane = traces + (size_t)(2 * E - layer) * tb;   // axis 0, side 1, last layer
   const int left = (c->rank - 1 + c->nranks) % c->nranks;
   const int right = (c->rank + 1) % c->nranks;
-  ncclResult_t r = ncclGroupStart();
-  if (r == ncclSuccess) r = ncclSend(lo_plane, n, ncclDouble, left, c->nccl, st);
-  if (r == ncclSuccess) r = ncclRecv(ghost_hi, n, ncclDouble, right, c->nccl, st);
-  if (r == ncclSuccess) r = ncclSend(hi_plane, n, ncclDouble, right, c->nccl, st);
-  if (r == ncclSuccess) r = ncclRecv(ghost_lo, n, ncclDouble, left, c->nccl, st);
-  ncclResult_t r2 = ncclGroupEnd();
+  ncclResult_t r = nccl().groupStart();
+  if (r == ncclSuccess) r = nccl().send(lo_plane, n, ncclDouble, left, c->nccl, st);
+  if (r == ncclSuccess) r = nccl().recv(ghost_hi, n, ncclDouble, right, c->nccl, st);
+  if (r == ncclSuccess) r = nccl().send(hi_plane, n, ncclDouble, right, c->nccl, st);
+  if (r == ncclSuccess) r = nccl().recv(ghost_lo, n, ncclDouble, left, c->nccl, st);
+  ncclResult_t r2 = nccl().groupEnd();
   return nccl_fail(r != ncclSuccess ? r : r2, err);
 }
 
@@ -96,15 +150,15 @@ int halo_exchange(adg_comm* c, const adg_grid* g, const double* traces, double* 
 // like unsigned integers), n_admissible / n_nonfinite SUM
 int allreduce_record(adg_comm* c, adg_reduce* red, cudaStream_t st, std::string* err) {
   uint64_t* w = reinterpret_cast<uint64_t*>(red);
-  ncclResult_t r = ncclGroupStart();
-  if (r == ncclSuccess) r = ncclAllReduce(w, w, 3, ncclUint64, ncclMax, c->nccl, st);
-  if (r == ncclSuccess) r = ncclAllReduce(w + 3, w + 3, 2, ncclUint64, ncclSum, c->nccl, st);
-  ncclResult_t r2 = ncclGroupEnd();
+  ncclResult_t r = nccl().groupStart();
+  if (r == ncclSuccess) r = nccl().allReduce(w, w, 3, ncclUint64, ncclMax, c->nccl, st);
+  if (r == ncclSuccess) r = nccl().allReduce(w + 3, w + 3, 2, ncclUint64, ncclSum, c->nccl, st);
+  ncclResult_t r2 = nccl().groupEnd();
   return nccl_fail(r != ncclSuccess ? r : r2, err);
 }
 
 int allreduce_sum(adg_comm* c, double* buf, int64_t n, cudaStream_t st, std::string* err) {
-  return nccl_fail(ncclAllReduce(buf, buf, (size_t)n, ncclDouble, ncclSum, c->nccl, st), err);
+  return nccl_fail(nccl().allReduce(buf, buf, (size_t)n, ncclDouble, ncclSum, c->nccl, st), err);
 }
 
 }  // namespace adg

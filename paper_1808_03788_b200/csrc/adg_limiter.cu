@@ -23,9 +23,10 @@
 
 namespace adg {
 
-template <int D, int P>
+template <int D, int P, int SYS>
 struct LimCfg {
-  static constexpr int M = D + 2;
+  // SYS 0: CompressibleEuler (m = d + 2); SYS 1: LinearAdvection (m = 1)
+  static constexpr int M = SYS == 1 ? 1 : D + 2;
   static constexpr int S = 2 * P - 1;
   static constexpr int PD = ipow(P, D);
   static constexpr int SD = ipow(S, D);
@@ -42,6 +43,7 @@ struct LimGrid {
   double gm1, gamma;
   double h[3];  // subcell widths dx_j / S
   int prim;     // predictor_mode == "primitive": MUSCL-Hancock in primitive variables
+  double a[3];  // LinearAdvection velocity (SYS 1)
   // ADG_BC_GHOST ("exact") faces: caller-evaluated exterior subcell slabs
   // (adg_subcell_ghosts); L = their layer count
   const double* slab[3][2];
@@ -55,6 +57,53 @@ __device__ __forceinline__ int64_t cell_index(const int64_t* c, const int64_t* n
 #pragma unroll
   for (int j = 0; j < D; ++j) e = e * n[j] + c[j];
   return e;
+}
+
+
+// ------------------------------------------------- system policy (SYS)
+// The limiter's physics (limiter.py runs on any HyperbolicSystem):
+// admissibility, directional flux, the subcell Rusanov pair and the
+// primitive-mode conversions.  SYS 0 = CompressibleEuler (systems.py:112-234),
+// SYS 1 = LinearAdvection (systems.py:77-109: admissible = finite, F_j = a_j q,
+// |lambda| = |a_j|, reflect = identity, primitives = conserved).
+template <int D, int SYS>
+__device__ __forceinline__ bool lim_adm(const double* q, double gm1) {
+  if constexpr (SYS == 1) return isfinite(q[0]);
+  else return admissible<D>(q, gm1);
+}
+template <int D, int SYS>
+__device__ __forceinline__ bool lim_adm_fast(const double* q, double gm1) {
+  if constexpr (SYS == 1) return isfinite(q[0]);
+  else return admissible_fast<D>(q, gm1);
+}
+template <int D, int SYS>
+__device__ __forceinline__ void lim_flux(const double* q, const LimGrid& G, int j, double* f) {
+  if constexpr (SYS == 1) f[0] = G.a[j] * q[0];
+  else flux_axis<D>(q, G.gm1, j, f);
+}
+template <int D, int SYS>
+__device__ __forceinline__ void lim_rusanov(const double* qm, const double* qp, int j,
+                                            const LimGrid& G, double* dlow, double* dhigh) {
+  if constexpr (SYS == 1) {
+    // face_fluxes (corrector.py:100-129) with s = max(|a_j|, |a_j|)
+    const double s = fabs(G.a[j]);
+    const double central = 0.5 * (G.a[j] * qm[0] + G.a[j] * qp[0]);
+    const double diss = (0.5 * s) * (qp[0] - qm[0]);
+    dlow[0] = (central + 0.0) - diss;
+    dhigh[0] = (-central + 0.0) + diss;
+  } else {
+    rusanov_pair<D>(qm, qp, j, G.gamma, G.gm1, dlow, dhigh);
+  }
+}
+template <int D, int SYS>
+__device__ __forceinline__ void lim_cons_to_prim(const double* q, double gm1, double* v) {
+  if constexpr (SYS == 1) v[0] = q[0];
+  else cons_to_prim<D>(q, gm1, v);
+}
+template <int D, int SYS>
+__device__ __forceinline__ void lim_prim_to_cons(const double* v, double gm1, double* q) {
+  if constexpr (SYS == 1) q[0] = v[0];
+  else prim_to_cons<D>(v, gm1, q);
 }
 
 // map a global subcell coordinate along axis j into the grid; returns false
@@ -90,10 +139,10 @@ __device__ __forceinline__ bool map_axis(int64_t g, int64_t nS, int bc_lo, int b
 // the grid (wall: mirror + normal-momentum flip); an exact face reads the
 // caller's slab, which was evaluated at the raw coordinates of the axes
 // padded before it (corners included) and the mapped ones of those after.
-template <int D, int P>
+template <int D, int P, int SYS>
 __device__ __forceinline__ void fetch_sub(const double* __restrict__ sub, const LimGrid& G,
                                           const int64_t* gs, double* out) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   constexpr int S = C::S, M = C::M;
   int64_t g[3] = {0, 0, 0};
   bool flip[3] = {false, false, false};
@@ -143,9 +192,11 @@ __device__ __forceinline__ void fetch_sub(const double* __restrict__ sub, const 
   }
 #pragma unroll
   for (int v = 0; v < M; ++v) out[v] = p[v];
+  if constexpr (SYS == 0) {   // reflect (systems.py:231-234); advection: identity
 #pragma unroll
-  for (int j = 0; j < D; ++j)
-    if (flip[j]) out[1 + j] = -out[1 + j];
+    for (int j = 0; j < D; ++j)
+      if (flip[j]) out[1 + j] = -out[1 + j];
+  }
 }
 
 // subcell averages of one cell's nodal data held in shared memory:
@@ -154,11 +205,11 @@ __device__ __forceinline__ void fetch_sub(const double* __restrict__ sub, const 
 // Ps: the projection matrix P_sub [S][P] staged in shared memory (the
 // lanes of a pass index different rows: constant-bank reads would replay
 // once per distinct row); null -> the constant tables
-template <int D, int P, bool WARP = false, bool SPS = false>
+template <int D, int P, int SYS, bool WARP = false, bool SPS = false>
 __device__ void project_cell(const double* __restrict__ nodal, double* __restrict__ tmp,
                              double* __restrict__ out, int tid, int nt,
                              const double* __restrict__ Ps = nullptr) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   constexpr int S = C::S, M = C::M;
   const DegreeTables& T = tab<P>();
   auto pm = [&](int idx) { return SPS ? Ps[idx] : T.sub_project[idx]; };
@@ -255,9 +306,9 @@ __device__ void project_cell(const double* __restrict__ nodal, double* __restric
   }
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 __device__ __forceinline__ size_t proj_scratch() {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   return D == 3 ? (size_t)C::S * C::S * P * C::M : (size_t)C::S * P * C::M;
 }
 
@@ -265,9 +316,9 @@ __device__ __forceinline__ size_t proj_scratch() {
 // Limiter screening is one warp per cell: a cell's projection is a few
 // hundred short dot products, so a warp keeps all lanes busy without
 // block-wide barriers, and 8 cells share a CTA.
-template <int D, int P>
+template <int D, int P, int SYS>
 struct WarpCfg {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   static constexpr int SCR = D == 3 ? C::S * C::S * P * C::M : C::S * P * C::M;
   static constexpr int OUT = (D == 3 ? C::S * P * P * C::M : 0) > C::SD * C::M
                                  ? C::S * P * P * C::M : C::SD * C::M;
@@ -284,9 +335,9 @@ struct WarpCfg {
 };
 
 // P_sub of this degree into the CTA's shared copy (before any warp uses it)
-template <int D, int P>
+template <int D, int P, int SYS>
 __device__ __forceinline__ const double* stage_psub(double* dst) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   const DegreeTables& T = tab<P>();
   for (int x = threadIdx.x; x < C::S * P; x += blockDim.x) dst[x] = T.sub_project[x];
   __syncthreads();
@@ -295,9 +346,9 @@ __device__ __forceinline__ const double* stage_psub(double* dst) {
 
 // per-block scratch of the block-per-cell kernels (doubles); above 227 KB
 // they run on an L2-resident global scratch instead of shared memory
-template <int D, int P>
+template <int D, int P, int SYS>
 struct LimDbl {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   static constexpr size_t TMP = D == 3 ? (size_t)P * C::S * C::S * C::M + (size_t)P * P * C::S * C::M
                                        : (size_t)P * C::S * C::M;
   static constexpr size_t RESCUE = (size_t)C::WD * C::M + (size_t)C::RD * C::M * (1 + D) +
@@ -313,14 +364,14 @@ struct LimDbl {
 
 // per-cell subcell averages + extrema of nodal data staged in a warp's
 // shared slice; writes sub / cmin / cmax of cell e when they are non-null
-template <int D, int P>
+template <int D, int P, int SYS>
 __device__ __forceinline__ void warp_project_store(double* nodal, double* out, double* tmp,
                                                    int lane, int64_t e, double* sub,
                                                    double* cmin, double* cmax,
                                                    const double* Ps) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   constexpr int M = C::M, SD = C::SD;
-  project_cell<D, P, true, true>(nodal, tmp, out, lane, 32, Ps);
+  project_cell<D, P, SYS, true, true>(nodal, tmp, out, lane, 32, Ps);
   __syncwarp();
   if (sub)
     for (int x = lane; x < SD * M; x += 32) sub[(size_t)e * SD * M + x] = out[x];
@@ -346,35 +397,35 @@ __device__ __forceinline__ void warp_project_store(double* nodal, double* out, d
 }
 
 // prev_sub + per-cell extrema of u^n
-template <int D, int P>
-__global__ void __launch_bounds__(WarpCfg<D, P>::WPBX * 32)
+template <int D, int P, int SYS>
+__global__ void __launch_bounds__(WarpCfg<D, P, SYS>::WPBX * 32)
 subcell_prep_kernel(const double* __restrict__ u, int64_t E, double* __restrict__ sub,
                     double* __restrict__ cmin, double* __restrict__ cmax, double* gscr) {
-  using C = LimCfg<D, P>;
-  using W = WarpCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
+  using W = WarpCfg<D, P, SYS>;
   constexpr int M = C::M, PD = C::PD;
   extern __shared__ __align__(16) double lsm_s[];
   double* lsm = W::GS ? gscr + (size_t)blockIdx.x * W::BLOCK_DBL : lsm_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* Ps = stage_psub<D, P>(lsm + W::WPBX * W::PER_WARP);
+  const double* Ps = stage_psub<D, P, SYS>(lsm + W::WPBX * W::PER_WARP);
   double* nodal = lsm + warp * W::PER_WARP;
   double* out = nodal + PD * M;
   double* tmp = out + W::OUT;
   for (int64_t e = (int64_t)blockIdx.x * W::WPBX + warp; e < E; e += (int64_t)gridDim.x * W::WPBX) {
     for (int x = lane; x < PD * M; x += 32) nodal[x] = u[(size_t)e * PD * M + x];
     __syncwarp();
-    warp_project_store<D, P>(nodal, out, tmp, lane, e, sub, cmin, cmax, Ps);
+    warp_project_store<D, P, SYS>(nodal, out, tmp, lane, e, sub, cmin, cmax, Ps);
     __syncwarp();
   }
 }
 
 // min/max over the ghost cell beyond face (axis j, side) of cell c: the
 // reference pads S subcell layers through the face kind (driver.py:317-340)
-template <int D, int P>
+template <int D, int P, int SYS>
 __device__ void ghost_extrema(const double* __restrict__ sub, const double* __restrict__ cmin,
                               const double* __restrict__ cmax, const LimGrid& G,
                               const int64_t* c, int j, int side, double* lo, double* hi) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   constexpr int S = C::S, M = C::M;
   const int kind = G.bc[j][side];
   int64_t cc[3] = {c[0], c[1], c[2]};
@@ -404,7 +455,7 @@ __device__ void ghost_extrema(const double* __restrict__ sub, const double* __re
         gs[a] = a == j ? (side ? G.n[j] * S + ia : ia - S) : c[a] * S + ia;
       }
       double q[M];
-      fetch_sub<D, P>(sub, G, gs, q);
+      fetch_sub<D, P, SYS>(sub, G, gs, q);
 #pragma unroll
       for (int v = 0; v < M; ++v) {
         lo[v] = fmin(lo[v], q[v]);
@@ -420,9 +471,11 @@ __device__ void ghost_extrema(const double* __restrict__ sub, const double* __re
       lo[v] = cmin[e * M + v];
       hi[v] = cmax[e * M + v];
     }
-    const double a = lo[1 + j], b = hi[1 + j];
-    lo[1 + j] = -b;
-    hi[1 + j] = -a;
+    if constexpr (SYS == 0) {
+      const double a = lo[1 + j], b = hi[1 + j];
+      lo[1 + j] = -b;
+      hi[1 + j] = -a;
+    }
     return;
   }
   // outflow: every ghost layer repeats the edge subcell layer
@@ -453,21 +506,21 @@ __device__ void ghost_extrema(const double* __restrict__ sub, const double* __re
 // sub_out / cmin_out / cmax_out (when non-null): for every cell the rescue
 // leaves alone they are exactly the next step's prev_sub, so the driver
 // skips the separate projection of u^(n+1).
-template <int D, int P>
-__global__ void __launch_bounds__(WarpCfg<D, P>::WPBX * 32)
+template <int D, int P, int SYS>
+__global__ void __launch_bounds__(WarpCfg<D, P, SYS>::WPBX * 32)
 detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cmin,
               const double* __restrict__ cmax, const double* __restrict__ cand,
               const uint8_t* __restrict__ pred_bad, LimGrid G, int64_t E, double delta0,
               double eps, int force_all, uint8_t* __restrict__ troubled, int32_t* idx,
               int32_t* count, double* __restrict__ sub_out, double* __restrict__ cmin_out,
               double* __restrict__ cmax_out, double* gscr) {
-  using C = LimCfg<D, P>;
-  using W = WarpCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
+  using W = WarpCfg<D, P, SYS>;
   constexpr int M = C::M, SD = C::SD, PD = C::PD;
   extern __shared__ __align__(16) double lsm_s[];
   double* lsm = W::GS ? gscr + (size_t)blockIdx.x * W::BLOCK_DBL : lsm_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* Ps = stage_psub<D, P>(lsm + W::WPBX * W::PER_WARP);
+  const double* Ps = stage_psub<D, P, SYS>(lsm + W::WPBX * W::PER_WARP);
   double* nodal = lsm + warp * W::PER_WARP;
   double* out = nodal + PD * M;
   double* tmp = out + W::OUT;
@@ -514,7 +567,7 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
           lo = fmin(lo, nlo[2 * j + side]);
           hi = fmax(hi, nhi[2 * j + side]);
         } else {   // warp-uniform: a boundary face of this cell
-          if (lane == 0) ghost_extrema<D, P>(prev_sub, cmin, cmax, G, c, j, side, s_lo, s_hi);
+          if (lane == 0) ghost_extrema<D, P, SYS>(prev_sub, cmin, cmax, G, c, j, side, s_lo, s_hi);
           __syncwarp();
           lo = fmin(lo, s_lo[vq]);
           hi = fmax(hi, s_hi[vq]);
@@ -530,15 +583,15 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
       }
     }
     __syncwarp();
-    warp_project_store<D, P>(nodal, out, tmp, lane, e, sub_out, cmin_out, cmax_out, Ps);
+    warp_project_store<D, P, SYS>(nodal, out, tmp, lane, e, sub_out, cmin_out, cmax_out, Ps);
     int bad = lane == 0 ? (force_all || pred_bad[e]) : 0;
     for (int x = lane; x < SD; x += 32) {
       const double* q = out + x * M;
 #pragma unroll
       for (int v = 0; v < M; ++v) bad |= (q[v] < s_lo[v]) | (q[v] > s_hi[v]);
-      bad |= !admissible_fast<D>(q, G.gm1);
+      bad |= !lim_adm_fast<D, SYS>(q, G.gm1);
     }
-    for (int nd = lane; nd < PD; nd += 32) bad |= !admissible_fast<D>(nodal + nd * M, G.gm1);
+    for (int nd = lane; nd < PD; nd += 32) bad |= !lim_adm_fast<D, SYS>(nodal + nd * M, G.gm1);
     bad = __any_sync(0xffffffffu, bad);
     if (lane == 0) {
       troubled[e] = (uint8_t)bad;
@@ -551,25 +604,27 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
 // Rusanov one-sided terms (corrector.py:100-129) live in adg_common.cuh
 // face states of the primitive-mode half step back to conservative
 // (limiter.py:160-171)
-template <int D>
+template <int D, int SYS>
 __device__ __forceinline__ void to_cons2(double* a, double* b, double gm1) {
-  constexpr int M = D + 2;
-  double t[M];
-  prim_to_cons<D>(a, gm1, t);
+  if constexpr (SYS == 0) {
+    constexpr int M = D + 2;
+    double t[M];
+    prim_to_cons<D>(a, gm1, t);
 #pragma unroll
-  for (int v = 0; v < M; ++v) a[v] = t[v];
-  prim_to_cons<D>(b, gm1, t);
+    for (int v = 0; v < M; ++v) a[v] = t[v];
+    prim_to_cons<D>(b, gm1, t);
 #pragma unroll
-  for (int v = 0; v < M; ++v) b[v] = t[v];
+    for (int v = 0; v < M; ++v) b[v] = t[v];
+  }
 }
 
 // nodal polynomial of one cell from its S^d subcell averages
 // (recover_from_subcells, limiter.py:36-42): sequential per-axis
 // contraction with R_sub; tmp needs P S^(D-1) m (+ P^2 S m for D = 3) doubles
-template <int D, int P>
+template <int D, int P, int SYS>
 __device__ void recover_cell(const double* __restrict__ nw, double* __restrict__ tmp,
                              double* __restrict__ nod, int tid, int NT) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   constexpr int M = C::M, S = C::S, PD = C::PD;
   const DegreeTables& T = tab<P>();
     if (D == 1) {
@@ -629,21 +684,21 @@ __device__ void recover_cell(const double* __restrict__ nw, double* __restrict__
 // *failed.  WIN = 1: muscl_subcell_step on caller windows (limiter.py:104-121):
 // window b is windows[b], the new averages go to avg_out[b] and the
 // per-window failure flag to fail_each[b].
-template <int D, int P, int WIN>
-__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+template <int D, int P, int SYS, int WIN>
+__global__ void __launch_bounds__(LimCfg<D, P, SYS>::NT)
 rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ idx,
               const int32_t* __restrict__ count, LimGrid G, const double* __restrict__ dt_dev,
               double* __restrict__ u_out, int32_t* failed, const double* __restrict__ windows,
               double* __restrict__ avg_out, uint8_t* __restrict__ fail_each,
               double* __restrict__ sub_next, double* __restrict__ cmin_next,
               double* __restrict__ cmax_next, double* gscr) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   constexpr int M = C::M, S = C::S, SD = C::SD, PD = C::PD, W = C::W, WD = C::WD, R = C::R,
                 RD = C::RD, NT = C::NT;
   const DegreeTables& T = tab<P>();
-  constexpr bool GS = LimDbl<D, P>::RESCUE > LimDbl<D, P>::LIM;
+  constexpr bool GS = LimDbl<D, P, SYS>::RESCUE > LimDbl<D, P, SYS>::LIM;
   extern __shared__ __align__(16) double lsm_s[];
-  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P>::RESCUE : lsm_s;
+  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P, SYS>::RESCUE : lsm_s;
   double* win = lsm;                    // [WD][M]
   double* vh = win + WD * M;            // [RD][M]  half-step states
   double* sl = vh + RD * M;             // [RD][D][M] limited slopes
@@ -676,11 +731,11 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
           gs[j] = c[j] * S - 2 + rem % W;
           rem /= W;
         }
-        fetch_sub<D, P>(prev_sub, G, gs, win + w * M);
+        fetch_sub<D, P, SYS>(prev_sub, G, gs, win + w * M);
       }
       if (G.prim) {   // limiter.py:127-128: the window in primitive variables
         double vv[M];
-        cons_to_prim<D>(win + w * M, G.gm1, vv);
+        lim_cons_to_prim<D, SYS>(win + w * M, G.gm1, vv);
 #pragma unroll
         for (int v = 0; v < M; ++v) win[w * M + v] = vv[v];
       }
@@ -724,7 +779,7 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
         for (int v = 0; v < M; ++v) rate[v] = 0.0;
         if (G.prim) {
           // limiter.py:146-147: half = c + dt/2 primitive_rhs(c, slopes)
-          primitive_rhs<D>(cq, slope, G.gamma, rate);
+          if constexpr (SYS == 0) primitive_rhs<D>(cq, slope, G.gamma, rate);
         } else {
 #pragma unroll
         for (int j = 0; j < D; ++j) {
@@ -735,8 +790,8 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
             qh[v] = cq[v] + off;
             ql[v] = cq[v] - off;
           }
-          flux_axis<D>(qh, G.gm1, j, fh);
-          flux_axis<D>(ql, G.gm1, j, fl);
+          lim_flux<D, SYS>(qh, G, j, fh);
+          lim_flux<D, SYS>(ql, G, j, fl);
 #pragma unroll
           for (int v = 0; v < M; ++v) rate[v] = rate[v] - (fh[v] - fl[v]) / G.h[j];
         }
@@ -760,14 +815,14 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
           }
           if (G.prim) {
             double tq[M];
-            prim_to_cons<D>(lo, G.gm1, tq);
+            lim_prim_to_cons<D, SYS>(lo, G.gm1, tq);
 #pragma unroll
             for (int v = 0; v < M; ++v) lo[v] = tq[v];
-            prim_to_cons<D>(hi, G.gm1, tq);
+            lim_prim_to_cons<D, SYS>(hi, G.gm1, tq);
 #pragma unroll
             for (int v = 0; v < M; ++v) hi[v] = tq[v];
           }
-          ok = ok && admissible<D>(lo, G.gm1) && admissible<D>(hi, G.gm1);
+          ok = ok && lim_adm<D, SYS>(lo, G.gm1) && lim_adm<D, SYS>(hi, G.gm1);
         }
         if (!ok) s_ok = 0;
       }
@@ -796,7 +851,7 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
         } else if (G.prim) {
           int64_t gs[3] = {0, 0, 0};
           for (int j = 0; j < D; ++j) gs[j] = c[j] * S + si[j];
-          fetch_sub<D, P>(prev_sub, G, gs, q);
+          fetch_sub<D, P, SYS>(prev_sub, G, gs, q);
         } else {
 #pragma unroll
           for (int v = 0; v < M; ++v) q[v] = win[wcore() * M + v];
@@ -811,21 +866,21 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
             a[v] = vh[rc * M + v] + sl[(rc * D + j) * M + v];
             bq[v] = vh[rh * M + v] - sl[(rh * D + j) * M + v];
           }
-          if (G.prim) to_cons2<D>(a, bq, G.gm1);
-          rusanov_pair<D>(a, bq, j, G.gamma, G.gm1, dlo_h, dhi_h);
+          if (G.prim) to_cons2<D, SYS>(a, bq, G.gm1);
+          lim_rusanov<D, SYS>(a, bq, j, G, dlo_h, dhi_h);
           // low face: minus = hi state of previous, plus = lo state of this
 #pragma unroll
           for (int v = 0; v < M; ++v) {
             a[v] = vh[rl * M + v] + sl[(rl * D + j) * M + v];
             bq[v] = vh[rc * M + v] - sl[(rc * D + j) * M + v];
           }
-          if (G.prim) to_cons2<D>(a, bq, G.gm1);
-          rusanov_pair<D>(a, bq, j, G.gamma, G.gm1, dlo_l, dhi_l);
+          if (G.prim) to_cons2<D, SYS>(a, bq, G.gm1);
+          lim_rusanov<D, SYS>(a, bq, j, G, dlo_l, dhi_l);
           const double c_j = dt / G.h[j];
 #pragma unroll
           for (int v = 0; v < M; ++v) q[v] -= c_j * (dlo_h[v] + dhi_l[v]);
         }
-        if (!admissible<D>(q, G.gm1)) s_ok = 0;
+        if (!lim_adm<D, SYS>(q, G.gm1)) s_ok = 0;
 #pragma unroll
         for (int v = 0; v < M; ++v) nw[s * M + v] = q[v];
       }
@@ -846,21 +901,21 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
       __syncthreads();
       continue;
     }
-    recover_cell<D, P>(nw, tmp, nod, tid, NT);
+    recover_cell<D, P, SYS>(nw, tmp, nod, tid, NT);
     __syncthreads();
     // flatten_inadmissible (limiter.py:205-223): nodal and its subcell
     // projection must be admissible, else the cell becomes its mean
     if (tid == 0) s_flat = 0;
     __syncthreads();
     for (int nd = tid; nd < PD; nd += NT)
-      if (!admissible<D>(nod + nd * M, G.gm1)) s_flat = 1;
+      if (!lim_adm<D, SYS>(nod + nd * M, G.gm1)) s_flat = 1;
     __syncthreads();
     if (!s_flat) {
       double* pj = vh;    // reuse: projection of the recovered polynomial
-      project_cell<D, P>(nod, tmp + PD * M * 0 + (D == 3 ? P * S * S * M : P * S * M), pj, tid, NT);
+      project_cell<D, P, SYS>(nod, tmp + PD * M * 0 + (D == 3 ? P * S * S * M : P * S * M), pj, tid, NT);
       __syncthreads();
       for (int s = tid; s < SD; s += NT)
-        if (!admissible<D>(pj + s * M, G.gm1)) s_flat = 1;
+        if (!lim_adm<D, SYS>(pj + s * M, G.gm1)) s_flat = 1;
       __syncthreads();
     }
     double* dst = u_out + (size_t)e * PD * M;
@@ -881,7 +936,7 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
       // (same arithmetic as the screen's projection of unrescued cells)
       __syncthreads();
       double* pj = vh;
-      project_cell<D, P>(nod, tmp + (D == 3 ? P * S * S * M : P * S * M), pj, tid, NT);
+      project_cell<D, P, SYS>(nod, tmp + (D == 3 ? P * S * S * M : P * S * M), pj, tid, NT);
       __syncthreads();
       for (int x = tid; x < SD * M; x += NT) sub_next[(size_t)e * SD * M + x] = pj[x];
       if (tid < 32) {
@@ -910,15 +965,15 @@ rescue_kernel(const double* __restrict__ prev_sub, const int32_t* __restrict__ i
 
 // recover_from_subcells (limiter.py:36-42) on E cells: ubar [E][S^d][m] ->
 // nodal [E][P^d][m]
-template <int D, int P>
-__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+template <int D, int P, int SYS>
+__global__ void __launch_bounds__(LimCfg<D, P, SYS>::NT)
 recover_kernel(const double* __restrict__ ubar, int64_t E, double* __restrict__ out,
                double* gscr) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
-  constexpr bool GS = LimDbl<D, P>::RECOVER > LimDbl<D, P>::LIM;
+  constexpr bool GS = LimDbl<D, P, SYS>::RECOVER > LimDbl<D, P, SYS>::LIM;
   extern __shared__ __align__(16) double lsm_s[];
-  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P>::RECOVER : lsm_s;
+  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P, SYS>::RECOVER : lsm_s;
   double* nw = lsm;
   double* nod = nw + SD * M;
   double* tmp = nod + PD * M;
@@ -926,7 +981,7 @@ recover_kernel(const double* __restrict__ ubar, int64_t E, double* __restrict__ 
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
     for (int x = tid; x < SD * M; x += NT) nw[x] = ubar[(size_t)e * SD * M + x];
     __syncthreads();
-    recover_cell<D, P>(nw, tmp, nod, tid, NT);
+    recover_cell<D, P, SYS>(nw, tmp, nod, tid, NT);
     __syncthreads();
     for (int x = tid; x < PD * M; x += NT) out[(size_t)e * PD * M + x] = nod[x];
     __syncthreads();
@@ -936,15 +991,15 @@ recover_kernel(const double* __restrict__ ubar, int64_t E, double* __restrict__ 
 // flatten_inadmissible (limiter.py:205-223) on E cells, in place on nodal:
 // a cell whose nodal states or their subcell projection are inadmissible
 // becomes the mean of its subcell averages; *nflat counts them
-template <int D, int P>
-__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+template <int D, int P, int SYS>
+__global__ void __launch_bounds__(LimCfg<D, P, SYS>::NT)
 flatten_cells_kernel(double* __restrict__ nodal, const double* __restrict__ averages, int64_t E,
                      double gm1, int32_t* nflat, double* gscr) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
-  constexpr bool GS = LimDbl<D, P>::PROJ > LimDbl<D, P>::LIM;
+  constexpr bool GS = LimDbl<D, P, SYS>::PROJ > LimDbl<D, P, SYS>::LIM;
   extern __shared__ __align__(16) double lsm_s[];
-  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P>::PROJ : lsm_s;
+  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P, SYS>::PROJ : lsm_s;
   double* nod = lsm;
   double* pj = nod + PD * M;
   double* tmp = pj + SD * M;
@@ -956,11 +1011,11 @@ flatten_cells_kernel(double* __restrict__ nodal, const double* __restrict__ aver
     for (int x = tid; x < PD * M; x += NT) nod[x] = ne[x];
     if (tid == 0) s_flat = 0;
     __syncthreads();
-    project_cell<D, P>(nod, tmp, pj, tid, NT);
+    project_cell<D, P, SYS>(nod, tmp, pj, tid, NT);
     __syncthreads();
     int bad = 0;
-    for (int nd = tid; nd < PD; nd += NT) bad |= !admissible<D>(nod + nd * M, gm1);
-    for (int x = tid; x < SD; x += NT) bad |= !admissible<D>(pj + x * M, gm1);
+    for (int nd = tid; nd < PD; nd += NT) bad |= !lim_adm<D, SYS>(nod + nd * M, gm1);
+    for (int x = tid; x < SD; x += NT) bad |= !lim_adm<D, SYS>(pj + x * M, gm1);
     if (bad) s_flat = 1;
     __syncthreads();
     if (s_flat) {
@@ -978,16 +1033,16 @@ flatten_cells_kernel(double* __restrict__ nodal, const double* __restrict__ aver
 }
 
 // IC flattening (driver.py:137-152): one block per cell
-template <int D, int P>
-__global__ void __launch_bounds__(LimCfg<D, P>::NT)
+template <int D, int P, int SYS>
+__global__ void __launch_bounds__(LimCfg<D, P, SYS>::NT)
 flatten_ic_kernel(double* __restrict__ u, int64_t E, double gm1, int32_t* nflat,
                   double* gscr) {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   constexpr int M = C::M, SD = C::SD, PD = C::PD, NT = C::NT;
   const DegreeTables& T = tab<P>();
-  constexpr bool GS = LimDbl<D, P>::PROJ > LimDbl<D, P>::LIM;
+  constexpr bool GS = LimDbl<D, P, SYS>::PROJ > LimDbl<D, P, SYS>::LIM;
   extern __shared__ __align__(16) double lsm_s[];
-  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P>::PROJ : lsm_s;
+  double* lsm = GS ? gscr + (size_t)blockIdx.x * LimDbl<D, P, SYS>::PROJ : lsm_s;
   double* nodal = lsm;
   double* out = nodal + PD * M;
   double* tmp = out + SD * M;
@@ -998,11 +1053,11 @@ flatten_ic_kernel(double* __restrict__ u, int64_t E, double gm1, int32_t* nflat,
     for (int x = tid; x < PD * M; x += NT) nodal[x] = ue[x];
     if (tid == 0) s_bad = 0;
     __syncthreads();
-    project_cell<D, P>(nodal, tmp, out, tid, NT);
+    project_cell<D, P, SYS>(nodal, tmp, out, tid, NT);
     __syncthreads();
     int bad = 0;
-    for (int s = tid; s < SD; s += NT) bad |= !admissible<D>(out + s * M, gm1);
-    for (int nd = tid; nd < PD; nd += NT) bad |= !admissible<D>(nodal + nd * M, gm1);
+    for (int s = tid; s < SD; s += NT) bad |= !lim_adm<D, SYS>(out + s * M, gm1);
+    for (int nd = tid; nd < PD; nd += NT) bad |= !lim_adm<D, SYS>(nodal + nd * M, gm1);
     if (bad) s_bad = 1;
     __syncthreads();
     if (s_bad) {
@@ -1062,22 +1117,23 @@ static LimGrid lim_grid(const adg_grid* g, const adg_subcell_ghosts* gh = nullpt
   }
   G.gamma = g->gamma;
   G.gm1 = g->gamma - 1.0;
-  G.prim = g->mode == ADG_MODE_PRIMITIVE ? 1 : 0;
+  G.prim = (g->system == ADG_SYS_EULER && g->mode == ADG_MODE_PRIMITIVE) ? 1 : 0;
+  for (int j = 0; j < 3; ++j) G.a[j] = j < g->dim ? g->velocity[j] : 0.0;
   return G;
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 static size_t proj_smem() {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   const size_t out = D == 3 ? (size_t)C::S * P * P * C::M : (size_t)C::SD * C::M;
   const size_t tmp = D == 3 ? (size_t)C::S * C::S * P * C::M : (size_t)C::S * P * C::M;
   return ((size_t)C::PD * C::M + (out > (size_t)C::SD * C::M ? out : (size_t)C::SD * C::M) +
           tmp) * 8;
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 static size_t rescue_smem() {
-  using C = LimCfg<D, P>;
+  using C = LimCfg<D, P, SYS>;
   const size_t tmp = D == 3 ? (size_t)P * C::S * C::S * C::M + (size_t)P * P * C::S * C::M
                             : (size_t)P * C::S * C::M;
   return ((size_t)C::WD * C::M + (size_t)C::RD * C::M * (1 + D) + (size_t)C::SD * C::M + tmp +
@@ -1104,43 +1160,50 @@ static bool lim_supported(const adg_grid* g, const adg_subcell_ghosts* gh, std::
   return true;
 }
 
-#define ADG_LIM_SWITCH(FN, ...)                                                 \
+#define ADG_LIM_SWITCH_S(SYS_, FN, ...)                                                 \
   do {                                                                          \
     switch (g->dim * 16 + g->degree + 1) {                                      \
-      case 17: rc = FN<1, 1>(__VA_ARGS__); break;                               \
-      case 18: rc = FN<1, 2>(__VA_ARGS__); break;                               \
-      case 19: rc = FN<1, 3>(__VA_ARGS__); break;                               \
-      case 20: rc = FN<1, 4>(__VA_ARGS__); break;                               \
-      case 21: rc = FN<1, 5>(__VA_ARGS__); break;                               \
-      case 22: rc = FN<1, 6>(__VA_ARGS__); break;                               \
-      case 23: rc = FN<1, 7>(__VA_ARGS__); break;                               \
-      case 24: rc = FN<1, 8>(__VA_ARGS__); break;                               \
-      case 25: rc = FN<1, 9>(__VA_ARGS__); break;                               \
-      case 26: rc = FN<1, 10>(__VA_ARGS__); break;                              \
-      case 33: rc = FN<2, 1>(__VA_ARGS__); break;                               \
-      case 34: rc = FN<2, 2>(__VA_ARGS__); break;                               \
-      case 35: rc = FN<2, 3>(__VA_ARGS__); break;                               \
-      case 36: rc = FN<2, 4>(__VA_ARGS__); break;                               \
-      case 37: rc = FN<2, 5>(__VA_ARGS__); break;                               \
-      case 38: rc = FN<2, 6>(__VA_ARGS__); break;                               \
-      case 39: rc = FN<2, 7>(__VA_ARGS__); break;                               \
-      case 40: rc = FN<2, 8>(__VA_ARGS__); break;                               \
-      case 41: rc = FN<2, 9>(__VA_ARGS__); break;                               \
-      case 42: rc = FN<2, 10>(__VA_ARGS__); break;                              \
-      case 49: rc = FN<3, 1>(__VA_ARGS__); break;                               \
-      case 50: rc = FN<3, 2>(__VA_ARGS__); break;                               \
-      case 51: rc = FN<3, 3>(__VA_ARGS__); break;                               \
-      case 52: rc = FN<3, 4>(__VA_ARGS__); break;                               \
-      case 53: rc = FN<3, 5>(__VA_ARGS__); break;                               \
-      case 54: rc = FN<3, 6>(__VA_ARGS__); break;                               \
-      case 55: rc = FN<3, 7>(__VA_ARGS__); break;                               \
-      case 56: rc = FN<3, 8>(__VA_ARGS__); break;                               \
-      case 57: rc = FN<3, 9>(__VA_ARGS__); break;                               \
-      case 58: rc = FN<3, 10>(__VA_ARGS__); break;                              \
+      case 17: rc = FN<1, 1, SYS_>(__VA_ARGS__); break;                               \
+      case 18: rc = FN<1, 2, SYS_>(__VA_ARGS__); break;                               \
+      case 19: rc = FN<1, 3, SYS_>(__VA_ARGS__); break;                               \
+      case 20: rc = FN<1, 4, SYS_>(__VA_ARGS__); break;                               \
+      case 21: rc = FN<1, 5, SYS_>(__VA_ARGS__); break;                               \
+      case 22: rc = FN<1, 6, SYS_>(__VA_ARGS__); break;                               \
+      case 23: rc = FN<1, 7, SYS_>(__VA_ARGS__); break;                               \
+      case 24: rc = FN<1, 8, SYS_>(__VA_ARGS__); break;                               \
+      case 25: rc = FN<1, 9, SYS_>(__VA_ARGS__); break;                               \
+      case 26: rc = FN<1, 10, SYS_>(__VA_ARGS__); break;                              \
+      case 33: rc = FN<2, 1, SYS_>(__VA_ARGS__); break;                               \
+      case 34: rc = FN<2, 2, SYS_>(__VA_ARGS__); break;                               \
+      case 35: rc = FN<2, 3, SYS_>(__VA_ARGS__); break;                               \
+      case 36: rc = FN<2, 4, SYS_>(__VA_ARGS__); break;                               \
+      case 37: rc = FN<2, 5, SYS_>(__VA_ARGS__); break;                               \
+      case 38: rc = FN<2, 6, SYS_>(__VA_ARGS__); break;                               \
+      case 39: rc = FN<2, 7, SYS_>(__VA_ARGS__); break;                               \
+      case 40: rc = FN<2, 8, SYS_>(__VA_ARGS__); break;                               \
+      case 41: rc = FN<2, 9, SYS_>(__VA_ARGS__); break;                               \
+      case 42: rc = FN<2, 10, SYS_>(__VA_ARGS__); break;                              \
+      case 49: rc = FN<3, 1, SYS_>(__VA_ARGS__); break;                               \
+      case 50: rc = FN<3, 2, SYS_>(__VA_ARGS__); break;                               \
+      case 51: rc = FN<3, 3, SYS_>(__VA_ARGS__); break;                               \
+      case 52: rc = FN<3, 4, SYS_>(__VA_ARGS__); break;                               \
+      case 53: rc = FN<3, 5, SYS_>(__VA_ARGS__); break;                               \
+      case 54: rc = FN<3, 6, SYS_>(__VA_ARGS__); break;                               \
+      case 55: rc = FN<3, 7, SYS_>(__VA_ARGS__); break;                               \
+      case 56: rc = FN<3, 8, SYS_>(__VA_ARGS__); break;                               \
+      case 57: rc = FN<3, 9, SYS_>(__VA_ARGS__); break;                               \
+      case 58: rc = FN<3, 10, SYS_>(__VA_ARGS__); break;                              \
       default:                                                                  \
         *err = "subcell limiter on the device: unsupported dim / degree";      \
         return ADG_ERR_UNSUPPORTED;                                             \
     }                                                                           \
+  } while (0)
+
+// Euler or advection instantiation of a launcher, by the grid's plugin
+#define ADG_LIM_SWITCH(FN, ...)                                                 \
+  do {                                                                          \
+    if (g->system == ADG_SYS_ADVECTION) ADG_LIM_SWITCH_S(1, FN, __VA_ARGS__);   \
+    else ADG_LIM_SWITCH_S(0, FN, __VA_ARGS__);                                  \
   } while (0)
 
 static int lerr(std::string* err) {
@@ -1152,11 +1215,11 @@ static int lerr(std::string* err) {
   return ADG_OK;
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 static int launch_prep(const adg_grid* g, const double* u, double* sub, double* cmin,
                        double* cmax, cudaStream_t st, std::string* err) {
-  using W = WarpCfg<D, P>;
-  if (!W::GS && !set_smem(subcell_prep_kernel<D, P>, W::SMEM)) {
+  using W = WarpCfg<D, P, SYS>;
+  if (!W::GS && !set_smem(subcell_prep_kernel<D, P, SYS>, W::SMEM)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
@@ -1166,19 +1229,19 @@ static int launch_prep(const adg_grid* g, const double* u, double* sub, double* 
   const unsigned grid = (unsigned)(nb < cap ? nb : cap);
   double* gs = nullptr;
   if (W::GS && !(gs = lim_scratch((size_t)grid * W::BLOCK_DBL * 8, err))) return ADG_ERR_CUDA;
-  subcell_prep_kernel<D, P><<<grid, W::WPBX * 32, W::GS ? 0 : W::SMEM, st>>>(u, E, sub, cmin,
+  subcell_prep_kernel<D, P, SYS><<<grid, W::WPBX * 32, W::GS ? 0 : W::SMEM, st>>>(u, E, sub, cmin,
                                                                            cmax, gs);
   return lerr(err);
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 static int launch_detect(const adg_grid* g, const double* prev_sub, const double* cmin,
                          const double* cmax, const double* cand, const uint8_t* pred_bad,
                          double d0, double eps, int force, const adg_subcell_ghosts* gh,
                          uint8_t* troubled, int32_t* idx, int32_t* count, double* sub_out,
                          double* cmin_out, double* cmax_out, cudaStream_t st, std::string* err) {
-  using W = WarpCfg<D, P>;
-  if (!W::GS && !set_smem(detect_kernel<D, P>, W::SMEM)) {
+  using W = WarpCfg<D, P, SYS>;
+  if (!W::GS && !set_smem(detect_kernel<D, P, SYS>, W::SMEM)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
@@ -1189,41 +1252,41 @@ static int launch_detect(const adg_grid* g, const double* prev_sub, const double
   double* gs = nullptr;
   if (W::GS && !(gs = lim_scratch((size_t)grid * W::BLOCK_DBL * 8, err))) return ADG_ERR_CUDA;
   cudaMemsetAsync(count, 0, sizeof(int32_t), st);
-  detect_kernel<D, P><<<grid, W::WPBX * 32, W::GS ? 0 : W::SMEM, st>>>(
+  detect_kernel<D, P, SYS><<<grid, W::WPBX * 32, W::GS ? 0 : W::SMEM, st>>>(
       prev_sub, cmin, cmax, cand, pred_bad, lim_grid(g, gh), E, d0, eps, force, troubled, idx,
       count, sub_out, cmin_out, cmax_out, gs);
   return lerr(err);
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 static int launch_rescue(const adg_grid* g, const double* prev_sub, const int32_t* idx,
                          const int32_t* count, int32_t cmax, const double* dt,
                          const adg_subcell_ghosts* gh, double* u_out, int32_t* failed,
                          double* sub_next, double* cmin_next, double* cmax_next,
                          cudaStream_t st, std::string* err) {
-  constexpr bool GS = LimDbl<D, P>::RESCUE > LimDbl<D, P>::LIM;
-  const size_t sm = GS ? 0 : rescue_smem<D, P>();
-  if (!GS && !set_smem(rescue_kernel<D, P, 0>, sm)) {
+  constexpr bool GS = LimDbl<D, P, SYS>::RESCUE > LimDbl<D, P, SYS>::LIM;
+  const size_t sm = GS ? 0 : rescue_smem<D, P, SYS>();
+  if (!GS && !set_smem(rescue_kernel<D, P, SYS, 0>, sm)) {
     *err = "limiter window exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
   if (cmax <= 0) return ADG_OK;
   const unsigned grid = (unsigned)(GS && cmax > kScratchBlocks ? kScratchBlocks : cmax);
   double* gs = nullptr;
-  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::RESCUE * 8, err))) return ADG_ERR_CUDA;
-  rescue_kernel<D, P, 0><<<grid, LimCfg<D, P>::NT, sm, st>>>(
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P, SYS>::RESCUE * 8, err))) return ADG_ERR_CUDA;
+  rescue_kernel<D, P, SYS, 0><<<grid, LimCfg<D, P, SYS>::NT, sm, st>>>(
       prev_sub, idx, count, lim_grid(g, gh), dt, u_out, failed, nullptr, nullptr, nullptr,
       sub_next, cmin_next, cmax_next, gs);
   return lerr(err);
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 static int launch_muscl_windows(const adg_grid* g, const double* windows, int64_t nwin,
                                 const int32_t* count_dev, const double* dt, double* avg_out,
                                 uint8_t* fail_each, cudaStream_t st, std::string* err) {
-  constexpr bool GS = LimDbl<D, P>::RESCUE > LimDbl<D, P>::LIM;
-  const size_t sm = GS ? 0 : rescue_smem<D, P>();
-  if (!GS && !set_smem(rescue_kernel<D, P, 1>, sm)) {
+  constexpr bool GS = LimDbl<D, P, SYS>::RESCUE > LimDbl<D, P, SYS>::LIM;
+  const size_t sm = GS ? 0 : rescue_smem<D, P, SYS>();
+  if (!GS && !set_smem(rescue_kernel<D, P, SYS, 1>, sm)) {
     *err = "limiter window exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
@@ -1231,22 +1294,22 @@ static int launch_muscl_windows(const adg_grid* g, const double* windows, int64_
   const int64_t cap = GS ? kScratchBlocks : 65535 * 8;
   const unsigned grid = (unsigned)(nwin < cap ? nwin : cap);
   double* gs = nullptr;
-  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::RESCUE * 8, err))) return ADG_ERR_CUDA;
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P, SYS>::RESCUE * 8, err))) return ADG_ERR_CUDA;
   LimGrid G = lim_grid(g);
   for (int j = 0; j < 3; ++j) G.h[j] = j < g->dim ? g->dx[j] : 1.0;   // dx = subcell widths here
-  rescue_kernel<D, P, 1><<<grid, LimCfg<D, P>::NT, sm, st>>>(
+  rescue_kernel<D, P, SYS, 1><<<grid, LimCfg<D, P, SYS>::NT, sm, st>>>(
       nullptr, nullptr, count_dev, G, dt, nullptr, nullptr, windows, avg_out, fail_each, nullptr,
       nullptr, nullptr, gs);
   return lerr(err);
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 static int launch_recover(const adg_grid* g, const double* ubar, double* out, cudaStream_t st,
                           std::string* err) {
-  using C = LimCfg<D, P>;
-  constexpr bool GS = LimDbl<D, P>::RECOVER > LimDbl<D, P>::LIM;
-  const size_t sm = GS ? 0 : LimDbl<D, P>::RECOVER * 8;
-  if (!GS && !set_smem(recover_kernel<D, P>, sm)) {
+  using C = LimCfg<D, P, SYS>;
+  constexpr bool GS = LimDbl<D, P, SYS>::RECOVER > LimDbl<D, P, SYS>::LIM;
+  const size_t sm = GS ? 0 : LimDbl<D, P, SYS>::RECOVER * 8;
+  if (!GS && !set_smem(recover_kernel<D, P, SYS>, sm)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
@@ -1254,17 +1317,17 @@ static int launch_recover(const adg_grid* g, const double* ubar, double* out, cu
   const int64_t cap = GS ? kScratchBlocks : 65535 * 8;
   const unsigned grid = (unsigned)(E < cap ? E : cap);
   double* gs = nullptr;
-  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::RECOVER * 8, err))) return ADG_ERR_CUDA;
-  recover_kernel<D, P><<<grid, C::NT, sm, st>>>(ubar, E, out, gs);
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P, SYS>::RECOVER * 8, err))) return ADG_ERR_CUDA;
+  recover_kernel<D, P, SYS><<<grid, C::NT, sm, st>>>(ubar, E, out, gs);
   return lerr(err);
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 static int launch_flatten_cells(const adg_grid* g, double* nodal, const double* averages,
                                 int32_t* nflat, cudaStream_t st, std::string* err) {
-  constexpr bool GS = LimDbl<D, P>::PROJ > LimDbl<D, P>::LIM;
-  const size_t sm = GS ? 0 : proj_smem<D, P>();
-  if (!GS && !set_smem(flatten_cells_kernel<D, P>, sm)) {
+  constexpr bool GS = LimDbl<D, P, SYS>::PROJ > LimDbl<D, P, SYS>::LIM;
+  const size_t sm = GS ? 0 : proj_smem<D, P, SYS>();
+  if (!GS && !set_smem(flatten_cells_kernel<D, P, SYS>, sm)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
@@ -1272,19 +1335,19 @@ static int launch_flatten_cells(const adg_grid* g, double* nodal, const double* 
   const int64_t cap = GS ? kScratchBlocks : 65535 * 8;
   const unsigned grid = (unsigned)(E < cap ? E : cap);
   double* gs = nullptr;
-  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::PROJ * 8, err))) return ADG_ERR_CUDA;
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P, SYS>::PROJ * 8, err))) return ADG_ERR_CUDA;
   cudaMemsetAsync(nflat, 0, sizeof(int32_t), st);
-  flatten_cells_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(nodal, averages, E,
+  flatten_cells_kernel<D, P, SYS><<<grid, LimCfg<D, P, SYS>::NT, sm, st>>>(nodal, averages, E,
                                                                  g->gamma - 1.0, nflat, gs);
   return lerr(err);
 }
 
-template <int D, int P>
+template <int D, int P, int SYS>
 static int launch_flatten(const adg_grid* g, double* u, int32_t* nflat, cudaStream_t st,
                           std::string* err) {
-  constexpr bool GS = LimDbl<D, P>::PROJ > LimDbl<D, P>::LIM;
-  const size_t sm = GS ? 0 : proj_smem<D, P>();
-  if (!GS && !set_smem(flatten_ic_kernel<D, P>, sm)) {
+  constexpr bool GS = LimDbl<D, P, SYS>::PROJ > LimDbl<D, P, SYS>::LIM;
+  const size_t sm = GS ? 0 : proj_smem<D, P, SYS>();
+  if (!GS && !set_smem(flatten_ic_kernel<D, P, SYS>, sm)) {
     *err = "limiter tile exceeds shared memory";
     return ADG_ERR_UNSUPPORTED;
   }
@@ -1292,9 +1355,9 @@ static int launch_flatten(const adg_grid* g, double* u, int32_t* nflat, cudaStre
   const int64_t cap = GS ? kScratchBlocks : 65535 * 8;
   const unsigned grid = (unsigned)(E < cap ? E : cap);
   double* gs = nullptr;
-  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P>::PROJ * 8, err))) return ADG_ERR_CUDA;
+  if (GS && !(gs = lim_scratch((size_t)grid * LimDbl<D, P, SYS>::PROJ * 8, err))) return ADG_ERR_CUDA;
   cudaMemsetAsync(nflat, 0, sizeof(int32_t), st);
-  flatten_ic_kernel<D, P><<<grid, LimCfg<D, P>::NT, sm, st>>>(u, E, g->gamma - 1.0, nflat, gs);
+  flatten_ic_kernel<D, P, SYS><<<grid, LimCfg<D, P, SYS>::NT, sm, st>>>(u, E, g->gamma - 1.0, nflat, gs);
   return lerr(err);
 }
 

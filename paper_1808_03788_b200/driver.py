@@ -124,18 +124,21 @@ class Simulation:
         if predictor_mode not in ("conservative", "primitive"):
             raise ValueError(f"unknown predictor mode {predictor_mode!r}")
         if name in ("advection", "elasticity-di"):
-            # the advection / elasticity kernels cover the unlimited
-            # conservative step with periodic / outflow / wall faces (SURVEY.md
-            # §8(f) rank 4)
-            if use_limiter:
-                raise NotImplementedError(f"{name} on the device: no subcell limiter")
-            if predictor_mode != "conservative":
-                raise NotImplementedError(f"{name} on the device: conservative predictor")
-            kinds = normalize_boundary(boundary, mesh.dim).values()
-            if "exact" in kinds:
-                raise NotImplementedError(f"{name} on the device: no exact faces")
-            if name == "elasticity-di" and degree > 5:
-                raise NotImplementedError("elasticity-di on the device: degree <= 5")
+            # both plugins have identity primitives (systems.py:60-64) and a
+            # primitive_rhs equal to the conservative rate: predictor_mode
+            # "primitive" iterates the same variables with the same rate
+            self._iterate_mode = "conservative"
+            if name == "elasticity-di":
+                # the NCP plugin: unlimited step, periodic / outflow / wall faces
+                if use_limiter:
+                    raise NotImplementedError("elasticity-di on the device: no subcell limiter")
+                kinds = normalize_boundary(boundary, mesh.dim).values()
+                if "exact" in kinds:
+                    raise NotImplementedError("elasticity-di on the device: no exact faces")
+                if degree > 5:
+                    raise NotImplementedError("elasticity-di on the device: degree <= 5")
+        else:
+            self._iterate_mode = predictor_mode
         self.mesh = mesh
         self.system = system
         self.tables = basis_tables(degree)
@@ -194,7 +197,7 @@ class Simulation:
         g.dim = d
         g.degree = self.tables.degree
         g.nvars = self.system.n_vars
-        g.mode = _lib.MODE_CODES[self.predictor_mode]
+        g.mode = _lib.MODE_CODES[self._iterate_mode]
         for j in range(3):
             g.cells[j] = int(cells[j]) if j < d else 1
             g.dx[j] = float(spacings[j]) if j < d else 1.0

@@ -134,9 +134,12 @@ def gen_predictor():
 
 
 def run_case(name, mesh, sysd, degree, cfl, ic, steps, boundary="periodic",
-             use_limiter=False, store_first=False, predictor_mode="conservative"):
+             use_limiter=False, store_first=False, predictor_mode="conservative",
+             force_limit_all=False, exact_solution=None):
     sim = aderdg.Simulation(mesh, sysd, degree, cfl, boundary=boundary,
-                            use_limiter=use_limiter, predictor_mode=predictor_mode)
+                            use_limiter=use_limiter, predictor_mode=predictor_mode,
+                            exact_solution=exact_solution)
+    sim.force_limit_all = force_limit_all
     u0 = sim.project_initial_condition(ic).copy()
     dts, iters, flags, fracs, lam = [], [], [], [], []
     orig = predictor.picard_solve
@@ -314,6 +317,32 @@ def gen_advection():
          boundary="wall")
 
 
+def gen_advection_limited():
+    """LinearAdvection with the subcell limiter, primitive mode and exact faces
+    (the reference's own limiter-in-driver cases, test_mesh_driver.py:396-432,
+    plus 2-D / wall / exact variants)."""
+    from aderdg.driver import default_cfl
+    from aderdg.systems import LinearAdvection
+
+    def case(name, ext, cells, vel, degree, prob, steps, boundary="periodic", force=False,
+             mode="conservative", exact=False):
+        sysd = LinearAdvection(len(cells), velocity=vel)
+        ic, ex = aderdg.build_problem(prob, sysd)
+        run_case(name, aderdg.CartesianMesh(ext, cells), sysd, degree, default_cfl(degree), ic,
+                 steps, boundary=boundary, use_limiter=True, force_limit_all=force,
+                 predictor_mode=mode, exact_solution=ex if exact else None)
+
+    case("adv_lim_step_1d", [(0, 1)], (50,), [1.0], 2, "step", 30)
+    case("adv_lim_sine_forced", [(0, 1)], (16,), [1.0], 2, "sine", 5, force=True)
+    case("adv_lim_step_wall_2d", [(0, 1), (0, 1)], (12, 10), [0.7, -0.4], 3, "step", 8,
+         boundary="wall")
+    case("adv_lim_step_prim_2d", [(0, 1), (0, 1)], (10, 8), [0.6, 0.5], 2, "step", 6,
+         mode="primitive")
+    case("adv_lim_pulse_exact_1d", [(0, 1)], (24,), [1.0], 4, "pulse", 12,
+         boundary={0: ("exact", "outflow")}, exact=True)
+    case("adv_lim_step_3d", [(0, 1)] * 3, (5, 4, 4), [1.0, 0.5, -0.3], 2, "step", 4)
+
+
 def gen_elasticity():
     """DiffuseInterfaceElasticity plugin (systems.py:237-345): the registry's
     P-wave toward the diffuse free surface (problems.py:135-173) with
@@ -384,9 +413,12 @@ def gen_plugins():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tables", "pointwise", "predictor", "cases", "primitive", "output",
-                             "exact", "advection", "elasticity", "plugins"]
+                             "exact", "advection", "elasticity", "plugins",
+                             "advection_limited"]
     if "plugins" in which:
         gen_plugins()
+    if "advection_limited" in which:
+        gen_advection_limited()
     if "elasticity" in which:
         gen_elasticity()
     if "advection" in which:

@@ -159,11 +159,8 @@ def test_simulation_argument_errors_precede_device_use():
         Simulation(mesh, el, 3, 0.05, use_limiter=True)
     with pytest.raises(NotImplementedError):
         Simulation(mesh, el, 6, 0.05)                 # device kernels to N = 5
-    adv = make_system("advection", 2, velocity=[1.0, 0.5])
     with pytest.raises(NotImplementedError):
-        Simulation(mesh, adv, 3, 0.05, use_limiter=True)
-    with pytest.raises(NotImplementedError):
-        Simulation(mesh, adv, 3, 0.05, predictor_mode="primitive")
+        Simulation(mesh, el, 3, 0.05, boundary="exact", exact_solution=lambda x, t: x)
     with pytest.raises(ValueError):
         make_system("advection", 2, velocity=[1.0])
     import torch

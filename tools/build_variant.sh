@@ -12,5 +12,5 @@ FL="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -rdc=true -
 (cd paper_1808_03788_b200/csrc && $NV $FL $2 -c $SRC.cu -o ../../build/variants/pred_$1.o 2> ../../build/variants/pred_$1.log)
 $NV -gencode arch=compute_100a,code=sm_100a -rdc=true -shared -Xcompiler -fPIC \
   $(ls build/obj/*.o | grep -v "$SRC.o") build/variants/pred_$1.o \
-  -o paper_1808_03788_b200/variants/lib$1.so -lnccl
+  -o paper_1808_03788_b200/variants/lib$1.so -ldl
 python tools/ptxas_regs.py build/variants/pred_$1.log "predict_kernel<3, 5, 0>" 2>/dev/null || true
