@@ -1154,7 +1154,10 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   }
   // a caller's starting iterate or a startup-only call runs the shared-tile
   // kernel (its large-tile variant for 3-D N >= 7)
-  const bool plain = q_init == nullptr && !startup_only;
+  // ADG_PREDICTOR=tile: the shared-tile kernel's large-tile variant for the
+  // 3-D N >= 7 grids too (A/B runs against the slice-streaming kernel)
+  const char* pv = getenv("ADG_PREDICTOR");
+  const bool plain = q_init == nullptr && !startup_only && !(pv && pv[0] == 't');
   // 3-D tiles beyond one SM's shared memory: one CTA per element streaming
   // time slices through shared memory (adg_predictor_stream.cu)
   if (plain && !getenv("ADG_CLUSTER_PREDICTOR") && predict_stream_supported(g))

@@ -157,8 +157,24 @@ __device__ __forceinline__ void st_line_half(const double* src0, int stride, dou
     st_line<P, DIR, MODE, StCfg<P>::NH - 1>(src0, stride, gm1, dd, T, acc, ok);
 }
 
+// register budget: a CTA's warps are spread over the SM's four 16K-register
+// sub-partitions, so 9 or 12 warps (P = 9, 10) allow at most 168 registers
+// per thread, and P >= 9 spill the P x m line accumulators there (~1 KB per
+// thread).  ADG_STREAM_MAXNREG sets the cap explicitly for A/B builds
+// (profiles/r02_stream_regs.md: more registers cost P = 8 its second CTA per
+// SM, and P = 9 / 10 cannot launch above 168)
+#ifdef ADG_STREAM_MAXNREG
+// (P = 8 keeps the launch bounds: two CTAs per SM at 168 registers)
+#define ADG_STREAM_ATTR                                                               \
+  __maxnreg__(P == 8 ? 168                                                            \
+                     : ((ADG_STREAM_MAXNREG < (65536 / StCfg<P>::NT) / 8 * 8 - 8)     \
+                            ? ADG_STREAM_MAXNREG                                      \
+                            : (65536 / StCfg<P>::NT) / 8 * 8 - 8))
+#else
+#define ADG_STREAM_ATTR __launch_bounds__(StCfg<P>::NT, StCfg<P>::MINB)
+#endif
 template <int P>
-__global__ void __launch_bounds__(StCfg<P>::NT, StCfg<P>::MINB)
+__global__ void ADG_STREAM_ATTR
 predict_stream_kernel(const __grid_constant__ StArgs a) {
   using C = StCfg<P>;
   constexpr int M = C::M, PP = C::PP, PD = C::PD, NT = C::NT, NW = C::NW, H = C::H, NH = C::NH;
