@@ -159,6 +159,32 @@ def cpu_oracle_dofs(cells, degree, steps, warmup=0):
     return dof / wall, wall
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_sample(cells, degree, steps, threads, warmup=0):
+    """oracle port timing in a fresh process with `threads` BLAS threads
+    (OpenBLAS reads its thread count once, at load)."""
+    env = dict(os.environ)
+    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        env[var] = str(threads)
+    code = (f"import sys, json; sys.path.insert(0, {ROOT!r}); import bench; "
+            f"v, w = bench.cpu_oracle_dofs({cells}, {degree}, {steps}, {warmup}); "
+            f"print(json.dumps([v, w]))")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         check=True).stdout.strip().splitlines()[-1]
+    v, w = json.loads(out)
+    return v, w
+
+
 def reference_arm(args, rank):
     if rank != 0:
         return
@@ -178,6 +204,7 @@ def reference_arm(args, rank):
                                "of the 64^3 C2 grid; TDU is size independent)",
                    "degree": args.degree, "cells": [cells] * 3},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": n, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{cells}^3 elements x {args.steps} steps of oracle/ "
                                    "(numpy restatement of the reference, BLAS threads = "
                                    f"{n})"},
@@ -345,11 +372,15 @@ def ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ncores = os.cpu_count() or 1
-        val, wall = cpu_oracle_dofs(16, N, 1)
+        # the reference arm's per-step sample (12^3 elements of the C2
+        # workload), 2 steps with every host thread and 2 with one
+        val, wall = cpu_sample(12, N, 2, ncores)
+        val1, wall1 = cpu_sample(12, N, 2, 1)
         cpu = {"value": val, "unit": UNIT, "cores": ncores, "kind": "port",
-               "sample": f"16^3 elements x 1 step of the C2 workload through oracle/ "
-                         f"(numpy restatement of the reference; {wall:.1f} s wall, BLAS "
-                         f"threads = {ncores})"}
+               "value_1thread": val1, "cpu_model": cpu_model(),
+               "sample": f"12^3 elements x 2 steps of the C2 workload (the reference arm's "
+                         f"sample) through oracle/ (numpy restatement of the reference): "
+                         f"{wall:.1f} s with {ncores} BLAS threads, {wall1:.1f} s with 1"}
 
     if rank == 0:
         out = {

@@ -719,6 +719,21 @@ class Simulation:
         bb["graphs"][key] = g
         return g
 
+    def _pair_graphs_both(self, bb, nsteps):
+        """The graph of the current buffer roles and of the swapped ones: a
+        batch that starts on the other parity then replays instead of
+        capturing inside the caller's (timed) region."""
+        g = self._pair_graph(bb, nsteps)
+        if self._red_cur is not None:
+            self._u, self._u_next = self._u_next, self._u
+            self._red_cur = 1 - self._red_cur
+            try:
+                self._pair_graph(bb, nsteps)
+            finally:
+                self._u, self._u_next = self._u_next, self._u
+                self._red_cur = 1 - self._red_cur
+        return g
+
     def _run_batch(self, k):
         """k device-resident steps with one host synchronisation at the end."""
         if k <= 0:
@@ -743,7 +758,7 @@ class Simulation:
                                 reverse=True):
                     if k - s < n:
                         continue
-                    g = self._pair_graph(bb, n)
+                    g = self._pair_graphs_both(bb, n)
                     while k - s >= n:
                         g.replay()
                         s += n
