@@ -77,5 +77,19 @@ def test_elasticity_unsupported_paths_fail_loudly(pkg):
     system = pkg.make_system("elasticity-di", 2)
     with pytest.raises(NotImplementedError):
         pkg.Simulation(mesh, system, 3, 0.05, use_limiter=True)
-    with pytest.raises(NotImplementedError):
-        pkg.Simulation(mesh, system, 3, 0.05, predictor_mode="primitive")
+
+
+def test_elasticity_primitive_mode_is_the_conservative_step(pkg):
+    """The reference's elasticity plugin has identity primitives
+    (systems.py:58-63) and primitive_rhs = -ncp(v, grad v) (systems.py:333-334),
+    the conservative rate: predictor_mode="primitive" is the same step."""
+    mesh = pkg.CartesianMesh([(0.0, 1.0), (0.0, 1.0)], (6, 5))
+    system = pkg.make_system("elasticity-di", 2)
+    ic, _ = pkg.build_problem("pwave", system)
+    out = []
+    for mode in ("conservative", "primitive"):
+        sim = pkg.Simulation(mesh, system, 3, 0.05, boundary="outflow", predictor_mode=mode)
+        sim.project_initial_condition(ic)
+        sim.run(np.inf, max_steps=3)
+        out.append(sim.u.cpu().numpy())
+    assert np.array_equal(out[0], out[1])

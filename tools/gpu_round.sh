@@ -2,7 +2,7 @@
 # One GPU session: tests, smoke, bench (+ reference arm), per-config timings
 # with clocks, ncu launch list.  Usage: tools/gpu_round.sh TAG
 T=${1:-r02x}
-O=gpurun_out
+O=gpurun_out; mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/${T}_tests.log 2>&1; tail -3 $O/${T}_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${T}_smoke.log 2>&1; tail -2 $O/${T}_smoke.log
 timeout 600 python bench.py > $O/${T}_bench.json 2> $O/${T}_bench.err; tail -c 300 $O/${T}_bench.json
