@@ -56,7 +56,8 @@ ts = []
 for _ in range(7):
     a.record(); launch(); b.record()
     torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
-print(json.dumps({"lib": os.environ["ADG_LIB"], "step_ms": step_ms, "pred_ms_min": min(ts),
+chk = [float(vol.double().sum().item()), float(tr[:, :, :pd * m].sum().item()), int(sw.sum().item()), int(bad.sum().item())]
+print(json.dumps({"lib": os.path.basename(os.environ["ADG_LIB"]), "chk": chk, "step_ms": step_ms, "pred_ms_min": min(ts),
                   "pred_ms_med": sorted(ts)[3], "cells": n, "degree": deg}))
 '''
 
