@@ -245,7 +245,7 @@ int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double*
   DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
-  rc = grow_workspace(h, adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms));
+  rc = grow_workspace(h, adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms, adg::n_elements(g)));
   if (rc) return rc;
   std::string e;
   if (is_adv(g))
@@ -277,7 +277,7 @@ int adg_predict_ex(adg_handle* h, const adg_grid* g, const double* u, const doub
   if (is_el(g))
     return fail(h, ADG_ERR_UNSUPPORTED,
                 "elasticity-di on the device: no starting iterate / startup-only predictor");
-  rc = grow_workspace(h, adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms));
+  rc = grow_workspace(h, adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms, adg::n_elements(g)));
   if (rc) return rc;
   return wrap(h, adg::predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out, traces,
                               pred_bad, sweeps, (cudaStream_t)stream, h->num_sms, h->ws,
@@ -324,7 +324,7 @@ int adg_predict_range(adg_handle* h, const adg_grid* g, int64_t e_begin, int64_t
   if (rc) return rc;
   if (!adg_predict_range_supported(g))
     return fail(h, ADG_ERR_UNSUPPORTED, "adg_predict_range: grid runs a whole-grid predictor");
-  rc = grow_workspace(h, adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms));
+  rc = grow_workspace(h, adg::predict_workspace_bytes(g->dim, g->degree + 1, h->num_sms, adg::n_elements(g)));
   if (rc) return rc;
   std::string e;
   return wrap(h, adg::predict(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol_out, traces,

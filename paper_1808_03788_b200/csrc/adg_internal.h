@@ -33,7 +33,7 @@ int64_t n_elements(const adg_grid* g);
 int64_t reduce_blocks(const adg_grid* g);
 int64_t update_blocks(const adg_grid* g);
 
-size_t predict_workspace_bytes(int dim, int P, int num_sms);
+size_t predict_workspace_bytes(int dim, int P, int num_sms, int64_t n_elem = 0);
 int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol, int max_iter,
             int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
             int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
@@ -45,6 +45,13 @@ bool predict_range_supported(const adg_grid* g);
 bool predict_stream_supported(const adg_grid* g);
 size_t predict_stream_workspace_bytes(int P, int num_sms);
 int predict_stream(const adg_grid* g, const double* u, const double* dt_dev, double tol,
+                   int max_iter, int min_iter, double* q_out, double* vol, double* traces,
+                   uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms, double* ws,
+                   size_t ws_bytes, std::string* err);
+// phase kernels over element batches for the 3-D N >= 7 tiles (adg_predictor_phased.cu)
+bool predict_phased_supported(const adg_grid* g);
+size_t predict_phased_workspace_bytes(int P, int64_t n_elem);
+int predict_phased(const adg_grid* g, const double* u, const double* dt_dev, double tol,
                    int max_iter, int min_iter, double* q_out, double* vol, double* traces,
                    uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms, double* ws,
                    size_t ws_bytes, std::string* err);

@@ -1111,7 +1111,7 @@ static size_t ws_need(int num_sms) {
     case 10: return FN<D, 10>(__VA_ARGS__);              \
   }
 
-size_t predict_workspace_bytes(int dim, int P, int num_sms) {
+size_t predict_workspace_bytes(int dim, int P, int num_sms, int64_t n_elem) {
   if (dim == 1) { ADG_DISPATCH_P(1, ws_need, num_sms) }
   if (dim == 2) { ADG_DISPATCH_P(2, ws_need, num_sms) }
   if (dim == 3) {
@@ -1125,7 +1125,9 @@ size_t predict_workspace_bytes(int dim, int P, int num_sms) {
       case 10: t = ws_need<3, 10>(num_sms); break;
       default: { ADG_DISPATCH_P(3, ws_need, num_sms) }
     }
-    return s > t ? s : t;
+    const size_t ph = (P >= 8 && n_elem > 0) ? predict_phased_workspace_bytes(P, n_elem) : 0;
+    const size_t st = s > t ? s : t;
+    return st > ph ? st : ph;
   }
   return 0;
 }
@@ -1160,6 +1162,14 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   const bool plain = q_init == nullptr && !startup_only && !(pv && pv[0] == 't');
   // 3-D tiles beyond one SM's shared memory: one CTA per element streaming
   // time slices through shared memory (adg_predictor_stream.cu)
+  // ... or, from N = 8 up (ADG_PREDICTOR=phased: N = 7 too; =stream: never), as
+  // phase kernels over element batches with the iterate in HBM
+  // (adg_predictor_phased.cu): 34.5 vs 51.4 ms at N = 8, 58.6 vs 78.3 ms at
+  // N = 9 on 32^3 elements, 18.3 vs 17.4 ms at N = 7
+  if (plain && !(pv && pv[0] == 's') && !getenv("ADG_CLUSTER_PREDICTOR") &&
+      predict_phased_supported(g) && (g->degree >= 8 || (pv && pv[0] == 'p')))
+    return predict_phased(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
+                          sweeps, st, num_sms, ws, ws_bytes, err);
   if (plain && !getenv("ADG_CLUSTER_PREDICTOR") && predict_stream_supported(g))
     return predict_stream(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
                           sweeps, st, num_sms, ws, ws_bytes, err);

@@ -1,0 +1,822 @@
+// adg_predictor_phased.cu -- the ADER-DG predictor for the large 3-D
+// space-time tiles (P = N+1 = 8..10: 160-391 KB per element, more than one
+// SM's shared memory) as a sequence of phase kernels over a batch of
+// elements, the space-time iterate and its rates in HBM.
+//
+// Same algorithm and outputs as predict_kernel (adg_predictor.cu): startup
+// guess (predictor.py:99-126), Picard sweeps with per-element freezing
+// (predictor.py:135-191), admissibility (:188-189), face traces (:218-230)
+// and the volume integral (corrector.py:141-177).
+//
+// Why phases.  A fused per-element kernel at these degrees holds one 30-40 KB
+// time slice and 45-50 line accumulators per thread: one CTA of 9 warps per SM,
+// every slice a serial load -> contract -> store chain (measured: 75 % of the
+// cycles without an eligible warp, FP64 pipe at 17 %).  B200 has 6.5 TB/s of
+// HBM for 37 TFLOP/s of FP64, so the tile can afford to travel: the Picard
+// rate L(q_t) = -sum_dir D_dir F_dir(q_t) only couples the nodes of ONE time
+// slice and the time operator only the time levels of ONE node, so
+//   startup  one CTA per element: k1 = L(u), k2 = L(u + dt k1), q_t at every t;
+//   rates    one CTA per (element, time slice): slice -> shared memory, the
+//            P^2 line owners contract z, y, x flux lines (one shared partial
+//            buffer, accumulated in place), rate slice -> HBM;
+//   time     one CTA per element, streaming: q_new = dt gw rate + g0 u,
+//            residual, convergence flag, q <- q_new;
+//   final    one CTA per element: traces, admissibility, flux sums, volume.
+// Slices are independent tasks, so every SM holds several CTAs in different
+// phases of their slices, and each pass streams at HBM speed.  Frozen
+// elements are skipped by every later rates / time launch; a device counter
+// of active elements turns the remaining launches of the host's max_iter
+// loop into immediate exits (no host synchronisation, graph-capturable).
+#include <algorithm>
+
+#include "adg_common.cuh"
+#include "adg_internal.h"
+
+namespace adg {
+
+// l loop of the line contractions: fully unrolled by default (D/dx entries
+// become constant-bank operands; measured 34.5 vs 35.1 ms at N = 8, 58.6 vs
+// 63.2 ms at N = 9 against the rolled loop)
+#ifndef ADG_PH_LUNROLL
+#define ADG_PH_LUNROLL 16
+#endif
+// 1 / rho and the pressure of every node of the slice computed once into
+// shared memory (instead of once per direction by the line owners)
+// (measured 2-7 % SLOWER at N = 7..9: the kernel is latency-bound, not
+// FP64-issue-bound, and the extra shared traffic costs more than the saved
+// flux arithmetic; kept for A/B builds)
+#ifndef ADG_PH_RP
+#define ADG_PH_RP 0
+#endif
+
+template <int P>
+struct PhCfg {
+  static constexpr int M = 5;
+  static constexpr int PP = P * P;
+  static constexpr int PD = P * P * P;
+  // padded slice layouts (tools/cluster_bankcheck.py): Q node-major
+  // [i][j][k][v] strides (SI, SJ, M); B x-line-major [j][k][i][v] strides
+  // (TJ, TK, M)
+  static constexpr int SJ = P * M + (P == 8 ? 1 : (P == 10 ? 3 : 0));
+  static constexpr int SI = P * SJ;
+  static constexpr int TK = P * M + (P == 8 ? 2 : (P == 10 ? 1 : 0));
+  static constexpr int TJ = P * TK + (P == 8 ? 1 : 0);
+  static constexpr int QSZ = P * SI;
+  static constexpr int BSZ = P * TJ;
+  static constexpr int QSZP = QSZ + (QSZ & 1);
+  static constexpr int BSZP = BSZ + (BSZ & 1);
+  static constexpr int RP = ((PP + 31) / 32) * 32;   // line owners, whole warps
+  static constexpr int NW = RP / 32;
+  static constexpr int CSTP = (2 * P + 1) / 2 * 2;
+  static constexpr size_t SLICE = (size_t)PD * M;    // doubles per time slice
+  static constexpr size_t TILE = (size_t)P * SLICE;  // doubles per space-time tile
+  static constexpr int TB = PD * M + ((PD * M) & 1); // trace block (face kernel layout)
+  // rates / startup: one slice + one partial buffer
+  static constexpr int XSZ = ADG_PH_RP ? 2 * PD : 0;   // (1 / rho, p) per node
+  static constexpr size_t SMEM_A = ((size_t)QSZP + BSZP + XSZ) * 8;
+  // register cap of the line kernels: 168 per thread (a warp's registers
+  // come from its scheduler's 16 K: more would cost the third CTA per SM)
+  static constexpr int MINB_A = 384 / RP;
+  // traces: one slice, three line-owner groups side by side
+  static constexpr int NT_F = 3 * RP;
+  static constexpr int TRS = 6 * PP * M;             // staged traces of one slice
+  static constexpr size_t SMEM_TR = ((size_t)QSZP + TRS) * 8;
+  static constexpr int MINB_TR = NT_F > 288 ? 3 : 4;
+  // vol: slice + y partials + z partials
+  static constexpr size_t SMEM_V = ((size_t)QSZP + 2 * BSZP) * 8;
+  static constexpr int NT_T = 256;                   // time kernel
+};
+
+struct PhArgs {
+  const double* u;      // batch's first element
+  const double* dt;
+  double* q_out;        // batch's first element, or null
+  double* vol;
+  double* traces;       // batch's first element inside face plane 0
+  uint8_t* pred_bad;
+  int32_t* sweeps;
+  double* qg;           // [n][P][node][v] iterate
+  double* rg;           // [n][P][node][v] rates; after the sweeps slices 0..2 = Fbar_x/y/z
+  double* kg;           // [n][2][node][v] startup rates k1, k2
+  int32_t* state;       // [4][n]: frozen, converged, sweeps executed, inadmissible
+  int32_t* n_active;
+  int64_t n_elem;       // elements in the batch
+  int64_t tr_elems;     // elements per face plane of the trace array
+  double dx[3];
+  double gamma;
+  double tol;
+  int max_iter;
+  int min_iter;
+  int it;               // sweep index (rates / time launches)
+  double dd[3 * kMaxP * kMaxP];   // D / dx_dir, [dir][P][P]
+};
+
+// one line's P states (src + l * stride) -> flux along DIR -> D/dx_DIR
+// contraction, l-outer: every line state is loaded, turned into its flux and
+// folded into all P outputs (same per-output fma order as a row-by-row
+// mat-vec)
+template <int P, int DIR>
+__device__ __forceinline__ void ph_line(const double* src0, int stride, const double* x0,
+                                        int xstride, double gm1, const double* dd,
+                                        double (&acc)[P][5]) {
+  constexpr int M = 5;
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+#pragma unroll
+    for (int v = 0; v < M; ++v) acc[i][v] = 0.0;
+  constexpr int LU = ADG_PH_LUNROLL;
+#pragma unroll LU
+  for (int l = 0; l < P; ++l) {
+    double q[M], f[M];
+    const double* src = src0 + l * stride;
+#pragma unroll
+    for (int v = 0; v < M; ++v) q[v] = src[v];
+    if constexpr (ADG_PH_RP) {
+      // flux_axis with the node's 1 / rho and p from the slice pre-pass (the
+      // same values flux_axis would form)
+      const double2 rp = *reinterpret_cast<const double2*>(x0 + l * xstride);
+      const double va = q[1 + DIR] * rp.x;
+      const double ep = q[4] + rp.y;
+      f[0] = q[1 + DIR];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) f[1 + i] = q[1 + i] * va;
+      f[1 + DIR] += rp.y;
+      f[4] = ep * va;
+    } else {
+      flux_axis<3>(q, gm1, DIR, f);
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const double d = dd[DIR * P * P + i * P + l];
+#pragma unroll
+      for (int v = 0; v < M; ++v) acc[i][v] = fma(d, f[v], acc[i][v]);
+    }
+  }
+}
+
+// 1 / rho and p of every node of the padded slice Q -> X[node] (node-major,
+// unpadded), exactly as flux_axis forms them
+template <int P, int NT>
+__device__ __forceinline__ void ph_prepass(const double* Q, double* X, double gm1, int tid) {
+  using C = PhCfg<P>;
+  if constexpr (ADG_PH_RP) {
+    for (int n = tid; n < C::PD; n += NT) {
+      const int i = n / C::PP, j = (n / P) % P, k = n % P;
+      const double* q = Q + i * C::SI + j * C::SJ + k * C::M;
+      const double r = rcp_nr(q[0]);
+      double kin = q[1] * q[1];
+      kin = kin + q[2] * q[2];
+      kin = kin + q[3] * q[3];
+      const double pr = gm1 * (q[4] - 0.5 * kin * r);
+      *reinterpret_cast<double2*>(X + 2 * n) = make_double2(r, pr);
+    }
+    __syncthreads();
+  }
+}
+
+// the line-owner indices of thread rr (< P^2) in the three roles
+template <int P>
+struct PhRoles {
+  int a0, b0;
+  __device__ __forceinline__ explicit PhRoles(int rr) : a0(rr / P), b0(rr - (rr / P) * P) {}
+  using C = PhCfg<P>;
+  // first node of the owned line in the padded slice, and the line's stride
+  __device__ __forceinline__ int qbase(int role) const {
+    return role == 0 ? a0 * C::SJ + b0 * C::M
+                     : (role == 1 ? a0 * C::SI + b0 * C::M : a0 * C::SI + b0 * C::SJ);
+  }
+  __device__ __forceinline__ int qstride(int role) const {
+    return role == 0 ? C::SI : (role == 1 ? C::SJ : C::M);
+  }
+  // unpadded node index of the line's first node and the node stride
+  __device__ __forceinline__ int nbase(int role) const {
+    return role == 0 ? a0 * P + b0 : (role == 1 ? a0 * C::PP + b0 : a0 * C::PP + b0 * P);
+  }
+  __device__ __forceinline__ int nstride(int role) const {
+    return role == 0 ? C::PP : (role == 1 ? P : 1);
+  }
+  // where the y (role 1) / z (role 2) owner's output i lands in the
+  // x-line-major partial buffer: pbase + i * pstride
+  __device__ __forceinline__ int pbase(int role) const {
+    return role == 1 ? b0 * C::TK + a0 * C::M : b0 * C::TJ + a0 * C::M;
+  }
+  __device__ __forceinline__ int pstride(int role) const { return role == 1 ? C::TJ : C::TK; }
+  __device__ __forceinline__ int xrow() const { return a0 * C::TJ + b0 * C::TK; }
+};
+
+// a [node][v] slice (global) into the padded slice buffer: P^2 rows (i, j) of
+// P m contiguous doubles, one warp per row, asynchronous 8-byte copies
+template <int P, int NWARPS>
+__device__ __forceinline__ void ph_fetch(double* buf, const double* src, int warp, int lane) {
+  using C = PhCfg<P>;
+  for (int row = warp; row < C::PP; row += NWARPS) {
+    const int i = row / P, j = row - (row / P) * P;
+    double* dst = buf + i * C::SI + j * C::SJ;
+    const double* sr = src + row * (P * C::M);
+    for (int o = lane; o < P * C::M; o += 32) cp_async8(dst + o, sr + o);
+  }
+  cp_async_commit();
+}
+
+// rates of the slice in Q -> rt ([node][v], global): the owners contract their
+// z line (partials published x-line-major in B), then their y line (added in
+// place), then their x line: rate = -D_x F_x - (D_z F_z + D_y F_y).
+// (Staging the slice of rates in shared memory for coalesced stores was
+// measured neutral here: 8.26 vs 8.08 ms per sweep at N = 8, and it costs
+// 30-50 registers.)
+template <int P>
+__device__ __forceinline__ void ph_slice_rates(const double* Q, double* B, double* X,
+                                               double* rt, const PhRoles<P>& R, bool owner,
+                                               double gm1, const double* dd, int tid) {
+  constexpr int M = 5;
+  ph_prepass<P, PhCfg<P>::RP>(Q, X, gm1, tid);
+  double acc[P][M];
+  if (owner) {
+    ph_line<P, 2>(Q + R.qbase(2), R.qstride(2), X + 2 * R.nbase(2), 2 * R.nstride(2), gm1, dd,
+                  acc);
+    const int pb = R.pbase(2), ps = R.pstride(2);
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int v = 0; v < M; ++v) B[pb + i * ps + v] = acc[i][v];
+  }
+  __syncthreads();
+  if (owner) {
+    ph_line<P, 1>(Q + R.qbase(1), R.qstride(1), X + 2 * R.nbase(1), 2 * R.nstride(1), gm1, dd,
+                  acc);
+    const int pb = R.pbase(1), ps = R.pstride(1);
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int v = 0; v < M; ++v) B[pb + i * ps + v] += acc[i][v];
+  }
+  __syncthreads();
+  if (owner) {
+    ph_line<P, 0>(Q + R.qbase(0), R.qstride(0), X + 2 * R.nbase(0), 2 * R.nstride(0), gm1, dd,
+                  acc);
+    const int xr = R.xrow(), nb = R.nbase(0), ns = R.nstride(0);
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double* out = rt + (size_t)(nb + i * ns) * M;
+#pragma unroll
+      for (int v = 0; v < M; ++v) out[v] = -acc[i][v] - B[xr + i * M + v];
+    }
+  }
+}
+
+// the startup iterate at time level t (predictor.py:116-124): q_t = u +
+// s_t k1 + s_t^2 / (2 dt) (k2 - k1), one expression for every kernel that
+// forms it
+__device__ __forceinline__ double ph_startup_q(double un, double k1, double k2, double s,
+                                               double c2) {
+  return fma(c2, k2 - k1, fma(s, k1, un));
+}
+
+// ---------------------------------------------------------------- startup
+// predictor.py:99-126: k1 = L(u), k2 = L(u + dt k1) into the element's K
+// slices; the iterate itself is never stored (the first sweep's kernels form
+// it from u, k1, k2).  Resets the element's state.
+template <int P>
+__global__ void __launch_bounds__(PhCfg<P>::RP, PhCfg<P>::MINB_A)
+ph_startup_kernel(const __grid_constant__ PhArgs a) {
+  using C = PhCfg<P>;
+  constexpr int M = C::M, PP = C::PP, NW = C::NW;
+  extern __shared__ __align__(16) double smem[];
+  double* Q = smem;
+  double* B = Q + C::QSZP;
+  double* X = B + C::BSZP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool owner = tid < PP;
+  const PhRoles<P> R(owner ? tid : 0);
+  const double gm1 = a.gamma - 1.0;
+  const double dt = *a.dt;
+  for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
+    const double* ue = a.u + (size_t)e * C::SLICE;
+    double* ke = a.kg + (size_t)e * 2 * C::SLICE;
+    __syncthreads();   // previous element done with Q / B
+    ph_fetch<P, NW>(Q, ue, warp, lane);
+    cp_async_wait_all();
+    __syncthreads();
+    ph_slice_rates<P>(Q, B, X, ke, R, owner, gm1, a.dd, tid);          // k1
+    __syncthreads();   // k1 stored, every line of Q read
+    // w = u + dt k1 in the tile (k1 read back from this CTA's own stores)
+    for (int row = warp; row < PP; row += NW) {
+      const int i = row / P, j = row - (row / P) * P;
+      double* dst = Q + i * C::SI + j * C::SJ;
+      const double* k1 = ke + row * (P * M);
+      for (int o = lane; o < P * M; o += 32) dst[o] = dst[o] + dt * k1[o];
+    }
+    __syncthreads();
+    ph_slice_rates<P>(Q, B, X, ke + C::SLICE, R, owner, gm1, a.dd, tid);   // k2
+    if (tid == 0) {
+      a.state[e] = 0;
+      a.state[a.n_elem + e] = 0;
+      a.state[2 * a.n_elem + e] = 0;
+      a.state[3 * a.n_elem + e] = 0;
+      atomicAdd(a.n_active, 1);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ rates
+// one task per (element, time slice) of the elements still iterating; the
+// first sweep (it == 0) forms its slice of the startup iterate from u, k1, k2
+template <int P>
+__global__ void __launch_bounds__(PhCfg<P>::RP, PhCfg<P>::MINB_A)
+ph_rates_kernel(const __grid_constant__ PhArgs a) {
+  using C = PhCfg<P>;
+  constexpr int M = C::M, PP = C::PP, NW = C::NW;
+  if (*a.n_active <= 0) return;
+  const DegreeTables& T = tab<P>();
+  extern __shared__ __align__(16) double smem[];
+  double* Q = smem;
+  double* B = Q + C::QSZP;
+  double* X = B + C::BSZP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool owner = tid < PP;
+  const PhRoles<P> R(owner ? tid : 0);
+  const double gm1 = a.gamma - 1.0;
+  const double dt = *a.dt;
+  const int64_t ntask = a.n_elem * P;
+  for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
+    const int64_t e = task / P;
+    const int t = (int)(task - e * P);
+    if (a.state[e]) continue;
+    __syncthreads();   // previous task done with Q / B
+    if (a.it == 0) {
+      const double s = T.nodes[t] * dt, c2 = 0.5 * s * s / dt;
+      const double* ue = a.u + (size_t)e * C::SLICE;
+      const double* ke = a.kg + (size_t)e * 2 * C::SLICE;
+      // eight values per thread in flight: their 24 loads issue before the
+      // first use
+      constexpr int NB = 8, NT = C::RP, SL = (int)C::SLICE;
+      for (int x0 = tid; x0 < SL; x0 += NB * NT) {
+        double un[NB], k1[NB], k2[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int x = x0 + b * NT < SL ? x0 + b * NT : x0;
+          un[b] = ue[x];
+          k1[b] = ke[x];
+          k2[b] = ke[SL + x];
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int x = x0 + b * NT;
+          if (x < SL) {
+            const int row = x / (P * M), o = x - row * (P * M);
+            const int i = row / P, j = row - i * P;
+            Q[i * C::SI + j * C::SJ + o] = ph_startup_q(un[b], k1[b], k2[b], s, c2);
+          }
+        }
+      }
+    } else {
+      ph_fetch<P, NW>(Q, a.qg + (size_t)e * C::TILE + (size_t)t * C::SLICE, warp, lane);
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    ph_slice_rates<P>(Q, B, X, a.rg + (size_t)e * C::TILE + (size_t)t * C::SLICE, R, owner,
+                      gm1, a.dd, tid);
+  }
+}
+
+// ------------------------------------------------------------------- time
+// predictor.py:175-185 over an element's P^3 m values: q_new(t) = dt sum_s
+// gw[t][s] rate(s) + g0[t] u, residual norms (fixed-order block sum), the
+// convergence test and per-element freezing; q <- q_new.  One CTA per
+// element, one (node, quantity) per thread and pass: its P rates and P old
+// iterates are loaded up front (all independent: HBM latency overlapped)
+template <int P>
+__global__ void __launch_bounds__(PhCfg<P>::NT_T, 3)
+ph_time_kernel(const __grid_constant__ PhArgs a) {
+  using C = PhCfg<P>;
+  constexpr int M = C::M, PD = C::PD, NT = C::NT_T, NW = NT / 32;
+  if (*a.n_active <= 0) return;
+  const DegreeTables& T = tab<P>();
+  __shared__ double red[2 * NW];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double dt = *a.dt;
+  for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
+    if (a.state[e]) continue;
+    const double* ue = a.u + (size_t)e * C::SLICE;
+    const double* ke = a.kg + (size_t)e * 2 * C::SLICE;
+    double* Qg = a.qg + (size_t)e * C::TILE;
+    const double* Rg = a.rg + (size_t)e * C::TILE;
+    double sd = 0.0, sq = 0.0;
+    for (int x = tid; x < PD * M; x += NT) {
+      double r[P], qo[P];
+#pragma unroll
+      for (int s2 = 0; s2 < P; ++s2) r[s2] = __ldcs(Rg + s2 * C::SLICE + x);
+      const double uu = ue[x];
+      if (a.it == 0) {
+        const double k1 = ke[x], k2 = ke[C::SLICE + x];
+#pragma unroll
+        for (int t2 = 0; t2 < P; ++t2) {
+          const double s = T.nodes[t2] * dt, c2 = 0.5 * s * s / dt;
+          qo[t2] = ph_startup_q(uu, k1, k2, s, c2);
+        }
+      } else {
+#pragma unroll
+        for (int t2 = 0; t2 < P; ++t2) qo[t2] = Qg[t2 * C::SLICE + x];
+      }
+#pragma unroll
+      for (int t2 = 0; t2 < P; ++t2) {
+        double cc = 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < P; ++s2) cc = fma(T.gw[t2 * P + s2], r[s2], cc);
+        const double qn = cc * dt + T.g0[t2] * uu;
+        const double dq = qo[t2] - qn;
+        sd = fma(dq, dq, sd);
+        sq = fma(qn, qn, sq);
+        Qg[t2 * C::SLICE + x] = qn;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sd += __shfl_xor_sync(0xffffffffu, sd, o);
+      sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    }
+    __syncthreads();   // previous element's readers of red are done
+    if (lane == 0) {
+      red[2 * warp] = sd;
+      red[2 * warp + 1] = sq;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        t1 += red[2 * w];
+        t2 += red[2 * w + 1];
+      }
+      const double res = T.k1_opnorm * sqrt(t1);
+      const double scale = 1.0 + sqrt(t2);
+      const int c = res <= a.tol * scale;
+      a.state[a.n_elem + e] = c;
+      a.state[2 * a.n_elem + e] = a.it + 1;
+      if ((c && a.it + 1 >= a.min_iter) || a.it + 1 >= a.max_iter) {
+        a.state[e] = 1;
+        atomicSub(a.n_active, 1);
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------- traces
+// one task per (element, time slice): the 3 P^2 line owners extrapolate their
+// line to both faces (predictor.py:218-230; face-kernel block layouts
+// x [j][k][t][v], y [k][t][i][v], z [t][i][j][v]); optional q output
+template <int P>
+__global__ void __launch_bounds__(PhCfg<P>::NT_F, PhCfg<P>::MINB_TR)
+ph_traces_kernel(const __grid_constant__ PhArgs a) {
+  using C = PhCfg<P>;
+  constexpr int M = C::M, PP = C::PP, PD = C::PD, NT = C::NT_F, NW = NT / 32;
+  const DegreeTables& T = tab<P>();
+  extern __shared__ __align__(16) double smem[];
+  double* Q = smem;
+  double* S = Q + C::QSZP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = tid / C::RP;
+  const int rr0 = tid - grp * C::RP;
+  const bool owner = rr0 < PP;
+  const int role = grp;
+  const PhRoles<P> R(owner ? rr0 : 0);
+  const int qbase = R.qbase(role), qstride = R.qstride(role);
+  const int64_t ntask = a.n_elem * P;
+  const size_t fs = (size_t)a.tr_elems * C::TB;
+  for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
+    const int64_t e = task / P;
+    const int t = (int)(task - e * P);
+    __syncthreads();   // previous task done with Q
+    ph_fetch<P, NW>(Q, a.qg + (size_t)e * C::TILE + (size_t)t * C::SLICE, warp, lane);
+    cp_async_wait_all();
+    __syncthreads();
+    if (owner) {
+      double lo[M], hi[M];
+#pragma unroll
+      for (int v = 0; v < M; ++v) lo[v] = hi[v] = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double* src = Q + qbase + l * qstride;
+        const double pl = T.left[l], pr = T.right[l];
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          lo[v] = fma(pl, src[v], lo[v]);
+          hi[v] = fma(pr, src[v], hi[v]);
+        }
+      }
+      double* slo = S + ((2 * role) * PP + rr0) * M;
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        slo[v] = lo[v];
+        slo[PP * M + v] = hi[v];
+      }
+    }
+    __syncthreads();
+    // staged [face][line][v] -> the face blocks: consecutive threads write
+    // consecutive doubles of a line's 40-byte block (z faces: one contiguous
+    // P^2 m run per slice)
+    for (int x = tid; x < C::TRS; x += NT) {
+      const int f = x / (PP * M);
+      const int y = x - f * (PP * M);
+      const int ln = y / M, v = y - ln * M;
+      const int la = ln / P, lb = ln - la * P;
+      const int rl = f >> 1;
+      const int pos = rl == 0 ? (la * P + lb) * P + t
+                              : (rl == 1 ? (lb * P + t) * P + la : (t * P + la) * P + lb);
+      a.traces[(size_t)f * fs + (size_t)e * C::TB + (size_t)pos * M + v] = S[x];
+    }
+    if (a.q_out) {
+      for (int n = tid; n < PD; n += NT) {
+        const int i = n / PP, j = (n / P) % P, k = n % P;
+        const double* qn = Q + i * C::SI + j * C::SJ + k * M;
+#pragma unroll
+        for (int v = 0; v < M; ++v) a.q_out[(((size_t)e * PD + n) * P + t) * M + v] = qn[v];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------- fbar
+// streaming over the batch's nodes: admissibility of the final iterate
+// (predictor.py:188-189) and the time-weighted fluxes Fbar_dir = sum_t w_t
+// F_dir(q_t) (corrector.py:166) into the element's (now free) rate slices
+// 0 / 1 / 2 = x / y / z, [node][v]
+template <int P>
+__global__ void __launch_bounds__(256)
+ph_fbar_kernel(const __grid_constant__ PhArgs a) {
+  using C = PhCfg<P>;
+  constexpr int M = C::M, PD = C::PD;
+  const DegreeTables& T = tab<P>();
+  const double gm1 = a.gamma - 1.0;
+  const int64_t total = a.n_elem * PD;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = g / PD;
+    const int n = (int)(g - e * PD);
+    const double* qe = a.qg + (size_t)e * C::TILE + (size_t)n * M;
+    double fb[3][M];
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < P; ++t) {
+      double q[M];
+#pragma unroll
+      for (int v = 0; v < M; ++v) q[v] = qe[(size_t)t * C::SLICE + v];
+      ok = ok && admissible<3>(q, gm1);
+      const double wt = T.weights[t];
+      double f[M];
+#pragma unroll
+      for (int dir = 0; dir < 3; ++dir) {
+        flux_axis<3>(q, gm1, dir, f);
+#pragma unroll
+        for (int v = 0; v < M; ++v) fb[dir][v] = t == 0 ? wt * f[v] : fb[dir][v] + wt * f[v];
+      }
+    }
+    // (staged, coalesced stores were measured slower here: 2.87 vs 2.66 ms)
+    double* re = a.rg + (size_t)e * C::TILE + (size_t)n * M;
+#pragma unroll
+    for (int dir = 0; dir < 3; ++dir)
+#pragma unroll
+      for (int v = 0; v < M; ++v) re[(size_t)dir * C::SLICE + v] = fb[dir][v];
+    if (!ok) atomicOr(a.state + 3 * a.n_elem + e, 1);
+  }
+}
+
+// -------------------------------------------------------------------- vol
+// per element: one stiffness contraction per direction of its Fbar slices
+// (corrector.py:169-176), y and z partials published x-line-major, the x-owner
+// scales and sums; the element's flags leave with it
+template <int P>
+__device__ __forceinline__ void ph_stiff_line(const double* src0, int stride,
+                                              const DegreeTables& T, double (&acc)[P][5]) {
+  constexpr int M = 5;
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+#pragma unroll
+    for (int v = 0; v < M; ++v) acc[i][v] = 0.0;
+#pragma unroll 1
+  for (int l = 0; l < P; ++l) {
+    double f[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) f[v] = src0[l * stride + v];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const double d = T.stiff[i * P + l];
+#pragma unroll
+      for (int v = 0; v < M; ++v) acc[i][v] = fma(d, f[v], acc[i][v]);
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(PhCfg<P>::RP)
+ph_vol_kernel(const __grid_constant__ PhArgs a) {
+  using C = PhCfg<P>;
+  constexpr int M = C::M, PP = C::PP, PD = C::PD, NW = C::NW;
+  const DegreeTables& T = tab<P>();
+  extern __shared__ __align__(16) double smem[];
+  double* Q = smem;
+  double* B1 = Q + C::QSZP;
+  double* B2 = B1 + C::BSZP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool owner = tid < PP;
+  const PhRoles<P> R(owner ? tid : 0);
+  const int a0 = R.a0, b0 = R.b0;
+  const double dt = *a.dt;
+  const double cv = a.dx[0] * a.dx[1] * a.dx[2];
+  const double sc0 = dt * cv / a.dx[0], sc1 = dt * cv / a.dx[1], sc2 = dt * cv / a.dx[2];
+  for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
+    const double* fe = a.rg + (size_t)e * C::TILE;
+    double acc[P][M];
+#pragma unroll 1
+    for (int role = 2; role >= 0; --role) {
+      __syncthreads();   // previous readers of Q are done
+      ph_fetch<P, NW>(Q, fe + (size_t)role * C::SLICE, warp, lane);
+      cp_async_wait_all();
+      __syncthreads();
+      if (owner) {
+        ph_stiff_line<P>(Q + R.qbase(role), R.qstride(role), T, acc);
+        if (role > 0) {
+          double* pdst = role == 1 ? B1 : B2;
+          const int pb = R.pbase(role), ps = R.pstride(role);
+#pragma unroll
+          for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int v = 0; v < M; ++v) pdst[pb + i * ps + v] = acc[i][v];
+        }
+      }
+    }
+    __syncthreads();   // partials published, every x line of Q read
+    if (owner) {
+      const int xrow = R.xrow(), nbase = R.nbase(0), nstride = R.nstride(0);
+      const double wa = T.weights[a0], wb = T.weights[b0];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const double wi = T.weights[i];
+        const double s0 = sc0 * (wa * wb), s1 = sc1 * (wi * wb), s2 = sc2 * (wi * wa);
+        double* out = Q + (nbase + i * nstride) * M;   // node-major, unpadded
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          double vv = s0 * acc[i][v];
+          vv += s1 * B1[xrow + i * M + v];
+          vv += s2 * B2[xrow + i * M + v];
+          out[v] = vv;
+        }
+      }
+    }
+    __syncthreads();
+    {
+      double* vole = a.vol + (size_t)e * PD * M;
+      for (int x = tid; x < PD * M; x += C::RP) vole[x] = Q[x];
+    }
+    if (tid == 0) {
+      const int conv = a.state[a.n_elem + e], nsw = a.state[2 * a.n_elem + e];
+      const int bad = a.state[3 * a.n_elem + e];
+      a.pred_bad[e] = (conv ? 0 : ADG_PRED_NOT_CONVERGED) | (bad ? ADG_PRED_INADMISSIBLE : 0);
+      a.sweeps[e] = nsw;
+    }
+  }
+}
+
+// ------------------------------------------------------------------- host
+template <int P>
+static size_t phased_bytes_per_element() {
+  return (2 * PhCfg<P>::TILE + 2 * PhCfg<P>::SLICE) * 8 + 4 * sizeof(int32_t);
+}
+
+// elements per batch: the whole grid, capped so the iterate + rates stay
+// within kPhasedCapBytes
+constexpr size_t kPhasedCapBytes = (size_t)28 << 30;
+
+template <int P>
+static int64_t phased_batch(int64_t n_elem) {
+  const int64_t cap = (int64_t)(kPhasedCapBytes / phased_bytes_per_element<P>());
+  return std::max<int64_t>(1, std::min<int64_t>(n_elem, cap));
+}
+
+template <int P>
+static size_t phased_ws_need(int64_t n_elem) {
+  return (size_t)phased_batch<P>(n_elem) * phased_bytes_per_element<P>() + 256;
+}
+
+template <class K>
+static int set_smem(K kern, size_t bytes, PerDevice* flag, std::string* err) {
+  if (!flag->first()) return ADG_OK;
+  if (bytes <= 48 * 1024) return ADG_OK;
+  cudaError_t ce =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (ce != cudaSuccess) {
+    *err = cudaGetErrorString(ce);
+    return ADG_ERR_CUDA;
+  }
+  return ADG_OK;
+}
+
+template <int P>
+static int launch_phased(const PhArgs& a0, int64_t n_all, cudaStream_t st, int num_sms,
+                         double* ws, size_t ws_bytes, std::string* err) {
+  using C = PhCfg<P>;
+  static PerDevice f_start, f_rates, f_tr, f_vol;
+  int rc;
+  if ((rc = set_smem(ph_startup_kernel<P>, C::SMEM_A, &f_start, err))) return rc;
+  if ((rc = set_smem(ph_rates_kernel<P>, C::SMEM_A, &f_rates, err))) return rc;
+  if ((rc = set_smem(ph_traces_kernel<P>, C::SMEM_TR, &f_tr, err))) return rc;
+  if ((rc = set_smem(ph_vol_kernel<P>, C::SMEM_V, &f_vol, err))) return rc;
+  const int64_t batch = phased_batch<P>(n_all);
+  if (!ws || ws_bytes < phased_ws_need<P>(n_all)) {
+    *err = "predictor workspace too small";
+    return ADG_ERR_RUNTIME;
+  }
+  int occ_a = 1, occ_t = 1, occ_tr = 1, occ_v = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, ph_rates_kernel<P>, C::RP, C::SMEM_A);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, ph_time_kernel<P>, C::NT_T, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tr, ph_traces_kernel<P>, C::NT_F,
+                                                C::SMEM_TR);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_v, ph_vol_kernel<P>, C::RP, C::SMEM_V);
+  occ_a = std::max(occ_a, 1);
+  occ_t = std::max(occ_t, 1);
+  occ_tr = std::max(occ_tr, 1);
+  occ_v = std::max(occ_v, 1);
+  for (int64_t e0 = 0; e0 < n_all; e0 += batch) {
+    const int64_t n = std::min<int64_t>(batch, n_all - e0);
+    PhArgs a = a0;
+    a.u = a0.u + (size_t)e0 * C::SLICE;
+    a.q_out = a0.q_out ? a0.q_out + (size_t)e0 * C::TILE : nullptr;
+    a.vol = a0.vol + (size_t)e0 * C::SLICE;
+    a.traces = a0.traces + (size_t)e0 * C::TB;
+    a.pred_bad = a0.pred_bad + e0;
+    a.sweeps = a0.sweeps + e0;
+    a.n_elem = n;
+    a.tr_elems = n_all;
+    a.qg = ws;
+    a.rg = ws + (size_t)batch * C::TILE;
+    a.kg = ws + 2 * (size_t)batch * C::TILE;
+    a.state = reinterpret_cast<int32_t*>(a.kg + 2 * (size_t)batch * C::SLICE);
+    a.n_active = a.state + 4 * batch;
+    cudaMemsetAsync(a.n_active, 0, sizeof(int32_t), st);
+    const auto grid = [&](int64_t tasks, int occ, int waves) {
+      return (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>(tasks, (int64_t)num_sms * occ * waves));
+    };
+    ph_startup_kernel<P><<<grid(n, occ_a, 4), C::RP, C::SMEM_A, st>>>(a);
+    for (int it = 0; it < a.max_iter; ++it) {
+      a.it = it;
+      ph_rates_kernel<P><<<grid(n * P, occ_a, 4), C::RP, C::SMEM_A, st>>>(a);
+      ph_time_kernel<P><<<grid(n, occ_t, 4), C::NT_T, 0, st>>>(a);
+    }
+    ph_traces_kernel<P><<<grid(n * P, occ_tr, 4), C::NT_F, C::SMEM_TR, st>>>(a);
+    ph_fbar_kernel<P><<<grid((n * C::PD + 255) / 256, 8, 4), 256, 0, st>>>(a);
+    ph_vol_kernel<P><<<grid(n, occ_v, 4), C::RP, C::SMEM_V, st>>>(a);
+  }
+  cudaError_t ce = cudaGetLastError();
+  if (ce != cudaSuccess) {
+    *err = cudaGetErrorString(ce);
+    return ADG_ERR_CUDA;
+  }
+  return ADG_OK;
+}
+
+bool predict_phased_supported(const adg_grid* g) {
+  return g->dim == 3 && g->degree >= 7 && g->degree <= 9 && g->mode != ADG_MODE_PRIMITIVE;
+}
+
+size_t predict_phased_workspace_bytes(int P, int64_t n_elem) {
+  switch (P) {
+    case 8: return phased_ws_need<8>(n_elem);
+    case 9: return phased_ws_need<9>(n_elem);
+    case 10: return phased_ws_need<10>(n_elem);
+  }
+  return 0;
+}
+
+int predict_phased(const adg_grid* g, const double* u, const double* dt_dev, double tol,
+                   int max_iter, int min_iter, double* q_out, double* vol, double* traces,
+                   uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms, double* ws,
+                   size_t ws_bytes, std::string* err) {
+  PhArgs a{};
+  a.u = u;
+  a.dt = dt_dev;
+  a.q_out = q_out;
+  a.vol = vol;
+  a.traces = traces;
+  a.pred_bad = pred_bad;
+  a.sweeps = sweeps;
+  const int64_t n_all = g->cells[0] * g->cells[1] * g->cells[2];
+  for (int j = 0; j < 3; ++j) a.dx[j] = g->dx[j];
+  a.gamma = g->gamma;
+  a.tol = tol;
+  a.max_iter = max_iter > 0 ? max_iter : 2 * g->degree + 2;
+  a.min_iter = min_iter;
+  const int P = g->degree + 1;
+  for (int dir = 0; dir < 3; ++dir)
+    for (int x = 0; x < P * P; ++x) a.dd[dir * P * P + x] = h_tab[g->degree].diff[x] / g->dx[dir];
+  if (n_all < 1) return ADG_OK;
+  switch (P) {
+    case 8: return launch_phased<8>(a, n_all, st, num_sms, ws, ws_bytes, err);
+    case 9: return launch_phased<9>(a, n_all, st, num_sms, ws, ws_bytes, err);
+    case 10: return launch_phased<10>(a, n_all, st, num_sms, ws, ws_bytes, err);
+  }
+  *err = "phased predictor: unsupported degree";
+  return ADG_ERR_UNSUPPORTED;
+}
+
+}  // namespace adg

@@ -249,20 +249,19 @@ def test_fused_subcell_reuse_is_bitwise(pkg):
     assert torch.equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("cluster", [False, True], ids=["stream", "cluster"])
+@pytest.mark.parametrize("variant", ["phased", "stream"])
 @pytest.mark.parametrize("n", [6, 7, 8, 9])
-def test_large_tile_predictor_matches_oracle(pkg, n, cluster, monkeypatch):
-    """3-D N>=7 tiles run on the slice-streaming kernel (one CTA per element,
-    one time slice at a time in shared memory, q and rates in an L2-resident
-    scratch) or, with ADG_CLUSTER_PREDICTOR=1, on the thread-block cluster
-    kernel (one time slice per CTA, time operator over DSMEM): q, traces,
-    volume and sweep counts against the oracle's per-element Picard on
-    seeded, anisotropic data (N=6 is the single-CTA shared-memory kernel, for
+def test_large_tile_predictor_matches_oracle(pkg, n, variant, monkeypatch):
+    """3-D N>=7 tiles run as phase kernels over element batches (startup /
+    rates per time slice / time operator / final, the iterate in HBM) or, with
+    ADG_PREDICTOR=stream, on the fused slice-streaming kernel (one CTA per
+    element, q and rates in an L2-resident scratch): q, traces, volume and
+    sweep counts against the oracle's per-element Picard on seeded,
+    anisotropic data (N=6 is the single-CTA shared-memory kernel, for
     comparison)."""
-    if cluster:
-        if n < 7:
-            pytest.skip("the cluster kernel covers N = 7..9")
-        monkeypatch.setenv("ADG_CLUSTER_PREDICTOR", "1")
+    if n < 7 and variant != "phased":
+        pytest.skip("variants cover N = 7..9")
+    monkeypatch.setenv("ADG_PREDICTOR", variant)
     from oracle import dg
     from oracle.basis import oracle_tables
     from oracle.euler import EulerOracle
