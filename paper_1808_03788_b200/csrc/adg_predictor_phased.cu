@@ -48,6 +48,12 @@ namespace adg {
 #ifndef ADG_PH_RP
 #define ADG_PH_RP 0
 #endif
+// output halves per line: with NH = 2 two warp groups own the same lines and
+// each accumulates half of the P outputs (half the accumulator registers,
+// twice the warps per CTA; the line's fluxes are formed by both)
+#ifndef ADG_PH_NH
+#define ADG_PH_NH 1
+#endif
 
 template <int P>
 struct PhCfg {
@@ -64,19 +70,28 @@ struct PhCfg {
   static constexpr int QSZ = P * SI;
   static constexpr int BSZ = P * TJ;
   static constexpr int QSZP = QSZ + (QSZ & 1);
-  static constexpr int BSZP = BSZ + (BSZ & 1);
+  // (the partial buffer also stages a stored slice in the first sweep)
+  static constexpr int BSZP = (BSZ > QSZ ? BSZ : QSZ) + ((BSZ > QSZ ? BSZ : QSZ) & 1);
   static constexpr int RP = ((PP + 31) / 32) * 32;   // line owners, whole warps
-  static constexpr int NW = RP / 32;
+  static constexpr int NH = ADG_PH_NH;
+  static constexpr int H = (P + NH - 1) / NH;        // outputs per thread
+  static constexpr int NT_A = NH * RP;               // threads of the line kernels
+  static constexpr int NW = NT_A / 32;
   static constexpr int CSTP = (2 * P + 1) / 2 * 2;
   static constexpr size_t SLICE = (size_t)PD * M;    // doubles per time slice
   static constexpr size_t TILE = (size_t)P * SLICE;  // doubles per space-time tile
+  // the iterate is stored slice by slice in the PADDED shared-memory layout
+  // (QSZP doubles, even: 16-byte aligned), so a slice lands in shared memory
+  // with one bulk copy (cp.async.bulk, TMA) instead of P^3 m 8-byte copies
+  static constexpr size_t TILEQ = (size_t)P * QSZP;
+  static constexpr bool DENSE = (SJ == P * M) && (SI == P * SJ);
   static constexpr int TB = PD * M + ((PD * M) & 1); // trace block (face kernel layout)
   // rates / startup: one slice + one partial buffer
   static constexpr int XSZ = ADG_PH_RP ? 2 * PD : 0;   // (1 / rho, p) per node
   static constexpr size_t SMEM_A = ((size_t)QSZP + BSZP + XSZ) * 8;
   // register cap of the line kernels: 168 per thread (a warp's registers
   // come from its scheduler's 16 K: more would cost the third CTA per SM)
-  static constexpr int MINB_A = 384 / RP;
+  static constexpr int MINB_A = NH == 1 ? 384 / RP : (640 / NT_A > 0 ? 640 / NT_A : 1);
   // traces: one slice, three line-owner groups side by side
   static constexpr int NT_F = 3 * RP;
   static constexpr int TRS = 6 * PP * M;             // staged traces of one slice
@@ -97,7 +112,7 @@ struct PhArgs {
   int32_t* sweeps;
   double* qg;           // [n][P][node][v] iterate
   double* rg;           // [n][P][node][v] rates; after the sweeps slices 0..2 = Fbar_x/y/z
-  double* kg;           // [n][2][node][v] startup rates k1, k2
+  double* kg;           // [n][3] stored (padded) slices: u, k1, k2 - k1
   int32_t* state;       // [4][n]: frozen, converged, sweeps executed, inadmissible
   int32_t* n_active;
   int64_t n_elem;       // elements in the batch
@@ -115,13 +130,13 @@ struct PhArgs {
 // contraction, l-outer: every line state is loaded, turned into its flux and
 // folded into all P outputs (same per-output fma order as a row-by-row
 // mat-vec)
-template <int P, int DIR>
-__device__ __forceinline__ void ph_line(const double* src0, int stride, const double* x0,
-                                        int xstride, double gm1, const double* dd,
-                                        double (&acc)[P][5]) {
-  constexpr int M = 5;
+template <int P, int DIR, int HF>
+__device__ __forceinline__ void ph_line_h(const double* src0, int stride, const double* x0,
+                                          int xstride, double gm1, const double* dd,
+                                          double (&acc)[PhCfg<P>::H][5]) {
+  constexpr int M = 5, H = PhCfg<P>::H, IB = HF * H;
 #pragma unroll
-  for (int i = 0; i < P; ++i)
+  for (int i = 0; i < H; ++i)
 #pragma unroll
     for (int v = 0; v < M; ++v) acc[i][v] = 0.0;
   constexpr int LU = ADG_PH_LUNROLL;
@@ -146,12 +161,23 @@ __device__ __forceinline__ void ph_line(const double* src0, int stride, const do
       flux_axis<3>(q, gm1, DIR, f);
     }
 #pragma unroll
-    for (int i = 0; i < P; ++i) {
-      const double d = dd[DIR * P * P + i * P + l];
+    for (int i = 0; i < H; ++i) {
+      if (IB + i < P) {
+        const double d = dd[DIR * P * P + (IB + i) * P + l];
 #pragma unroll
-      for (int v = 0; v < M; ++v) acc[i][v] = fma(d, f[v], acc[i][v]);
+        for (int v = 0; v < M; ++v) acc[i][v] = fma(d, f[v], acc[i][v]);
+      }
     }
   }
+}
+template <int P, int DIR>
+__device__ __forceinline__ void ph_line(const double* src0, int stride, const double* x0,
+                                        int xstride, double gm1, const double* dd, int half,
+                                        double (&acc)[PhCfg<P>::H][5]) {
+  if (PhCfg<P>::NH == 1 || half == 0)
+    ph_line_h<P, DIR, 0>(src0, stride, x0, xstride, gm1, dd, acc);
+  else
+    ph_line_h<P, DIR, PhCfg<P>::NH - 1>(src0, stride, x0, xstride, gm1, dd, acc);
 }
 
 // 1 / rho and p of every node of the padded slice Q -> X[node] (node-major,
@@ -204,18 +230,42 @@ struct PhRoles {
   __device__ __forceinline__ int xrow() const { return a0 * C::TJ + b0 * C::TK; }
 };
 
-// a [node][v] slice (global) into the padded slice buffer: P^2 rows (i, j) of
-// P m contiguous doubles, one warp per row, asynchronous 8-byte copies
-template <int P, int NWARPS>
-__device__ __forceinline__ void ph_fetch(double* buf, const double* src, int warp, int lane) {
+// offset of the x-th double of a [node][v] slice in the padded slice layout
+template <int P>
+__device__ __forceinline__ int ph_pad(int x) {
   using C = PhCfg<P>;
-  for (int row = warp; row < C::PP; row += NWARPS) {
-    const int i = row / P, j = row - (row / P) * P;
-    double* dst = buf + i * C::SI + j * C::SJ;
-    const double* sr = src + row * (P * C::M);
-    for (int o = lane; o < P * C::M; o += 32) cp_async8(dst + o, sr + o);
+  if constexpr (C::DENSE) {
+    return x;
+  } else {
+    const int row = x / (P * C::M), o = x - row * (P * C::M);
+    const int i = row / P, j = row - i * P;
+    return i * C::SI + j * C::SJ + o;
   }
+}
+
+// a dense [node][v] slice (global) into the padded slice buffer, asynchronous
+// 8-byte copies, consecutive threads on consecutive doubles
+template <int P, int NT>
+__device__ __forceinline__ void ph_fetch(double* buf, const double* src, int tid) {
+  using C = PhCfg<P>;
+  for (int x = tid; x < (int)C::SLICE; x += NT) cp_async8(buf + ph_pad<P>(x), src + x);
   cp_async_commit();
+}
+
+// a stored (padded) slice of the iterate into the slice buffer: one bulk copy
+// issued by thread 0, completion on the CTA's mbarrier.  Call after a
+// __syncthreads() that ends every generic access to buf.
+template <int P>
+__device__ __forceinline__ void ph_fetch_bulk(double* buf, const double* src, uint64_t* bar,
+                                              uint32_t& phase, int tid) {
+  using C = PhCfg<P>;
+  if (tid == 0) {
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, (uint32_t)(C::QSZP * 8));
+    bulk_g2s(buf, src, (uint32_t)(C::QSZP * 8), bar);
+  }
+  mbar_wait(bar, phase);
+  phase ^= 1u;
 }
 
 // rates of the slice in Q -> rt ([node][v], global): the owners contract their
@@ -224,52 +274,67 @@ __device__ __forceinline__ void ph_fetch(double* buf, const double* src, int war
 // (Staging the slice of rates in shared memory for coalesced stores was
 // measured neutral here: 8.26 vs 8.08 ms per sweep at N = 8, and it costs
 // 30-50 registers.)
-template <int P>
+// OUT 0: rt is a dense [node][v] slice; OUT 1: a padded slice (the stored
+// layout); OUT 2: padded, and the value stored is the rate minus the same
+// thread's earlier OUT 1 output at sub (the startup's k2 - k1)
+template <int P, int OUT>
 __device__ __forceinline__ void ph_slice_rates(const double* Q, double* B, double* X,
-                                               double* rt, const PhRoles<P>& R, bool owner,
+                                               double* rt, const double* sub,
+                                               const PhRoles<P>& R, bool owner, int half,
                                                double gm1, const double* dd, int tid) {
-  constexpr int M = 5;
-  ph_prepass<P, PhCfg<P>::RP>(Q, X, gm1, tid);
-  double acc[P][M];
+  using C = PhCfg<P>;
+  constexpr int M = 5, H = C::H;
+  const int ib = half * H;
+  ph_prepass<P, C::NT_A>(Q, X, gm1, tid);
+  double acc[H][M];
   if (owner) {
     ph_line<P, 2>(Q + R.qbase(2), R.qstride(2), X + 2 * R.nbase(2), 2 * R.nstride(2), gm1, dd,
-                  acc);
+                  half, acc);
     const int pb = R.pbase(2), ps = R.pstride(2);
 #pragma unroll
-    for (int i = 0; i < P; ++i)
+    for (int i = 0; i < H; ++i)
+      if (ib + i < P)
 #pragma unroll
-      for (int v = 0; v < M; ++v) B[pb + i * ps + v] = acc[i][v];
+        for (int v = 0; v < M; ++v) B[pb + (ib + i) * ps + v] = acc[i][v];
   }
   __syncthreads();
   if (owner) {
     ph_line<P, 1>(Q + R.qbase(1), R.qstride(1), X + 2 * R.nbase(1), 2 * R.nstride(1), gm1, dd,
-                  acc);
+                  half, acc);
     const int pb = R.pbase(1), ps = R.pstride(1);
 #pragma unroll
-    for (int i = 0; i < P; ++i)
+    for (int i = 0; i < H; ++i)
+      if (ib + i < P)
 #pragma unroll
-      for (int v = 0; v < M; ++v) B[pb + i * ps + v] += acc[i][v];
+        for (int v = 0; v < M; ++v) B[pb + (ib + i) * ps + v] += acc[i][v];
   }
   __syncthreads();
   if (owner) {
     ph_line<P, 0>(Q + R.qbase(0), R.qstride(0), X + 2 * R.nbase(0), 2 * R.nstride(0), gm1, dd,
-                  acc);
+                  half, acc);
     const int xr = R.xrow(), nb = R.nbase(0), ns = R.nstride(0);
+    const int qb = R.qbase(0), qs = R.qstride(0);
 #pragma unroll
-    for (int i = 0; i < P; ++i) {
-      double* out = rt + (size_t)(nb + i * ns) * M;
+    for (int i = 0; i < H; ++i) {
+      if (ib + i < P) {
+        const int o = OUT == 0 ? (nb + (ib + i) * ns) * M : qb + (ib + i) * qs;
 #pragma unroll
-      for (int v = 0; v < M; ++v) out[v] = -acc[i][v] - B[xr + i * M + v];
+        for (int v = 0; v < M; ++v) {
+          double val = -acc[i][v] - B[xr + (ib + i) * M + v];
+          if (OUT == 2) val = val - sub[o + v];
+          rt[o + v] = val;
+        }
+      }
     }
   }
 }
 
 // the startup iterate at time level t (predictor.py:116-124): q_t = u +
-// s_t k1 + s_t^2 / (2 dt) (k2 - k1), one expression for every kernel that
-// forms it
-__device__ __forceinline__ double ph_startup_q(double un, double k1, double k2, double s,
+// s_t k1 + s_t^2 / (2 dt) (k2 - k1) from u, k1 and d = k2 - k1: one expression
+// for every kernel that forms it
+__device__ __forceinline__ double ph_startup_q(double un, double k1, double d, double s,
                                                double c2) {
-  return fma(c2, k2 - k1, fma(s, k1, un));
+  return fma(c2, d, fma(s, k1, un));
 }
 
 // ---------------------------------------------------------------- startup
@@ -277,7 +342,7 @@ __device__ __forceinline__ double ph_startup_q(double un, double k1, double k2, 
 // slices; the iterate itself is never stored (the first sweep's kernels form
 // it from u, k1, k2).  Resets the element's state.
 template <int P>
-__global__ void __launch_bounds__(PhCfg<P>::RP, PhCfg<P>::MINB_A)
+__global__ void __launch_bounds__(PhCfg<P>::NT_A, PhCfg<P>::MINB_A)
 ph_startup_kernel(const __grid_constant__ PhArgs a) {
   using C = PhCfg<P>;
   constexpr int M = C::M, PP = C::PP, NW = C::NW;
@@ -286,28 +351,29 @@ ph_startup_kernel(const __grid_constant__ PhArgs a) {
   double* B = Q + C::QSZP;
   double* X = B + C::BSZP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool owner = tid < PP;
-  const PhRoles<P> R(owner ? tid : 0);
+  const int half = tid / C::RP, rr0 = tid - half * C::RP;
+  const bool owner = rr0 < PP;
+  const PhRoles<P> R(owner ? rr0 : 0);
   const double gm1 = a.gamma - 1.0;
   const double dt = *a.dt;
   for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
     const double* ue = a.u + (size_t)e * C::SLICE;
-    double* ke = a.kg + (size_t)e * 2 * C::SLICE;
+    double* ke = a.kg + (size_t)e * 3 * C::QSZP;   // stored slices: u, k1, k2 - k1
     __syncthreads();   // previous element done with Q / B
-    ph_fetch<P, NW>(Q, ue, warp, lane);
+    ph_fetch<P, C::NT_A>(Q, ue, tid);
     cp_async_wait_all();
     __syncthreads();
-    ph_slice_rates<P>(Q, B, X, ke, R, owner, gm1, a.dd, tid);          // k1
+    for (int x = tid; x < C::QSZP; x += C::NT_A) ke[x] = Q[x];   // u in the stored layout
+    ph_slice_rates<P, 1>(Q, B, X, ke + C::QSZP, nullptr, R, owner, half, gm1, a.dd, tid);   // k1
     __syncthreads();   // k1 stored, every line of Q read
     // w = u + dt k1 in the tile (k1 read back from this CTA's own stores)
-    for (int row = warp; row < PP; row += NW) {
-      const int i = row / P, j = row - (row / P) * P;
-      double* dst = Q + i * C::SI + j * C::SJ;
-      const double* k1 = ke + row * (P * M);
-      for (int o = lane; o < P * M; o += 32) dst[o] = dst[o] + dt * k1[o];
+    for (int x = tid; x < (int)C::SLICE; x += C::NT_A) {
+      const int xp = ph_pad<P>(x);
+      Q[xp] = Q[xp] + dt * ke[C::QSZP + xp];
     }
     __syncthreads();
-    ph_slice_rates<P>(Q, B, X, ke + C::SLICE, R, owner, gm1, a.dd, tid);   // k2
+    ph_slice_rates<P, 2>(Q, B, X, ke + 2 * C::QSZP, ke + C::QSZP, R, owner, half, gm1, a.dd,
+                         tid);   // k2 - k1
     if (tid == 0) {
       a.state[e] = 0;
       a.state[a.n_elem + e] = 0;
@@ -322,7 +388,7 @@ ph_startup_kernel(const __grid_constant__ PhArgs a) {
 // one task per (element, time slice) of the elements still iterating; the
 // first sweep (it == 0) forms its slice of the startup iterate from u, k1, k2
 template <int P>
-__global__ void __launch_bounds__(PhCfg<P>::RP, PhCfg<P>::MINB_A)
+__global__ void __launch_bounds__(PhCfg<P>::NT_A, PhCfg<P>::MINB_A)
 ph_rates_kernel(const __grid_constant__ PhArgs a) {
   using C = PhCfg<P>;
   constexpr int M = C::M, PP = C::PP, NW = C::NW;
@@ -333,49 +399,55 @@ ph_rates_kernel(const __grid_constant__ PhArgs a) {
   double* B = Q + C::QSZP;
   double* X = B + C::BSZP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool owner = tid < PP;
-  const PhRoles<P> R(owner ? tid : 0);
+  const int half = tid / C::RP, rr0 = tid - half * C::RP;
+  const bool owner = rr0 < PP;
+  const PhRoles<P> R(owner ? rr0 : 0);
   const double gm1 = a.gamma - 1.0;
   const double dt = *a.dt;
   const int64_t ntask = a.n_elem * P;
+  __shared__ __align__(8) uint64_t bar;
+  uint32_t phase = 0;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
     const int64_t e = task / P;
     const int t = (int)(task - e * P);
     if (a.state[e]) continue;
-    __syncthreads();   // previous task done with Q / B
+    __syncthreads();   // previous task done with Q / B (first pass: barrier initialised)
     if (a.it == 0) {
+      // the startup iterate's slice from the stored u, k1, k2 - k1: u and k1
+      // land in Q and B by bulk copy while d travels through registers
+      // (coalesced loads issued before the wait), one pass folds them
       const double s = T.nodes[t] * dt, c2 = 0.5 * s * s / dt;
-      const double* ue = a.u + (size_t)e * C::SLICE;
-      const double* ke = a.kg + (size_t)e * 2 * C::SLICE;
-      // eight values per thread in flight: their 24 loads issue before the
-      // first use
-      constexpr int NB = 8, NT = C::RP, SL = (int)C::SLICE;
-      for (int x0 = tid; x0 < SL; x0 += NB * NT) {
-        double un[NB], k1[NB], k2[NB];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const int x = x0 + b * NT < SL ? x0 + b * NT : x0;
-          un[b] = ue[x];
-          k1[b] = ke[x];
-          k2[b] = ke[SL + x];
-        }
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const int x = x0 + b * NT;
-          if (x < SL) {
-            const int row = x / (P * M), o = x - row * (P * M);
-            const int i = row / P, j = row - i * P;
-            Q[i * C::SI + j * C::SJ + o] = ph_startup_q(un[b], k1[b], k2[b], s, c2);
-          }
-        }
+      const double* ke = a.kg + (size_t)e * 3 * C::QSZP;
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(&bar, (uint32_t)(2 * C::QSZP * 8));
+        bulk_g2s(Q, ke, (uint32_t)(C::QSZP * 8), &bar);
+        bulk_g2s(B, ke + C::QSZP, (uint32_t)(C::QSZP * 8), &bar);
       }
+      constexpr int NI = (C::QSZP + C::NT_A - 1) / C::NT_A;
+      double dreg[NI];
+#pragma unroll
+      for (int k = 0; k < NI; ++k) {
+        const int x = tid + k * C::NT_A;
+        dreg[k] = x < C::QSZP ? __ldcs(ke + 2 * C::QSZP + x) : 0.0;
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+#pragma unroll
+      for (int k = 0; k < NI; ++k) {
+        const int x = tid + k * C::NT_A;
+        if (x < C::QSZP) Q[x] = ph_startup_q(Q[x], B[x], dreg[k], s, c2);
+      }
+      __syncthreads();
     } else {
-      ph_fetch<P, NW>(Q, a.qg + (size_t)e * C::TILE + (size_t)t * C::SLICE, warp, lane);
-      cp_async_wait_all();
+      ph_fetch_bulk<P>(Q, a.qg + (size_t)e * C::TILEQ + (size_t)t * C::QSZP, &bar, phase, tid);
     }
-    __syncthreads();
-    ph_slice_rates<P>(Q, B, X, a.rg + (size_t)e * C::TILE + (size_t)t * C::SLICE, R, owner,
-                      gm1, a.dd, tid);
+    ph_slice_rates<P, 0>(Q, B, X, a.rg + (size_t)e * C::TILE + (size_t)t * C::SLICE, nullptr, R,
+                         owner, half, gm1, a.dd, tid);
   }
 }
 
@@ -393,30 +465,35 @@ ph_time_kernel(const __grid_constant__ PhArgs a) {
   if (*a.n_active <= 0) return;
   const DegreeTables& T = tab<P>();
   __shared__ double red[2 * NW];
+  __shared__ double cst[2 * P];   // startup coefficients s_t, s_t^2 / (2 dt)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double dt = *a.dt;
+  if (tid < P) {
+    const double s = T.nodes[tid] * dt;
+    cst[tid] = s;
+    cst[P + tid] = 0.5 * s * s / dt;
+  }
+  __syncthreads();
   for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
     if (a.state[e]) continue;
     const double* ue = a.u + (size_t)e * C::SLICE;
-    const double* ke = a.kg + (size_t)e * 2 * C::SLICE;
-    double* Qg = a.qg + (size_t)e * C::TILE;
+    const double* ke = a.kg + (size_t)e * 3 * C::QSZP;
+    double* Qg = a.qg + (size_t)e * C::TILEQ;
     const double* Rg = a.rg + (size_t)e * C::TILE;
     double sd = 0.0, sq = 0.0;
     for (int x = tid; x < PD * M; x += NT) {
+      const int xp = ph_pad<P>(x);   // position inside a stored (padded) slice
       double r[P], qo[P];
 #pragma unroll
       for (int s2 = 0; s2 < P; ++s2) r[s2] = __ldcs(Rg + s2 * C::SLICE + x);
       const double uu = ue[x];
       if (a.it == 0) {
-        const double k1 = ke[x], k2 = ke[C::SLICE + x];
+        const double k1 = ke[C::QSZP + xp], d = ke[2 * C::QSZP + xp];
 #pragma unroll
-        for (int t2 = 0; t2 < P; ++t2) {
-          const double s = T.nodes[t2] * dt, c2 = 0.5 * s * s / dt;
-          qo[t2] = ph_startup_q(uu, k1, k2, s, c2);
-        }
+        for (int t2 = 0; t2 < P; ++t2) qo[t2] = ph_startup_q(uu, k1, d, cst[t2], cst[P + t2]);
       } else {
 #pragma unroll
-        for (int t2 = 0; t2 < P; ++t2) qo[t2] = Qg[t2 * C::SLICE + x];
+        for (int t2 = 0; t2 < P; ++t2) qo[t2] = Qg[t2 * C::QSZP + xp];
       }
 #pragma unroll
       for (int t2 = 0; t2 < P; ++t2) {
@@ -427,7 +504,7 @@ ph_time_kernel(const __grid_constant__ PhArgs a) {
         const double dq = qo[t2] - qn;
         sd = fma(dq, dq, sd);
         sq = fma(qn, qn, sq);
-        Qg[t2 * C::SLICE + x] = qn;
+        Qg[t2 * C::QSZP + xp] = qn;
       }
     }
 #pragma unroll
@@ -483,13 +560,17 @@ ph_traces_kernel(const __grid_constant__ PhArgs a) {
   const int qbase = R.qbase(role), qstride = R.qstride(role);
   const int64_t ntask = a.n_elem * P;
   const size_t fs = (size_t)a.tr_elems * C::TB;
+  __shared__ __align__(8) uint64_t bar;
+  uint32_t phase = 0;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
     const int64_t e = task / P;
     const int t = (int)(task - e * P);
-    __syncthreads();   // previous task done with Q
-    ph_fetch<P, NW>(Q, a.qg + (size_t)e * C::TILE + (size_t)t * C::SLICE, warp, lane);
-    cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();   // previous task done with Q / S
+    ph_fetch_bulk<P>(Q, a.qg + (size_t)e * C::TILEQ + (size_t)t * C::QSZP, &bar, phase, tid);
     if (owner) {
       double lo[M], hi[M];
 #pragma unroll
@@ -553,14 +634,14 @@ ph_fbar_kernel(const __grid_constant__ PhArgs a) {
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = g / PD;
     const int n = (int)(g - e * PD);
-    const double* qe = a.qg + (size_t)e * C::TILE + (size_t)n * M;
+    const double* qe = a.qg + (size_t)e * C::TILEQ + ph_pad<P>(n * M);
     double fb[3][M];
     bool ok = true;
 #pragma unroll
     for (int t = 0; t < P; ++t) {
       double q[M];
 #pragma unroll
-      for (int v = 0; v < M; ++v) q[v] = qe[(size_t)t * C::SLICE + v];
+      for (int v = 0; v < M; ++v) q[v] = qe[(size_t)t * C::QSZP + v];
       ok = ok && admissible<3>(q, gm1);
       const double wt = T.weights[t];
       double f[M];
@@ -611,7 +692,7 @@ template <int P>
 __global__ void __launch_bounds__(PhCfg<P>::RP)
 ph_vol_kernel(const __grid_constant__ PhArgs a) {
   using C = PhCfg<P>;
-  constexpr int M = C::M, PP = C::PP, PD = C::PD, NW = C::NW;
+  constexpr int M = C::M, PP = C::PP, PD = C::PD, NW = C::RP / 32;
   const DegreeTables& T = tab<P>();
   extern __shared__ __align__(16) double smem[];
   double* Q = smem;
@@ -630,7 +711,7 @@ ph_vol_kernel(const __grid_constant__ PhArgs a) {
 #pragma unroll 1
     for (int role = 2; role >= 0; --role) {
       __syncthreads();   // previous readers of Q are done
-      ph_fetch<P, NW>(Q, fe + (size_t)role * C::SLICE, warp, lane);
+      ph_fetch<P, C::RP>(Q, fe + (size_t)role * C::SLICE, tid);
       cp_async_wait_all();
       __syncthreads();
       if (owner) {
@@ -680,7 +761,7 @@ ph_vol_kernel(const __grid_constant__ PhArgs a) {
 // ------------------------------------------------------------------- host
 template <int P>
 static size_t phased_bytes_per_element() {
-  return (2 * PhCfg<P>::TILE + 2 * PhCfg<P>::SLICE) * 8 + 4 * sizeof(int32_t);
+  return (PhCfg<P>::TILEQ + PhCfg<P>::TILE + 3 * PhCfg<P>::QSZP) * 8 + 4 * sizeof(int32_t);
 }
 
 // elements per batch: the whole grid, capped so the iterate + rates stay
@@ -727,7 +808,7 @@ static int launch_phased(const PhArgs& a0, int64_t n_all, cudaStream_t st, int n
     return ADG_ERR_RUNTIME;
   }
   int occ_a = 1, occ_t = 1, occ_tr = 1, occ_v = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, ph_rates_kernel<P>, C::RP, C::SMEM_A);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, ph_rates_kernel<P>, C::NT_A, C::SMEM_A);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, ph_time_kernel<P>, C::NT_T, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tr, ph_traces_kernel<P>, C::NT_F,
                                                 C::SMEM_TR);
@@ -748,19 +829,19 @@ static int launch_phased(const PhArgs& a0, int64_t n_all, cudaStream_t st, int n
     a.n_elem = n;
     a.tr_elems = n_all;
     a.qg = ws;
-    a.rg = ws + (size_t)batch * C::TILE;
-    a.kg = ws + 2 * (size_t)batch * C::TILE;
-    a.state = reinterpret_cast<int32_t*>(a.kg + 2 * (size_t)batch * C::SLICE);
+    a.rg = a.qg + (size_t)batch * C::TILEQ;
+    a.kg = a.rg + (size_t)batch * C::TILE;
+    a.state = reinterpret_cast<int32_t*>(a.kg + 3 * (size_t)batch * C::QSZP);
     a.n_active = a.state + 4 * batch;
     cudaMemsetAsync(a.n_active, 0, sizeof(int32_t), st);
     const auto grid = [&](int64_t tasks, int occ, int waves) {
       return (unsigned)std::max<int64_t>(
           1, std::min<int64_t>(tasks, (int64_t)num_sms * occ * waves));
     };
-    ph_startup_kernel<P><<<grid(n, occ_a, 4), C::RP, C::SMEM_A, st>>>(a);
+    ph_startup_kernel<P><<<grid(n, occ_a, 4), C::NT_A, C::SMEM_A, st>>>(a);
     for (int it = 0; it < a.max_iter; ++it) {
       a.it = it;
-      ph_rates_kernel<P><<<grid(n * P, occ_a, 4), C::RP, C::SMEM_A, st>>>(a);
+      ph_rates_kernel<P><<<grid(n * P, occ_a, 4), C::NT_A, C::SMEM_A, st>>>(a);
       ph_time_kernel<P><<<grid(n, occ_t, 4), C::NT_T, 0, st>>>(a);
     }
     ph_traces_kernel<P><<<grid(n * P, occ_tr, 4), C::NT_F, C::SMEM_TR, st>>>(a);
