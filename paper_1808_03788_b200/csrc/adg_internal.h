@@ -55,12 +55,6 @@ int predict_phased(const adg_grid* g, const double* u, const double* dt_dev, dou
                    int max_iter, int min_iter, double* q_out, double* vol, double* traces,
                    uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms, double* ws,
                    size_t ws_bytes, std::string* err);
-bool predict_cluster_supported(const adg_grid* g);
-int predict_cluster(const adg_grid* g, const double* u, const double* dt_dev, double tol,
-                    int max_iter, int min_iter, double* q_out, double* vol, double* traces,
-                    uint8_t* pred_bad, int32_t* sweeps, cudaStream_t st, int num_sms,
-                    std::string* err);
-
 // linear advection (adg_advection.cu)
 int adv_predict(const adg_grid* g, const double* u, const double* dt_dev, double tol,
                 int max_iter, int min_iter, double* q_out, double* vol, double* traces,

@@ -1132,10 +1132,7 @@ size_t predict_workspace_bytes(int dim, int P, int num_sms, int64_t n_elem) {
   return 0;
 }
 
-bool predict_range_supported(const adg_grid* g) {
-  return !(predict_stream_supported(g) || getenv("ADG_CLUSTER_PREDICTOR") ||
-           predict_cluster_supported(g));
-}
+bool predict_range_supported(const adg_grid* g) { return !predict_stream_supported(g); }
 
 int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol, int max_iter,
             int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
@@ -1151,7 +1148,7 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   }
   const bool whole = e_begin == 0 && e_count == n_all;
   if (!whole && !predict_range_supported(g)) {
-    *err = "element ranges need the shared-tile predictor (not the 3-D N>=7 stream/cluster kernels)";
+    *err = "element ranges need the shared-tile predictor (not the 3-D N>=7 phased / stream kernels)";
     return ADG_ERR_UNSUPPORTED;
   }
   // a caller's starting iterate or a startup-only call runs the shared-tile
@@ -1160,26 +1157,19 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   // 3-D N >= 7 grids too (A/B runs against the slice-streaming kernel)
   const char* pv = getenv("ADG_PREDICTOR");
   const bool plain = q_init == nullptr && !startup_only && !(pv && pv[0] == 't');
-  // 3-D tiles beyond one SM's shared memory: one CTA per element streaming
-  // time slices through shared memory (adg_predictor_stream.cu)
-  // ... or, from N = 8 up (ADG_PREDICTOR=phased: N = 7 too; =stream: never), as
-  // phase kernels over element batches with the iterate in HBM
-  // (adg_predictor_phased.cu): 34.5 vs 51.4 ms at N = 8, 58.6 vs 78.3 ms at
-  // N = 9 on 32^3 elements, 18.3 vs 17.4 ms at N = 7
-  if (plain && !(pv && pv[0] == 's') && !getenv("ADG_CLUSTER_PREDICTOR") &&
-      predict_phased_supported(g) && (g->degree >= 8 || (pv && pv[0] == 'p')))
+  // 3-D tiles beyond one SM's shared memory (N >= 7): from N = 8 up as phase
+  // kernels over element batches with the iterate in HBM
+  // (adg_predictor_phased.cu: 30.1 vs 51.4 ms at N = 8, 56.1 vs 78.3 ms at N = 9
+  // on 32^3 elements), at N = 7 as one CTA per element streaming time slices
+  // through shared memory (adg_predictor_stream.cu: 17.4 vs 18.2 ms);
+  // ADG_PREDICTOR=phased / stream forces one of them for A/B runs
+  if (plain && predict_phased_supported(g) && !(pv && pv[0] == 's') &&
+      (g->degree >= 8 || (pv && pv[0] == 'p')))
     return predict_phased(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
                           sweeps, st, num_sms, ws, ws_bytes, err);
-  if (plain && !getenv("ADG_CLUSTER_PREDICTOR") && predict_stream_supported(g))
+  if (plain && predict_stream_supported(g))
     return predict_stream(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
                           sweeps, st, num_sms, ws, ws_bytes, err);
-#ifndef ADG_NO_CLUSTER
-  // the earlier design: thread-block cluster, one time slice per CTA
-  // (adg_predictor_cluster.cu), kept for A/B runs (ADG_CLUSTER_PREDICTOR=1)
-  if (plain && predict_cluster_supported(g))
-    return predict_cluster(g, u, dt_dev, tol, max_iter, min_iter, q_out, vol, traces, pred_bad,
-                           sweeps, st, num_sms, err);
-#endif
   // an element range [e_begin, e_begin + e_count) is the same launch on
   // pointers advanced to its first element; only the trace planes keep the
   // whole grid's stride (the slab decomposition predicts its boundary layers

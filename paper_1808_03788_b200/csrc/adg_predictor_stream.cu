@@ -14,14 +14,13 @@
 // only couples the time levels of one spatial node.  So a sweep is
 //   (1) for t = 0..P-1: slice t of q -> shared memory (cp.async; the next
 //       slice is fetched while the current slice's rates are stored), the
-//       3 P^2 line owners contract flux lines as in the cluster kernel, and
+//       3 P^2 line owners contract the slice's flux lines, and
 //       the x-owner stores the slice's rates to the scratch;
 //   (2) node phase: every thread takes nodes n, reads rate[0..P-1][n] (P x m
 //       values in registers), forms q_new at every time, the residual
 //       partials and stores q_new over q.
-// All CTAs of the GPU stay busy on their own element (no cluster scheduling
-// constraints), and the spatial phase keeps the cluster kernel's
-// conflict-light padded slice layouts.  The startup guess needs only two
+// All CTAs of the GPU stay busy on their own element; the slice buffers use
+// conflict-light padded layouts (tools/slice_bankcheck.py).  The startup guess needs only two
 // spatial passes on u (k1 = L(u), k2 = L(u + dt k1)); the q at every time is a
 // pointwise formula of (u, k1, k2).
 #include <algorithm>
@@ -44,7 +43,7 @@ struct StCfg {
   static constexpr int M = 5;
   static constexpr int PP = P * P;
   static constexpr int PD = P * P * P;
-  // padded slice layouts (tools/cluster_bankcheck.py): Q node-major
+  // padded slice layouts (tools/slice_bankcheck.py): Q node-major
   // [i][j][k][v] strides (SI, SJ, M); B x-line-major [j][k][i][v] strides
   // (TJ, TK, M)
   static constexpr int SJ = P * M + (P == 8 ? 1 : (P == 10 ? 3 : 0));

@@ -249,7 +249,7 @@ def test_fused_subcell_reuse_is_bitwise(pkg):
     assert torch.equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("variant", ["phased", "stream"])
+@pytest.mark.parametrize("variant", ["phased", "phased-batches", "stream"])
 @pytest.mark.parametrize("n", [6, 7, 8, 9])
 def test_large_tile_predictor_matches_oracle(pkg, n, variant, monkeypatch):
     """3-D N>=7 tiles run as phase kernels over element batches (startup /
@@ -261,7 +261,10 @@ def test_large_tile_predictor_matches_oracle(pkg, n, variant, monkeypatch):
     comparison)."""
     if n < 7 and variant != "phased":
         pytest.skip("variants cover N = 7..9")
-    monkeypatch.setenv("ADG_PREDICTOR", variant)
+    monkeypatch.setenv("ADG_PREDICTOR", variant.split("-")[0])
+    if variant == "phased-batches":
+        # 1 MB of iterate + rates per batch: the 6 elements run as 2..6 batches
+        monkeypatch.setenv("ADG_PHASED_CAP_MB", "1")
     from oracle import dg
     from oracle.basis import oracle_tables
     from oracle.euler import EulerOracle

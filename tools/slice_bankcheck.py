@@ -1,4 +1,4 @@
-"""Padding search for the cluster predictor's slice buffers (adg_predictor_cluster.cu):
+"""Padding search for the slice buffers of the 3-D N >= 7 predictors (adg_predictor_stream.cu, adg_predictor_phased.cu):
 Q node-major [i][j][k][v] with strides (SI, SJ, M); B x-line-major
 [j][k][i][v] with strides (TJ, TK, M).  Lanes of each owner role map to
 (a0, b0) = (rr // P, rr % P).  Prints the wavefronts per access pattern
