@@ -55,6 +55,10 @@ namespace adg {
 #ifndef ADG_PH_NH
 #define ADG_PH_NH 1
 #endif
+// (node, quantity) items per thread in flight in the time kernel
+#ifndef ADG_PH_TNB
+#define ADG_PH_TNB 1
+#endif
 
 
 template <int P>
@@ -461,7 +465,7 @@ ph_rates_kernel(const __grid_constant__ PhArgs a) {
 // element, one (node, quantity) per thread and pass: its P rates and P old
 // iterates are loaded up front (all independent: HBM latency overlapped)
 template <int P>
-__global__ void __launch_bounds__(PhCfg<P>::NT_T, 3)
+__global__ void __launch_bounds__(PhCfg<P>::NT_T, ADG_PH_TNB == 1 ? 3 : 2)
 ph_time_kernel(const __grid_constant__ PhArgs a) {
   using C = PhCfg<P>;
   constexpr int M = C::M, PD = C::PD, NT = C::NT_T, NW = NT / 32;
@@ -484,30 +488,47 @@ ph_time_kernel(const __grid_constant__ PhArgs a) {
     double* Qg = a.qg + (size_t)e * C::TILEQ;
     const double* Rg = a.rg + (size_t)e * C::TILE;
     double sd = 0.0, sq = 0.0;
-    for (int x = tid; x < PD * M; x += NT) {
-      const int xp = ph_pad<P>(x);   // position inside a stored (padded) slice
-      double r[P], qo[P];
+    // NB items per thread in flight: their loads all issue before the first
+    // use (the kernel is bound by HBM latency x bytes in flight)
+    constexpr int NB = ADG_PH_TNB;
+    for (int x0 = tid; x0 < PD * M; x0 += NB * NT) {
+      double r[NB][P], qo[NB][P], uu[NB];
+      int xp[NB];
 #pragma unroll
-      for (int s2 = 0; s2 < P; ++s2) r[s2] = __ldcs(Rg + s2 * C::SLICE + x);
-      const double uu = ue[x];
-      if (a.it == 0) {
-        const double k1 = ke[C::QSZP + xp], d = ke[2 * C::QSZP + xp];
+      for (int b = 0; b < NB; ++b) {
+        const int x = x0 + b * NT < PD * M ? x0 + b * NT : x0;
+        xp[b] = ph_pad<P>(x);   // position inside a stored (padded) slice
 #pragma unroll
-        for (int t2 = 0; t2 < P; ++t2) qo[t2] = ph_startup_q(uu, k1, d, cst[t2], cst[P + t2]);
-      } else {
+        for (int s2 = 0; s2 < P; ++s2) r[b][s2] = __ldcs(Rg + s2 * C::SLICE + x);
+        uu[b] = ue[x];
+        if (a.it == 0) {
+          qo[b][0] = ke[C::QSZP + xp[b]];
+          qo[b][1] = ke[2 * C::QSZP + xp[b]];
+        } else {
 #pragma unroll
-        for (int t2 = 0; t2 < P; ++t2) qo[t2] = Qg[t2 * C::QSZP + xp];
+          for (int t2 = 0; t2 < P; ++t2) qo[b][t2] = Qg[t2 * C::QSZP + xp[b]];
+        }
       }
 #pragma unroll
-      for (int t2 = 0; t2 < P; ++t2) {
-        double cc = 0.0;
+      for (int b = 0; b < NB; ++b) {
+        if (x0 + b * NT >= PD * M) break;
+        if (a.it == 0) {
+          const double k1 = qo[b][0], d = qo[b][1];
 #pragma unroll
-        for (int s2 = 0; s2 < P; ++s2) cc = fma(T.gw[t2 * P + s2], r[s2], cc);
-        const double qn = cc * dt + T.g0[t2] * uu;
-        const double dq = qo[t2] - qn;
-        sd = fma(dq, dq, sd);
-        sq = fma(qn, qn, sq);
-        Qg[t2 * C::QSZP + xp] = qn;
+          for (int t2 = 0; t2 < P; ++t2)
+            qo[b][t2] = ph_startup_q(uu[b], k1, d, cst[t2], cst[P + t2]);
+        }
+#pragma unroll
+        for (int t2 = 0; t2 < P; ++t2) {
+          double cc = 0.0;
+#pragma unroll
+          for (int s2 = 0; s2 < P; ++s2) cc = fma(T.gw[t2 * P + s2], r[b][s2], cc);
+          const double qn = cc * dt + T.g0[t2] * uu[b];
+          const double dq = qo[b][t2] - qn;
+          sd = fma(dq, dq, sd);
+          sq = fma(qn, qn, sq);
+          Qg[t2 * C::QSZP + xp[b]] = qn;
+        }
       }
     }
 #pragma unroll
