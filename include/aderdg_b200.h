@@ -143,7 +143,10 @@ int adg_log_step(adg_handle* h, const double* row, int64_t ncols, const int32_t*
  *           axis x: [j][k][t][v], y: [k][t][i][v], z: [t][i][j][v]
  * pred_bad: [E] uint8, ADG_PRED_* bits; 0 = converged && admissible
  *           (driver.py:212)
- * sweeps  : [E] int32 Picard sweeps taken                                 */
+ * sweeps  : [E] int32 Picard sweeps taken
+ * 3-D N >= 8 grids keep the space-time iterate and its rates in a
+ * library-owned HBM workspace of the handle (element batches of at most
+ * 28 GiB; grown on the first call, never freed under a captured graph).  */
 int adg_predict(adg_handle* h, const adg_grid* g, const double* u, const double* dt_dev,
                 double tol, int max_iter, int min_iter, double* q_out, double* vol_out,
                 double* traces, uint8_t* pred_bad, int32_t* sweeps, void* stream);
@@ -192,7 +195,7 @@ int adg_spacetime_rate(adg_handle* h, const adg_grid* g, const double* q, double
  *    their halo exchange with the interior (no reference counterpart: the
  *    reference is single-process).  ADG_ERR_UNSUPPORTED unless
  *    adg_predict_range_supported(g) (3-D N >= 7 conservative grids run the
- *    slice-streaming kernel, which takes the whole grid). */
+ *    whole-grid phased / slice-streaming predictors). */
 int adg_predict_range(adg_handle* h, const adg_grid* g, int64_t e_begin, int64_t e_count,
                       const double* u, const double* dt_dev, double tol, int max_iter,
                       int min_iter, double* q_out, double* vol_out, double* traces,
