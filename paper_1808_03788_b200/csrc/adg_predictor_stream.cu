@@ -38,6 +38,10 @@ namespace adg {
 #define ADG_STREAM_NH 0   // 0: per-degree default below; 1 / 2: force
 #endif
 
+#ifndef ADG_STREAM_DBUF
+#define ADG_STREAM_DBUF 0   // 1: second slice buffer (measured neutral: C3 N=7..9 within 1 %)
+#endif
+
 template <int P>
 struct StCfg {
   static constexpr int M = 5;
@@ -68,9 +72,6 @@ struct StCfg {
   static constexpr int NW = NT / 32;
   static constexpr int CSTP = (2 * P + 1) / 2 * 2;  // startup coefficients, padded to 16 B
   // two slice buffers (the next slice lands while the current one is contracted)
-#ifndef ADG_STREAM_DBUF
-#define ADG_STREAM_DBUF 0   // 1: second slice buffer (measured neutral: C3 N=7..9 within 1 %)
-#endif
   static constexpr int NQB = ADG_STREAM_DBUF ? 2 : 1;
   static constexpr size_t SMEM = (NQB * (size_t)QSZP + 2 * (size_t)BSZP + 2 * NW + CSTP) * 8;
   // CTAs per SM: what shared memory allows, capped so each thread keeps
@@ -85,7 +86,16 @@ struct StCfg {
   static constexpr int MINB = MINB1 < 1 ? 1 : MINB1;
   static constexpr int TB = PD * M + ((PD * M) & 1);   // trace block (face kernel layout)
   static constexpr size_t SLICE = (size_t)PD * M;      // doubles per time slice
-  static constexpr size_t SCR = 2 * (size_t)P * SLICE; // q + rates per CTA (doubles)
+  // the iterate's slices sit in the scratch in the PADDED shared layout (QSZP
+  // doubles, even), so a slice is one 16-byte-aligned bulk copy (TMA) into Q
+  // instead of P^3 m 8-byte cp.async (ADG_STREAM_BULK=0: dense slices)
+#ifndef ADG_STREAM_BULK
+#define ADG_STREAM_BULK 1
+#endif
+  static constexpr bool BULK = ADG_STREAM_BULK;
+  static constexpr size_t QSL = BULK ? (size_t)QSZP : SLICE;   // stored slice stride
+  static constexpr size_t SCR0 = (size_t)P * QSL + (size_t)P * SLICE;   // q + rates per CTA
+  static constexpr size_t SCR = SCR0 + (SCR0 & 1);
 };
 
 struct StArgs {
@@ -188,7 +198,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
   double* const Qa = Q;             // the two slice buffers; Q is the current one
   double* const Qb = C::NQB == 2 ? cst + C::CSTP : Qa;
   double* Qg = a.scr + (size_t)blockIdx.x * C::SCR;   // q[t][node][v]
-  double* Rg = Qg + P * C::SLICE;                      // rate[t][node][v]; k1 at startup
+  double* Rg = Qg + P * C::QSL;                        // rate[t][node][v]; k1 at startup
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -255,6 +265,45 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     cp_async_commit();
   };
   auto fetch = [&](const double* src) { fetch_to(Q, src); };
+  // position of the x-th double of a dense [node][v] slice inside a stored slice
+  auto spad = [&](int x) {
+    if (!C::BULK) return x;
+    const int row = x / (P * M), o = x - row * (P * M);
+    const int i = row / P, j = row - i * P;
+    return i * SI + j * SJ + o;
+  };
+  // a stored slice -> Q by one bulk copy (thread 0, after a barrier that ends
+  // every access to Q; the scratch writers fenced their stores for the async
+  // proxy); completion on the CTA's mbarrier
+  __shared__ __align__(8) uint64_t bar;
+  uint32_t bphase = 0;
+  bool bulk_pending = false;   // uniform: the fetch in flight is a bulk copy
+  if (C::BULK && tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  auto fetch_slice_to = [&](double* buf, const double* src) {
+    if (C::BULK) {
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(&bar, (uint32_t)(C::QSZP * 8));
+        bulk_g2s(buf, src, (uint32_t)(C::QSZP * 8), &bar);
+      }
+      bulk_pending = true;
+    } else {
+      fetch_to(buf, src);
+    }
+  };
+  auto fetch_slice = [&](const double* src) { fetch_slice_to(Q, src); };
+  auto wait_fetch = [&]() {
+    if (C::BULK && bulk_pending) {
+      mbar_wait(&bar, bphase);
+      bphase ^= 1u;
+      bulk_pending = false;
+    } else {
+      cp_async_wait_all();
+    }
+  };
   // fixed-order block sum of two partials (warp trees, warps in order)
   auto block_sum2 = [&](double& s1, double& s2) {
 #pragma unroll
@@ -280,18 +329,18 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
   // rates of the slice in Q at the line owners' nodes -> rt ([node][v]);
   // the next slice (if any) is fetched into the other buffer meanwhile
   auto slice_rates = [&](const double* next, double* rt) {
-    cp_async_wait_all();
+    wait_fetch();
     __syncthreads();
     // the other buffer held the previous slice (its readers passed the
     // barrier above): the next slice lands there during this contraction
     double* const Qn = Q == Qa ? Qb : Qa;
-    if (C::NQB == 2 && next) fetch_to(Qn, next);
+    if (C::NQB == 2 && next) fetch_slice_to(Qn, next);
     double acc[H][M];
     bool dummy = true;
     if (owner) line_contract(0, acc, dummy);
     if (role == 1 || role == 2) publish(acc);
     __syncthreads();
-    if (C::NQB == 1 && next) fetch_to(Q, next);   // single buffer: Q is dead now
+    if (C::NQB == 1 && next) fetch_slice(next);   // single buffer: Q is dead now
     if (role == 0) {
 #pragma unroll
       for (int ii = 0; ii < H; ++ii) {
@@ -314,13 +363,15 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     constexpr int NB = 2;
     for (int x0 = tid; x0 < PD * M; x0 += NB * NT) {
       double r[NB][P], qo[NB][P], uu[NB];
+      int xp[NB];
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const int x = x0 + b * NT < PD * M ? x0 + b * NT : x0;
+        xp[b] = spad(x);
 #pragma unroll
         for (int s2 = 0; s2 < P; ++s2) r[b][s2] = Rg[s2 * C::SLICE + x];
 #pragma unroll
-        for (int t2 = 0; t2 < P; ++t2) qo[b][t2] = Qg[t2 * C::SLICE + x];
+        for (int t2 = 0; t2 < P; ++t2) qo[b][t2] = Qg[t2 * C::QSL + xp[b]];
         uu[b] = ue[x];
       }
 #pragma unroll
@@ -336,10 +387,11 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
           const double dq = qo[b][t2] - qn;
           sd = fma(dq, dq, sd);
           sq = fma(qn, qn, sq);
-          Qg[t2 * C::SLICE + x] = qn;
+          Qg[t2 * C::QSL + xp[b]] = qn;
         }
       }
     }
+    if (C::BULK) asm volatile("fence.proxy.async;" ::: "memory");   // stores -> bulk reads
   };
 
   for (int64_t e = blockIdx.x; e < a.n_elem; e += gridDim.x) {
@@ -356,7 +408,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
 #pragma unroll 1
     while (true) {
       double* rt = Rg + (stage < 2 ? stage : t) * C::SLICE;
-      const double* next = (stage == 2 && t + 1 < P) ? Qg + (t + 1) * C::SLICE : nullptr;
+      const double* next = (stage == 2 && t + 1 < P) ? Qg + (t + 1) * C::QSL : nullptr;
       slice_rates(next, rt);
       if (stage == 0) {
         __syncthreads();   // k1 stored
@@ -375,15 +427,17 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
         // q_t = u + s_t k1 + s_t^2 / (2 dt) (k2 - k1) at every time (predictor.py:116-124)
         for (int x = tid; x < PD * M; x += NT) {
           const double k1 = Rg[x], k2 = Rg[C::SLICE + x], un = ue[x];
+          const int xq = spad(x);
 #pragma unroll 1
           for (int tt = 0; tt < P; ++tt)
-            Qg[tt * C::SLICE + x] = un + cst[tt] * k1 + cst[P + tt] * (k2 - k1);
+            Qg[tt * C::QSL + xq] = un + cst[tt] * k1 + cst[P + tt] * (k2 - k1);
         }
+        if (C::BULK) asm volatile("fence.proxy.async;" ::: "memory");   // stores -> bulk reads
         if (fz) break;
         stage = 2;
         t = 0;
         __syncthreads();   // startup iterate stored
-        fetch(Qg);
+        fetch_slice(Qg);
         continue;
       }
       if (++t < P) continue;
@@ -403,7 +457,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
       if (fz || it >= a.max_iter) break;
       t = 0;
       __syncthreads();   // node-phase stores visible
-      fetch(Qg);
+      fetch_slice(Qg);
     }
 
     // ---------------- traces, admissibility, volume ---------------------
@@ -416,10 +470,10 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
     constexpr int NPT = (PD + NT - 1) / NT;   // nodes per thread
     double fbx[NPT][M];                        // Fbar_x of the thread's nodes
     __syncthreads();   // node-phase stores of the final iterate visible
-    fetch(Qg);
+    fetch_slice(Qg);
 #pragma unroll 1
     for (int t = 0; t < P; ++t) {
-      cp_async_wait_all();
+      wait_fetch();
       __syncthreads();
       if (owner && half == 0) {
         // face traces of the line at time t (face-kernel block layouts:
@@ -477,7 +531,7 @@ predict_stream_kernel(const __grid_constant__ StArgs a) {
         for (int v = 0; v < M; ++v) B2[bx + v] = t == 0 ? wt * f[v] : B2[bx + v] + wt * f[v];
       }
       __syncthreads();
-      if (t + 1 < P) fetch(Qg + (t + 1) * C::SLICE);
+      if (t + 1 < P) fetch_slice(Qg + (t + 1) * C::QSL);
     }
     // Fbar_x into Q (own nodes); the y / z owners contract Fbar_y / Fbar_z
     // in place (each reads and writes only its own line of B1 / B2)

@@ -57,8 +57,8 @@ print(json.dumps({"predictor": os.environ.get("ADG_PREDICTOR", "phased"), "degre
                   "step_ms": step_ms, "pred_ms_min": min(ts), "chk": chk}))
 '''
 
-# usage: pred_large_ab.py [N ...] [-- variant ...]; a variant is "phased" (default
-# library and predictor), "stream" (ADG_PREDICTOR=stream) or a library path
+# usage: pred_large_ab.py [N ...] [-- variant ...]; a variant is "phased" or
+# "stream" (ADG_PREDICTOR), optionally followed by ":path of a library build"
 args = sys.argv[1:]
 variants = ["phased", "stream"]
 if "--" in args:
@@ -70,11 +70,11 @@ for deg in degs:
         env = dict(os.environ, AB_DEG=str(deg))
         env.pop("ADG_PREDICTOR", None)
         env.pop("ADG_LIB", None)
-        if var in ("stream", "phased"):
-            env["ADG_PREDICTOR"] = var
-        else:
-            env["ADG_PREDICTOR"] = "phased"
-            env["ADG_LIB"] = os.path.abspath(var)
+        # "phased" / "stream", optionally ":library path"
+        kind, _, lib = var.partition(":")
+        env["ADG_PREDICTOR"] = kind
+        if lib:
+            env["ADG_LIB"] = os.path.abspath(lib)
         r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
         out = r.stdout.strip().splitlines()
         if out:
