@@ -40,6 +40,11 @@ namespace adg {
 #ifndef ADG_PASS_UNROLL
 #define ADG_PASS_UNROLL 2
 #endif
+// dedicated u^n prefetch buffer for 3-D tiles too (0: 1-D / 2-D only, for A/B)
+#ifndef ADG_PF_3D
+#define ADG_PF_3D 1
+#endif
+#define ADG_PF_DED3(D) ((D) <= 2 || ADG_PF_3D)
 constexpr int kPassUnroll = ADG_PASS_UNROLL;
 
 template <int D, int P>
@@ -124,12 +129,14 @@ struct PredCfg {
   static constexpr int FLAGS = 5 * EPB + 1;
   static constexpr size_t SMALL_BYTES = SMALL_DBL * 8 + ((FLAGS * 4 + 15) / 16) * 16;
   static constexpr size_t TILE_BYTES = (size_t)EPB * ELEM * 8;
-  // 1-D / 2-D groups prefetch the next group's u^n into a dedicated buffer
-  // behind the tiles (when it still fits the CTAs per SM the tiles allow)
+  // 1-D / 2-D groups, and the 3-D two-buffer tiles (N = 5, 6), prefetch the
+  // next group's u^n into a dedicated buffer behind the tiles (when it still
+  // fits the CTAs per SM the tiles allow): at N = 6 the synchronous u^n load
+  // held 9 % of the kernel's stall samples (one CTA per SM)
   static constexpr size_t PFB_BYTES = (size_t)EPB * PD * M * 8;
   static constexpr bool SMEM_TILES0 = (SMALL_BYTES + TILE_BYTES) <= 220 * 1024;
   static constexpr int CTAS0 = (int)((228 * 1024) / (SMALL_BYTES + TILE_BYTES + 1024));
-  static constexpr bool PF_DED = ADG_PREFETCH_U && D <= 2 && SMEM_TILES0 &&
+  static constexpr bool PF_DED = ADG_PREFETCH_U && !PREFETCH && ADG_PF_DED3(D) && SMEM_TILES0 &&
       (SMALL_BYTES + TILE_BYTES + PFB_BYTES) <= 220 * 1024 &&
       (int)((228 * 1024) / (SMALL_BYTES + TILE_BYTES + PFB_BYTES + 1024)) >= CTAS0;
   static constexpr bool SMEM_TILES = SMEM_TILES0;
