@@ -322,7 +322,10 @@ struct WarpCfg {
   static constexpr int SCR = D == 3 ? C::S * C::S * P * C::M : C::S * P * C::M;
   static constexpr int OUT = (D == 3 ? C::S * P * P * C::M : 0) > C::SD * C::M
                                  ? C::S * P * P * C::M : C::SD * C::M;
-  static constexpr int PER_WARP = C::PD * C::M + OUT + SCR + 2 * C::M;   // doubles
+  // (the second nodal block: the next cell's candidate lands there by
+  // cp.async while the warp screens the current one, adg_detect)
+  static constexpr int NOD2 = C::PD * C::M;
+  static constexpr int PER_WARP = C::PD * C::M + OUT + SCR + 2 * C::M + NOD2;   // doubles
   static constexpr int W0 = (200 * 1024) / (PER_WARP * 8);
   static constexpr int WPB = W0 >= 8 ? 8 : (W0 >= 1 ? W0 : 1);   // warps (cells) per CTA
   static constexpr int PS = ((C::S * P + 1) / 2) * 2;   // staged P_sub (16-byte multiple)
@@ -521,13 +524,38 @@ detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cm
   double* lsm = W::GS ? gscr + (size_t)blockIdx.x * W::BLOCK_DBL : lsm_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* Ps = stage_psub<D, P, SYS>(lsm + W::WPBX * W::PER_WARP);
-  double* nodal = lsm + warp * W::PER_WARP;
-  double* out = nodal + PD * M;
+  double* nod0 = lsm + warp * W::PER_WARP;
+  double* out = nod0 + PD * M;
   double* tmp = out + W::OUT;
   double* s_lo = tmp + W::SCR;
   double* s_hi = s_lo + M;
-  for (int64_t e = (int64_t)blockIdx.x * W::WPBX + warp; e < E; e += (int64_t)gridDim.x * W::WPBX) {
-    for (int x = lane; x < PD * M; x += 32) nodal[x] = cand[(size_t)e * PD * M + x];
+  double* nod1 = s_hi + M;
+  // the candidate of the warp's NEXT cell is fetched (cp.async) while the
+  // current one is screened: the synchronous load held 29 % of the kernel's
+  // stall samples at C4 (global-scratch variant: plain loads)
+  constexpr bool PF = !W::GS;
+  const int64_t estride = (int64_t)gridDim.x * W::WPBX;
+  auto prefetch = [&](int64_t ee, double* dst) {
+    const double* src = cand + (size_t)ee * PD * M;
+    for (int x = lane; x < PD * M; x += 32) cp_async8(dst + x, src + x);
+    cp_async_commit();
+  };
+  int64_t e0 = (int64_t)blockIdx.x * W::WPBX + warp;
+  if (PF && e0 < E) prefetch(e0, nod0);
+  int par = 0;
+  for (int64_t e = e0; e < E; e += estride, par ^= 1) {
+    double* nodal = PF && par ? nod1 : nod0;
+    if (PF) {
+      if (e + estride < E) {
+        prefetch(e + estride, par ? nod0 : nod1);
+        cp_async_wait_1();
+      } else {
+        cp_async_wait_all();
+      }
+      __syncwarp();
+    } else {
+      for (int x = lane; x < PD * M; x += 32) nodal[x] = cand[(size_t)e * PD * M + x];
+    }
     // DMP bounds: lane v < M owns quantity v; own cell, then the face
     // neighbours in axis order, low then high (min / max are order-free)
     int64_t c[3] = {0, 0, 0};
