@@ -239,6 +239,12 @@ int adg_totals_finalize(adg_handle* h, const adg_grid* g, const double* totals_p
 int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partial,
                double* totals_out, void* stream);
 
+/* adg_wavespeed and adg_totals of the same state in ONE pass over u (the
+ * limited step re-records a state the rescue changed: corrector.py:30-55 and
+ * driver.py:344-350 together); results bitwise those of the two calls */
+int adg_state_record(adg_handle* h, const adg_grid* g, const double* u, adg_reduce* red,
+                     double* partial, double* totals_out, void* stream);
+
 /* -- a posteriori subcell limiter (limiter.py; driver.py:265-299) ------- */
 /* Exterior subcell averages for ADG_BC_GHOST ("exact") faces, the
  * reference's _boundary_slab (driver.py:317-340) evaluated by the caller at

@@ -400,6 +400,22 @@ int adg_totals(adg_handle* h, const adg_grid* g, const double* u, double* partia
                                       (cudaStream_t)stream, &e), e);
 }
 
+int adg_state_record(adg_handle* h, const adg_grid* g, const double* u, adg_reduce* red,
+                     double* partial, double* totals_out, void* stream) {
+  DeviceGuard dg(h);
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (!red || !partial || !totals_out)
+    return fail(h, ADG_ERR_INVALID, "adg_state_record: null array");
+  std::string e;
+  rc = is_adv(g)  ? adg::adv_state_reduce(g, u, red, partial, (cudaStream_t)stream, &e)
+       : is_el(g) ? adg::el_state_reduce(g, u, red, partial, (cudaStream_t)stream, &e)
+                  : adg::state_reduce(g, u, red, partial, (cudaStream_t)stream, &e);
+  if (rc) return wrap(h, rc, e);
+  return wrap(h, adg::totals_finalize(g, partial, adg::reduce_blocks(g), totals_out,
+                                      (cudaStream_t)stream, &e), e);
+}
+
 int adg_project_subcells(adg_handle* h, const adg_grid* g, const double* u, double* sub_out,
                          double* cmin_out, double* cmax_out, void* stream) {
   DeviceGuard dg(h);

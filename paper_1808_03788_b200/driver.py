@@ -635,10 +635,10 @@ class Simulation:
                      _ptr(lb["failed"]), _ptr(lb["sub_n"]), _ptr(lb["cmin_n"]),
                      _ptr(lb["cmax_n"]), sp)
         # rescued cells changed u_next: its wave speeds / counts again (the
-        # update epilogue folded the candidate's), then the conserved totals
-        self._h.call("adg_wavespeed", self._gp(), _ptr(self._u_next), _ptr(buf.red[nxt]), sp)
-        self._h.call("adg_totals", self._gp(), _ptr(self._u_next), _ptr(buf.partial),
-                     _ptr(row[2:]), sp)
+        # update epilogue folded the candidate's) and the conserved totals, in
+        # one pass over the state
+        self._h.call("adg_state_record", self._gp(), _ptr(self._u_next), _ptr(buf.red[nxt]),
+                     _ptr(buf.partial), _ptr(row[2:]), sp)
         self._h.call("adg_advance_time", _ptr(buf.t), _ptr(dt_dev), _ptr(row[1:2]), sp)
         return nxt
 
