@@ -171,6 +171,14 @@ class Simulation:
         self._exact_faces = [k for k, v in self.boundary.items()
                              if v == "exact" and k not in self._ghost]
         self._exact_trace = {}
+        # an exact_solution marked `device_capable` (the package's closed-form
+        # cases; any callable that evaluates torch tensors) forms the boundary
+        # data ON THE DEVICE from the device-resident t and dt: no host
+        # evaluation or upload per step, and the batched / limited device
+        # loops stay available (driver.py:250-261, :317-340)
+        self._exact_dev = bool(self._exact_faces) and bool(
+            getattr(exact_solution, "device_capable", False))
+        self._exact_cache = {}
         d = mesh.dim
         self._P = degree + 1
         self._m = system.n_vars
@@ -299,6 +307,8 @@ class Simulation:
         (driver._ghost_trace, driver.py:250-261), in trace-block layout."""
         if not self._exact_faces:
             return
+        if self._exact_dev:
+            return self._fill_exact_traces_device(self.t, dt)
         buf = self._buf
         P, m, d = self._P, self._m, self.mesh.dim
         for (axis, side) in self._exact_faces:
@@ -325,6 +335,78 @@ class Simulation:
                 self._exact_trace[(axis, side)] = dst
             dst.copy_(torch.from_numpy(block.reshape(-1)))
 
+    def _trace_cols(self, axis):
+        """Positions (in doubles) of a face's [tangential.., time, m] values
+        inside its trace block (the predictor's owner-role order)."""
+        P, m, d = self._P, self._m, self.mesh.dim
+        tang, st = self._trace_strides(axis)
+        pos = np.zeros((P,) * (d - 1) + (P,), dtype=np.int64)
+        for k, stride in enumerate(tang):
+            sh = [1] * d
+            sh[k] = P
+            pos = pos + stride * np.arange(P).reshape(sh)
+        sh = [1] * d
+        sh[d - 1] = P
+        pos = pos + st * np.arange(P).reshape(sh)
+        return (pos[..., None] * m + np.arange(m)).reshape(-1)
+
+    def _fill_exact_traces_device(self, t, dt):
+        """_fill_exact_traces with exact_solution evaluated on the device; t
+        and dt are floats or one-element device tensors (the batched loops
+        pass the device clock and the step adg_timestep just formed)."""
+        buf = self._buf
+        f64 = dict(dtype=torch.float64, device=self.device)
+        for (axis, side) in self._exact_faces:
+            c = self._exact_cache.get(("tr", axis, side))
+            if c is None:
+                pts = torch.as_tensor(np.ascontiguousarray(
+                    self.mesh.face_node_coords(self.tables, axis, side)), **f64)
+                nplanes = self.mesh.n_elements // self.mesh.cells[axis]
+                cols = torch.as_tensor(self._trace_cols(axis), device=self.device)
+                dst = torch.zeros(nplanes * buf.tb, **f64)
+                c = (pts, nplanes, cols, dst)
+                self._exact_cache[("tr", axis, side)] = c
+                self._exact_trace[(axis, side)] = dst
+            pts, nplanes, cols, dst = c
+            vals = torch.stack([self.exact_solution(pts, t + float(tau) * dt)
+                                for tau in self.tables.nodes], dim=-2)
+            dst.view(nplanes, buf.tb).index_copy_(1, cols, vals.reshape(nplanes, -1))
+
+    def _exact_subcell_ghosts_device(self, t):
+        """_exact_subcell_ghosts evaluated on the device at t (float or
+        one-element device tensor) into persistent slabs."""
+        c = self._exact_cache.get("gh")
+        if c is None:
+            d = self.mesh.dim
+            S = self.tables.n_subcells
+            L = max(S, 2)
+            gh = _lib.SubcellGhosts()
+            gh.layers = L
+            slabs = []
+            for (axis, side) in self._exact_faces:
+                coords = []
+                for i in range(d):
+                    if i < axis:
+                        coords.append(self.mesh.subcell_axis_coords(i, S, L))
+                    elif i == axis:
+                        full = self.mesh.subcell_axis_coords(i, S, L)
+                        coords.append(full[:L] if side == 0 else full[-L:])
+                    else:
+                        coords.append(self.mesh.subcell_axis_coords(i, S, 0))
+                pts = torch.as_tensor(np.ascontiguousarray(
+                    np.stack(np.meshgrid(*coords, indexing="ij"), axis=-1)),
+                    dtype=torch.float64, device=self.device)
+                dev = torch.empty(pts.shape[:-1] + (self._m,), dtype=torch.float64,
+                                  device=self.device)
+                gh.slab[axis][side] = dev.data_ptr()
+                slabs.append((pts, dev))
+            c = (gh, slabs)
+            self._exact_cache["gh"] = c
+        gh, slabs = c
+        for pts, dev in slabs:
+            dev.copy_(self.exact_solution(pts, t))
+        return gh
+
     def _exact_subcell_ghosts(self):
         """adg_subcell_ghosts for the exact faces at t_n (driver._boundary_slab,
         driver.py:317-340): slab (j, s) spans the axes padded before j with
@@ -332,6 +414,8 @@ class Simulation:
         the later axes."""
         if not self._exact_faces:
             return None
+        if self._exact_dev:
+            return self._exact_subcell_ghosts_device(self.t)
         d = self.mesh.dim
         S = self.tables.n_subcells
         L = max(S, 2)
@@ -528,12 +612,19 @@ class Simulation:
         self._ensure_buffers()
         scale = abs(t_end) if np.isfinite(t_end) else 1.0
         tiny = 1e-12 * max(1.0, scale)
+        if self._exact_dev and not self._exact_cache:
+            # node coordinates / index tables of the exact faces go to the
+            # device once, outside any graph capture
+            self._fill_exact_traces_device(self.t, 0.0)
+            if self.use_limiter:
+                self._exact_subcell_ghosts_device(self.t)
         fast = (on_step is None and not self.use_limiter and not np.isfinite(t_end)
-                and max_steps is not None and not self._exact_faces)
+                and max_steps is not None and (not self._exact_faces or self._exact_dev))
         if fast:
             self._run_batch(max(0, max_steps - self.step_count))
             return self.step_count
-        if self.use_limiter and not self._exact_faces and self._exchange is None:
+        if (self.use_limiter and (not self._exact_faces or self._exact_dev)
+                and self._exchange is None):
             return self._run_limited(t_end, tiny, max_steps, on_step)
         while self.t < t_end - tiny:
             if max_steps is not None and self.step_count >= max_steps:
@@ -619,19 +710,25 @@ class Simulation:
             self._h.call("adg_project_subcells", self._gp(), _ptr(self._u), _ptr(lb["sub"]),
                          _ptr(lb["cmin"]), _ptr(lb["cmax"]), sp)
             lb["sub_of"] = self._u
+        ghp = None
+        if self._exact_dev:
+            # exact faces from the device clock: traces for this trial step,
+            # subcell slabs at t^n
+            self._fill_exact_traces_device(buf.t, dt_dev)
+            ghp = _lib.ctypes.byref(self._exact_subcell_ghosts_device(buf.t))
         self._predict(dt_dev)
         self._faces()
         nxt = self._update(dt_dev, None)
         self._h.call("adg_detect", self._gp(), _ptr(lb["sub"]), _ptr(lb["cmin"]),
                      _ptr(lb["cmax"]), _ptr(self._u_next), _ptr(buf.pred_bad), self.dmp_delta0,
-                     self.dmp_eps, int(bool(self.force_limit_all)), None, _ptr(lb["troubled"]),
+                     self.dmp_eps, int(bool(self.force_limit_all)), ghp, _ptr(lb["troubled"]),
                      _ptr(lb["idx"]), _ptr(lb["count"]), _ptr(lb["sub_n"]), _ptr(lb["cmin_n"]),
                      _ptr(lb["cmax_n"]), sp)
         lb["failed"].zero_()
         # a fixed grid of rescue blocks strides over the device-side count
         cap = min(self.mesh.n_elements, self._rescue_blocks)
         self._h.call("adg_rescue", self._gp(), _ptr(lb["sub"]), _ptr(lb["idx"]),
-                     _ptr(lb["count"]), cap, _ptr(dt_dev), None, _ptr(self._u_next),
+                     _ptr(lb["count"]), cap, _ptr(dt_dev), ghp, _ptr(self._u_next),
                      _ptr(lb["failed"]), _ptr(lb["sub_n"]), _ptr(lb["cmin_n"]),
                      _ptr(lb["cmax_n"]), sp)
         # rescued cells changed u_next: its wave speeds / counts again (the
@@ -664,6 +761,8 @@ class Simulation:
         """Enqueue one unlimited step writing its history row / status /
         sweep count into slot s of the given device buffers."""
         self._timestep_into(rows[s, 0:1], status[s:s + 1], math.inf)
+        if self._exact_dev:
+            self._fill_exact_traces_device(self._buf.t, rows[s, 0:1])
         self._enqueue_unlimited(rows[s, 0:1], rows[s, 2:], rows[s, 1:2])
         torch.amax(self._buf.sweeps, dim=0, keepdim=True, out=sweeps[s:s + 1])
 
@@ -709,6 +808,8 @@ class Simulation:
             for j in range(nsteps):
                 srow, sst = bb["srow"][j % 2], bb["sst"][j % 2:j % 2 + 1]
                 self._timestep_into(srow[0:1], sst, math.inf)
+                if self._exact_dev:
+                    self._fill_exact_traces_device(self._buf.t, srow[0:1])
                 self._enqueue_unlimited(srow[0:1], srow[2:], srow[1:2])
                 # history row, status and max sweep count into slot cnt
                 self._h.call("adg_log_step", _ptr(srow), ncols, _ptr(sst),

@@ -10,6 +10,22 @@ returns (ic, exact): ic(points) -> states, exact(points, t) or None.
 import numpy as np
 
 
+def _xp(a):
+    """numpy, or torch for a torch tensor: the closed-form exact solutions
+    below evaluate on either, so `Simulation` can form "exact" boundary data
+    on the device (their `device_capable` attribute says so); t may then be
+    a one-element device tensor."""
+    if type(a).__module__.split(".")[0] == "torch":
+        import torch
+        return torch
+    return np
+
+
+def _device_capable(fn):
+    fn.device_capable = True
+    return fn
+
+
 def isentropic_vortex(system, beta=5.0, center=(5.0, 5.0), domain_size=(10.0, 10.0)):
     """problems.py:14-51 (C1)."""
     if system.name != "euler" or system.dim != 2:
@@ -21,20 +37,22 @@ def isentropic_vortex(system, beta=5.0, center=(5.0, 5.0), domain_size=(10.0, 10
     b = float(beta)
     tcoef = (g - 1.0) * b * b / (8.0 * g * np.pi * np.pi)
 
+    @_device_capable
     def exact(points, t):
+        xp = _xp(points)
         rx = points[..., 0] - cx - t
         ry = points[..., 1] - cy - t
-        rx -= lx * np.round(rx / lx)
-        ry -= ly * np.round(ry / ly)
+        rx = rx - lx * xp.round(rx / lx)
+        ry = ry - ly * xp.round(ry / ly)
         r2 = rx * rx + ry * ry
-        bump = np.exp(0.5 * (1.0 - r2))
+        bump = xp.exp(0.5 * (1.0 - r2))
         vx = 1.0 + (-amp * bump * ry)
         vy = 1.0 + amp * bump * rx
-        temp = 1.0 - tcoef * np.exp(1.0 - r2)
+        temp = 1.0 - tcoef * xp.exp(1.0 - r2)
         rho = temp ** (1.0 / (g - 1.0))
         p = temp ** (g / (g - 1.0))
         energy = p / (g - 1.0) + 0.5 * rho * (vx * vx + vy * vy)
-        return np.stack([rho, rho * vx, rho * vy, energy], axis=-1)
+        return xp.stack([rho, rho * vx, rho * vy, energy], -1)
 
     return (lambda points: exact(points, 0.0)), exact
 
@@ -48,19 +66,20 @@ def density_wave(system, amplitude=0.2, velocity=None, pressure=1.0):
     g = system.gamma
     vel = np.ones(d) if velocity is None else np.asarray(velocity, float)
 
+    @_device_capable
     def exact(points, t):
-        arg = np.zeros(points.shape[:-1])
+        xp = _xp(points)
+        arg = xp.zeros_like(points[..., 0])
         for j in range(d):
-            arg = arg + (points[..., j] - vel[j] * t)
-        rho = 1.0 + amplitude * np.sin(2.0 * np.pi * arg)
-        out = np.empty(points.shape[:-1] + (d + 2,))
-        out[..., 0] = rho
+            arg = arg + (points[..., j] - float(vel[j]) * t)
+        rho = 1.0 + amplitude * xp.sin(2.0 * np.pi * arg)
+        cols = [rho]
         v2 = 0.0
         for j in range(d):
-            out[..., 1 + j] = rho * vel[j]
-            v2 = v2 + vel[j] * vel[j]
-        out[..., -1] = pressure / (g - 1.0) + 0.5 * rho * v2
-        return out
+            cols.append(rho * float(vel[j]))
+            v2 = v2 + float(vel[j]) * float(vel[j])
+        cols.append(pressure / (g - 1.0) + 0.5 * rho * v2)
+        return xp.stack(cols, -1)
 
     return (lambda points: exact(points, 0.0)), exact
 
@@ -118,11 +137,13 @@ def advected_sine(system):
         raise ValueError("the sine case needs the advection system")
     vel = system.velocity
 
+    @_device_capable
     def exact(points, t):
-        phase = np.zeros(points.shape[:-1])
+        xp = _xp(points)
+        phase = xp.zeros_like(points[..., 0])
         for j in range(system.dim):
-            phase += points[..., j] - vel[j] * t
-        return np.sin(2.0 * np.pi * phase)[..., None]
+            phase = phase + (points[..., j] - float(vel[j]) * t)
+        return xp.sin(2.0 * np.pi * phase)[..., None]
 
     return (lambda points: exact(points, 0.0)), exact
 
@@ -133,12 +154,14 @@ def gaussian_pulse(system, center=0.25, width=0.08, amplitude=1.0):
         raise ValueError("the pulse case needs the advection system")
     vel = system.velocity
 
+    @_device_capable
     def exact(points, t):
-        r2 = np.zeros(points.shape[:-1])
+        xp = _xp(points)
+        r2 = xp.zeros_like(points[..., 0])
         for j in range(system.dim):
-            d = points[..., j] - center - vel[j] * t
-            r2 += d * d
-        return (amplitude * np.exp(-r2 / (2.0 * width * width)))[..., None]
+            d = points[..., j] - center - float(vel[j]) * t
+            r2 = r2 + d * d
+        return (amplitude * xp.exp(-r2 / (2.0 * width * width)))[..., None]
 
     return (lambda points: exact(points, 0.0)), exact
 
@@ -164,7 +187,12 @@ def constant_state(system, values=None):
     if q0.shape != (system.n_vars,):
         raise ValueError(f"constant state needs {system.n_vars} entries")
 
+    @_device_capable
     def exact(points, t):
+        if _xp(points) is not np:
+            import torch
+            q = torch.as_tensor(q0, dtype=points.dtype, device=points.device)
+            return q.expand(tuple(points.shape[:-1]) + tuple(q0.shape)).clone()
         return np.broadcast_to(q0, points.shape[:-1] + q0.shape).copy()
 
     return (lambda points: exact(points, 0.0)), exact

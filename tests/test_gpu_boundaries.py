@@ -126,3 +126,53 @@ def test_exact_sod_1d_vs_oracle(pkg):
         sim.run(np.inf, max_steps=s + 1)
         np.testing.assert_array_equal(sim.last_troubled.cpu().numpy(), osim.last_troubled)
     assert rel_linf(sim.u, osim.u) <= TOL
+
+
+def _exact_wave_sim(pkg, exact, limiter, **kw):
+    system = pkg.make_system("euler", 2)
+    ic, _ = pkg.build_problem("density_wave", system, velocity=(1.0, 0.5))
+    mesh = pkg.CartesianMesh([(0.0, 1.0), (0.0, 0.8)], (6, 5))
+    sim = pkg.Simulation(mesh, system, 3, 0.9 / (2 * 7), boundary="exact",
+                         exact_solution=exact, use_limiter=limiter, **kw)
+    sim.project_initial_condition(ic)
+    return sim
+
+
+@pytest.mark.parametrize("limiter", [False, True])
+def test_exact_device_resident_matches_host_evaluation(pkg, limiter):
+    """A `device_capable` exact_solution (the package's closed-form cases) is
+    evaluated on the device from the device clock: boundary traces and the
+    limiter's subcell slabs without host evaluation or upload, the batched /
+    limited device loops stay on.  Same run with the same function hidden
+    behind a plain lambda (host evaluation, driver.py:250-261, :317-340)."""
+    system = pkg.make_system("euler", 2)
+    _, ex = pkg.build_problem("density_wave", system, velocity=(1.0, 0.5))
+    assert getattr(ex, "device_capable", False)
+    a = _exact_wave_sim(pkg, ex, limiter)
+    b = _exact_wave_sim(pkg, lambda x, t: ex(x, t), limiter)
+    assert a._exact_dev and not b._exact_dev
+    a.run(np.inf, max_steps=6)
+    b.run(np.inf, max_steps=6)
+    assert a.step_count == b.step_count == 6
+    np.testing.assert_allclose([h["dt"] for h in a.history], [h["dt"] for h in b.history],
+                               rtol=1e-13)
+    assert rel_linf(a.u, b.u.cpu().numpy()) <= 1e-12
+    if limiter:
+        assert torch.equal(a.last_troubled, b.last_troubled)
+
+
+def test_exact_device_resident_batched_equals_stepwise(pkg):
+    """Unlimited run with device-resident exact faces: the batched (CUDA graph)
+    loop against the step-by-step loop (an on_step callback forces it)."""
+    system = pkg.make_system("euler", 2)
+    _, ex = pkg.build_problem("density_wave", system, velocity=(1.0, 0.5))
+    a = _exact_wave_sim(pkg, ex, False)
+    b = _exact_wave_sim(pkg, ex, False)
+    a.run(np.inf, max_steps=7)
+    b.run(np.inf, max_steps=7, on_step=lambda s: None)
+    np.testing.assert_allclose([h["dt"] for h in a.history], [h["dt"] for h in b.history],
+                               rtol=1e-14)
+    assert rel_linf(a.u, b.u.cpu().numpy()) <= 1e-13
+    # and against the exact solution itself: boundary data consistent in time
+    err = a.error_norms()
+    assert err["linf"].max() < 5e-3
