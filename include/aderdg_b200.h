@@ -298,6 +298,28 @@ int adg_rescue(adg_handle* h, const adg_grid* g, const double* prev_sub, const i
 int adg_flatten_ic(adg_handle* h, const adg_grid* g, double* u, int32_t* nflat,
                    void* stream);
 
+/* -- limiter module helpers with the reference's array interfaces
+ *    (limiter.py:45-101); Simulation uses the fused adg_detect / adg_rescue */
+/* minmod (limiter.py:45-48), elementwise over n doubles */
+int adg_minmod(adg_handle* h, int64_t n, const double* a, const double* b, double* out,
+               void* stream);
+/* relaxed_bounds (limiter.py:51-73): padded_sub [(cells_j + 2)..][nsub][m]
+ * (nsub = S^d subcells per cell) -> lo, hi [cells..][m]; cmin_pad / cmax_pad
+ * are scratch of (prod (cells_j + 2)) m doubles; cells is a host int64[dim] */
+int adg_relaxed_bounds(adg_handle* h, int dim, int nvars, const int64_t* cells, int nsub,
+                       const double* padded_sub, double delta0, double eps, double* cmin_pad,
+                       double* cmax_pad, double* lo_out, double* hi_out, void* stream);
+/* detect_troubled (limiter.py:76-86): cand [E][P^d][m], cand_sub [E][S^d][m],
+ * lo / hi [E][m] -> troubled [E] uint8 (E, dim, degree, system from g) */
+int adg_detect_cells(adg_handle* h, const adg_grid* g, const double* cand,
+                     const double* cand_sub, const double* lo, const double* hi,
+                     uint8_t* troubled, void* stream);
+/* gather_windows (limiter.py:89-101): padded [padded_dims..][m] (host
+ * int64[dim]), starts [nwin][dim] (device int64) -> out [nwin][size^dim][m] */
+int adg_gather_windows(adg_handle* h, int dim, int nvars, const int64_t* padded_dims,
+                       const double* padded, const int64_t* starts, int64_t nwin, int size,
+                       double* out, void* stream);
+
 /* -- module-level pieces: the reference's corrector / limiter functions on
  *    arrays in the reference layouts (element grid flattened: E = product
  *    of g->cells), for callers of the module API rather than Simulation.
@@ -313,6 +335,8 @@ int adg_face_fluxes(adg_handle* h, const adg_grid* g, int axis, int64_t n, const
  * -- and, for the nonconservative system, path_integral_B (corrector.py:65-78):
  * bpath [n][m][m] (may be NULL; mode -1 computes only it).  Euler, advection
  * and elasticity-di. */
+/* mode 2 (Euler, advection): out_a [n] = rusanov_theta (corrector.py:58-62),
+ * the larger |eigenvalue . n| of the two states (NaN propagates) */
 int adg_riemann_points(adg_handle* h, const adg_grid* g, int64_t n, const double* normal,
                        int mode, const double* q_minus, const double* q_plus, double* out_a,
                        double* out_b, double* bpath, void* stream);

@@ -38,7 +38,7 @@ STATUS_NONFINITE = 2
 EXPORTS = (
     "adg_create", "adg_destroy", "adg_last_error", "adg_version", "adg_set_tables",
     "adg_wavespeed", "adg_timestep", "adg_advance_time", "adg_predict", "adg_face_flux", "adg_update",
-    "adg_update_blocks", "adg_trace_block", "adg_totals_finalize", "adg_totals", "adg_state_record", "adg_project_subcells",
+    "adg_update_blocks", "adg_trace_block", "adg_totals_finalize", "adg_totals", "adg_state_record", "adg_minmod", "adg_relaxed_bounds", "adg_detect_cells", "adg_gather_windows", "adg_project_subcells",
     "adg_detect", "adg_rescue", "adg_flatten_ic", "adg_face_fluxes", "adg_volume_integral",
     "adg_face_integral", "adg_element_update", "adg_muscl_windows", "adg_recover_subcells",
     "adg_flatten_cells", "adg_log_step", "adg_predict_range", "adg_predict_range_supported",
@@ -111,6 +111,10 @@ _SIGS = {
     "adg_totals_finalize": (_I, [_P, _P, _P, _I64, _P, _P]),
     "adg_totals": (_I, [_P, _P, _P, _P, _P, _P]),
     "adg_state_record": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "adg_minmod": (_I, [_P, _I64, _P, _P, _P, _P]),
+    "adg_relaxed_bounds": (_I, [_P, _I, _I, _P, _I, _P, _D, _D, _P, _P, _P, _P, _P]),
+    "adg_detect_cells": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    "adg_gather_windows": (_I, [_P, _I, _I, _P, _P, _P, _I64, _I, _P, _P]),
     "adg_project_subcells": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "adg_detect": (_I, [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _P, _P, _P,
                         _P]),

@@ -69,10 +69,27 @@ def compute_timestep(u, system, spacings, cfl, degree):
 
 
 def rusanov_theta(q_minus, q_plus, normal, system):
-    """max |eigenvalue| over both states (corrector.py:58-62)."""
+    """max |eigenvalue| over both states (corrector.py:58-62):
+    adg_riemann_points, speed mode (Euler, advection; the NCP system's c_p
+    speed is a short device expression of its plugin)."""
     qm, qp = as_device(q_minus), as_device(q_plus)
-    n = torch.as_tensor(np.asarray(normal, dtype=float), device=qm.device)
-    return torch.maximum(system.max_abs_eigenvalue(qm, n), system.max_abs_eigenvalue(qp, n))
+    if getattr(system, "name", None) not in ("euler", "advection"):
+        n = torch.as_tensor(np.asarray(normal, dtype=float), device=qm.device)
+        return torch.maximum(system.max_abs_eigenvalue(qm, n), system.max_abs_eigenvalue(qp, n))
+    qm, qp = torch.broadcast_tensors(qm, qp)
+    qm, qp = qm.contiguous(), qp.contiguous()
+    lead = tuple(qm.shape[:-1])
+    n = int(np.prod(lead)) if lead else 1
+    out = torch.empty(lead, dtype=torch.float64, device=qm.device)
+    nv = np.zeros(3)
+    nv[:system.dim] = np.asarray(normal, dtype=float)
+    nvec = (_lib.ctypes.c_double * 3)(*nv)
+    g = flat_grid(system, 0, n)
+    h = _lib.Handle.get(qm.device.index)
+    h.ensure_tables(basis_tables(0))
+    h.call("adg_riemann_points", _lib.ctypes.byref(g), n, nvec, 2, qm.data_ptr(), qp.data_ptr(),
+           out.data_ptr(), None, None, h.stream())
+    return out
 
 
 def _points(q_minus, q_plus, system, normal, mode, want_b=False):

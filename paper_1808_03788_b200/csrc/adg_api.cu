@@ -470,7 +470,9 @@ int adg_riemann_points(adg_handle* h, const adg_grid* g, int64_t n, const double
   DeviceGuard dg(h);
   int rc = check_grid(h, g);
   if (rc) return rc;
-  if (!normal || n < 0 || mode < -1 || mode > 1 || (n > 0 && (!q_minus || !q_plus)) ||
+  if (mode == 2 && is_el(g))
+    return fail(h, ADG_ERR_UNSUPPORTED, "adg_riemann_points: speed mode for Euler and advection");
+  if (!normal || n < 0 || mode < -1 || mode > 2 || (n > 0 && (!q_minus || !q_plus)) ||
       (mode >= 0 && !out_a) || (mode == 1 && !out_b))
     return fail(h, ADG_ERR_INVALID, "adg_riemann_points: bad arguments");
   std::string e;
@@ -480,6 +482,52 @@ int adg_riemann_points(adg_handle* h, const adg_grid* g, int64_t n, const double
   if (mode < 0) return fail(h, ADG_ERR_INVALID, "path integral: nonconservative systems only");
   return wrap(h, adg::riemann_points(g, n, normal, mode, q_minus, q_plus, out_a, out_b,
                                      (cudaStream_t)stream, &e), e);
+}
+
+int adg_minmod(adg_handle* h, int64_t n, const double* a, const double* b, double* out,
+               void* stream) {
+  DeviceGuard dg(h);
+  if (n < 0 || (n > 0 && (!a || !b || !out))) return fail(h, ADG_ERR_INVALID, "adg_minmod: bad arguments");
+  std::string e;
+  return wrap(h, adg::lim_minmod(a, b, n, out, (cudaStream_t)stream, &e), e);
+}
+
+int adg_relaxed_bounds(adg_handle* h, int dim, int nvars, const int64_t* cells, int nsub,
+                       const double* padded_sub, double delta0, double eps, double* cmin_pad,
+                       double* cmax_pad, double* lo_out, double* hi_out, void* stream) {
+  DeviceGuard dg(h);
+  if (dim < 1 || dim > 3 || nvars < 1 || !cells || nsub < 1 || !padded_sub || !cmin_pad ||
+      !cmax_pad || !lo_out || !hi_out)
+    return fail(h, ADG_ERR_INVALID, "adg_relaxed_bounds: bad arguments");
+  std::string e;
+  return wrap(h, adg::lim_relaxed_bounds(dim, nvars, cells, nsub, padded_sub, delta0, eps,
+                                         cmin_pad, cmax_pad, lo_out, hi_out,
+                                         (cudaStream_t)stream, &e), e);
+}
+
+int adg_detect_cells(adg_handle* h, const adg_grid* g, const double* cand,
+                     const double* cand_sub, const double* lo, const double* hi,
+                     uint8_t* troubled, void* stream) {
+  DeviceGuard dg(h);
+  int rc = check_grid(h, g);
+  if (rc) return rc;
+  if (!cand || !cand_sub || !lo || !hi || !troubled)
+    return fail(h, ADG_ERR_INVALID, "adg_detect_cells: null array");
+  std::string e;
+  return wrap(h, adg::lim_detect_cells(g, cand, cand_sub, lo, hi, troubled,
+                                       (cudaStream_t)stream, &e), e);
+}
+
+int adg_gather_windows(adg_handle* h, int dim, int nvars, const int64_t* padded_dims,
+                       const double* padded, const int64_t* starts, int64_t nwin, int size,
+                       double* out, void* stream) {
+  DeviceGuard dg(h);
+  if (dim < 1 || dim > 3 || nvars < 1 || !padded_dims || size < 1 || nwin < 0 ||
+      (nwin > 0 && (!padded || !starts || !out)))
+    return fail(h, ADG_ERR_INVALID, "adg_gather_windows: bad arguments");
+  std::string e;
+  return wrap(h, adg::lim_gather_windows(dim, nvars, padded_dims, padded, starts, nwin, size,
+                                         out, (cudaStream_t)stream, &e), e);
 }
 
 int adg_volume_integral(adg_handle* h, const adg_grid* g, const double* q, const double* dt_dev,

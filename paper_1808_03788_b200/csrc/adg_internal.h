@@ -143,6 +143,18 @@ int element_update(const adg_grid* g, const double* u, const double* vol,
                    const double* const* accs, int nacc, double* out, cudaStream_t st,
                    std::string* err);
 
+// limiter module pieces (adg_pieces.cu)
+int lim_minmod(const double* a, const double* b, int64_t n, double* out, cudaStream_t st,
+               std::string* err);
+int lim_relaxed_bounds(int dim, int m, const int64_t* cells, int nsub, const double* padded_sub,
+                       double delta0, double eps, double* cmin_pad, double* cmax_pad, double* lo,
+                       double* hi, cudaStream_t st, std::string* err);
+int lim_detect_cells(const adg_grid* g, const double* cand, const double* sub, const double* lo,
+                     const double* hi, uint8_t* out, cudaStream_t st, std::string* err);
+int lim_gather_windows(int dim, int m, const int64_t* dims, const double* padded,
+                       const int64_t* starts, int64_t nwin, int size, double* out,
+                       cudaStream_t st, std::string* err);
+
 void upload_tables(int degree, const double* blob, int64_t n, std::string* err, int* rc);
 
 // multi-GPU exchange (adg_comm.cu, NCCL)

@@ -83,6 +83,10 @@ riemann_points_kernel(const double* __restrict__ qm_all, const double* __restric
       for (int j = 0; j < D; ++j) an = an + av[j] * nv[j];
       s = fabs(an);
     }
+    if (mode == 2) {   // rusanov_theta (corrector.py:58-62): the speed alone, [n]
+      out_a[i] = s;
+      continue;
+    }
     double out[M], fm[M], fp[M];
 #pragma unroll
     for (int v = 0; v < M; ++v) out[v] = -0.5 * s * (qp[v] - qm[v]);
@@ -114,6 +118,133 @@ riemann_points_kernel(const double* __restrict__ qm_all, const double* __restric
 #pragma unroll
       for (int v = 0; v < M; ++v) out_a[i * M + v] = out[v];
     }
+  }
+}
+
+
+// ---- limiter module pieces (limiter.py:45-101), array interfaces ----------
+// minmod (limiter.py:45-48): the smaller-magnitude argument where the signs
+// agree, else 0
+__global__ void __launch_bounds__(kPieceThreads)
+minmod_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+              double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = a[i], y = b[i];
+    const double pick = fabs(x) <= fabs(y) ? x : y;
+    out[i] = x * y > 0.0 ? pick : 0.0;
+  }
+}
+
+// per-cell extrema of a subcell field [ncell][nsub][m] (NaN propagates like
+// numpy's amin / amax)
+__global__ void __launch_bounds__(kPieceThreads)
+cell_extrema_kernel(const double* __restrict__ x, int64_t ncell, int nsub, int m,
+                    double* __restrict__ cmin, double* __restrict__ cmax) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncell * m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / m;
+    const int v = (int)(i - c * m);
+    const double* p = x + c * nsub * m + v;
+    double lo = p[0], hi = p[0];
+    for (int s = 1; s < nsub; ++s) {
+      const double q = p[(int64_t)s * m];
+      lo = (q < lo || q != q) ? q : lo;
+      hi = (q > hi || q != q) ? q : hi;
+    }
+    cmin[i] = lo;
+    cmax[i] = hi;
+  }
+}
+
+// relaxed DMP bounds (limiter.py:51-73) of the core cells of a one-cell
+// padded grid: own and 2 d face-neighbour extrema, widened by
+// max(delta0, eps (hi - lo))
+__global__ void __launch_bounds__(kPieceThreads)
+relaxed_bounds_kernel(const double* __restrict__ cmin, const double* __restrict__ cmax, int dim,
+                      int64_t n0, int64_t n1, int64_t n2, int m, double delta0, double eps,
+                      double* __restrict__ lo_out, double* __restrict__ hi_out) {
+  const int64_t n[3] = {n0, n1, n2};
+  const int64_t ncore = n0 * (dim >= 2 ? n1 : 1) * (dim == 3 ? n2 : 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncore * m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / m;
+    const int v = (int)(i - c * m);
+    int64_t k[3] = {0, 0, 0}, r = c;
+    for (int j = dim - 1; j >= 0; --j) {
+      k[j] = r % n[j];
+      r /= n[j];
+    }
+    auto padded = [&](const int64_t* kk) {
+      int64_t idx = 0;
+      for (int j = 0; j < dim; ++j) idx = idx * (n[j] + 2) + (kk[j] + 1);
+      return idx * m + v;
+    };
+    double lo = cmin[padded(k)], hi = cmax[padded(k)];
+    for (int j = 0; j < dim; ++j)
+      for (int sh = -1; sh <= 1; sh += 2) {
+        int64_t kk[3] = {k[0], k[1], k[2]};
+        kk[j] += sh;
+        const double a = cmin[padded(kk)], b = cmax[padded(kk)];
+        lo = (a < lo || a != a) ? a : lo;      // torch.minimum / maximum: NaN propagates
+        hi = (b > hi || b != b) ? b : hi;
+      }
+    const double w = eps * (hi - lo);
+    const double delta = w != w ? w : (w < delta0 ? delta0 : w);   // clamp(min=delta0)
+    lo_out[i] = lo - delta;
+    hi_out[i] = hi + delta;
+  }
+}
+
+// detect_troubled (limiter.py:76-86): a subcell outside the bounds, or an
+// inadmissible nodal or subcell state.  SYS 0: Euler; SYS 1: finite only
+// (advection, elasticity-di)
+template <int SYS, int D>
+__global__ void __launch_bounds__(kPieceThreads)
+detect_cells_kernel(const double* __restrict__ cand, const double* __restrict__ sub,
+                    const double* __restrict__ lo, const double* __restrict__ hi, int64_t E,
+                    int pd, int sd, int m, double gm1, uint8_t* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    bool bad = false;
+    auto adm = [&](const double* q) {
+      if (SYS == 0) return admissible<D>(q, gm1);
+      bool fin = true;
+      for (int v = 0; v < m; ++v) fin = fin && isfinite(q[v]);
+      return fin;
+    };
+    for (int s = 0; s < sd; ++s) {
+      const double* q = sub + (e * sd + s) * m;
+      for (int v = 0; v < m; ++v) bad = bad || q[v] < lo[e * m + v] || q[v] > hi[e * m + v];
+      bad = bad || !adm(q);
+    }
+    for (int nd = 0; nd < pd; ++nd) bad = bad || !adm(cand + (e * pd + nd) * m);
+    out[e] = bad ? 1 : 0;
+  }
+}
+
+// gather_windows (limiter.py:89-101): out[w][a..][v] = padded[start_w + a][v]
+__global__ void __launch_bounds__(kPieceThreads)
+gather_windows_kernel(const double* __restrict__ padded, int dim, int64_t d0, int64_t d1,
+                      int64_t d2, int m, const int64_t* __restrict__ starts, int64_t nwin,
+                      int size, double* __restrict__ out) {
+  const int64_t dims[3] = {d0, d1, d2};
+  int64_t per = m;
+  for (int j = 0; j < dim; ++j) per *= size;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nwin * per;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = i / per;
+    int64_t r = i - w * per;
+    const int v = (int)(r % m);
+    r /= m;
+    int64_t a[3] = {0, 0, 0};
+    for (int j = dim - 1; j >= 0; --j) {
+      a[j] = r % size;
+      r /= size;
+    }
+    int64_t idx = 0;
+    for (int j = 0; j < dim; ++j) idx = idx * dims[j] + (starts[w * dim + j] + a[j]);
+    out[i] = padded[idx * m + v];
   }
 }
 
@@ -501,6 +632,66 @@ int riemann_points(const adg_grid* g, int64_t n, const double* normal, int mode,
   if (sys == 1 && g->dim == 2) ADG_RIEMANN(1, 2);
   if (sys == 1 && g->dim == 3) ADG_RIEMANN(1, 3);
 #undef ADG_RIEMANN
+  return lerr(err);
+}
+
+
+int lim_minmod(const double* a, const double* b, int64_t n, double* out, cudaStream_t st,
+               std::string* err) {
+  if (n <= 0) return ADG_OK;
+  minmod_kernel<<<grid_for(n), kPieceThreads, 0, st>>>(a, b, n, out);
+  return lerr(err);
+}
+
+int lim_relaxed_bounds(int dim, int m, const int64_t* cells, int nsub, const double* padded_sub,
+                       double delta0, double eps, double* cmin_pad, double* cmax_pad, double* lo,
+                       double* hi, cudaStream_t st, std::string* err) {
+  int64_t npad = 1, ncore = 1;
+  for (int j = 0; j < dim; ++j) {
+    npad *= cells[j] + 2;
+    ncore *= cells[j];
+  }
+  if (ncore <= 0) return ADG_OK;
+  cell_extrema_kernel<<<grid_for(npad * m), kPieceThreads, 0, st>>>(padded_sub, npad, nsub, m,
+                                                                    cmin_pad, cmax_pad);
+  relaxed_bounds_kernel<<<grid_for(ncore * m), kPieceThreads, 0, st>>>(
+      cmin_pad, cmax_pad, dim, cells[0], dim >= 2 ? cells[1] : 1, dim == 3 ? cells[2] : 1, m,
+      delta0, eps, lo, hi);
+  return lerr(err);
+}
+
+int lim_detect_cells(const adg_grid* g, const double* cand, const double* sub, const double* lo,
+                     const double* hi, uint8_t* out, cudaStream_t st, std::string* err) {
+  const int64_t E = n_elements(g);
+  if (E <= 0) return ADG_OK;
+  const int P = g->degree + 1, S = 2 * g->degree + 1;
+  int pd = 1, sd = 1;
+  for (int j = 0; j < g->dim; ++j) {
+    pd *= P;
+    sd *= S;
+  }
+  const unsigned grid = grid_for(E);
+  const double gm1 = g->gamma - 1.0;
+  const int m = g->nvars;
+  if (g->system == ADG_SYS_EULER) {
+    if (g->dim == 1) detect_cells_kernel<0, 1><<<grid, kPieceThreads, 0, st>>>(cand, sub, lo, hi, E, pd, sd, m, gm1, out);
+    if (g->dim == 2) detect_cells_kernel<0, 2><<<grid, kPieceThreads, 0, st>>>(cand, sub, lo, hi, E, pd, sd, m, gm1, out);
+    if (g->dim == 3) detect_cells_kernel<0, 3><<<grid, kPieceThreads, 0, st>>>(cand, sub, lo, hi, E, pd, sd, m, gm1, out);
+  } else {
+    detect_cells_kernel<1, 1><<<grid, kPieceThreads, 0, st>>>(cand, sub, lo, hi, E, pd, sd, m, gm1, out);
+  }
+  return lerr(err);
+}
+
+int lim_gather_windows(int dim, int m, const int64_t* dims, const double* padded,
+                       const int64_t* starts, int64_t nwin, int size, double* out,
+                       cudaStream_t st, std::string* err) {
+  int64_t per = m;
+  for (int j = 0; j < dim; ++j) per *= size;
+  if (nwin * per <= 0) return ADG_OK;
+  gather_windows_kernel<<<grid_for(nwin * per), kPieceThreads, 0, st>>>(
+      padded, dim, dims[0], dim >= 2 ? dims[1] : 1, dim == 3 ? dims[2] : 1, m, starts, nwin, size,
+      out);
   return lerr(err);
 }
 

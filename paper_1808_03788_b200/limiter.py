@@ -2,11 +2,11 @@
 
 Same names, arguments and results as the reference module for callers
 that run the subcell limiter pieces themselves; Simulation uses the fused
-adg_detect / adg_rescue path instead.  The subcell projection, recovery,
-MUSCL-Hancock step and flattening run in the library's kernels; the
-bound / screen / gather helpers are short device tensor expressions over
-their outputs.  Inputs may be numpy arrays or CUDA tensors; results are
-CUDA tensors.  Euler only.
+adg_detect / adg_rescue path instead.  Every function runs in the library's
+kernels (torch only holds the device buffers).  Inputs may be numpy arrays
+or CUDA tensors; results are CUDA tensors.  The projection, recovery, MUSCL
+step and flattening are Euler's; minmod, the bounds, the screen (Euler,
+advection, elasticity-di) and the window gather take any state width.
 """
 
 import numpy as np
@@ -71,60 +71,70 @@ def recover_from_subcells(ubar, tables, dim):
 
 
 def minmod(a, b):
-    """Componentwise minmod (limiter.py:45-48)."""
+    """Componentwise minmod (limiter.py:45-48): adg_minmod."""
     a, b = as_device(a), as_device(b)
-    pick = torch.where(torch.abs(a) <= torch.abs(b), a, b)
-    return torch.where(a * b > 0.0, pick, torch.zeros_like(a))
+    a, b = torch.broadcast_tensors(a, b)
+    a, b = a.contiguous(), b.contiguous()
+    out = torch.empty_like(a)
+    h = _lib.Handle.get(a.device.index)
+    h.call("adg_minmod", int(a.numel()), a.data_ptr(), b.data_ptr(), out.data_ptr(), h.stream())
+    return out
 
 
 def relaxed_bounds(prev_sub_cells, dim, delta0=DMP_DELTA0, eps=DMP_EPS):
     """DMP bounds over the own and 2d face-neighbour cells of a one-cell
-    padded grid (limiter.py:51-73)."""
-    x = as_device(prev_sub_cells)
-    sub_axes = tuple(range(dim, 2 * dim))
-    cmin = torch.amin(x, dim=sub_axes)
-    cmax = torch.amax(x, dim=sub_axes)
-    core = tuple(slice(1, -1) for _ in range(dim))
-    lo = cmin[core].clone()
-    hi = cmax[core].clone()
-    for j in range(dim):
-        for shift in (-1, 1):
-            sl = tuple(slice(1 + shift, (-1 + shift) or None) if i == j else slice(1, -1)
-                       for i in range(dim))
-            lo = torch.minimum(lo, cmin[sl])
-            hi = torch.maximum(hi, cmax[sl])
-    delta = torch.clamp(eps * (hi - lo), min=delta0)
-    return lo - delta, hi + delta
+    padded grid (limiter.py:51-73): adg_relaxed_bounds."""
+    x = as_device(prev_sub_cells).contiguous()
+    if x.ndim != 2 * dim + 1 or any(n < 3 for n in x.shape[:dim]):
+        raise ValueError("prev_sub_cells must be (cells + 2.., s.., m) with a one-cell pad")
+    m = int(x.shape[-1])
+    cells = [int(n) - 2 for n in x.shape[:dim]]
+    nsub = int(np.prod(x.shape[dim:2 * dim]))
+    npad = int(np.prod(x.shape[:dim]))
+    f64 = dict(dtype=torch.float64, device=x.device)
+    cmin, cmax = torch.empty(npad * m, **f64), torch.empty(npad * m, **f64)
+    lo, hi = torch.empty(tuple(cells) + (m,), **f64), torch.empty(tuple(cells) + (m,), **f64)
+    carr = (_lib.ctypes.c_int64 * dim)(*cells)
+    h = _lib.Handle.get(x.device.index)
+    h.call("adg_relaxed_bounds", dim, m, carr, nsub, x.data_ptr(), float(delta0), float(eps),
+           cmin.data_ptr(), cmax.data_ptr(), lo.data_ptr(), hi.data_ptr(), h.stream())
+    return lo, hi
 
 
 def detect_troubled(candidate, cand_sub, bounds, system, dim):
-    """True where a candidate cell needs the FV rescue (limiter.py:76-86)."""
-    cand = as_device(candidate)
-    sub = as_device(cand_sub)
-    lo, hi = (as_device(b) for b in bounds)
-    sub_axes = tuple(range(cand.ndim - 1 - dim, cand.ndim - 1))
-    grid_nd = cand.ndim - 1 - dim
-    expand = (slice(None),) * grid_nd + (None,) * dim
-    outside = (sub < lo[expand]) | (sub > hi[expand])
-    troubled = torch.any(outside, dim=sub_axes + (sub.ndim - 1,))
-    node_ok = torch.all(system.admissible(cand), dim=sub_axes)
-    sub_ok = torch.all(system.admissible(sub), dim=sub_axes)
-    return troubled | ~node_ok | ~sub_ok
+    """True where a candidate cell needs the FV rescue (limiter.py:76-86):
+    adg_detect_cells."""
+    from .corrector import _device_system
+
+    _device_system(system)
+    cand = as_device(candidate).contiguous()
+    sub = as_device(cand_sub).contiguous()
+    lo, hi = (as_device(b).contiguous() for b in bounds)
+    lead, E = _lead(cand, dim)
+    P = int(cand.shape[-2])
+    out = torch.empty(lead if lead else (1,), dtype=torch.uint8, device=cand.device)
+    g = flat_grid(system, P - 1, E)
+    h = _lib.Handle.get(cand.device.index)
+    h.ensure_tables(basis_tables(P - 1))
+    h.call("adg_detect_cells", _lib.ctypes.byref(g), cand.data_ptr(), sub.data_ptr(),
+           lo.data_ptr(), hi.data_ptr(), out.data_ptr(), h.stream())
+    out = out.bool()
+    return out if lead else out[0]
 
 
 def gather_windows(padded, starts, size, dim):
     """(T, size.., m) windows out of a padded global subcell field
-    (limiter.py:89-101)."""
-    x = as_device(padded)
-    st = torch.as_tensor(np.asarray(starts), dtype=torch.int64, device=x.device)
-    n = st.shape[0]
-    idx = []
-    for j in range(dim):
-        shape = [n] + [1] * dim
-        shape[1 + j] = size
-        ar = torch.arange(size, device=x.device)
-        idx.append((st[:, j][:, None] + ar[None, :]).reshape(shape))
-    return x[tuple(idx)]
+    (limiter.py:89-101): adg_gather_windows."""
+    x = as_device(padded).contiguous()
+    st = torch.as_tensor(np.asarray(starts), dtype=torch.int64, device=x.device).reshape(-1, dim)
+    st = st.contiguous()
+    n, m = int(st.shape[0]), int(x.shape[-1])
+    out = torch.empty((n,) + (int(size),) * dim + (m,), dtype=torch.float64, device=x.device)
+    darr = (_lib.ctypes.c_int64 * dim)(*[int(v) for v in x.shape[:dim]])
+    h = _lib.Handle.get(x.device.index)
+    h.call("adg_gather_windows", dim, m, darr, x.data_ptr(), st.data_ptr(), n, int(size),
+           out.data_ptr(), h.stream())
+    return out
 
 
 def muscl_subcell_step(windows, system, sub_spacings, dt, mode="conservative"):

@@ -201,3 +201,59 @@ def test_muscl_subcell_step(mods, mode):
     onew, ofailed = olim.muscl_step(wins, EulerOracle(2), (0.02, 0.03), 1e-3, mode=mode)
     np.testing.assert_array_equal(host(failed), ofailed)
     assert rel(new, onew) <= 1e-12
+
+
+def test_rusanov_theta_and_screen_edge_cases(mods):
+    """rusanov_theta (corrector.py:58-62) and the limiter helpers as library
+    kernels against plain torch expressions of the same ops: general normals,
+    the advection plugin, NaN propagation, inadmissible states."""
+    corrector, limiter, make_system = mods
+    for d in (1, 2, 3):
+        e = make_system("euler", d)
+        qm, qp = states(d, 257, 3 + d), states(d, 257, 30 + d)
+        nrm = np.random.default_rng(d).standard_normal(d)
+        nrm /= np.linalg.norm(nrm)
+        got = corrector.rusanov_theta(qm, qp, nrm, e)
+        tm, tp = torch.as_tensor(qm).cuda(), torch.as_tensor(qp).cuda()
+        nt = torch.as_tensor(nrm).cuda()
+        ref = torch.maximum(e.max_abs_eigenvalue(tm, nt), e.max_abs_eigenvalue(tp, nt))
+        assert got.shape == ref.shape
+        assert rel(got, host(ref)) <= 1e-14
+    adv = make_system("advection", 2)
+    q = np.random.default_rng(0).standard_normal((5, 7, 1))
+    got = corrector.rusanov_theta(q, 2 * q, (0.6, 0.8), adv)
+    assert got.shape == (5, 7)
+    np.testing.assert_allclose(host(got), abs(0.6 * adv.velocity[0] + 0.8 * adv.velocity[1]),
+                               rtol=1e-15)
+    # screen: a NaN subcell, a negative density node and a negative pressure
+    # subcell are troubled; cells inside their bounds are not
+    e2 = make_system("euler", 2)
+    S, P = 3, 2
+    cand = np.broadcast_to(np.array([1.0, 0.1, 0.2, 2.5]), (4, P, P, 4)).copy()
+    csub = np.broadcast_to(np.array([1.0, 0.1, 0.2, 2.5]), (4, S, S, 4)).copy()
+    lo = np.broadcast_to(np.array([0.9, 0.0, 0.1, 2.4]), (4, 4)).copy()
+    hi = np.broadcast_to(np.array([1.1, 0.2, 0.3, 2.6]), (4, 4)).copy()
+    csub[1, 2, 1, 2] = np.nan
+    cand[2, 0, 1, 0] = -1.0
+    csub[3, 0, 0, 3] = 0.001          # p < 0 at this subcell, inside no bound either
+    flags = host(limiter.detect_troubled(cand, csub, (lo, hi), e2, 2))
+    np.testing.assert_array_equal(flags, [False, True, True, True])
+    # finite-only screen of the advection plugin, 1-D
+    a1 = make_system("advection", 1)
+    c1 = np.zeros((3, 2, 1))
+    s1 = np.zeros((3, 3, 1))
+    s1[1, 2, 0] = 0.5
+    c1[2, 1, 0] = np.inf
+    f1 = host(limiter.detect_troubled(c1, s1, (np.full((3, 1), -0.1), np.full((3, 1), 0.1)),
+                                      a1, 1))
+    np.testing.assert_array_equal(f1, [False, True, True])
+    # minmod broadcasting and the bounds' NaN propagation like the torch ops
+    a = torch.tensor([[1.0, -2.0, 3.0]], dtype=torch.float64).cuda()
+    b = torch.tensor([[2.0], [-1.0]], dtype=torch.float64).cuda()
+    pick = torch.where(a.abs() <= b.abs(), a, b)
+    ref = torch.where(a * b > 0.0, pick, torch.zeros_like(pick))
+    assert torch.equal(limiter.minmod(a, b), ref)
+    pad = np.random.default_rng(2).uniform(0.5, 2.0, (5, 3, 1))
+    pad[2, 1, 0] = np.nan
+    lo2, hi2 = limiter.relaxed_bounds(pad, 1)
+    assert np.isnan(host(lo2)).all() and np.isnan(host(hi2)).all()
