@@ -59,6 +59,10 @@ namespace adg {
 #ifndef ADG_PH_TNB
 #define ADG_PH_TNB 1
 #endif
+// CTAs per SM the time kernel is compiled for (register cap 65536 / (256 n))
+#ifndef ADG_PH_TMINB
+#define ADG_PH_TMINB (ADG_PH_TNB == 1 ? 3 : 2)
+#endif
 
 
 template <int P>
@@ -465,7 +469,7 @@ ph_rates_kernel(const __grid_constant__ PhArgs a) {
 // element, one (node, quantity) per thread and pass: its P rates and P old
 // iterates are loaded up front (all independent: HBM latency overlapped)
 template <int P>
-__global__ void __launch_bounds__(PhCfg<P>::NT_T, ADG_PH_TNB == 1 ? 3 : 2)
+__global__ void __launch_bounds__(PhCfg<P>::NT_T, ADG_PH_TMINB)
 ph_time_kernel(const __grid_constant__ PhArgs a) {
   using C = PhCfg<P>;
   constexpr int M = C::M, PD = C::PD, NT = C::NT_T, NW = NT / 32;
@@ -810,6 +814,28 @@ static size_t phased_ws_need(int64_t n_elem) {
   return (size_t)phased_batch<P>(n_elem) * phased_bytes_per_element<P>() + 256;
 }
 
+// per-device side stream + fork / join events of the two-stream schedule
+struct SideStream {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream* side_stream() {
+  static SideStream tab[32];
+  int d = 0;
+  cudaGetDevice(&d);
+  SideStream* s = &tab[d & 31];
+  if (!s->stream) {
+    if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming) != cudaSuccess) {
+      s->stream = nullptr;
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
+  return s;
+}
+
 template <class K>
 static int set_smem(K kern, size_t bytes, PerDevice* flag, std::string* err) {
   if (!flag->first()) return ADG_OK;
@@ -848,40 +874,89 @@ static int launch_phased(const PhArgs& a0, int64_t n_all, cudaStream_t st, int n
   occ_t = std::max(occ_t, 1);
   occ_tr = std::max(occ_tr, 1);
   occ_v = std::max(occ_v, 1);
+  // Two halves of a batch run their kernel sequences on two streams, the
+  // second one kernel behind the first: the FP64-bound kernels (startup,
+  // rates) of one half overlap the HBM-bound ones (time, traces, flux sums)
+  // of the other (ADG_PH_STREAMS=1: one stream).  The side stream forks from
+  // and joins the caller's stream by events (graph-capturable).
+  const char* sv = getenv("ADG_PH_STREAMS");
+  const int want_parts = sv ? atoi(sv) : 2;
+  SideStream* side = want_parts > 1 ? side_stream() : nullptr;
+  const auto grid = [&](int64_t tasks, int occ, int waves) {
+    return (unsigned)std::max<int64_t>(1,
+                                       std::min<int64_t>(tasks, (int64_t)num_sms * occ * waves));
+  };
   for (int64_t e0 = 0; e0 < n_all; e0 += batch) {
     const int64_t n = std::min<int64_t>(batch, n_all - e0);
-    PhArgs a = a0;
-    a.u = a0.u + (size_t)e0 * C::SLICE;
-    a.q_out = a0.q_out ? a0.q_out + (size_t)e0 * C::TILE : nullptr;
-    a.vol = a0.vol + (size_t)e0 * C::SLICE;
-    a.traces = a0.traces + (size_t)e0 * C::TB;
-    a.pred_bad = a0.pred_bad + e0;
-    a.sweeps = a0.sweeps + e0;
-    a.n_elem = n;
-    a.tr_elems = n_all;
+    const int nparts = (side && n >= 4 * (int64_t)num_sms) ? 2 : 1;
+    double* qg = ws;
     // bulk-copied arrays first (16-byte aligned: QSZP is even), the dense
     // rates (odd slice sizes at P = 9) behind them
-    a.qg = ws;
-    a.kg = a.qg + (size_t)batch * C::TILEQ;
-    a.rg = a.kg + 3 * (size_t)batch * C::QSZP;
-    a.state = reinterpret_cast<int32_t*>(a.rg + (size_t)batch * C::TILE);
-    a.n_active = a.state + 4 * batch;
-    cudaMemsetAsync(a.n_active, 0, sizeof(int32_t), st);
-    const auto grid = [&](int64_t tasks, int occ, int waves) {
-      return (unsigned)std::max<int64_t>(
-          1, std::min<int64_t>(tasks, (int64_t)num_sms * occ * waves));
-    };
-    ph_startup_kernel<P><<<grid(n, occ_a, 4), C::NT_A, C::SMEM_A, st>>>(a);
-    for (int it = 0; it < a.max_iter; ++it) {
-      a.it = it;
-      ph_rates_kernel<P><<<grid(n * P, occ_a, 4), C::NT_A, C::SMEM_A, st>>>(a);
-      ph_time_kernel<P><<<grid(n, occ_t, 4), C::NT_T, 0, st>>>(a);
+    double* kg = qg + (size_t)batch * C::TILEQ;
+    double* rg = kg + 3 * (size_t)batch * C::QSZP;
+    int32_t* state = reinterpret_cast<int32_t*>(rg + (size_t)batch * C::TILE);
+    int32_t* n_active = state + 4 * batch;
+    cudaMemsetAsync(n_active, 0, 2 * sizeof(int32_t), st);
+    PhArgs part[2];
+    cudaStream_t pst[2] = {st, nparts == 2 ? side->stream : st};
+    for (int p = 0; p < nparts; ++p) {
+      const int64_t off = p == 0 ? 0 : n / 2;
+      const int64_t np = nparts == 1 ? n : (p == 0 ? n / 2 : n - n / 2);
+      PhArgs& a = part[p];
+      a = a0;
+      a.u = a0.u + (size_t)(e0 + off) * C::SLICE;
+      a.q_out = a0.q_out ? a0.q_out + (size_t)(e0 + off) * C::TILE : nullptr;
+      a.vol = a0.vol + (size_t)(e0 + off) * C::SLICE;
+      a.traces = a0.traces + (size_t)(e0 + off) * C::TB;
+      a.pred_bad = a0.pred_bad + e0 + off;
+      a.sweeps = a0.sweeps + e0 + off;
+      a.n_elem = np;
+      a.tr_elems = n_all;
+      a.qg = qg + (size_t)off * C::TILEQ;
+      a.kg = kg + 3 * (size_t)off * C::QSZP;
+      a.rg = rg + (size_t)off * C::TILE;
+      a.state = state + 4 * off;
+      a.n_active = n_active + p;
     }
-    // (one fused per-element kernel for traces + flux sums, slices double
-    // buffered by bulk copies, was measured equal: 6.18 vs 6.38 ms at N = 8)
-    ph_traces_kernel<P><<<grid(n * P, occ_tr, 4), C::NT_F, C::SMEM_TR, st>>>(a);
-    ph_fbar_kernel<P><<<grid((n * C::PD + 255) / 256, 8, 4), 256, 0, st>>>(a);
-    ph_vol_kernel<P><<<grid(n, occ_v, 4), C::RP, C::SMEM_V, st>>>(a);
+    if (nparts == 2) {
+      cudaEventRecord(side->fork, st);
+      cudaStreamWaitEvent(side->stream, side->fork, 0);
+    }
+    // kernel k of a part's sequence: 0 startup, 1 + 2 it rates, 2 + 2 it
+    // time, then traces, flux sums, volume
+    const int nk = 1 + 2 * a0.max_iter + 3;
+    const auto launch = [&](int p, int k) {
+      PhArgs& a = part[p];
+      cudaStream_t s = pst[p];
+      const int64_t np = a.n_elem;
+      if (k == 0) {
+        ph_startup_kernel<P><<<grid(np, occ_a, 4), C::NT_A, C::SMEM_A, s>>>(a);
+      } else if (k <= 2 * a0.max_iter) {
+        a.it = (k - 1) / 2;
+        if (k & 1)
+          ph_rates_kernel<P><<<grid(np * P, occ_a, 4), C::NT_A, C::SMEM_A, s>>>(a);
+        else
+          ph_time_kernel<P><<<grid(np, occ_t, 4), C::NT_T, 0, s>>>(a);
+      } else if (k == nk - 3) {
+        // (one fused per-element kernel for traces + flux sums, slices double
+        // buffered by bulk copies, was measured equal: 6.18 vs 6.38 ms at N = 8)
+        ph_traces_kernel<P><<<grid(np * P, occ_tr, 4), C::NT_F, C::SMEM_TR, s>>>(a);
+      } else if (k == nk - 2) {
+        ph_fbar_kernel<P><<<grid((np * C::PD + 255) / 256, 8, 4), 256, 0, s>>>(a);
+      } else {
+        ph_vol_kernel<P><<<grid(np, occ_v, 4), C::RP, C::SMEM_V, s>>>(a);
+      }
+    };
+    const int lag = nparts == 2 ? 1 : 0;
+    for (int k = 0; k < nk + lag; ++k)
+      for (int p = 0; p < nparts; ++p) {
+        const int kp = k - p * lag;
+        if (kp >= 0 && kp < nk) launch(p, kp);
+      }
+    if (nparts == 2) {
+      cudaEventRecord(side->join, side->stream);
+      cudaStreamWaitEvent(st, side->join, 0);
+    }
   }
   cudaError_t ce = cudaGetLastError();
   if (ce != cudaSuccess) {

@@ -336,3 +336,31 @@ def test_c4_full_size_determinism(pkg):
     assert torch.equal(res[0][0], res[1][0])
     for a, b in zip(res[0][1], res[1][1]):
         assert torch.equal(a, b)
+
+
+def test_phased_predictor_two_streams_graph_replay(pkg, monkeypatch):
+    """3-D N = 8 on 10 x 10 x 6 elements: large enough for the phased
+    predictor's two-stream schedule (two halves of the batch, the second one
+    kernel behind the first, side stream forked / joined by events) and small
+    enough for the batched CUDA-graph loop, so the fork / join is captured and
+    replayed.  Bitwise equal to the one-stream schedule, stepwise and batched."""
+    system = pkg.make_system("euler", 3)
+    ic = pkg.build_problem("density_wave", system)[0]
+
+    def run(streams, batched):
+        monkeypatch.setenv("ADG_PH_STREAMS", str(streams))
+        sim = pkg.Simulation(pkg.CartesianMesh([(0, 1)] * 3, (10, 10, 6)), system, 8,
+                             0.9 / (3 * 17))
+        sim.project_initial_condition(ic)
+        if batched:
+            sim.run(np.inf, max_steps=4)
+        else:
+            sim.run(np.inf, max_steps=4, on_step=lambda s: None)
+        return sim.u.clone(), [h["dt"] for h in sim.history]
+
+    u1, dt1 = run(1, False)
+    u2, dt2 = run(2, False)
+    u3, dt3 = run(2, True)
+    assert dt1 == dt2 == dt3
+    assert torch.equal(u1, u2)
+    assert torch.equal(u1, u3)
