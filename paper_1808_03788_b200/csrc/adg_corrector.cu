@@ -501,6 +501,13 @@ update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
   __shared__ double s_w[P], s_l[P], s_r[P];
   const DegreeTables& T = tab<P>();
   const int tid = threadIdx.x;
+  // The grid has one block per totals partial (never fewer than the
+  // reduction kernels use); on small grids most blocks own no chunk: they
+  // leave their zero partial and exit (what block_fold would write)
+  if ((int64_t)blockIdx.x >= E / EB && !(blockIdx.x == 0 && E % EB)) {
+    if (partial && tid < M) partial[(size_t)blockIdx.x * M + tid] = 0.0;
+    return;
+  }
   if (tid < P) {
     s_w[tid] = T.weights[tid];
     s_l[tid] = T.left[tid];
