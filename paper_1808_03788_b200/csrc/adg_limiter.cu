@@ -335,6 +335,9 @@ struct WarpCfg {
   static constexpr bool GS = SMEM > 227 * 1024;
   static constexpr int WPBX = GS ? 4 : WPB;
   static constexpr size_t BLOCK_DBL = (size_t)WPBX * PER_WARP + PS;
+  // adg_detect: compiled for three CTAs per SM where shared memory allows
+  // them (80 instead of 106 registers at 2-D N = 5: C4 step 4.42 -> 4.30 ms)
+  static constexpr int DET_MINB = (!GS && 3 * (SMEM + 1024) <= 228 * 1024) ? 3 : 1;
 };
 
 // P_sub of this degree into the CTA's shared copy (before any warp uses it)
@@ -510,7 +513,7 @@ __device__ void ghost_extrema(const double* __restrict__ sub, const double* __re
 // leaves alone they are exactly the next step's prev_sub, so the driver
 // skips the separate projection of u^(n+1).
 template <int D, int P, int SYS>
-__global__ void __launch_bounds__(WarpCfg<D, P, SYS>::WPBX * 32)
+__global__ void __launch_bounds__(WarpCfg<D, P, SYS>::WPBX * 32, WarpCfg<D, P, SYS>::DET_MINB)
 detect_kernel(const double* __restrict__ prev_sub, const double* __restrict__ cmin,
               const double* __restrict__ cmax, const double* __restrict__ cand,
               const uint8_t* __restrict__ pred_bad, LimGrid G, int64_t E, double delta0,
