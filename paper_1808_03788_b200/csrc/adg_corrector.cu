@@ -487,8 +487,11 @@ __device__ __forceinline__ void update_chunk(const double* SU_in, const double* 
   }
 }
 
+#ifndef ADG_UPD_MINB
+#define ADG_UPD_MINB 3   // 80 registers: three CTAs per SM (C2 step 11.92 -> 11.87 ms)
+#endif
 template <int D, int P>
-__global__ void __launch_bounds__(kReduceThreads)
+__global__ void __launch_bounds__(kReduceThreads, ADG_UPD_MINB)
 update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
               const double* __restrict__ fd, const double* __restrict__ dt_dev,
               double* __restrict__ u_out, int64_t E, double dx0, double dx1, double dx2,

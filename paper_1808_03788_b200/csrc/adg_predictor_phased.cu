@@ -60,6 +60,9 @@ namespace adg {
 #define ADG_PH_TNB 1
 #endif
 // CTAs per SM the time kernel is compiled for (register cap 65536 / (256 n))
+#ifndef ADG_PH_FMINB
+#define ADG_PH_FMINB 3   // flux-sums kernel: three CTAs per SM (N = 8: 30.07 -> 29.79 ms)
+#endif
 #ifndef ADG_PH_TMINB
 #define ADG_PH_TMINB (ADG_PH_TNB == 1 ? 3 : 2)
 #endif
@@ -651,7 +654,7 @@ ph_traces_kernel(const __grid_constant__ PhArgs a) {
 // F_dir(q_t) (corrector.py:166) into the element's (now free) rate slices
 // 0 / 1 / 2 = x / y / z, [node][v]
 template <int P>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, ADG_PH_FMINB)
 ph_fbar_kernel(const __grid_constant__ PhArgs a) {
   using C = PhCfg<P>;
   constexpr int M = C::M, PD = C::PD;
