@@ -61,7 +61,7 @@ namespace adg {
 #endif
 // CTAs per SM the time kernel is compiled for (register cap 65536 / (256 n))
 #ifndef ADG_PH_FMINB
-#define ADG_PH_FMINB 3   // flux-sums kernel: three CTAs per SM (N = 8: 30.07 -> 29.79 ms)
+#define ADG_PH_FMINB 2   // flux-sums kernel: 128 registers hold the pipelined loads (3: spills, +0.8 ms at N = 8)
 #endif
 #ifndef ADG_PH_TMINB
 #define ADG_PH_TMINB (ADG_PH_TNB == 1 ? 3 : 2)
@@ -591,6 +591,23 @@ ph_traces_kernel(const __grid_constant__ PhArgs a) {
   const int qbase = R.qbase(role), qstride = R.qstride(role);
   const int64_t ntask = a.n_elem * P;
   const size_t fs = (size_t)a.tr_elems * C::TB;
+  // copy-out map of the staged traces, fixed per thread: entry k of this
+  // thread is staged double x = tid + k NT; it lands at face f, block
+  // position (base + t * tstride) * M + v
+  constexpr int NC = (C::TRS + NT - 1) / NT;
+  int cface[NC], cbase[NC], cstr[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int x = tid + k * NT < C::TRS ? tid + k * NT : 0;
+    const int f = x / (PP * M);
+    const int y = x - f * (PP * M);
+    const int ln = y / M, v = y - ln * M;
+    const int la = ln / P, lb = ln - la * P;
+    const int rl = f >> 1;
+    cface[k] = f;
+    cbase[k] = (rl == 0 ? (la * P + lb) * P : (rl == 1 ? lb * P * P + la : la * P + lb)) * M + v;
+    cstr[k] = (rl == 0 ? 1 : (rl == 1 ? P : P * P)) * M;
+  }
   __shared__ __align__(8) uint64_t bar;
   uint32_t phase = 0;
   if (tid == 0) {
@@ -624,18 +641,14 @@ ph_traces_kernel(const __grid_constant__ PhArgs a) {
       }
     }
     __syncthreads();
-    // staged [face][line][v] -> the face blocks: consecutive threads write
-    // consecutive doubles of a line's 40-byte block (z faces: one contiguous
-    // P^2 m run per slice)
-    for (int x = tid; x < C::TRS; x += NT) {
-      const int f = x / (PP * M);
-      const int y = x - f * (PP * M);
-      const int ln = y / M, v = y - ln * M;
-      const int la = ln / P, lb = ln - la * P;
-      const int rl = f >> 1;
-      const int pos = rl == 0 ? (la * P + lb) * P + t
-                              : (rl == 1 ? (lb * P + t) * P + la : (t * P + la) * P + lb);
-      a.traces[(size_t)f * fs + (size_t)e * C::TB + (size_t)pos * M + v] = S[x];
+    // staged [face][line][v] -> the face blocks (x [j][k][t][v], y [k][t][i][v],
+    // z [t][i][j][v]): consecutive threads write consecutive doubles of a
+    // line's 40-byte block (z faces: one contiguous P^2 m run per slice)
+    double* te = a.traces + (size_t)e * C::TB;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int x = tid + k * NT;
+      if (x < C::TRS) te[(size_t)cface[k] * fs + cbase[k] + t * cstr[k]] = S[x];
     }
     if (a.q_out) {
       for (int n = tid; n < PD; n += NT) {
@@ -668,12 +681,21 @@ ph_fbar_kernel(const __grid_constant__ PhArgs a) {
     const double* qe = a.qg + (size_t)e * C::TILEQ + ph_pad<P>(n * M);
     double fb[3][M];
     bool ok = true;
+    // the next time level's state is loaded before this one is used (the
+    // kernel waited on every level's load in turn: 59 % of its stall samples)
+    double qn[M];
+#pragma unroll
+    for (int v = 0; v < M; ++v) qn[v] = qe[v];
 #pragma unroll
     for (int t = 0; t < P; ++t) {
       double q[M];
 #pragma unroll
-      for (int v = 0; v < M; ++v) q[v] = qe[(size_t)t * C::QSZP + v];
-      ok = ok && admissible<3>(q, gm1);
+      for (int v = 0; v < M; ++v) q[v] = qn[v];
+      if (t + 1 < P) {
+#pragma unroll
+        for (int v = 0; v < M; ++v) qn[v] = qe[(size_t)(t + 1) * C::QSZP + v];
+      }
+      ok = admissible<3>(q, gm1) && ok;
       const double wt = T.weights[t];
       double f[M];
 #pragma unroll
