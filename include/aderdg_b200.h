@@ -67,6 +67,15 @@ typedef struct adg_handle adg_handle;
  * nonconservative product with path-conservative faces (corrector.py:65-129) */
 #define ADG_SYS_ELASTICITY 2
 
+/* adg_grid.flags.  ADG_GRID_FOLD_STATE: the predictor's volume output is
+ * w = u^n + vol / mass (mass = |cell| w_node) instead of the volume integral
+ * itself, and adg_update forms u^(n+1) = w - (sum of face terms) / mass from
+ * it without reading u^n again (one array less through HBM; the reference's
+ * u + (vol - faces) / mass, corrector.py:199-205, re-associated: differences
+ * at the 1e-16 level).  Only where adg_fold_supported(g): Euler, conservative
+ * predictor, shared-tile kernel (not 3-D N >= 7). */
+#define ADG_GRID_FOLD_STATE 1
+
 typedef struct adg_grid {
   int32_t dim;
   int32_t degree;
@@ -77,7 +86,7 @@ typedef struct adg_grid {
   double gamma;
   int32_t bc[3][2];
   int32_t system;       /* ADG_SYS_* */
-  int32_t reserved0;
+  int32_t flags;        /* ADG_GRID_* (0: none) */
   double velocity[3];   /* ADG_SYS_ADVECTION: a_j (unused entries 0) */
 } adg_grid;
 
@@ -201,6 +210,8 @@ int adg_predict_range(adg_handle* h, const adg_grid* g, int64_t e_begin, int64_t
                       int min_iter, double* q_out, double* vol_out, double* traces,
                       uint8_t* pred_bad, int32_t* sweeps, void* stream);
 int adg_predict_range_supported(const adg_grid* g);
+/* 1 if this grid's predictor / update pair implements ADG_GRID_FOLD_STATE */
+int adg_fold_supported(const adg_grid* g);
 
 /* -- face coupling along one axis: driver._face_states (driver.py:234-261)
  *    + corrector.face_fluxes (corrector.py:100-129) + the time weighting of

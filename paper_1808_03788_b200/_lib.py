@@ -20,6 +20,7 @@ ADG_ERR_UNSUPPORTED = 4
 
 BC_CODES = {"periodic": 0, "outflow": 1, "wall": 2, "exact": 3, "ghost": 3}
 MODE_CODES = {"conservative": 0, "primitive": 1}   # adg_grid.mode (ADG_MODE_*)
+GRID_FOLD_STATE = 1   # adg_grid.flags (ADG_GRID_FOLD_STATE)
 SYSTEM_CODES = {"euler": 0, "advection": 1, "elasticity-di": 2}        # adg_grid.system (ADG_SYS_*)
 
 
@@ -38,7 +39,7 @@ STATUS_NONFINITE = 2
 EXPORTS = (
     "adg_create", "adg_destroy", "adg_last_error", "adg_version", "adg_set_tables",
     "adg_wavespeed", "adg_timestep", "adg_advance_time", "adg_predict", "adg_face_flux", "adg_update",
-    "adg_update_blocks", "adg_trace_block", "adg_totals_finalize", "adg_totals", "adg_state_record", "adg_minmod", "adg_relaxed_bounds", "adg_detect_cells", "adg_gather_windows", "adg_project_subcells",
+    "adg_update_blocks", "adg_trace_block", "adg_totals_finalize", "adg_totals", "adg_state_record", "adg_fold_supported", "adg_minmod", "adg_relaxed_bounds", "adg_detect_cells", "adg_gather_windows", "adg_project_subcells",
     "adg_detect", "adg_rescue", "adg_flatten_ic", "adg_face_fluxes", "adg_volume_integral",
     "adg_face_integral", "adg_element_update", "adg_muscl_windows", "adg_recover_subcells",
     "adg_flatten_cells", "adg_log_step", "adg_predict_range", "adg_predict_range_supported",
@@ -59,7 +60,7 @@ class Grid(ctypes.Structure):
                 ("nvars", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("cells", ctypes.c_int64 * 3), ("dx", ctypes.c_double * 3),
                 ("gamma", ctypes.c_double), ("bc", (ctypes.c_int32 * 2) * 3),
-                ("system", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("system", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("velocity", ctypes.c_double * 3)]
 
 
@@ -111,6 +112,7 @@ _SIGS = {
     "adg_totals_finalize": (_I, [_P, _P, _P, _I64, _P, _P]),
     "adg_totals": (_I, [_P, _P, _P, _P, _P, _P]),
     "adg_state_record": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "adg_fold_supported": (_I, [_P]),
     "adg_minmod": (_I, [_P, _I64, _P, _P, _P, _P]),
     "adg_relaxed_bounds": (_I, [_P, _I, _I, _P, _I, _P, _D, _D, _P, _P, _P, _P, _P]),
     "adg_detect_cells": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),

@@ -123,6 +123,11 @@ static int check_grid(adg_handle* h, const adg_grid* g) {
   }
   if (!h->tables_loaded[g->degree])
     return fail(h, ADG_ERR_INVALID, "tables for this degree not uploaded (adg_set_tables)");
+  if (g->flags & ~ADG_GRID_FOLD_STATE) return fail(h, ADG_ERR_INVALID, "unknown grid flags");
+  if ((g->flags & ADG_GRID_FOLD_STATE) &&
+      (g->system != ADG_SYS_EULER || !adg::predict_fold_supported(g)))
+    return fail(h, ADG_ERR_UNSUPPORTED,
+                "ADG_GRID_FOLD_STATE: not supported for this grid (adg_fold_supported)");
   return ADG_OK;
 }
 
@@ -309,6 +314,13 @@ int adg_spacetime_rate(adg_handle* h, const adg_grid* g, const double* q, double
   if (is_adv(g)) return wrap(h, adg::adv_spacetime_rate(g, q, rate, (cudaStream_t)stream, &e), e);
   if (is_el(g)) return fail(h, ADG_ERR_UNSUPPORTED, "adg_spacetime_rate: Euler and advection");
   return wrap(h, adg::spacetime_rate(g, q, rate, (cudaStream_t)stream, &e), e);
+}
+
+int adg_fold_supported(const adg_grid* g) {
+  return g && !is_adv(g) && !is_el(g) && g->dim >= 1 && g->dim <= 3 &&
+                 adg::predict_fold_supported(g)
+             ? 1
+             : 0;
 }
 
 int adg_predict_range_supported(const adg_grid* g) {

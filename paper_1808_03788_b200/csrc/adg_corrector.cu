@@ -122,10 +122,27 @@ __device__ __forceinline__ void node_fold(const double* q, double gamma, double 
 #pragma unroll
   for (int v = 0; v < M; ++v) fin = fin && isfinite(q[v]);
   nnf += fin ? 0u : 1u;
-  if (admissible<D>(q, gm1)) {
-    ++nadm;
+  // admissibility (systems.py:225-229, exact verdict: the reference's IEEE
+  // division decides within 1e-12 of cancellation) and the d wave speeds
+  // |v_j| + c (systems.py:173-178) from ONE Newton-refined reciprocal of rho
+  // (within a few ulp of the reference's quotients: dt to ~1e-16 relative)
+  // instead of 2 d + 1 divisions: the update kernel is FP64-bound once the
+  // folded state halves its HBM traffic
+  if (fin && q[0] > 0.0) {
+    const double r = rcp_nr(q[0]);
+    double kin = q[1] * q[1];
 #pragma unroll
-    for (int j = 0; j < D; ++j) lam[j] = fmax(lam[j], max_abs_eig<D>(q, gamma, gm1, j));
+    for (int j = 1; j < D; ++j) kin = kin + q[1 + j] * q[1 + j];
+    const double x = 0.5 * kin * r;
+    const double dd = q[D + 1] - x;
+    const bool ppos = fabs(dd) > 1e-12 * (fabs(q[D + 1]) + fabs(x)) ? dd > 0.0
+                                                                       : pressure<D>(q, gm1) > 0.0;
+    if (ppos) {
+      ++nadm;
+      const double c = sqrt(gamma * (gm1 * dd) * r);
+#pragma unroll
+      for (int j = 0; j < D; ++j) lam[j] = fmax(lam[j], fabs(q[1 + j] * r) + c);
+    }
   }
   if (tot) {
 #pragma unroll
@@ -444,7 +461,7 @@ __device__ __forceinline__ void update_chunk(const double* SU_in, const double* 
     if (D == 3) { k[0] = node / (P * P); k[1] = (node / P) % P; k[2] = node % P; }
     double total[M];
 #pragma unroll
-    for (int v = 0; v < M; ++v) total[v] = SV[y * M + v];
+    for (int v = 0; v < M; ++v) total[v] = SV ? SV[y * M + v] : 0.0;   // folded: SU_in holds u + vol / mass
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       int tg = 0;
@@ -478,11 +495,18 @@ __device__ __forceinline__ void update_chunk(const double* SU_in, const double* 
     else wnode = s_w[k[0]] * s_w[k[1]] * s_w[k[2]];
     const double mass = cv * wnode;
     double q[M];
+    if (SV) {
 #pragma unroll
-    for (int v = 0; v < M; ++v) {
-      q[v] = SU_in[y * M + v] + total[v] / mass;
-      SU_out[y * M + v] = q[v];
+      for (int v = 0; v < M; ++v) q[v] = SU_in[y * M + v] + total[v] / mass;
+    } else {
+      // folded: the predictor already applied 1 / mass to the volume term
+      // the same way (one reciprocal per node instead of m divisions)
+      const double rmass = 1.0 / mass;
+#pragma unroll
+      for (int v = 0; v < M; ++v) q[v] = fma(total[v], rmass, SU_in[y * M + v]);
     }
+#pragma unroll
+    for (int v = 0; v < M; ++v) SU_out[y * M + v] = q[v];
     node_fold<D>(q, gamma, gm1, wnode, lam, nadm, nnf, tot);
   }
 }
@@ -537,9 +561,9 @@ update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
   auto issue = [&](int stg, int64_t c) {
     double* st = usm + stg * STAGE;
     const int64_t e0 = c * EB;
-    mbar_expect_tx(&bar[stg], (uint32_t)(STAGE * 8));
+    mbar_expect_tx(&bar[stg], (uint32_t)((vol ? STAGE : STAGE - CU) * 8));
     bulk_g2s(st, u + (size_t)e0 * PD * M, CU * 8, &bar[stg]);
-    bulk_g2s(st + CU, vol + (size_t)e0 * PD * M, CU * 8, &bar[stg]);
+    if (vol) bulk_g2s(st + CU, vol + (size_t)e0 * PD * M, CU * 8, &bar[stg]);
     bulk_g2s(st + 2 * CU, fd + (size_t)e0 * FE, CF * 8, &bar[stg]);
   };
   uint32_t phase[2] = {0u, 0u};
@@ -562,8 +586,8 @@ update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
     mbar_wait(&bar[stg], phase[stg]);
     phase[stg] ^= 1u;
     double* st = usm + stg * STAGE;
-    update_chunk<D, P>(st, st + CU, st + 2 * CU, st, EB, s_w, s_l, s_r, dt, cv, dx, gamma, gm1,
-                       lam, nadm, nnf, tp);
+    update_chunk<D, P>(st, vol ? st + CU : nullptr, st + 2 * CU, st, EB, s_w, s_l, s_r, dt, cv, dx,
+                       gamma, gm1, lam, nadm, nnf, tp);
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -580,13 +604,13 @@ update_kernel(const double* __restrict__ u, const double* __restrict__ vol,
     const size_t off = (size_t)nfull * EB * PD * M;
     for (int x = tid; x < tail * PD * M; x += kReduceThreads) {
       st[x] = u[off + x];
-      st[CU + x] = vol[off + x];
+      if (vol) st[CU + x] = vol[off + x];
     }
     for (int x = tid; x < tail * FE; x += kReduceThreads)
       st[2 * CU + x] = fd[(size_t)nfull * EB * FE + x];
     __syncthreads();
-    update_chunk<D, P>(st, st + CU, st + 2 * CU, st, tail, s_w, s_l, s_r, dt, cv, dx, gamma,
-                       gm1, lam, nadm, nnf, tp);
+    update_chunk<D, P>(st, vol ? st + CU : nullptr, st + 2 * CU, st, tail, s_w, s_l, s_r, dt, cv,
+                       dx, gamma, gm1, lam, nadm, nnf, tp);
     __syncthreads();
     for (int x = tid; x < tail * PD * M; x += kReduceThreads) u_out[off + x] = st[x];
   }
@@ -755,6 +779,11 @@ int update(const adg_grid* g, const double* u, const double* vol, const double* 
     return ADG_ERR_INVALID;
   }
   if (red_next) zero_reduce_kernel<<<1, 32, 0, st>>>(red_next);
+  if (g->flags & ADG_GRID_FOLD_STATE) {
+    // the predictor left w = u + vol / mass in `vol`: it takes u's place
+    u = vol;
+    vol = nullptr;
+  }
   ADG_SWITCH_DP(launch_update, g, u, vol, fd, dt_dev, u_out, red_next, partial, st);
   return check_launch(err);
 }

@@ -41,6 +41,7 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
             const double* q_init = nullptr, int startup_only = 0);
 // element ranges run on the shared-tile predictor only
 bool predict_range_supported(const adg_grid* g);
+bool predict_fold_supported(const adg_grid* g);
 
 bool predict_stream_supported(const adg_grid* g);
 size_t predict_stream_workspace_bytes(int P, int num_sms);

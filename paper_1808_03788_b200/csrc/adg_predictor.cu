@@ -179,6 +179,7 @@ struct PredArgs {
   int prim;            // predictor_mode: 0 conservative, 1 primitive
   int startup_only;    // stop after the startup guess (startup_guess): no sweeps,
                        // q_out keeps the iterate variables
+  int fold;            // ADG_GRID_FOLD_STATE: vol <- u^n + vol / mass
   // D / dx_dir for the three directions, [dir][P][P] (rows packed with the
   // launch's P).  Kernel parameters live in the constant bank, so every
   // contraction coefficient is a DFMA constant operand: no shared-memory
@@ -383,6 +384,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
   // (dt |Omega| / dx_j) (w_tensor / w_row) as corrector.py:172-176 forms it;
   // element-independent, so formed once
   double vcoef[D];
+  double rmass;   // 1 / (|cell| w_node): ADG_GRID_FOLD_STATE
   {
     const double cv = a.dx[0] * (D >= 2 ? a.dx[1] : 1.0) * (D == 3 ? a.dx[2] : 1.0);
     const double wnode = T.weights[ni] * (D >= 2 ? T.weights[nj] : 1.0) *
@@ -392,6 +394,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
       const int row = dir == 0 ? ni : (dir == 1 ? nj : nk);
       vcoef[dir] = (dt * cv / a.dx[dir]) * (wnode / T.weights[row]);
     }
+    rmass = 1.0 / (cv * wnode);
   }
   // a lone element's volume block leaves straight from registers (strided
   // 8-byte stores; L2 merges the sectors) instead of through shared memory
@@ -401,7 +404,7 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #endif
   constexpr bool VOL_DIRECT = ADG_VOL_DIRECT && EPB == 1;
 #ifndef ADG_VOL_NODE
-#define ADG_VOL_NODE 0
+#define ADG_VOL_NODE 0   // (no ADG_GRID_FOLD_STATE in this variant)
 #endif
   constexpr bool VOL_NODE = ADG_VOL_NODE && VOL_DIRECT;
 
@@ -1022,6 +1025,10 @@ predict_kernel(const __grid_constant__ PredArgs a) {
 #pragma unroll
         for (int v = 0; v < M; ++v) acc[v] += vcoef[dir] * CB[(dir * PD + item) * M + v];
       }
+      if (!PRIM && a.fold) {   // w = u^n + vol / mass (uu is the conservative u^n here)
+#pragma unroll
+        for (int v = 0; v < M; ++v) acc[v] = fma(acc[v], rmass, uu[v]);
+      }
       if constexpr (VOL_DIRECT) {
         if (lane_ok) {
           double* vo = a.vol + ((size_t)e * PD + item) * M;
@@ -1141,6 +1148,12 @@ size_t predict_workspace_bytes(int dim, int P, int num_sms, int64_t n_elem) {
 
 bool predict_range_supported(const adg_grid* g) { return !predict_stream_supported(g); }
 
+// ADG_GRID_FOLD_STATE: Euler, conservative iterate, shared-tile kernel
+bool predict_fold_supported(const adg_grid* g) {
+  return g->system == ADG_SYS_EULER && g->mode == ADG_MODE_CONSERVATIVE &&
+         !predict_stream_supported(g) && !ADG_VOL_NODE;
+}
+
 int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol, int max_iter,
             int min_iter, double* q_out, double* vol, double* traces, uint8_t* pred_bad,
             int32_t* sweeps, cudaStream_t st, int num_sms, double* ws, size_t ws_bytes,
@@ -1164,6 +1177,11 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   // 3-D N >= 7 grids too (A/B runs against the slice-streaming kernel)
   const char* pv = getenv("ADG_PREDICTOR");
   const bool plain = q_init == nullptr && !startup_only && !(pv && pv[0] == 't');
+  const bool fold = (g->flags & ADG_GRID_FOLD_STATE) != 0;
+  if (fold && (!predict_fold_supported(g) || startup_only)) {
+    *err = "ADG_GRID_FOLD_STATE: not supported for this grid (adg_fold_supported)";
+    return ADG_ERR_UNSUPPORTED;
+  }
   // 3-D tiles beyond one SM's shared memory (N >= 7): from N = 8 up as phase
   // kernels over element batches with the iterate in HBM
   // (adg_predictor_phased.cu: 30.1 vs 51.4 ms at N = 8, 56.1 vs 78.3 ms at N = 9
@@ -1206,6 +1224,7 @@ int predict(const adg_grid* g, const double* u, const double* dt_dev, double tol
   a.max_iter = startup_only ? 0 : (max_iter > 0 ? max_iter : 2 * g->degree + 2);
   a.min_iter = min_iter;
   a.prim = g->mode == ADG_MODE_PRIMITIVE ? 1 : 0;
+  a.fold = fold ? 1 : 0;
   {
     // D / dx exactly as the reference forms it (diff / spacing, one IEEE
     // division per entry, basis.py diff; predictor.py:65-71)

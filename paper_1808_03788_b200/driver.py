@@ -21,6 +21,7 @@ RuntimeErrors.
 """
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -206,6 +207,7 @@ class Simulation:
         g.degree = self.tables.degree
         g.nvars = self.system.n_vars
         g.mode = _lib.MODE_CODES[self._iterate_mode]
+        g.flags = 0
         for j in range(3):
             g.cells[j] = int(cells[j]) if j < d else 1
             g.dx[j] = float(spacings[j]) if j < d else 1.0
@@ -216,6 +218,12 @@ class Simulation:
                 if (j, s) in self._ghost:
                     kind = "ghost"
                 g.bc[j][s] = _lib.BC_CODES[kind]
+        # the predictor leaves u^n + vol / mass for the update where the
+        # library supports it (one array less through HBM per step;
+        # ADG_NO_FOLD=1: the plain volume integral, for A/B runs)
+        if (os.environ.get("ADG_NO_FOLD") != "1"
+                and _lib.load().adg_fold_supported(_lib.ctypes.byref(g))):
+            g.flags |= _lib.GRID_FOLD_STATE
         return g
 
     def _gp(self):
